@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: MinHash signature entries/s on B200 (BASELINE.json metric).
+
+One step = one pass of the signing hot path (mhb_sign_iterative_csr) over one
+full batch of the workload, inputs resident in HBM.  Default workload at N=1 is
+BASELINE configs[1] ("cfg2"): 1,000,000 sets, lognormal(median 120, sigma 1.0)
+sizes capped at 20,000, Zipf(1.1) ids over 2^24, N=256 hashes, iterative family.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Multi-GPU is weak scaling: every rank signs its own full-size cfg2 batch (distinct
+seeds; the batch shards by rows with no exchange), value = all ranks' entries /
+max-over-ranks device time.  --impl reference times the reference algorithm's CPU
+restatement (oracle/, C + OpenMP, all host cores) on a bounded sample of the same
+workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "minhash signature entries/sec (sets·hashes/s)"
+K_ITER = 2.5   # integer instructions per visit, iterative
+K_CW = 5.5     # random family
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--family", choices=["iterative", "random"], default="iterative")
+    ap.add_argument("--n-sets", type=int, default=None, help="override the config's set count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of signatures (N>1)")
+    return ap.parse_args()
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("sm_max_mhz", 1965.0), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        power = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(power) if power else None}
+
+
+def _ncu_traffic(config: str, family: str):
+    """Per-launch DRAM bytes of the main kernel from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    ent = d.get(f"{config}/{family}")
+    if not ent:
+        return None, None
+    return ent.get("dram_bytes_per_launch"), ent.get("source")
+
+
+def cpu_baseline_run(indptr_h, ids_h, fam, budget_s: float, threads: int):
+    """Oracle port (C + OpenMP) on a bounded prefix of the workload; returns entries/s and sample."""
+    import numpy as np
+
+    from oracle import oracle
+
+    n_total = indptr_h.size - 1
+    probe = min(n_total, 2000)
+    t0 = time.perf_counter()
+    oracle.sign_family_csr(indptr_h[:probe + 1], ids_h, fam, threads=threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    n = int(min(n_total, max(probe, probe * budget_s / dt)))
+    t0 = time.perf_counter()
+    oracle.sign_family_csr(indptr_h[:n + 1], ids_h, fam, threads=threads)
+    dt = time.perf_counter() - t0
+    nnz = int(indptr_h[n] - indptr_h[0])
+    return n * fam.size / dt, n, nnz, dt
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU restatement on host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+
+    from oracle import oracle
+    from paper_1401_6124_b200 import gen, make_family
+
+    cfg = gen.CONFIGS[args.config]
+    fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
+    threads = os.cpu_count() or 1
+    # bounded sample of the same workload (same generator and distributions), sized to ~3 s per step
+    n_sample = 4000
+    ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_sample)
+    ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
+    t0 = time.perf_counter()
+    oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
+    dt = time.perf_counter() - t0
+    n_step = int(max(1000, min(200_000, n_sample * 3.0 / max(dt, 1e-6))))
+    if n_step > n_sample:
+        ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_step)
+        ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
+    else:
+        ip_h = ip_h[:n_step + 1]
+    for _ in range(args.warmup):
+        oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
+        times.append(time.perf_counter() - t0)
+    step_s = statistics.mean(times)
+    value = n_step * fam.size / step_s
+    nnz = int(ip_h[n_step] - ip_h[0])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} sample ({n_step} sets, nnz {nnz}) of " + _workload_name(cfg, args.family),
+                   "n_hash": cfg.n_hash, "prime": cfg.prime, "family": args.family},
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
+                         "sample": f"first {n_step} sets of {cfg.name} (same generator), "
+                                   f"C restatement of kernels.py:21-73, OpenMP over sets"},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _workload_name(cfg, family):
+    if cfg.size_kind == "lognormal":
+        sizes = f"lognormal(median {cfg.size_a:g}, sigma {cfg.size_b:g}) capped {cfg.size_cap}"
+    else:
+        sizes = f"max(1, Poisson({cfg.size_a:g}))"
+    ids = f"Zipf({cfg.zipf_s:g})" if cfg.id_kind == "zipf" else "uniform"
+    return f"{cfg.n_sets} sets, {sizes}, {ids} ids over 2^{cfg.vocab_log2}, N={cfg.n_hash}, {family}"
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6124_b200 import _lib, gen, make_family, signatures_csr
+    from paper_1401_6124_b200.minhash import sign_csr_device
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    cfg = gen.CONFIGS[args.config]
+    n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
+    t0 = time.perf_counter()
+    indptr, ids = gen.make_csr(cfg, device=dev, n_sets=n_sets, seed=cfg.data_seed() + rank)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    nnz = int(ids.numel())
+    fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
+    N = fam.size
+    out = torch.empty((n_sets, N), dtype=torch.uint32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sign_csr_device(indptr, ids, fam, out, status, stream)
+
+    # correctness guard on a few hundred sets (the full parity suite lives in tests/)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if int(status.item()) != 0:
+        raise SystemExit(f"device status flags {int(status.item())}")
+    if rank == 0:
+        from oracle import oracle
+
+        k = 300
+        ip_h = indptr[:k + 1].cpu().numpy()
+        want = oracle.sign_family_csr(ip_h, ids[:int(ip_h[-1])].cpu().numpy().view(np.uint32), fam)
+        if not np.array_equal(out[:k].cpu().numpy().astype(np.int64), want):
+            raise SystemExit("bench guard: GPU signatures differ from the oracle")
+
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    _lib.check(lib.mhb_profile_begin(args.steps))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    import ctypes as C
+
+    kms, kn = C.c_float(0), C.c_int32(0)
+    _lib.check(lib.mhb_profile_end(C.byref(kms), C.byref(kn)))
+    clocks = clk.stop()
+    elapsed_ms = e0.elapsed_time(e1)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    value = world * n_sets * N * args.steps / (max_ms / 1e3)
+
+    gather_ms = None
+    if world > 1 and args.gather:
+        from paper_1401_6124_b200.dist import gather_blocks
+
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record()
+        gather_blocks(out, [n_sets] * world)
+        g1.record()
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1)
+
+    # ---- roofline of the main kernel ----
+    hbm_gbs, sm_max_mhz, peak_src = _peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    kernel_ms = kms.value / max(kn.value, 1)
+    visits = N * nnz
+    k_instr = K_ITER if args.family == "iterative" else K_CW
+    peak_visits = sms * 128 * sm_max_mhz * 1e6 / k_instr
+    achieved_visits = visits / (kernel_ms / 1e3)
+    alg_bytes = 4 * nnz + 8 * (n_sets + 1) + 4 * n_sets * N
+    traffic, traffic_src = _ncu_traffic(args.config, args.family)
+    probe_v, probe_ms = C.c_double(0), C.c_float(0)
+    _lib.check(lib.mhb_probe_visit_rate(1 << 20, 0 if args.family == "iterative" else 1,
+                                        C.byref(probe_v), C.byref(probe_ms), stream.cuda_stream))
+    probe_rate = probe_v.value / (probe_ms.value / 1e3)
+    roofline = {
+        "bound": "int", "unit": "Gvisit/s",
+        "achieved": achieved_visits / 1e9, "peak": peak_visits / 1e9, "frac": achieved_visits / peak_visits,
+        "traffic": traffic,
+        "peak_basis": f"{sms} SMs x 128 int lanes/clk x {sm_max_mhz:g} MHz ({peak_src} sm_max_mhz) / "
+                      f"{k_instr} instr per visit; visit = (set, hash, feature)",
+        "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
+        "frac_at_measured_clock": (achieved_visits / (sms * 128 * clocks["sm_mhz"] * 1e6 / k_instr)
+                                   if clocks.get("sm_mhz") else None),
+        "probe_register_only_gvisit_s": probe_rate / 1e9,
+        "frac_of_probe": achieved_visits / probe_rate,
+        "hbm": {"algorithmic_bytes": alg_bytes, "achieved_gbs": alg_bytes / (kernel_ms / 1e3) / 1e9,
+                "peak_gbs": hbm_gbs, "frac": alg_bytes / (kernel_ms / 1e3) / 1e9 / hbm_gbs,
+                "traffic_source": traffic_src},
+    }
+
+    # ---- e2e through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        ip_pin = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
+        ids_pin = torch.empty(ids.shape, dtype=torch.int32, pin_memory=True)
+        out_pin = torch.empty((n_sets, N), dtype=torch.int32, pin_memory=True)
+        ip_pin.copy_(indptr)
+        ids_pin.copy_(ids.view(torch.int32))
+        ip_np, ids_np = ip_pin.numpy(), ids_pin.numpy().view(np.uint32)
+        out_np = out_pin.numpy().view(np.uint32)
+        signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)  # warm buffers
+        if world > 1:
+            dist.barrier()
+        times = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)
+            times.append(time.perf_counter() - t0)
+        if not np.array_equal(out_np[:1000], out[:1000].cpu().numpy()):
+            raise SystemExit("e2e output differs from the device path")
+        e2e_s = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n_sets * N / float(e2e_s.item()), "unit": "entries/s",
+               "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
+               "ms_per_step": float(e2e_s.item()) * 1e3,
+               "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 3 streams)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        ip_h = indptr.cpu().numpy()
+        ids_h = ids.cpu().numpy().view(np.uint32)
+        v, n_s, nnz_s, dt = cpu_baseline_run(ip_h, ids_h, fam, args.cpu_seconds, threads)
+        cpu = {"value": v, "unit": "entries/s", "cores": threads, "kind": "port",
+               "sample": f"first {n_s} of {n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
+                         f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: " + _workload_name(cfg, args.family), "n_sets_per_rank": n_sets,
+                       "nnz_per_rank": nnz, "n_hash": N, "prime": cfg.prime, "family": args.family,
+                       "out": "uint32 argmin ids, resident in HBM",
+                       "l2": "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per step vs 126 MB L2)"
+                             % (4 * nnz / 1e9, 4 * n_sets * N / 1e9),
+                       "parallelism": f"dp{world} (row shards, no collective in the step)",
+                       "gen_seconds": round(gen_s, 2)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 3 * args.steps, "clocks": clocks,
+        }
+        if gather_ms is not None:
+            line["gather_ms"] = gather_ms
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

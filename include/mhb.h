@@ -1,0 +1,170 @@
+/*
+ * mhb.h -- C ABI of libmhb, the B200 (sm_100a) MinHash signature library.
+ *
+ * This is the drop-in boundary for the reference's compiled hot loops
+ * (arXiv 1401.6124 reference package `minhashlab`):
+ *
+ *   reference (numba, one set per call)                 this ABI (CUDA, CSR batch per call)
+ *   -------------------------------------------------   ---------------------------------------
+ *   kernels.sign_iterative(ids, a, b, p, n)             mhb_sign_iterative_csr
+ *       /root/reference/pkg/src/minhashlab/kernels.py:44-73
+ *   kernels.sign_random(ids, a, b, p)                   mhb_sign_random_csr
+ *       /root/reference/pkg/src/minhashlab/kernels.py:21-41
+ *   minhash.signature(s, family) dispatch               (Python host layer, calls the two above)
+ *       /root/reference/pkg/src/minhashlab/minhash.py:91-110
+ *   minhash.estimate_jaccard(g1, g2)                    mhb_jaccard_pairs / mhb_jaccard_block
+ *       /root/reference/pkg/src/minhashlab/minhash.py:130-137, bench.py:165-168
+ *   stats.bucket_uniformity_experiment counts           mhb_bucket_hist_iterative / _random
+ *       /root/reference/pkg/src/minhashlab/stats.py:221-224 (eval_all(x) % buckets, bincount)
+ *
+ * Output semantics are the reference's: out[s*n_hash + i] is the feature id of
+ * set s that minimises h_i over the set (argmin, not the min hash value), with
+ * h_i(x) = ((a+i)*x + i*b) mod p (iterative, families.py:124-131) or
+ * h_i(x) = (a_i*x + b_i) mod p (random, families.py:70-112).  Every member is a
+ * bijection on [0,p), so the reference's "smallest id wins ties" rule
+ * (minhash.py:94-96) never decides a result and the argmin is unique.
+ *
+ * Conventions
+ *  - All array pointers passed to mhb_sign_* / mhb_jaccard_* / mhb_bucket_hist_*
+ *    are DEVICE pointers owned by the caller.  The library allocates nothing on
+ *    these paths; scratch comes from the caller's workspace.
+ *  - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t, or
+ *    NULL for the legacy default stream).  No host synchronisation happens inside.
+ *  - CSR: indptr is int64[n_sets+1] (indptr[0] need not be 0: ids are addressed
+ *    as ids[indptr[s] .. indptr[s+1])), ids is uint32[>= indptr[n_sets]].
+ *    Ids may be in any order and may repeat inside a set (min is idempotent).
+ *  - Data errors found on the device are OR-ed into *status (reset to 0 by the
+ *    call): MHB_STATUS_EMPTY_SET mirrors minhash.py:97-98, MHB_STATUS_ID_GE_PRIME
+ *    mirrors minhash.py:99-101.  Rows with a flagged error hold unspecified ids.
+ *  - Return value: MHB_OK or an MHB_ERR_* code; mhb_last_error() gives the text
+ *    (thread-local).  Argument errors are detected before any launch.
+ *  - Supported modulus: 3 <= prime < 2^31, prime must be prime.  (Every BASELINE
+ *    configuration qualifies: the largest prime used is 1,073,741,827.)
+ */
+#ifndef MHB_H_
+#define MHB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mhb_error {
+    MHB_OK = 0,
+    MHB_ERR_INVALID = 1,     /* bad argument (maps to the reference's ValueError) */
+    MHB_ERR_CUDA = 2,        /* CUDA runtime error */
+    MHB_ERR_UNSUPPORTED = 3  /* valid for the reference, outside this library's range */
+};
+
+enum mhb_out_dtype {
+    MHB_OUT_U32 = 0,         /* uint32 argmin ids (compact; ids < prime < 2^31) */
+    MHB_OUT_I64 = 1          /* int64 argmin ids (the reference's dtype, kernels.py:29,51-52) */
+};
+
+enum mhb_status_bits {
+    MHB_STATUS_EMPTY_SET = 1,    /* some row has indptr[s+1] <= indptr[s] */
+    MHB_STATUS_ID_GE_PRIME = 2,  /* some feature id >= prime */
+    MHB_STATUS_BAD_PARAM = 4     /* random family: some a_i not in [1,p) or b_i not in [0,p) */
+};
+
+/* Library identification. */
+const char* mhb_version(void);
+
+/* Text of the last error raised on the calling thread ("" if none). */
+const char* mhb_last_error(void);
+
+/* Scratch bytes mhb_sign_* needs for this problem shape (same for both families). */
+size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash);
+
+/*
+ * Iterative family signatures (replaces kernels.sign_iterative, kernels.py:44-73,
+ * for a whole CSR batch).  a, b are the family base parameters
+ * (IterativeFamily.base.a / .base.b, families.py:133-147), with a + n_hash < prime.
+ * out: n_sets * n_hash entries of out_dtype, row-major.
+ */
+int mhb_sign_iterative_csr(const int64_t* indptr, const uint32_t* ids,
+                           int64_t n_sets, int64_t nnz,
+                           uint64_t a, uint64_t b, uint64_t prime, int32_t n_hash,
+                           void* out, int32_t out_dtype, int32_t* status,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Random (Carter-Wegman) family signatures (replaces kernels.sign_random,
+ * kernels.py:21-41).  a, b: device uint32[n_hash] (RandomFamily.a / .b,
+ * families.py:193-204), 1 <= a_i < prime, 0 <= b_i < prime.
+ */
+int mhb_sign_random_csr(const int64_t* indptr, const uint32_t* ids,
+                        int64_t n_sets, int64_t nnz,
+                        const uint32_t* a, const uint32_t* b, uint64_t prime, int32_t n_hash,
+                        void* out, int32_t out_dtype, int32_t* status,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Host-buffer entry (the end-to-end path an FFI caller uses): indptr/ids/out are
+ * HOST pointers (page-locked for full copy bandwidth; pageable also works).  The
+ * library stages chunks through its own device buffers on `device` with copy/
+ * compute overlap, and returns when out is complete.  kind: 0 iterative, 1 random
+ * (a_host/b_host used for random, a/b scalars for iterative).
+ */
+int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint32_t* ids,
+                      int64_t n_sets, int64_t nnz,
+                      uint64_t a, uint64_t b, const uint32_t* a_host, const uint32_t* b_host,
+                      uint64_t prime, int32_t n_hash,
+                      void* out, int32_t out_dtype, int32_t* status_host, int32_t device);
+
+/* Release the device buffers and streams cached by mhb_sign_csr_host. */
+void mhb_host_release(void);
+
+/*
+ * Pairwise Jaccard estimates for listed pairs (replaces estimate_jaccard,
+ * minhash.py:130-137): counts[k] = #{i : sig[pi[k]][i] == sig[pj[k]][i]};
+ * est[k] = (double)counts[k] / n_hash (IEEE division, bit-identical to numpy's
+ * mean of the 0/1 vector for n_hash < 2^53).  est may be NULL.
+ */
+int mhb_jaccard_pairs(const void* sig, int32_t sig_dtype, int32_t n_hash,
+                      const int64_t* pi, const int64_t* pj, int64_t n_pairs,
+                      uint32_t* counts, double* est, void* stream);
+
+/*
+ * Block x block estimates: counts[r*n_cols + c] = #{i : A[r][i] == B[c][i]} for
+ * signature blocks A (n_rows x n_hash) and B (n_cols x n_hash) of dtype sig_dtype.
+ */
+int mhb_jaccard_block(const void* sig_a, int64_t n_rows, const void* sig_b, int64_t n_cols,
+                      int32_t sig_dtype, int32_t n_hash, uint32_t* counts, void* stream);
+
+/*
+ * Bucket-uniformity histogram (generalises stats.py:221-224 from one x to a
+ * batch): counts[m] += #{(x, i) : x in xs, 0 <= i < n_hash, h_i(x) mod buckets == m}.
+ * counts is uint64[buckets], accumulated into (not cleared).  xs must be < prime.
+ */
+int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x,
+                              uint64_t a, uint64_t b, uint64_t prime, int32_t n_hash,
+                              uint32_t buckets, unsigned long long* counts, void* stream);
+int mhb_bucket_hist_random(const uint32_t* xs, int64_t n_x,
+                           const uint32_t* a, const uint32_t* b, uint64_t prime, int32_t n_hash,
+                           uint32_t buckets, unsigned long long* counts, void* stream);
+
+/*
+ * Instruction-rate probe for the roofline: runs the iterative visit sequence
+ * (add, conditional subtract, 3-way min) from registers only, `visits_per_thread`
+ * visits per thread on a persistent grid, and reports visits and device ms.
+ */
+int mhb_probe_visit_rate(int64_t visits_per_thread, int32_t kind,
+                         double* visits_out, float* ms_out, void* stream);
+
+/*
+ * Kernel timing for benchmarks: while enabled, every mhb_sign_* call records a CUDA
+ * event pair on its stream around the main signature kernel (up to max_launches
+ * calls).  mhb_profile_end synchronises on the recorded events and returns the
+ * summed device time of the main kernel and the number of launches timed.
+ */
+int mhb_profile_begin(int32_t max_launches);
+int mhb_profile_end(float* total_ms, int32_t* n_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MHB_H_ */

@@ -1,0 +1,329 @@
+// aux.cu -- Jaccard estimates over signature blocks, bucket-uniformity
+// histograms, and the visit-rate probe used for the roofline.
+//
+// Reference:
+//   estimate_jaccard   minhash.py:130-137  float(mean(g1.mins == g2.mins))
+//   _pair_estimate     bench.py:165-168    same, inline
+//   bucket histogram   stats.py:221-224    bincount(family.eval_all(x) % buckets)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.h"
+#include "modarith.cuh"
+
+namespace mhb {
+
+// ---------------------------------------------------------------------------
+// Jaccard: listed pairs, one warp per pair
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void jaccard_pairs_kernel(const T* __restrict__ sig, int32_t n_hash,
+                                     const int64_t* __restrict__ pi, const int64_t* __restrict__ pj,
+                                     int64_t n_pairs, uint32_t* __restrict__ counts,
+                                     double* __restrict__ est) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t k = warp0; k < n_pairs; k += nwarps) {
+        const T* r1 = sig + pi[k] * (int64_t)n_hash;
+        const T* r2 = sig + pj[k] * (int64_t)n_hash;
+        uint32_t c = 0;
+        for (int32_t i = lane; i < n_hash; i += 32) c += (__ldg(r1 + i) == __ldg(r2 + i));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) {
+            counts[k] = c;
+            if (est) est[k] = (double)c / (double)n_hash;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Jaccard: block x block, 32x32 output tile per CTA, hash dimension staged in smem
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void jaccard_block_kernel(const T* __restrict__ A, int64_t n_rows, const T* __restrict__ B,
+                                     int64_t n_cols, int32_t n_hash, uint32_t* __restrict__ counts) {
+    constexpr int TILE = 32, HC = 32;
+    __shared__ T sa[TILE][HC + 1];
+    __shared__ T sb[TILE][HC + 1];
+    const int tx = threadIdx.x & 31;  // column within tile
+    const int ty = threadIdx.x >> 5;  // 8 warps -> 4 rows each
+    const int64_t r0 = (int64_t)blockIdx.y * TILE, c0 = (int64_t)blockIdx.x * TILE;
+    uint32_t acc[4] = {0, 0, 0, 0};
+    for (int32_t h0 = 0; h0 < n_hash; h0 += HC) {
+        for (int t = threadIdx.x; t < TILE * HC; t += blockDim.x) {
+            const int rr = t / HC, hh = t % HC;
+            const int64_t gr = r0 + rr, gc = c0 + rr;
+            const int32_t gh = h0 + hh;
+            sa[rr][hh] = (gr < n_rows && gh < n_hash) ? A[gr * n_hash + gh] : (T)-1;
+            sb[rr][hh] = (gc < n_cols && gh < n_hash) ? B[gc * n_hash + gh] : (T)-2;
+        }
+        __syncthreads();
+        const int hn = (n_hash - h0) < HC ? (n_hash - h0) : HC;
+        for (int hh = 0; hh < hn; ++hh) {
+            const T bv = sb[tx][hh];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += (sa[ty * 4 + q][hh] == bv);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t r = r0 + ty * 4 + q, c = c0 + tx;
+        if (r < n_rows && c < n_cols) counts[r * n_cols + c] = acc[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Bucket histogram.  Work unit = (x, run of up to kRun consecutive members).
+// Bins live in shared memory when they fit (privatised per CTA), else in global.
+// ---------------------------------------------------------------------------
+constexpr int kRun = 256;
+
+struct HistArgs {
+    const uint32_t* xs;
+    int64_t n_x;
+    uint32_t p, b;
+    uint64_t a;
+    int32_t n_hash;
+    uint32_t m, mp;  // buckets, floor(2^32 / m) (m >= 2)
+    const uint32_t* ra;
+    const uint32_t* rb;
+    unsigned long long* counts;
+    int kind;
+    int use_smem;
+};
+
+__device__ __forceinline__ uint32_t mod_bucket(uint32_t h, uint32_t m, uint32_t mp) {
+    if (m == 1) return 0;
+    uint32_t r = h - __umulhi(h, mp) * m;  // in [0, 2m)
+    return __viaddmin_u32(r, 0u - m, r);
+}
+
+__global__ void hist_kernel(HistArgs H) {
+    extern __shared__ uint32_t bins[];
+    if (H.use_smem) {
+        for (uint32_t i = threadIdx.x; i < H.m; i += blockDim.x) bins[i] = 0;
+        __syncthreads();
+    }
+    const int64_t runs_per_x = (H.n_hash + kRun - 1) / kRun;
+    const int64_t units = H.n_x * runs_per_x;
+    const uint32_t p = H.p;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xi = u / runs_per_x;
+        const int32_t i0 = (int32_t)(u - xi * runs_per_x) * kRun;
+        const int32_t i1 = min(i0 + kRun, H.n_hash);
+        const uint32_t x = H.xs[xi];
+        if (H.kind == 0) {
+            // h_{i0}(x) = (a + i0) x + i0 b mod p, then the additive walk (families.py:153-176)
+            const uint64_t A = (H.a + (uint64_t)i0) % p;
+            const uint64_t Bv = (uint64_t)i0 * H.b % p;
+            uint32_t h = (uint32_t)((A * (x % p) + Bv) % p);
+            const uint32_t dh = (uint32_t)(((uint64_t)x + H.b) % p);
+            for (int32_t i = i0; i < i1; ++i) {
+                const uint32_t bin = mod_bucket(h, H.m, H.mp);
+                if (H.use_smem) atomicAdd(&bins[bin], 1u);
+                else atomicAdd(&H.counts[bin], 1ull);
+                h = reduce_once(h + dh, p);
+            }
+        } else {
+            for (int32_t i = i0; i < i1; ++i) {
+                const uint32_t h = (uint32_t)(((uint64_t)H.ra[i] * (x % p) + H.rb[i]) % p);
+                const uint32_t bin = mod_bucket(h, H.m, H.mp);
+                if (H.use_smem) atomicAdd(&bins[bin], 1u);
+                else atomicAdd(&H.counts[bin], 1ull);
+            }
+        }
+    }
+    if (H.use_smem) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < H.m; i += blockDim.x)
+            if (bins[i]) atomicAdd(&H.counts[i], (unsigned long long)bins[i]);
+    }
+}
+
+static int launch_hist(HistArgs H, cudaStream_t st) {
+    clear_error();
+    if (H.m < 1) return set_error(MHB_ERR_INVALID, "need at least one bucket, got %u", H.m);
+    if (H.n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function");
+    if (H.p < 3 || !is_prime_u64(H.p)) return set_error(MHB_ERR_INVALID, "modulus %u is not prime", H.p);
+    if (H.n_x <= 0) return MHB_OK;
+    H.mp = H.m >= 2 ? (uint32_t)((1ull << 32) / H.m) : 0;
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    size_t smem = (size_t)H.m * sizeof(uint32_t);
+    H.use_smem = smem <= 96 * 1024;
+    if (!H.use_smem) smem = 0;
+    if (smem > 48 * 1024) {
+        rc = cuda_check(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "hist smem attr");
+        if (rc) return rc;
+    }
+    const int64_t units = H.n_x * ((H.n_hash + kRun - 1) / kRun);
+    int64_t blocks = (units + 255) / 256;
+    if (blocks > (int64_t)dev.sms * 2) blocks = (int64_t)dev.sms * 2;
+    if (blocks < 1) blocks = 1;
+    hist_kernel<<<(unsigned)blocks, 256, smem, st>>>(H);
+    return cuda_check(cudaGetLastError(), "hist_kernel launch");
+}
+
+// ---------------------------------------------------------------------------
+// Visit-rate probe: the iterative inner loop from registers only.
+// ---------------------------------------------------------------------------
+__device__ uint32_t g_probe_sink;
+
+template <int K>
+__global__ void __launch_bounds__(256) probe_iter_kernel(int64_t rounds, uint32_t p, uint32_t seed) {
+    uint32_t best[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
+    uint32_t ha = (threadIdx.x * 2654435761u + seed) % p, hb = (ha * 7u + 13u) % p;
+    uint32_t da = (blockIdx.x * 40503u + 17u) % p, db = (da * 3u + 5u) % p;
+    for (int64_t r = 0; r < rounds; ++r) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            best[k] = __vimin3_u32(best[k], ha, hb);
+            ha = reduce_once(ha + da, p);
+            hb = reduce_once(hb + db, p);
+        }
+        da ^= (uint32_t)r & 1u;  // keep the loop from being folded
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_probe_sink = acc;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) probe_random_kernel(int64_t rounds, uint32_t p, uint32_t seed) {
+    uint32_t best[K], cA[K], cAp[K], cB[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        best[k] = 0xffffffffu;
+        cA[k] = (seed + 977u * k + threadIdx.x) % (p - 1) + 1;
+        cAp[k] = (uint32_t)(((uint64_t)cA[k] << 32) / p);
+        cB[k] = (seed * 31u + k) % p;
+    }
+    uint32_t xa = (threadIdx.x * 2654435761u + seed) % p, xb = (xa * 7u + 13u) % p;
+    for (int64_t r = 0; r < rounds; ++r) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            best[k] = __vimin3_u32(best[k], mul_add_mod_narrow(cA[k], cAp[k], cB[k], xa, p),
+                                   mul_add_mod_narrow(cA[k], cAp[k], cB[k], xb, p));
+        xa = reduce_once(xa + 1u, p);
+        xb = reduce_once(xb + 3u, p);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_probe_sink = acc;
+}
+
+}  // namespace mhb
+
+using namespace mhb;
+
+extern "C" int mhb_jaccard_pairs(const void* sig, int32_t sig_dtype, int32_t n_hash, const int64_t* pi,
+                                 const int64_t* pj, int64_t n_pairs, uint32_t* counts, double* est,
+                                 void* stream) {
+    clear_error();
+    if (n_hash < 1) return set_error(MHB_ERR_INVALID, "signature lengths must be positive");
+    if (n_pairs <= 0) return MHB_OK;
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int64_t blocks = (n_pairs * 32 + 255) / 256;
+    if (blocks > (int64_t)dev.sms * 16) blocks = (int64_t)dev.sms * 16;
+    if (sig_dtype == MHB_OUT_I64)
+        jaccard_pairs_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(
+            static_cast<const long long*>(sig), n_hash, pi, pj, n_pairs, counts, est);
+    else if (sig_dtype == MHB_OUT_U32)
+        jaccard_pairs_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(
+            static_cast<const uint32_t*>(sig), n_hash, pi, pj, n_pairs, counts, est);
+    else
+        return set_error(MHB_ERR_INVALID, "unknown sig_dtype %d", sig_dtype);
+    return cuda_check(cudaGetLastError(), "jaccard_pairs launch");
+}
+
+extern "C" int mhb_jaccard_block(const void* sig_a, int64_t n_rows, const void* sig_b, int64_t n_cols,
+                                 int32_t sig_dtype, int32_t n_hash, uint32_t* counts, void* stream) {
+    clear_error();
+    if (n_hash < 1) return set_error(MHB_ERR_INVALID, "signature lengths must be positive");
+    if (n_rows <= 0 || n_cols <= 0) return MHB_OK;
+    if ((n_rows + 31) / 32 > 65535) return set_error(MHB_ERR_INVALID, "n_rows too large for one call");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dim3 grid((unsigned)((n_cols + 31) / 32), (unsigned)((n_rows + 31) / 32));
+    if (sig_dtype == MHB_OUT_I64)
+        jaccard_block_kernel<long long><<<grid, 256, 0, st>>>(static_cast<const long long*>(sig_a), n_rows,
+                                                              static_cast<const long long*>(sig_b), n_cols,
+                                                              n_hash, counts);
+    else if (sig_dtype == MHB_OUT_U32)
+        jaccard_block_kernel<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(sig_a), n_rows,
+                                                             static_cast<const uint32_t*>(sig_b), n_cols,
+                                                             n_hash, counts);
+    else
+        return set_error(MHB_ERR_INVALID, "unknown sig_dtype %d", sig_dtype);
+    return cuda_check(cudaGetLastError(), "jaccard_block launch");
+}
+
+extern "C" int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x, uint64_t a, uint64_t b,
+                                         uint64_t prime, int32_t n_hash, uint32_t buckets,
+                                         unsigned long long* counts, void* stream) {
+    if (prime >= (1ull << 31)) return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^31 not supported");
+    if (a < 1 || a >= prime || b >= prime || a + (uint64_t)n_hash >= prime)
+        return set_error(MHB_ERR_INVALID, "iterative parameters out of range");
+    HistArgs H{};
+    H.xs = xs; H.n_x = n_x; H.p = (uint32_t)prime; H.b = (uint32_t)b; H.a = a;
+    H.n_hash = n_hash; H.m = buckets; H.counts = counts; H.kind = 0;
+    return launch_hist(H, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int mhb_bucket_hist_random(const uint32_t* xs, int64_t n_x, const uint32_t* a, const uint32_t* b,
+                                      uint64_t prime, int32_t n_hash, uint32_t buckets,
+                                      unsigned long long* counts, void* stream) {
+    if (prime >= (1ull << 31)) return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^31 not supported");
+    HistArgs H{};
+    H.xs = xs; H.n_x = n_x; H.p = (uint32_t)prime; H.n_hash = n_hash; H.m = buckets;
+    H.ra = a; H.rb = b; H.counts = counts; H.kind = 1;
+    return launch_hist(H, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int mhb_probe_visit_rate(int64_t visits_per_thread, int32_t kind, double* visits_out,
+                                    float* ms_out, void* stream) {
+    clear_error();
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    constexpr int K = 64;
+    const int64_t rounds = visits_per_thread / (2 * K) > 0 ? visits_per_thread / (2 * K) : 1;
+    int occ = 0;
+    const void* fn = kind == 0 ? (const void*)probe_iter_kernel<K> : (const void*)probe_random_kernel<K>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
+    if (occ < 1) occ = 1;
+    const int blocks = occ * dev.sms;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    // warm-up
+    if (kind == 0) probe_iter_kernel<K><<<blocks, 256, 0, st>>>(rounds / 10 + 1, 16777259u, 1u);
+    else probe_random_kernel<K><<<blocks, 256, 0, st>>>(rounds / 10 + 1, 16777259u, 1u);
+    cudaEventRecord(e0, st);
+    if (kind == 0) probe_iter_kernel<K><<<blocks, 256, 0, st>>>(rounds, 16777259u, 2u);
+    else probe_random_kernel<K><<<blocks, 256, 0, st>>>(rounds, 16777259u, 2u);
+    cudaEventRecord(e1, st);
+    rc = cuda_check(cudaEventSynchronize(e1), "probe sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    if (visits_out) *visits_out = (double)blocks * 256.0 * (double)rounds * 2.0 * K;
+    if (ms_out) *ms_out = ms;
+    return MHB_OK;
+}

@@ -1,0 +1,211 @@
+// host.cu -- host-buffer entry point: chunked, copy/compute-overlapped signing.
+//
+// The reference's callers hand numpy arrays to the signing loop and get numpy
+// arrays back (minhash.py:91-110, bench.py:97-102).  mhb_sign_csr_host is the
+// native equivalent for a whole CSR batch living in host memory: the sets are
+// cut into nnz-balanced chunks; each chunk goes H2D -> sign kernels -> D2H on
+// one of kLanes streams, so the copy engines (both directions) and the SMs
+// work on different chunks at the same time.  Device buffers are cached per
+// device between calls (mhb_host_release frees them).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.h"
+#include "sign_internal.h"
+
+namespace mhb {
+
+namespace {
+
+constexpr int kLanes = 3;
+
+struct Lane {
+    cudaStream_t stream = nullptr;
+    int64_t* indptr = nullptr;
+    size_t indptr_cap = 0;
+    uint32_t* ids = nullptr;
+    size_t ids_cap = 0;
+    void* out = nullptr;
+    size_t out_cap = 0;
+    void* ws = nullptr;
+    size_t ws_cap = 0;
+    int32_t* status = nullptr;
+};
+
+struct DeviceCache {
+    bool init = false;
+    Lane lanes[kLanes];
+    uint32_t* ra = nullptr;
+    uint32_t* rb = nullptr;
+    size_t ra_cap = 0;
+    size_t rb_cap = 0;
+};
+
+std::mutex g_mu;
+DeviceCache g_cache[64];
+
+int grow(void** ptr, size_t* cap, size_t need) {
+    if (*cap >= need && *ptr) return MHB_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    size_t want = need + need / 4 + 256;
+    int rc = cuda_check(cudaMalloc(ptr, want), "cudaMalloc (host pipeline buffer)");
+    if (rc) return rc;
+    *cap = want;
+    return MHB_OK;
+}
+
+struct Chunk {
+    int64_t s0, s1;  // sets [s0, s1)
+};
+
+std::vector<Chunk> plan_chunks(const int64_t* indptr, int64_t n_sets, int32_t n_hash, size_t out_bytes) {
+    const int64_t nnz = indptr[n_sets] - indptr[0];
+    // nnz-balanced cuts, ~16 chunks for large inputs, bounded rows so the output
+    // chunk stays <= 256 MB.
+    int64_t target_nnz = std::max<int64_t>(nnz / 16, 1 << 22);
+    int64_t max_rows = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)n_hash * out_bytes)));
+    std::vector<Chunk> out;
+    int64_t s = 0;
+    while (s < n_sets) {
+        const int64_t goal = indptr[s] + target_nnz;
+        int64_t e = std::upper_bound(indptr + s + 1, indptr + n_sets + 1, goal) - indptr - 1;
+        if (e <= s) e = s + 1;
+        if (e - s > max_rows) e = s + max_rows;
+        if (e > n_sets) e = n_sets;
+        out.push_back({s, e});
+        s = e;
+    }
+    return out;
+}
+
+}  // namespace
+
+}  // namespace mhb
+
+using namespace mhb;
+
+extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets,
+                                 int64_t nnz, uint64_t a, uint64_t b, const uint32_t* a_host,
+                                 const uint32_t* b_host, uint64_t prime, int32_t n_hash, void* out,
+                                 int32_t out_dtype, int32_t* status_host, int32_t device) {
+    clear_error();
+    if (kind != KIND_ITERATIVE && kind != KIND_RANDOM) return set_error(MHB_ERR_INVALID, "unknown kind %d", kind);
+    if (n_sets < 0) return set_error(MHB_ERR_INVALID, "n_sets must be >= 0");
+    if (status_host) *status_host = 0;
+    if (n_sets == 0) return MHB_OK;
+    if (!indptr || !out || (nnz > 0 && !ids)) return set_error(MHB_ERR_INVALID, "null host pointer");
+    if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
+    if (indptr[n_sets] - indptr[0] > nnz) return set_error(MHB_ERR_INVALID, "indptr exceeds nnz");
+    if (out_dtype != MHB_OUT_U32 && out_dtype != MHB_OUT_I64)
+        return set_error(MHB_ERR_INVALID, "unknown out_dtype %d", out_dtype);
+    if (device < 0 || device >= 64) return set_error(MHB_ERR_INVALID, "bad device %d", device);
+    const size_t out_bytes = out_dtype == MHB_OUT_I64 ? 8 : 4;
+
+    std::lock_guard<std::mutex> lock(g_mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (rc) return rc;
+    DeviceCache& dc = g_cache[device];
+    if (!dc.init) {
+        for (auto& ln : dc.lanes) {
+            rc = cuda_check(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking), "stream create");
+            if (rc) return rc;
+            rc = cuda_check(cudaMalloc((void**)&ln.status, sizeof(int32_t)), "cudaMalloc status");
+            if (rc) return rc;
+        }
+        dc.init = true;
+    }
+    if (kind == KIND_RANDOM) {
+        if (!a_host || !b_host) return set_error(MHB_ERR_INVALID, "random family needs a and b");
+        if ((rc = grow((void**)&dc.ra, &dc.ra_cap, (size_t)n_hash * 4))) return rc;
+        if ((rc = grow((void**)&dc.rb, &dc.rb_cap, (size_t)n_hash * 4))) return rc;
+        cudaStream_t s0 = dc.lanes[0].stream;
+        if ((rc = cuda_check(cudaMemcpyAsync(dc.ra, a_host, (size_t)n_hash * 4, cudaMemcpyHostToDevice, s0), "H2D a")))
+            return rc;
+        if ((rc = cuda_check(cudaMemcpyAsync(dc.rb, b_host, (size_t)n_hash * 4, cudaMemcpyHostToDevice, s0), "H2D b")))
+            return rc;
+        if ((rc = cuda_check(cudaStreamSynchronize(s0), "sync params"))) return rc;
+    }
+
+    const std::vector<Chunk> chunks = plan_chunks(indptr, n_sets, n_hash, out_bytes);
+    int32_t status_acc = 0;
+
+    for (size_t c = 0; c < chunks.size(); ++c) {
+        Lane& ln = dc.lanes[c % kLanes];
+        const int64_t s0 = chunks[c].s0, s1 = chunks[c].s1, rows = s1 - s0;
+        const int64_t id0 = indptr[s0], id1 = indptr[s1];
+        const int64_t cnnz = id1 - id0;
+        if (c >= (size_t)kLanes) {
+            // The lane's previous chunk must be fully drained before its buffers are reused;
+            // collect its device status at the same time.
+            if ((rc = cuda_check(cudaStreamSynchronize(ln.stream), "lane sync"))) return rc;
+            int32_t st = 0;
+            cudaMemcpy(&st, ln.status, sizeof(int32_t), cudaMemcpyDeviceToHost);
+            status_acc |= st;
+        }
+        if ((rc = grow((void**)&ln.indptr, &ln.indptr_cap, (size_t)(rows + 1) * sizeof(int64_t)))) return rc;
+        if ((rc = grow((void**)&ln.ids, &ln.ids_cap, (size_t)std::max<int64_t>(cnnz, 1) * sizeof(uint32_t))))
+            return rc;
+        if ((rc = grow(&ln.out, &ln.out_cap, (size_t)rows * n_hash * out_bytes))) return rc;
+        const size_t wsb = mhb_sign_workspace_bytes(rows, cnnz, n_hash);
+        if ((rc = grow(&ln.ws, &ln.ws_cap, wsb))) return rc;
+
+        if ((rc = cuda_check(cudaMemcpyAsync(ln.indptr, indptr + s0, (size_t)(rows + 1) * sizeof(int64_t),
+                                             cudaMemcpyHostToDevice, ln.stream), "H2D indptr")))
+            return rc;
+        if (cnnz > 0 &&
+            (rc = cuda_check(cudaMemcpyAsync(ln.ids, ids + id0, (size_t)cnnz * sizeof(uint32_t),
+                                             cudaMemcpyHostToDevice, ln.stream), "H2D ids")))
+            return rc;
+        // The chunk's indptr keeps global offsets; shift the ids base so ids[indptr[s]] lands in the chunk buffer.
+        const uint32_t* ids_base = reinterpret_cast<const uint32_t*>(
+            reinterpret_cast<uintptr_t>(ln.ids) - (uintptr_t)id0 * sizeof(uint32_t));
+        rc = launch_sign(kind, ln.indptr, ids_base, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
+                         out_dtype, ln.status, ln.ws, ln.ws_cap, ln.stream);
+        if (rc) return rc;
+        if ((rc = cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)s0 * n_hash * out_bytes, ln.out,
+                                             (size_t)rows * n_hash * out_bytes, cudaMemcpyDeviceToHost, ln.stream),
+                             "D2H out")))
+            return rc;
+    }
+    for (int l = 0; l < kLanes && (size_t)l < chunks.size(); ++l) {
+        Lane& ln = dc.lanes[l];
+        if ((rc = cuda_check(cudaStreamSynchronize(ln.stream), "final sync"))) return rc;
+        int32_t st = 0;
+        cudaMemcpy(&st, ln.status, sizeof(int32_t), cudaMemcpyDeviceToHost);
+        status_acc |= st;
+    }
+    if (status_host) *status_host = status_acc;
+    cudaSetDevice(prev);
+    return MHB_OK;
+}
+
+extern "C" void mhb_host_release(void) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (int d = 0; d < 64; ++d) {
+        DeviceCache& dc = g_cache[d];
+        if (!dc.init) continue;
+        cudaSetDevice(d);
+        for (auto& ln : dc.lanes) {
+            cudaStreamSynchronize(ln.stream);
+            cudaFree(ln.indptr);
+            cudaFree(ln.ids);
+            cudaFree(ln.out);
+            cudaFree(ln.ws);
+            cudaFree(ln.status);
+            cudaStreamDestroy(ln.stream);
+            ln = Lane{};
+        }
+        cudaFree(dc.ra);
+        cudaFree(dc.rb);
+        dc = DeviceCache{};
+    }
+}

@@ -1,0 +1,80 @@
+// sign_internal.h -- structures shared by the signature kernels and the host pipeline.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace mhb {
+
+enum { KIND_ITERATIVE = 0, KIND_RANDOM = 1 };
+
+constexpr int kChunk = 1024;  // features per work item; longer sets are split
+constexpr int kBlock = 256;   // threads per CTA of the main kernel
+
+// Per hash lane i: h_i(x) = (A*x + B) mod p, Ap = floor(A*2^32/p) (Shoup companion).
+struct LaneTab {
+    uint32_t A, Ap, B, pad;
+};
+// Per hash lane i: inv = A^{-1} mod p and its Shoup companion (argmin recovery).
+struct InvTab {
+    uint32_t inv, invp;
+};
+// One extra chunk (index >= 1) of a set longer than kChunk.
+struct Extra {
+    int64_t set;
+    int32_t sb;
+    int32_t chunk;
+};
+struct Sched {
+    unsigned long long next;     // dynamic work-item counter
+    unsigned long long n_extra;  // extra chunks planned
+    unsigned long long n_big;    // (set, lane pass) pairs in merge mode
+    unsigned long long pad;
+};
+
+struct Geometry {
+    int K;         // hash lanes per thread
+    int G;         // lane groups per warp
+    int F;         // feature slices per warp (G*F = 32)
+    int log2F;
+    int n_super;   // lane passes per set (n_hash > 32*K)
+    int L;         // lanes per pass = G*K
+    int64_t n_tot; // padded lane count = n_super*L
+};
+
+struct WorkspaceLayout {
+    size_t sched, tab, inv, big, extra, total;
+};
+
+struct SignArgs {
+    const int64_t* indptr;
+    const uint32_t* ids;
+    int64_t n_sets;
+    uint32_t p;
+    uint32_t b;
+    uint64_t ia;
+    int32_t n_hash;
+    int32_t F, log2F, n_super, L;
+    int64_t n_tot;
+    int32_t kind;
+    LaneTab* tab;
+    InvTab* inv;
+    Sched* sched;
+    int64_t* big;
+    Extra* extra;
+    int32_t* status;
+    void* out;
+    const uint32_t* ra;
+    const uint32_t* rb;
+};
+
+Geometry choose_geometry(int kind, int32_t n_hash);
+WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash);
+
+int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
+                uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
+                int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,
+                size_t workspace_bytes, cudaStream_t st);
+
+}  // namespace mhb

@@ -1,0 +1,168 @@
+"""Seeded synthetic CSR workloads for the BASELINE configurations.
+
+The reference measures on synthetic sets only (corpus.py:114-130);
+BASELINE.json names five shapes.  These generators reproduce those shapes:
+
+  cfg1  10,000 sets, max(1, Poisson(50)) distinct ids uniform in [0, 2^20), N=128
+  cfg2  1,000,000 sets, round(lognormal(ln 120, 1.0)) clipped [1, 20000],
+        Zipf(s=1.1) ids over 2^24, duplicates redrawn until the target size, N=256
+  cfg3  200,000 Poisson(300) base sets over 2^22 + one mutated copy each at a target
+        Jaccard J ~ U[0.1, 0.95], N=512 (planted near-duplicates; see planted_pairs)
+  cfg4  2,000,000 sets, max(1, Poisson(80)) uniform over 2^26, N=2048
+  cfg5  100,000,000 sets, lognormal(ln 60, 1.2) clipped [1, 50000], Zipf(1.05) over 2^30
+
+Definitions the reference leaves open (documented in DESIGN.md):
+  * Zipf is truncated to the vocabulary [1, V] (P(rank k) ~ k^-s) and rank k maps to
+    id = ((k-1) * 2654435761) mod V -- an odd-multiplier bijection on [0, V) for V a
+    power of two, so popular terms are scattered over the id space.
+  * Sets are canonical like FeatureSet (sorted, no repeats): a repeated draw is
+    redrawn until the set reaches its target size.
+
+Two implementations: ``cfg1_numpy`` (numpy PCG64; byte-identical wherever numpy 2.3
+runs -- the golden fixtures use it) and ``make_csr`` (torch; runs on the GPU for
+the full-size configurations).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .families import derive_seed
+from .modmath import choose_prime
+
+MASTER_SEED = 20260810  # the reference's acceptance master seed (tests/test_acceptance.py:20)
+ZIPF_SCRAMBLE = 2654435761
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n_sets: int
+    n_hash: int
+    vocab_log2: int
+    size_kind: str          # "poisson" | "lognormal"
+    size_a: float           # poisson mean | lognormal median
+    size_b: float           # unused | lognormal sigma
+    size_cap: int           # upper clip (lognormal)
+    id_kind: str            # "uniform" | "zipf"
+    zipf_s: float
+    families: tuple
+
+    @property
+    def vocab(self) -> int:
+        return 1 << self.vocab_log2
+
+    @property
+    def prime(self) -> int:
+        # choose_prime(max_id = V-1, N) (reference bench.py:66-70), fixed per config
+        return choose_prime(self.vocab - 1, self.n_hash)
+
+    def family_seed(self, kind: str) -> int:
+        return derive_seed(MASTER_SEED, int(self.name[-1]), 0 if kind == "random" else 1)
+
+    def data_seed(self) -> int:
+        return derive_seed(MASTER_SEED, int(self.name[-1]), 100)
+
+
+CONFIGS = {
+    "cfg1": Config("cfg1", 10_000, 128, 20, "poisson", 50.0, 0.0, 1 << 62, "uniform", 0.0,
+                   ("random", "iterative")),
+    "cfg2": Config("cfg2", 1_000_000, 256, 24, "lognormal", 120.0, 1.0, 20_000, "zipf", 1.1, ("iterative",)),
+    "cfg3": Config("cfg3", 200_000, 512, 22, "poisson", 300.0, 0.0, 1 << 62, "uniform", 0.0,
+                   ("random", "iterative")),
+    "cfg4": Config("cfg4", 2_000_000, 2048, 26, "poisson", 80.0, 0.0, 1 << 62, "uniform", 0.0, ("iterative",)),
+    "cfg5": Config("cfg5", 100_000_000, 256, 30, "lognormal", 60.0, 1.2, 50_000, "zipf", 1.05, ("iterative",)),
+}
+
+
+# ---------------------------------------------------------------------------
+# numpy: cfg1-shaped sets, reproducible bit for bit across machines
+# ---------------------------------------------------------------------------
+
+def cfg1_numpy(n_sets: int = 10_000, seed: int | None = None, mean: float = 50.0,
+               vocab: int = 1 << 20) -> tuple[np.ndarray, np.ndarray]:
+    """max(1, Poisson(mean)) distinct uniform ids per set, sorted; returns (indptr, ids uint32)."""
+    rng = np.random.default_rng(CONFIGS["cfg1"].data_seed() if seed is None else seed)
+    sizes = np.maximum(1, rng.poisson(mean, size=n_sets)).astype(np.int64)
+    rows = [np.sort(rng.choice(vocab, size=int(k), replace=False)) for k in sizes]
+    indptr = np.zeros(n_sets + 1, dtype=np.int64)
+    np.cumsum(sizes, out=indptr[1:])
+    ids = np.concatenate(rows).astype(np.uint32) if rows else np.zeros(0, np.uint32)
+    return indptr, ids
+
+
+# ---------------------------------------------------------------------------
+# torch: full-size workloads (GPU) with the same distributions
+# ---------------------------------------------------------------------------
+
+class _ZipfSampler:
+    """Inverse-CDF sampler for Zipf(s) truncated to ranks 1..V (exact table)."""
+
+    def __init__(self, s: float, vocab: int, device):
+        import torch
+
+        if vocab > (1 << 26):
+            raise NotImplementedError("exact Zipf table limited to V <= 2^26 in this round")
+        k = torch.arange(1, vocab + 1, dtype=torch.float64, device=device)
+        cdf = torch.cumsum(k.pow(-s), 0)
+        self.cdf = cdf / cdf[-1]
+        self.vocab = vocab
+
+    def sample(self, n: int, gen):
+        import torch
+
+        u = torch.rand(n, dtype=torch.float64, device=self.cdf.device, generator=gen)
+        rank0 = torch.searchsorted(self.cdf, u).clamp_(max=self.vocab - 1)
+        return (rank0 * ZIPF_SCRAMBLE) & (self.vocab - 1)
+
+
+def _draw_sizes(cfg: Config, n: int, gen, device):
+    import torch
+
+    if cfg.size_kind == "poisson":
+        rates = torch.full((n,), cfg.size_a, dtype=torch.float64, device=device)
+        sizes = torch.poisson(rates, generator=gen).to(torch.int64)
+        return sizes.clamp_(min=1, max=min(cfg.size_cap, cfg.vocab))
+    z = torch.randn(n, dtype=torch.float64, device=device, generator=gen)
+    sizes = torch.round(torch.exp(math.log(cfg.size_a) + cfg.size_b * z)).to(torch.int64)
+    return sizes.clamp_(min=1, max=min(cfg.size_cap, cfg.vocab))
+
+
+def make_csr(cfg: Config | str, device="cuda", n_sets: int | None = None, seed: int | None = None,
+             max_rounds: int = 400):
+    """(indptr int64[S+1], ids uint32[nnz]) on `device`; ids sorted within each set, distinct."""
+    import torch
+
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    n = cfg.n_sets if n_sets is None else int(n_sets)
+    device = torch.device(device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed((cfg.data_seed() if seed is None else int(seed)) & ((1 << 63) - 1))
+    sizes = _draw_sizes(cfg, n, gen, device)
+    zipf = _ZipfSampler(cfg.zipf_s, cfg.vocab, device) if cfg.id_kind == "zipf" else None
+
+    def draw(count: int):
+        if zipf is not None:
+            return zipf.sample(count, gen)
+        return torch.randint(0, cfg.vocab, (count,), dtype=torch.int64, device=device, generator=gen)
+
+    set_idx = torch.arange(n, dtype=torch.int64, device=device)
+    keys = (torch.repeat_interleave(set_idx, sizes) << 32) | draw(int(sizes.sum()))
+    for _ in range(max_rounds):
+        keys = torch.unique(keys, sorted=True)
+        have = torch.bincount(keys >> 32, minlength=n)
+        deficit = sizes - have
+        missing = int(deficit.sum())
+        if missing == 0:
+            break
+        extra = (torch.repeat_interleave(set_idx, deficit) << 32) | draw(missing)
+        keys = torch.cat([keys, extra])
+    else:
+        raise RuntimeError("duplicate redraw did not converge")
+    indptr = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(sizes, 0, out=indptr[1:])
+    ids = (keys & 0xFFFFFFFF).to(torch.uint32)
+    return indptr, ids

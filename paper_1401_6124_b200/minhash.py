@@ -1,0 +1,366 @@
+"""MinHash signatures and Jaccard estimation on B200 -- the drop-in API.
+
+Mirrors ``minhashlab.minhash`` (reference minhash.py:1-206): ``FeatureSet``,
+``Signature``, ``signature``, ``estimate_jaccard``, ``exact_jaccard`` and the
+signature-file readers/writers keep the reference's names, argument meaning and
+exceptions.  The per-set loop the reference runs on the CPU (kernels.py:21-73)
+is replaced by the batched CSR kernels of libmhb (``signatures_csr``); the
+per-set ``signature`` call is a batch of one.
+
+There is no CPU path for signing: if libmhb.so or a CUDA device is missing,
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .families import Family, IterativeFamily, RandomFamily
+from .modmath import MAX_KERNEL_PRIME
+
+
+class FeatureSet:
+    """Sorted, de-duplicated non-negative feature ids (reference minhash.py:21-62)."""
+
+    __slots__ = ("ids",)
+
+    def __init__(self, ids):
+        if isinstance(ids, np.ndarray):
+            arr = ids.astype(np.int64, copy=False)
+        else:
+            arr = np.array(list(ids), dtype=np.int64)
+        arr = np.unique(arr)
+        if arr.size and arr[0] < 0:
+            raise ValueError("feature ids must be non-negative")
+        arr.setflags(write=False)
+        self.ids = arr
+
+    def __len__(self) -> int:
+        return int(self.ids.size)
+
+    def __iter__(self):
+        return iter(self.ids.tolist())
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, FeatureSet):
+            return NotImplemented
+        return self.ids.shape == other.ids.shape and bool((self.ids == other.ids).all())
+
+    def __hash__(self):
+        return hash(self.ids.tobytes())
+
+    def __repr__(self) -> str:
+        return f"FeatureSet(size={len(self)})"
+
+    @property
+    def max_id(self) -> int:
+        if self.ids.size == 0:
+            raise ValueError("empty feature set has no max id")
+        return int(self.ids[-1])
+
+
+@dataclass(frozen=True, eq=False)
+class Signature:
+    """Per-hash argmin feature ids (int64, read-only) plus the family identity."""
+
+    mins: np.ndarray
+    family_key: tuple = field(default=())
+
+    def __post_init__(self):
+        arr = np.ascontiguousarray(self.mins, dtype=np.int64)
+        arr.setflags(write=False)
+        object.__setattr__(self, "mins", arr)
+
+    def __len__(self) -> int:
+        return int(self.mins.size)
+
+
+def exact_jaccard(s1: FeatureSet, s2: FeatureSet) -> float:
+    """|s1 & s2| / |s1 | s2|, 1.0 for two empty sets (reference minhash.py:81-88)."""
+    x, y = s1.ids, s2.ids
+    if x.size == 0 and y.size == 0:
+        return 1.0
+    inter = int(np.intersect1d(x, y, assume_unique=True).size)
+    return inter / (int(x.size) + int(y.size) - inter)
+
+
+# ---------------------------------------------------------------------------
+# Batched CSR signing (the hot path)
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _check_family(family: Family) -> None:
+    if not isinstance(family, (IterativeFamily, RandomFamily)):
+        raise TypeError(f"unsupported family type {type(family).__name__}")
+    if family.prime > MAX_KERNEL_PRIME:
+        raise NotImplementedError(
+            f"prime {family.prime} >= 2^31: the u32 CUDA kernels cover every prime < 2^31 "
+            f"(all BASELINE configurations); wider moduli are not implemented")
+
+
+def _raise_status(status: int, family: Family) -> None:
+    if status & _lib.STATUS_EMPTY_SET:
+        raise ValueError("cannot build a signature for an empty feature set")
+    if status & _lib.STATUS_ID_GE_PRIME:
+        raise ValueError(f"feature id >= family prime {family.prime}")
+    if status & _lib.STATUS_BAD_PARAM:
+        raise ValueError("family parameters outside [1,p) x [0,p)")
+
+
+def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) -> None:
+    """Raw asynchronous device call: indptr int64[S+1], ids uint32, out uint32/int64[S,N]
+    CUDA tensors on one device.  No validation beyond the library's, no sync."""
+    torch = _torch()
+    lib = _lib.load()
+    dev = ids.device
+    n_sets = indptr.numel() - 1
+    nnz = ids.numel()
+    n_hash = family.size
+    out_dtype = _lib.OUT_I64 if out.dtype == torch.int64 else _lib.OUT_U32
+    ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, nnz, n_hash)
+    with torch.cuda.device(dev):
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        sptr = st.cuda_stream
+        status_ptr = status.data_ptr() if status is not None else None
+        if isinstance(family, IterativeFamily):
+            rc = lib.mhb_sign_iterative_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
+                                            family.base.a, family.base.b, family.prime, n_hash,
+                                            out.data_ptr(), out_dtype, status_ptr,
+                                            ws.data_ptr(), ws_bytes, sptr)
+        else:
+            a, b = family.device_params(dev)
+            rc = lib.mhb_sign_random_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
+                                         a.data_ptr(), b.data_ptr(), family.prime, n_hash,
+                                         out.data_ptr(), out_dtype, status_ptr,
+                                         ws.data_ptr(), ws_bytes, sptr)
+    _lib.check(rc)
+
+
+def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
+                   validate: bool = True, device=None):
+    """Signatures of every set of a CSR batch.
+
+    indptr: int64[S+1]; ids: feature ids (< family.prime), any order, repeats allowed.
+    Device tensors in -> device tensor out (stream-ordered on the current stream;
+    ``validate`` synchronises once to turn device status flags into the reference's
+    ValueErrors).  numpy arrays in -> numpy array out through the host pipeline
+    (mhb_sign_csr_host: chunked H2D / kernels / D2H overlap).
+    Result: [S, family.size] argmin feature ids, int64 (reference dtype) or uint32.
+    """
+    _check_family(family)
+    torch = _torch()
+    if out_dtype not in ("int64", "uint32"):
+        raise ValueError(f"out_dtype must be 'int64' or 'uint32', got {out_dtype!r}")
+    if isinstance(ids, np.ndarray) or isinstance(indptr, np.ndarray):
+        return _signatures_csr_host(np.asarray(indptr), np.asarray(ids), family, out_dtype, out, device)
+
+    if not (ids.is_cuda and indptr.is_cuda):
+        raise ValueError("signatures_csr needs CUDA tensors (or numpy arrays for the host pipeline)")
+    if ids.dtype != torch.uint32:
+        if ids.dtype in (torch.int64, torch.int32) and validate:
+            if ids.numel() and int(ids.min()) < 0:
+                raise ValueError("feature ids must be non-negative")
+            if ids.numel() and int(ids.max()) >= family.prime:
+                raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+        ids = ids.to(torch.uint32)
+    ids = ids.contiguous()
+    indptr = indptr.to(torch.int64).contiguous()
+    n_sets = indptr.numel() - 1
+    tdt = torch.int64 if out_dtype == "int64" else torch.uint32
+    if out is None:
+        out = torch.empty((n_sets, family.size), dtype=tdt, device=ids.device)
+    elif out.dtype != tdt or tuple(out.shape) != (n_sets, family.size) or not out.is_contiguous():
+        raise ValueError("out has the wrong dtype, shape or layout")
+    status = torch.zeros(1, dtype=torch.int32, device=ids.device) if validate else None
+    sign_csr_device(indptr, ids, family, out, status)
+    if validate:
+        _raise_status(int(status.item()), family)
+    return out
+
+
+def _signatures_csr_host(indptr, ids, family, out_dtype, out, device):
+    torch = _torch()
+    lib = _lib.load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    if ids.dtype != np.uint32:
+        if ids.size and (ids.min() < 0 or ids.max() >= family.prime):
+            if ids.min() < 0:
+                raise ValueError("feature ids must be non-negative")
+            raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+        ids = ids.astype(np.uint32)
+    ids = np.ascontiguousarray(ids)
+    n_sets = indptr.size - 1
+    ndt = np.int64 if out_dtype == "int64" else np.uint32
+    if out is None:
+        out = np.empty((n_sets, family.size), dtype=ndt)
+    elif out.dtype != ndt or out.shape != (n_sets, family.size) or not out.flags.c_contiguous:
+        raise ValueError("out has the wrong dtype, shape or layout")
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    status = C.c_int32(0)
+    if isinstance(family, IterativeFamily):
+        rc = lib.mhb_sign_csr_host(_lib.KIND_ITERATIVE, indptr.ctypes.data, ids.ctypes.data, n_sets, ids.size,
+                                   family.base.a, family.base.b, None, None, family.prime, family.size,
+                                   out.ctypes.data, _lib.OUT_I64 if ndt == np.int64 else _lib.OUT_U32,
+                                   C.addressof(status), dev)
+    else:
+        a = np.ascontiguousarray(family.a, dtype=np.uint32)
+        b = np.ascontiguousarray(family.b, dtype=np.uint32)
+        rc = lib.mhb_sign_csr_host(_lib.KIND_RANDOM, indptr.ctypes.data, ids.ctypes.data, n_sets, ids.size,
+                                   0, 0, a.ctypes.data, b.ctypes.data, family.prime, family.size,
+                                   out.ctypes.data, _lib.OUT_I64 if ndt == np.int64 else _lib.OUT_U32,
+                                   C.addressof(status), dev)
+    _lib.check(rc)
+    _raise_status(status.value, family)
+    return out
+
+
+def signature(s: FeatureSet, family: Family) -> Signature:
+    """MinHash signature of one non-empty set (reference minhash.py:91-110): mins[i] is
+    the feature id minimising h_i over s.  Runs the CUDA kernel on the current device."""
+    if len(s) == 0:
+        raise ValueError("cannot build a signature for an empty feature set")
+    if s.max_id >= family.prime:
+        raise ValueError(f"feature id {s.max_id} >= family prime {family.prime}")
+    torch = _torch()
+    _check_family(family)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ids = torch.from_numpy(s.ids.astype(np.uint32)).to(dev, non_blocking=False)
+    indptr = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
+    out = signatures_csr(indptr, ids, family, out_dtype="int64", validate=False)
+    return Signature(out[0].cpu().numpy(), family.key)
+
+
+def signatures(sets, family: Family) -> list[Signature]:
+    """Batch form of ``signature`` for a list of FeatureSets: one CSR launch."""
+    sets = list(sets)
+    if any(len(s) == 0 for s in sets):
+        raise ValueError("cannot build a signature for an empty feature set")
+    if not sets:
+        return []
+    sizes = np.array([len(s) for s in sets], dtype=np.int64)
+    indptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ids = np.concatenate([s.ids for s in sets])
+    if ids.max() >= family.prime:
+        raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+    mat = signatures_csr(indptr, ids.astype(np.uint32), family, out_dtype="int64")
+    return [Signature(row, family.key) for row in mat]
+
+
+def estimate_jaccard(g1: Signature, g2: Signature) -> float:
+    """Fraction of positions holding the same feature id (reference minhash.py:130-137)."""
+    if g1.family_key != g2.family_key:
+        raise ValueError(
+            f"signatures come from different families: {g1.family_key} vs {g2.family_key}")
+    if len(g1) != len(g2):
+        raise ValueError("signature lengths differ")
+    return float(np.mean(g1.mins == g2.mins))
+
+
+def estimate_pairs(sig, pi, pj):
+    """Jaccard estimates for listed pairs of rows of a device signature matrix.
+
+    sig: CUDA [S, N] int64/uint32; pi, pj: int64 row indices.  Returns (counts uint32,
+    estimates float64) where estimate = counts / N exactly as np.mean of the 0/1 vector
+    (bench.py:165-168)."""
+    torch = _torch()
+    lib = _lib.load()
+    pi = torch.as_tensor(pi, dtype=torch.int64, device=sig.device).contiguous()
+    pj = torch.as_tensor(pj, dtype=torch.int64, device=sig.device).contiguous()
+    n_pairs = pi.numel()
+    if pj.numel() != n_pairs:
+        raise ValueError("pair index arrays differ in length")
+    counts = torch.empty(n_pairs, dtype=torch.uint32, device=sig.device)
+    est = torch.empty(n_pairs, dtype=torch.float64, device=sig.device)
+    dt = _lib.OUT_I64 if sig.dtype == torch.int64 else _lib.OUT_U32
+    with torch.cuda.device(sig.device):
+        rc = lib.mhb_jaccard_pairs(sig.data_ptr(), dt, sig.shape[1], pi.data_ptr(), pj.data_ptr(), n_pairs,
+                                   counts.data_ptr(), est.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc)
+    return counts, est
+
+
+def jaccard_block(sig_a, sig_b):
+    """counts[r, c] = #{i : sig_a[r, i] == sig_b[c, i]} for two device signature blocks."""
+    torch = _torch()
+    lib = _lib.load()
+    if sig_a.dtype != sig_b.dtype or sig_a.shape[1] != sig_b.shape[1]:
+        raise ValueError("signature blocks differ in dtype or length")
+    counts = torch.empty((sig_a.shape[0], sig_b.shape[0]), dtype=torch.uint32, device=sig_a.device)
+    dt = _lib.OUT_I64 if sig_a.dtype == torch.int64 else _lib.OUT_U32
+    with torch.cuda.device(sig_a.device):
+        rc = lib.mhb_jaccard_block(sig_a.contiguous().data_ptr(), sig_a.shape[0], sig_b.contiguous().data_ptr(),
+                                   sig_b.shape[0], dt, sig_a.shape[1], counts.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc)
+    return counts
+
+
+# ---------------------------------------------------------------------------
+# Signature files (reference minhash.py:140-206): "id N ids..." text lines and
+# little-endian u64 binary records.
+# ---------------------------------------------------------------------------
+
+def _record_mins(sig) -> np.ndarray:
+    mins = sig.mins if isinstance(sig, Signature) else np.asarray(sig, dtype=np.int64)
+    if mins.ndim != 1:
+        raise ValueError("signature record must be a 1-d id vector")
+    return mins
+
+
+def write_signatures_text(path, records) -> None:
+    with open(path, "w", encoding="utf-8") as fh:
+        for obj_id, sig in records:
+            mins = _record_mins(sig)
+            fh.write(f"{int(obj_id)} {mins.size} " + " ".join(map(str, mins.tolist())) + "\n")
+
+
+def read_signatures_text(path) -> list[tuple[int, np.ndarray]]:
+    records = []
+    with open(path, encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            fields = line.split()
+            if not fields:
+                continue
+            if len(fields) < 2:
+                raise ValueError(f"{path}:{lineno}: truncated signature record")
+            obj_id, n = int(fields[0]), int(fields[1])
+            ids = np.array([int(v) for v in fields[2:]], dtype=np.int64)
+            if ids.size != n:
+                raise ValueError(f"{path}:{lineno}: record declares {n} ids but carries {ids.size}")
+            records.append((obj_id, ids))
+    return records
+
+
+def write_signatures_binary(path, records) -> None:
+    with open(path, "wb") as fh:
+        for obj_id, sig in records:
+            mins = _record_mins(sig)
+            fh.write(struct.pack("<QQ", int(obj_id), mins.size))
+            fh.write(mins.astype("<u8").tobytes())
+
+
+def read_signatures_binary(path) -> list[tuple[int, np.ndarray]]:
+    records = []
+    with open(path, "rb") as fh:
+        while True:
+            head = fh.read(16)
+            if not head:
+                break
+            if len(head) < 16:
+                raise ValueError(f"{path}: truncated record header")
+            obj_id, n = struct.unpack("<QQ", head)
+            body = fh.read(8 * n)
+            if len(body) < 8 * n:
+                raise ValueError(f"{path}: truncated record body")
+            records.append((int(obj_id), np.frombuffer(body, dtype="<u8").astype(np.int64)))
+    return records

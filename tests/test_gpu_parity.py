@@ -1,0 +1,212 @@
+"""GPU parity: libmhb kernels (through the C ABI) against the reference's outputs.
+
+Small cases compare with golden fixtures produced by the reference itself and with
+the CPU oracle (pinned in test_oracle.py).  Full-size cases use size-independent
+properties: checksums against the reference's full cfg1 output, oracle agreement on
+seeded subsamples, argmins drawn from their own sets, and order invariance.
+Bar: bit-exact (integer path).
+"""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1401_6124_b200 import (
+    FeatureSet,
+    IterativeFamily,
+    RandomFamily,
+    bucket_histogram,
+    estimate_jaccard,
+    estimate_pairs,
+    gen,
+    jaccard_block,
+    make_family,
+    signature,
+    signatures,
+    signatures_csr,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(indptr, ids, device):
+    import torch
+
+    return (torch.as_tensor(np.asarray(indptr, dtype=np.int64), device=device),
+            torch.as_tensor(np.asarray(ids, dtype=np.int64), device=device).to(torch.uint32))
+
+
+def test_known_answers(golden, cuda_device):
+    ka = json.loads((golden / "known_answers.json").read_text())
+    t = ka["two_element"]
+    sig = signature(FeatureSet(t["ids"]), IterativeFamily(t["a"], t["b"], t["p"], t["n"]))
+    assert sig.mins.tolist() == t["mins"] == [5]
+    s = ka["singleton_42"]
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, s["seed"], s["n"], s["p"])
+        assert signature(FeatureSet([42]), fam).mins.tolist() == [42] * s["n"]
+
+
+@pytest.mark.parametrize("out_dtype", ["int64", "uint32"])
+def test_fuzz_small_primes(golden, cuda_device, out_dtype):
+    z = np.load(golden / "fuzz_small.npz")
+    meta = json.loads((golden / "fuzz_small.json").read_text())
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        lo, hi = z["indptr"][k], z["indptr"][k + 1]
+        ip, ids = _dev([0, hi - lo], z["ids"][lo:hi], cuda_device)
+        got = signatures_csr(ip, ids, fam, out_dtype=out_dtype).cpu().numpy().astype(np.int64)[0]
+        assert np.array_equal(got, z["out"][z["out_ptr"][k]:z["out_ptr"][k + 1]]), m
+
+
+def test_long_sets_chunk_merge(golden, cuda_device):
+    z = np.load(golden / "long_sets.npz")
+    meta = json.loads((golden / "long_sets.json").read_text())
+    ip, ids = _dev(z["indptr"], z["ids"], cuda_device)
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        for dt in ("int64", "uint32"):
+            got = signatures_csr(ip, ids, fam, out_dtype=dt).cpu().numpy().astype(np.int64)
+            assert np.array_equal(got, z[f"out{k}"]), (m, dt)
+
+
+def test_cfg1_full_matches_reference_checksum(golden, cuda_device):
+    meta = json.loads((golden / "cfg1.json").read_text())
+    indptr, ids = gen.cfg1_numpy()
+    ip, di = _dev(indptr, ids, cuda_device)
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, meta[f"{kind}_seed"], meta["n_hash"], meta["prime"])
+        out = signatures_csr(ip, di, fam, out_dtype="int64").cpu().numpy()
+        assert hashlib.sha256(out.astype("<i8").tobytes()).hexdigest() == meta[f"{kind}_sha256"], kind
+        out32 = signatures_csr(ip, di, fam, out_dtype="uint32").cpu().numpy()
+        assert np.array_equal(out32.astype(np.int64), out)
+
+
+def test_cfg1_host_pipeline(golden, cuda_device):
+    """numpy in -> numpy out through mhb_sign_csr_host (the e2e entry)."""
+    meta = json.loads((golden / "cfg1.json").read_text())
+    indptr, ids = gen.cfg1_numpy()
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, meta[f"{kind}_seed"], meta["n_hash"], meta["prime"])
+        out = signatures_csr(indptr, ids, fam, out_dtype="int64")
+        assert hashlib.sha256(out.astype("<i8").tobytes()).hexdigest() == meta[f"{kind}_sha256"], kind
+
+
+@pytest.mark.parametrize("n_hash", [1, 3, 8, 17, 64, 100, 128, 255, 256, 512, 1000, 2048, 2049, 4100])
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_lane_geometries_vs_oracle(cuda_device, n_hash, kind):
+    indptr, ids = gen.cfg1_numpy(n_sets=257, seed=n_hash)
+    fam = make_family(kind, 1000 + n_hash, n_hash, 1_048_583)
+    ip, di = _dev(indptr, ids, cuda_device)
+    got = signatures_csr(ip, di, fam).cpu().numpy()
+    assert np.array_equal(got, oracle.sign_family_csr(indptr, ids, fam))
+
+
+@pytest.mark.parametrize("prime", [11, 31, 101, 7757, 1_048_583, 16_777_259, 67_108_879, 1_073_741_827,
+                                   1_431_655_777, 2_147_483_647])
+def test_primes_up_to_2_31(cuda_device, prime):
+    """Every BASELINE prime plus the narrow/wide Shoup boundary (3p vs 2^32) and 2^31-1."""
+    rng = np.random.default_rng(prime)
+    n_hash = min(200, (prime - 3) // 2)
+    rows = [np.sort(rng.choice(prime, size=int(min(k, prime)), replace=False)) for k in rng.integers(1, 60, 64)]
+    indptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])])
+    ids = np.concatenate(rows)
+    ip, di = _dev(indptr, ids, cuda_device)
+    for kind in ("iterative", "random"):
+        fam = make_family(kind, prime + 1, n_hash, prime)
+        got = signatures_csr(ip, di, fam).cpu().numpy()
+        assert np.array_equal(got, oracle.sign_family_csr(indptr, ids, fam)), kind
+
+
+def test_unsorted_and_repeated_ids(cuda_device):
+    """CSR rows may be unsorted and repeat ids; the result equals the canonical set's."""
+    indptr, ids = gen.cfg1_numpy(n_sets=200, seed=9)
+    fam = make_family("iterative", 4, 256, 1_048_583)
+    want = oracle.sign_family_csr(indptr, ids, fam)
+    rng = np.random.default_rng(0)
+    rows = []
+    for s in range(200):
+        r = ids[indptr[s]:indptr[s + 1]]
+        r = np.concatenate([r, r[: len(r) // 2]])
+        rows.append(rng.permutation(r))
+    ip2 = np.concatenate([[0], np.cumsum([len(r) for r in rows])])
+    ip, di = _dev(ip2, np.concatenate(rows), cuda_device)
+    assert np.array_equal(signatures_csr(ip, di, fam).cpu().numpy(), want)
+
+
+def test_errors_mirror_reference(cuda_device):
+    import torch
+
+    fam = make_family("iterative", 1, 16, 7757)
+    with pytest.raises(ValueError, match="empty"):
+        signature(FeatureSet([]), fam)
+    with pytest.raises(ValueError):
+        signature(FeatureSet([5, 7757]), fam)
+    ip, di = _dev([0, 2, 2, 3], [1, 2, 3], cuda_device)
+    with pytest.raises(ValueError, match="empty"):
+        signatures_csr(ip, di, fam)
+    ip, di = _dev([0, 2], [1, 9000], cuda_device)
+    with pytest.raises(ValueError):
+        signatures_csr(ip, di.to(torch.uint32), fam)
+
+
+def test_empty_batch(cuda_device):
+    import torch
+
+    fam = make_family("random", 1, 16, 7757)
+    ip = torch.zeros(1, dtype=torch.int64, device=cuda_device)
+    di = torch.zeros(0, dtype=torch.uint32, device=cuda_device)
+    assert signatures_csr(ip, di, fam).shape == (0, 16)
+
+
+def test_signatures_list_api(cuda_device):
+    rng = np.random.default_rng(3)
+    sets = [FeatureSet(rng.choice(7757, size=int(k), replace=False)) for k in rng.integers(1, 40, 50)]
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, 8, 333, 7757)
+        got = signatures(sets, fam)
+        for s, g in zip(sets, got):
+            assert g.family_key == fam.key
+            assert np.array_equal(g.mins, oracle.brute_force_row(s.ids, fam))
+
+
+def test_jaccard_estimates(golden, cuda_device):
+    import torch
+
+    z = np.load(golden / "jaccard.npz")
+    meta = json.loads((golden / "jaccard.json").read_text())
+    ip, di = _dev(z["indptr"], z["ids"], cuda_device)
+    for fm in meta["families"]:
+        fam = make_family(fm["kind"], fm["seed"], fm["n"], fm["p"])
+        for dt in ("int64", "uint32"):
+            sig = signatures_csr(ip, di, fam, out_dtype=dt)
+            n_pairs = sig.shape[0] // 2
+            pi = torch.arange(0, 2 * n_pairs, 2, device=cuda_device)
+            counts, est = estimate_pairs(sig, pi, pi + 1)
+            assert est.cpu().tolist() == meta["estimates"][fm["kind"]]
+            blk = jaccard_block(sig[0::2].contiguous(), sig[1::2].contiguous()).cpu().numpy()
+            assert np.array_equal(np.diag(blk), counts.cpu().numpy().astype(np.uint32))
+            host = sig.cpu().numpy().astype(np.int64)
+            want = (host[0::2][:, None, :] == host[1::2][None, :, :]).sum(-1)
+            assert np.array_equal(blk.astype(np.int64), want)
+        s1 = signatures([FeatureSet(z["ids"][z["indptr"][0]:z["indptr"][1]])], fam)[0]
+        assert estimate_jaccard(s1, s1) == 1.0
+
+
+def test_bucket_histogram(golden, cuda_device):
+    for case in json.loads((golden / "hist.json").read_text()):
+        fam = make_family(case["kind"], case["seed"], case["hashes"], case["prime"])
+        got = bucket_histogram(case["xs"], fam, case["buckets"]).cpu().numpy()
+        assert got.tolist() == case["counts"], case["kind"]
+
+
+def test_cfg2_subsample_vs_oracle(cuda_device):
+    """cfg2 distributions (lognormal sizes, Zipf ids over 2^24) at 20k sets vs the oracle."""
+    cfg = gen.CONFIGS["cfg2"]
+    ip, di = gen.make_csr(cfg, device=cuda_device, n_sets=20_000)
+    fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+    got = signatures_csr(ip, di, fam, out_dtype="uint32").cpu().numpy().astype(np.int64)
+    indptr, ids = ip.cpu().numpy(), di.cpu().numpy()
+    assert np.array_equal(got, oracle.sign_family_csr(indptr, ids, fam))

@@ -1,0 +1,101 @@
+"""Pin the CPU oracle against the reference's own outputs and known answers (CPU only).
+
+The fixtures under tests/golden/ were produced by running the reference package
+(tests/golden/make_golden.py); the known-answer vectors come from the
+reference's tests (test_minhash.py:83-94, test_families.py:116-120).
+"""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1401_6124_b200 import IterativeFamily, gen, make_family
+
+
+def test_known_answer_two_element(golden):
+    ka = json.loads((golden / "known_answers.json").read_text())["two_element"]
+    out = oracle.sign_iterative_csr([0, 2], [2, 5], ka["a"], ka["b"], ka["p"], ka["n"])
+    assert out[0].tolist() == ka["mins"] == [5]
+
+
+def test_known_answer_eval_all(golden):
+    ka = json.loads((golden / "known_answers.json").read_text())["iterative_eval_all"]
+    fam = IterativeFamily(ka["a"], ka["b"], ka["p"], ka["n"])
+    assert oracle.member_values(fam, ka["x"]).tolist() == ka["values"] == [6, 6, 6]
+
+
+def test_known_answer_singleton(golden):
+    ka = json.loads((golden / "known_answers.json").read_text())["singleton_42"]
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, ka["seed"], ka["n"], ka["p"])
+        out = oracle.sign_family_csr([0, 1], [42], fam)
+        assert out[0].tolist() == ka["mins"][kind] == [42] * ka["n"]
+
+
+def test_fuzz_small_primes(golden):
+    z = np.load(golden / "fuzz_small.npz")
+    meta = json.loads((golden / "fuzz_small.json").read_text())
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        ip = z["indptr"][k:k + 2]
+        got = oracle.sign_family_csr(ip, z["ids"], fam)[0]
+        want = z["out"][z["out_ptr"][k]:z["out_ptr"][k + 1]]
+        assert np.array_equal(got, want), m
+        # and the brute-force restatement of tests/test_minhash.py:27-39
+        assert np.array_equal(oracle.brute_force_row(z["ids"][ip[0]:ip[1]], fam), want), m
+
+
+def test_long_sets(golden):
+    z = np.load(golden / "long_sets.npz")
+    meta = json.loads((golden / "long_sets.json").read_text())
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        assert np.array_equal(oracle.sign_family_csr(z["indptr"], z["ids"], fam), z[f"out{k}"]), m
+
+
+def test_cfg1_subsample(golden):
+    z = np.load(golden / "cfg1_sub.npz")
+    meta = json.loads((golden / "cfg1.json").read_text())
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, meta[f"{kind}_seed"], meta["n_hash"], meta["prime"])
+        got = oracle.sign_family_csr(z["indptr_sub"], z["ids_sub"], fam)
+        assert np.array_equal(got, z[f"out_sub_{kind}"])
+
+
+def test_cfg1_full_checksum(golden):
+    """Full cfg1 (10k sets, N=128): the oracle's output hashes to the reference's."""
+    meta = json.loads((golden / "cfg1.json").read_text())
+    indptr, ids = gen.cfg1_numpy()
+    assert hashlib.sha256(indptr.tobytes() + ids.tobytes()).hexdigest() == meta["input_sha256"]
+    for kind in ("random", "iterative"):
+        fam = make_family(kind, meta[f"{kind}_seed"], meta["n_hash"], meta["prime"])
+        out = oracle.sign_family_csr(indptr, ids, fam)
+        assert hashlib.sha256(out.astype("<i8").tobytes()).hexdigest() == meta[f"{kind}_sha256"]
+
+
+def test_histogram_restatement(golden):
+    for case in json.loads((golden / "hist.json").read_text()):
+        fam = make_family(case["kind"], case["seed"], case["hashes"], case["prime"])
+        got = oracle.bucket_histogram(fam, case["xs"], case["buckets"])
+        assert got.tolist() == case["counts"]
+
+
+def test_jaccard_restatement(golden):
+    z = np.load(golden / "jaccard.npz")
+    meta = json.loads((golden / "jaccard.json").read_text())
+    for fm in meta["families"]:
+        fam = make_family(fm["kind"], fm["seed"], fm["n"], fm["p"])
+        sig = oracle.sign_family_csr(z["indptr"], z["ids"], fam)
+        est = [oracle.jaccard_estimate(sig[2 * k], sig[2 * k + 1]) for k in range(sig.shape[0] // 2)]
+        assert est == meta["estimates"][fm["kind"]]
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_oracle_thread_count_invariant(threads):
+    indptr, ids = gen.cfg1_numpy(n_sets=300, seed=5)
+    fam = make_family("iterative", 1, 64, 1_048_583)
+    a = oracle.sign_family_csr(indptr, ids, fam, threads=threads)
+    b = oracle.sign_family_csr(indptr, ids, fam, threads=1)
+    assert np.array_equal(a, b)
