@@ -130,8 +130,10 @@ __global__ void setup_kernel(SignArgs A) {
         t.pad = 0;
         A.tab[i] = t;
         InvTab v;
+        v.B = c;
         v.inv = inv_mod(w, p);
         v.invp = shoup_companion(v.inv, p);
+        v.pad = 0;
         A.inv[i] = v;
     }
 
@@ -168,14 +170,16 @@ __global__ void setup_kernel(SignArgs A) {
 // Main kernel
 // ----------------------------------------------------------------------------
 
-__device__ __forceinline__ uint32_t invert_lane(const SignArgs& A, int64_t i, uint32_t h) {
-    // x = (h - B_i) * A_i^{-1} mod p
-    const uint32_t p = A.p;
-    const uint32_t B = __ldg(&A.tab[i].B);
-    const InvTab v = A.inv[i];
-    uint32_t d = h - B;
+// Argmin recovery: x = (h - B_i) * A_i^{-1} mod p, from a staged epilogue table entry.
+__device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, uint32_t p) {
+    uint32_t d = h - v.B;
     d = __viaddmin_u32(d, p, d);  // d in [0,p)
     return reduce_once(shoup_lazy(v.inv, v.invp, d, p), p);
+}
+
+__device__ __forceinline__ uint32_t invert_lane(const SignArgs& A, int64_t i, uint32_t h) {
+    const InvTab v = A.inv[i];
+    return invert_entry(v, h, A.p);
 }
 
 __device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) { atomicMin(p, v); }
@@ -192,29 +196,50 @@ __device__ __forceinline__ void store4(long long* dst, uint32_t a, uint32_t b, u
     v[1] = make_longlong2((long long)c, (long long)d);
 }
 
-template <int K>
+// Iterative walk over K lanes for two features at once.  Lookahead: h_{k+1} and
+// h_{k+2} are both derived from h_k (steps dh and 2dh mod p), which halves the
+// dependent chain and keeps the ALU pipe (VIADDMNMX + VIMNMX3) saturated
+// (tools/visit_probe.cu: 41.9 visits/clk/SM vs 36.3 for the plain chain).
+// FIRST: the item's first round initialises best instead of folding into it.
+template <int K, bool FIRST>
 __device__ __forceinline__ void walk2_iter(uint32_t (&best)[K], uint32_t ha, uint32_t da,
                                            uint32_t hb, uint32_t db, uint32_t p) {
+    const uint32_t da2 = reduce_once(da + da, p), db2 = reduce_once(db + db, p);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        best[k] = __vimin3_u32(best[k], ha, hb);
-        if (k + 1 < K) {
-            ha = reduce_once(ha + da, p);
-            hb = reduce_once(hb + db, p);
+    for (int k = 0; k < K; k += 2) {
+        const uint32_t ga = reduce_once(ha + da, p), gb = reduce_once(hb + db, p);
+        if (FIRST) {
+            best[k] = min(ha, hb);
+            best[k + 1] = min(ga, gb);
+        } else {
+            best[k] = __vimin3_u32(best[k], ha, hb);
+            best[k + 1] = __vimin3_u32(best[k + 1], ga, gb);
+        }
+        if (k + 2 < K) {
+            ha = reduce_once(ha + da2, p);
+            hb = reduce_once(hb + db2, p);
         }
     }
 }
 
-template <int K>
+template <int K, bool FIRST>
 __device__ __forceinline__ void walk1_iter(uint32_t (&best)[K], uint32_t ha, uint32_t da, uint32_t p) {
+    const uint32_t da2 = reduce_once(da + da, p);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        best[k] = min(best[k], ha);
-        if (k + 1 < K) ha = reduce_once(ha + da, p);
+    for (int k = 0; k < K; k += 2) {
+        const uint32_t ga = reduce_once(ha + da, p);
+        if (FIRST) {
+            best[k] = ha;
+            best[k + 1] = ga;
+        } else {
+            best[k] = min(best[k], ha);
+            best[k + 1] = min(best[k + 1], ga);
+        }
+        if (k + 2 < K) ha = reduce_once(ha + da2, p);
     }
 }
 
-template <int K, bool NARROW>
+template <int K, bool NARROW, bool FIRST>
 __device__ __forceinline__ void walk2_random(uint32_t (&best)[K], const uint32_t (&cA)[K],
                                              const uint32_t (&cAp)[K], const uint32_t (&cB)[K],
                                              uint32_t xa, uint32_t xb, uint32_t p) {
@@ -228,11 +253,11 @@ __device__ __forceinline__ void walk2_random(uint32_t (&best)[K], const uint32_t
             ra = mul_add_mod(cA[k], cAp[k], cB[k], xa, p);
             rb = mul_add_mod(cA[k], cAp[k], cB[k], xb, p);
         }
-        best[k] = __vimin3_u32(best[k], ra, rb);
+        best[k] = FIRST ? min(ra, rb) : __vimin3_u32(best[k], ra, rb);
     }
 }
 
-template <int K, bool NARROW>
+template <int K, bool NARROW, bool FIRST>
 __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t (&cA)[K],
                                              const uint32_t (&cAp)[K], const uint32_t (&cB)[K],
                                              uint32_t xa, uint32_t p) {
@@ -240,197 +265,397 @@ __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t
     for (int k = 0; k < K; ++k) {
         uint32_t ra = NARROW ? mul_add_mod_narrow(cA[k], cAp[k], cB[k], xa, p)
                              : mul_add_mod(cA[k], cAp[k], cB[k], xa, p);
-        best[k] = min(best[k], ra);
+        best[k] = FIRST ? ra : min(best[k], ra);
     }
 }
 
-template <int K, bool ITER, bool NARROW, typename OutT>
-__global__ void __launch_bounds__(kBlock) sign_kernel(SignArgs A) {
-    extern __shared__ uint4 smem_raw[];
-    constexpr int NQ = K / 4;                       // 16-byte chunks per thread
-    constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;      // chunk swizzle mask
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    uint32_t* red = reinterpret_cast<uint32_t*>(smem_raw) + warp * 32 * K;
+// ---- asynchronous global->shared copies (cp.async / LDGSTS) ----
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(long long* dst, const int64_t* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
+// Per-warp shared memory: a two-slot ring of item ids (the slot of the item being
+// processed doubles as the slice-combine scratch once its rounds are done) and the
+// CSR bounds of the current and next batch.
+struct WarpSmem {
+    uint32_t ids[2][kChunk];
+    long long ip[2][kBatch + 2];
+};
+
+// Warp-uniform description of one work item.
+struct ItemDesc {
+    int64_t f0;    // first feature (index into ids)
+    int64_t s;     // set index
+    int32_t n;     // features in the item (0: skip / no item)
+    int32_t sb;    // lane pass
+    int32_t merge; // long set: merge with atomicMin, finalize later
+};
+
+__device__ __forceinline__ ItemDesc make_item(int64_t s, int sb, int64_t f0, int64_t hi, bool long_set) {
+    ItemDesc d;
+    const int64_t n = hi - f0;
+    d.f0 = f0;
+    d.s = s;
+    d.sb = sb;
+    d.n = n <= 0 ? 0 : (n > kChunk ? kChunk : (int32_t)n);
+    d.merge = long_set;
+    return d;
+}
+
+__device__ __forceinline__ ItemDesc no_item() {
+    ItemDesc d;
+    d.f0 = 0; d.s = 0; d.n = 0; d.sb = 0; d.merge = 0;
+    return d;
+}
+
+// Stage an item's ids into a ring slot: lane-strided 4-byte async copies.
+__device__ __forceinline__ void stage_ids(const SignArgs& A, const ItemDesc& d, uint32_t* slot, int lane) {
+    const uint32_t* src = A.ids + d.f0;
+    for (int o = lane; o < d.n; o += 32) cp_async4(slot + o, src + o);
+}
+
+// Batch b covers primary items [b*kBatch, b*kBatch + kBatch).  Their sets span
+// [s_first, s_first + cnt); stage indptr[s_first .. s_first + cnt] (cnt+1 values).
+__device__ __forceinline__ int64_t batch_first_set(const SignArgs& A, unsigned long long b) {
+    const unsigned long long item = b * kBatch;
+    return A.n_super == 1 ? (int64_t)item : (int64_t)(item / (unsigned)A.n_super);
+}
+
+__device__ __forceinline__ void stage_bounds(const SignArgs& A, unsigned long long b, unsigned long long n_batches,
+                                             long long* ip, int lane) {
+    if (b >= n_batches) return;
+    const int64_t s0 = batch_first_set(A, b);
+    const unsigned long long last_item = min(b * kBatch + kBatch, (unsigned long long)A.n_sets * A.n_super) - 1;
+    const int64_t s1 = A.n_super == 1 ? (int64_t)last_item : (int64_t)(last_item / (unsigned)A.n_super);
+    const int cnt = (int)(s1 - s0) + 2;  // indptr values needed
+    if (lane < cnt) cp_async8(ip + lane, A.indptr + s0 + lane);
+}
+
+__device__ __forceinline__ ItemDesc batch_item(const SignArgs& A, unsigned long long b, int j, const long long* ip) {
+    const unsigned long long item = b * kBatch + j;
+    int64_t s;
+    int sb = 0;
+    if (A.n_super == 1) {
+        s = (int64_t)item;
+    } else {
+        s = (int64_t)(item / (unsigned)A.n_super);
+        sb = (int)(item - (unsigned long long)s * A.n_super);
+    }
+    const int64_t k = s - batch_first_set(A, b);
+    const int64_t lo = ip[k], hi = ip[k + 1];
+    return make_item(s, sb, lo, hi, (hi - lo) > kChunk);
+}
+
+// Per-thread hashing state: iterative start constants, or the K random-family lane constants.
+template <int K, bool ITER>
+struct LaneState {
+    uint32_t tA, tAp, tB;
+    uint32_t cA[ITER ? 1 : K], cAp[ITER ? 1 : K], cB[ITER ? 1 : K];
+};
+
+template <int K, bool ITER, bool NARROW, bool FIRST>
+__device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa, uint32_t xb,
+                                       uint32_t p, uint32_t bpar) {
+    if constexpr (ITER) {
+        const uint32_t ha = mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        const uint32_t hb = mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
+        walk2_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), hb, reduce_once(xb + bpar, p), p);
+    } else {
+        walk2_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p);
+    }
+}
+
+template <int K, bool ITER, bool NARROW, bool FIRST>
+__device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa,
+                                       uint32_t p, uint32_t bpar) {
+    if constexpr (ITER) {
+        const uint32_t ha = mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        walk1_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), p);
+    } else {
+        walk1_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, p);
+    }
+}
+
+template <int K, bool ITER, bool NARROW, bool FIRST>
+__device__ __forceinline__ void last_round(uint32_t (&best)[K], const LaneState<K, ITER>& ls, bool single,
+                                           uint32_t xa, uint32_t xb, uint32_t p, uint32_t bpar, uint32_t& maxid) {
+    if (single) {
+        maxid = max(maxid, xa);
+        round1<K, ITER, NARROW, FIRST>(best, ls, xa, p, bpar);
+    } else {
+        maxid = __vimax3_u32(maxid, xa, xb);
+        round2<K, ITER, NARROW, FIRST>(best, ls, xa, xb, p, bpar);
+    }
+}
+
+// Stage KP of each thread's minima (lanes k0..k0+KP) into the warp scratch `red`
+// with a 16-byte-chunk XOR swizzle (conflict-free writes and reads).
+template <int K, int K0>
+__device__ __forceinline__ void store_slice(const uint32_t (&best)[K], uint32_t* red, int lane) {
+    constexpr int KP = K < 32 ? K : 32;
+    constexpr int NQ = KP / 4;
+    constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int qq = q ^ (lane & SWZ);
+        *reinterpret_cast<uint4*>(red + lane * KP + qq * 4) =
+            make_uint4(best[K0 + 4 * q], best[K0 + 4 * q + 1], best[K0 + 4 * q + 2], best[K0 + 4 * q + 3]);
+    }
+}
+
+// Combine the F slices for lanes k0..k0+KP of every lane group, recover the argmin
+// ids and store them (or atomicMin the min hashes of a long set).
+template <int K, typename OutT>
+__device__ __forceinline__ void combine_emit(const SignArgs& A, const ItemDesc& cur, int k0, const uint32_t* red,
+                                             const InvTab* epi_s, bool epi_smem, int lane, int F) {
+    constexpr int KP = K < 32 ? K : 32;
+    constexpr int NQ = KP / 4;
+    constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
+    const uint32_t p = A.p;
+    const int32_t N = A.n_hash;
+    const int G = 32 / F;
+    const int n_chunks = G * KP / 4;
+    const bool vec_ok = ((N & 3) == 0);
+    OutT* row = reinterpret_cast<OutT*>(A.out) + cur.s * (int64_t)N;
+    for (int c = lane; c < n_chunks; c += 32) {
+        const int l4 = 4 * c;
+        const int gg = l4 / KP;
+        const int kk = l4 - gg * KP;
+        const int qk = kk / 4;
+        const uint32_t* src = red + gg * F * KP;
+        uint4 m = *reinterpret_cast<const uint4*>(src + (qk ^ ((gg * F) & SWZ)) * 4);
+        int ff = 1;
+        for (; ff + 1 < F; ff += 2) {
+            const int w0 = gg * F + ff, w1 = w0 + 1;
+            const uint4 v0 = *reinterpret_cast<const uint4*>(src + ff * KP + (qk ^ (w0 & SWZ)) * 4);
+            const uint4 v1 = *reinterpret_cast<const uint4*>(src + (ff + 1) * KP + (qk ^ (w1 & SWZ)) * 4);
+            m.x = __vimin3_u32(m.x, v0.x, v1.x); m.y = __vimin3_u32(m.y, v0.y, v1.y);
+            m.z = __vimin3_u32(m.z, v0.z, v1.z); m.w = __vimin3_u32(m.w, v0.w, v1.w);
+        }
+        if (ff < F) {
+            const int w0 = gg * F + ff;
+            const uint4 v0 = *reinterpret_cast<const uint4*>(src + ff * KP + (qk ^ (w0 & SWZ)) * 4);
+            m.x = min(m.x, v0.x); m.y = min(m.y, v0.y); m.z = min(m.z, v0.z); m.w = min(m.w, v0.w);
+        }
+        const int64_t i = (int64_t)cur.sb * A.L + (int64_t)gg * K + k0 + kk;
+        if (cur.merge) {
+            if (i + 0 < N) atomic_min_out(row + i + 0, m.x);
+            if (i + 1 < N) atomic_min_out(row + i + 1, m.y);
+            if (i + 2 < N) atomic_min_out(row + i + 2, m.z);
+            if (i + 3 < N) atomic_min_out(row + i + 3, m.w);
+            continue;
+        }
+        uint32_t x[4];
+        const uint32_t h[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            InvTab t;
+            if (epi_smem) {
+                t = epi_s[i + e];
+            } else {
+                t = A.inv[min(i + e, (int64_t)A.n_tot - 1)];
+            }
+            x[e] = invert_entry(t, h[e], p);
+        }
+        if (vec_ok && i + 3 < N) {
+            store4(row + i, x[0], x[1], x[2], x[3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (i + e < N) row[i + e] = (OutT)x[e];
+        }
+    }
+}
+
+// One work item whose ids are staged in `slot`: rounds (the first initialises the
+// minima; a last round with <= F features walks one feature per slice), then the
+// slice combine in `slot` (the ids are consumed by then) and the epilogue.
+template <int K, bool ITER, bool NARROW, typename OutT>
+__device__ __forceinline__ void run_item(const SignArgs& A, const ItemDesc& cur, uint32_t* slot,
+                                         LaneState<K, ITER>& ls, int& cur_sb, uint32_t& maxid,
+                                         const InvTab* epi_s, bool epi_smem, int lane, int g, int f, int F) {
     const uint32_t p = A.p;
     const uint32_t bpar = A.b;
+    if (cur.sb != cur_sb) {  // lane constants change only with the lane pass
+        const int64_t i0 = (int64_t)cur.sb * A.L + (int64_t)g * K;
+        if constexpr (ITER) {
+            const LaneTab t = A.tab[i0];
+            ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const LaneTab t = A.tab[i0 + k];
+                ls.cA[k] = t.A; ls.cAp[k] = t.Ap; ls.cB[k] = t.B;
+            }
+        }
+        cur_sb = cur.sb;
+    }
+
+    // rounds of 2F features; F is a power of two
+    uint32_t best[K];
+    const int n = cur.n;
+    const int last = n - 1;
+    const int sh = A.log2F + 1;
+    const int rounds = (n + (1 << sh) - 1) >> sh;
+    const bool single = rounds > 1 && (n - ((rounds - 1) << sh)) <= F;
+    {
+        const uint32_t xa = slot[min(f, last)], xb = slot[min(F + f, last)];
+        maxid = __vimax3_u32(maxid, xa, xb);
+        round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
+    }
+    // middle rounds are always full: no clamping, no branches
+    const int full_end = (rounds - 1) << sh;
+    int o = 2 * F + f;
+#pragma unroll 1
+    for (; o < full_end; o += 2 * F) {
+        const uint32_t xa = slot[o], xb = slot[o + F];
+        maxid = __vimax3_u32(maxid, xa, xb);
+        round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+    }
+    if (rounds > 1) {
+        const uint32_t xa = slot[min(o, last)], xb = slot[min(o + F, last)];
+        if (single) {
+            maxid = max(maxid, xa);
+            round1<K, ITER, NARROW, false>(best, ls, xa, p, bpar);
+        } else {
+            maxid = __vimax3_u32(maxid, xa, xb);
+            round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+        }
+    }
+    __syncwarp();  // every lane is done reading ids before the slot becomes scratch
+    constexpr int KP = K < 32 ? K : 32;
+    static_assert(K / KP <= 2, "at most two combine passes");
+#pragma unroll 1
+    for (int h = 0; h < K / KP; ++h) {
+        if (h == 0) store_slice<K, 0>(best, slot, lane);
+        else store_slice<K, (K > KP ? KP : 0)>(best, slot, lane);
+        __syncwarp();
+        combine_emit<K, OutT>(A, cur, h * KP, slot, epi_s, epi_smem, lane, F);
+        __syncwarp();
+    }
+}
+
+// Where the next work item comes from: first the extra chunks of long sets (one
+// atomic each), then batches of kBatch consecutive primary items whose CSR bounds
+// are staged in shared memory one batch ahead.
+struct ItemSource {
+    int phase;                   // 0 extras, 1 batches, 2 done
+    int j, slot_b, in_batch;
+    unsigned long long b_cur, b_nxt, b_nxt2;
+};
+
+__device__ __forceinline__ ItemDesc next_item(const SignArgs& A, ItemSource& src, WarpSmem* ws, int lane,
+                                              unsigned long long n_extra, unsigned long long n_primary,
+                                              unsigned long long n_batches) {
+    if (src.phase == 0) {
+        unsigned long long e = 0;
+        if (lane == 0) e = atomicAdd(&A.sched->next_extra, 1ull);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        if (e < n_extra) {
+            const Extra x = A.extra[e];
+            const int64_t lo = A.indptr[x.set], hi = A.indptr[x.set + 1];
+            return make_item(x.set, x.sb, lo + (int64_t)x.chunk * kChunk, hi, true);
+        }
+        // enter the batch phase: claim three batches, stage two batches of bounds
+        src.phase = 1;
+        if (lane == 0) {
+            src.b_cur = atomicAdd(&A.sched->next, 1ull);
+            src.b_nxt = atomicAdd(&A.sched->next, 1ull);
+            src.b_nxt2 = atomicAdd(&A.sched->next, 1ull);
+        }
+        src.b_cur = __shfl_sync(0xffffffffu, src.b_cur, 0);
+        src.b_nxt = __shfl_sync(0xffffffffu, src.b_nxt, 0);
+        if (src.b_cur >= n_batches) {
+            src.phase = 2;
+            return no_item();
+        }
+        src.slot_b = 0;
+        stage_bounds(A, src.b_cur, n_batches, ws->ip[0], lane);
+        stage_bounds(A, src.b_nxt, n_batches, ws->ip[1], lane);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        src.j = 0;
+        src.in_batch = (int)min((unsigned long long)kBatch, n_primary - src.b_cur * kBatch);
+        return batch_item(A, src.b_cur, 0, ws->ip[0]);
+    }
+    if (src.phase == 2) return no_item();
+    if (++src.j == src.in_batch) {
+        src.j = 0;
+        src.b_cur = src.b_nxt;
+        src.slot_b ^= 1;
+        src.b_nxt = __shfl_sync(0xffffffffu, src.b_nxt2, 0);
+        if (src.b_cur >= n_batches) {
+            src.phase = 2;
+            return no_item();
+        }
+        // The new current batch's bounds were staged a batch ago; make sure they landed.
+        cp_async_wait<0>();
+        __syncwarp();
+        stage_bounds(A, src.b_nxt, n_batches, ws->ip[src.slot_b ^ 1], lane);
+        if (lane == 0) src.b_nxt2 = atomicAdd(&A.sched->next, 1ull);
+        src.in_batch = (int)min((unsigned long long)kBatch, n_primary - src.b_cur * kBatch);
+    }
+    return batch_item(A, src.b_cur, src.j, ws->ip[src.slot_b]);
+}
+
+template <int K, bool ITER, bool NARROW, typename OutT>
+__global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) {
+    extern __shared__ uint4 smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw) + warp;
+    InvTab* epi_s = reinterpret_cast<InvTab*>(reinterpret_cast<WarpSmem*>(smem_raw) + kBlock / 32);
+
     const int F = A.F;
     const int g = lane >> A.log2F;
     const int f = lane & (F - 1);
-    const int L = A.L;
-    const int32_t N = A.n_hash;
-    OutT* out = reinterpret_cast<OutT*>(A.out);
+
+    // Stage the epilogue table (B_i, A_i^{-1}, companion) in shared memory.
+    const bool epi_smem = A.n_tot <= kEpiSmemLanes;
+    if (epi_smem) {
+        for (int i = threadIdx.x; i < A.n_tot; i += blockDim.x) epi_s[i] = A.inv[i];
+        __syncthreads();
+    }
+
+    LaneState<K, ITER> ls;
+    int cur_sb = -1;
+    uint32_t maxid = 0;
 
     const unsigned long long n_extra = *((volatile unsigned long long*)&A.sched->n_extra);
-    const unsigned long long total = n_extra + (unsigned long long)A.n_sets * A.n_super;
+    const unsigned long long n_primary = (unsigned long long)A.n_sets * A.n_super;
+    const unsigned long long n_batches = (n_primary + kBatch - 1) / kBatch;
+    ItemSource src;
+    src.phase = 0;
+    src.j = src.slot_b = src.in_batch = 0;
+    src.b_cur = src.b_nxt = src.b_nxt2 = 0;
 
-    unsigned long long item = 0;
-    if (lane == 0) item = atomicAdd(&A.sched->next, 1ull);
-    item = __shfl_sync(0xffffffffu, item, 0);
-
-    int cur_sb = -1;
-    uint32_t cA[K], cAp[K], cB[K];
-    bool bad = false;
-
-    while (item < total) {
-        unsigned long long nxt = 0;
-        if (lane == 0) nxt = atomicAdd(&A.sched->next, 1ull);
-
-        int64_t s, f0, f1;
-        int sb;
-        bool merge;
-        if (item < n_extra) {
-            const Extra e = A.extra[item];
-            s = e.set;
-            sb = e.sb;
-            const int64_t lo = A.indptr[s], hi = A.indptr[s + 1];
-            f0 = lo + (int64_t)e.chunk * kChunk;
-            f1 = min(f0 + (int64_t)kChunk, hi);
-            merge = true;
-        } else {
-            const unsigned long long pid = item - n_extra;
-            if (A.n_super == 1) {
-                s = (int64_t)pid;
-                sb = 0;
-            } else {
-                s = (int64_t)(pid / (unsigned)A.n_super);
-                sb = (int)(pid - (unsigned long long)s * A.n_super);
-            }
-            const int64_t lo = A.indptr[s], hi = A.indptr[s + 1];
-            f0 = lo;
-            f1 = min(lo + (int64_t)kChunk, hi);
-            merge = (hi - lo) > kChunk;
-        }
-
-        if (f1 > f0) {
-            const int64_t i0 = (int64_t)sb * L + (int64_t)g * K;
-            uint32_t tA = 0, tAp = 0, tB = 0;
-            if constexpr (ITER) {
-                const LaneTab t = A.tab[i0];
-                tA = t.A; tAp = t.Ap; tB = t.B;
-            } else {
-                if (sb != cur_sb) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        const LaneTab t = A.tab[i0 + k];
-                        cA[k] = t.A; cAp[k] = t.Ap; cB[k] = t.B;
-                    }
-                    cur_sb = sb;
-                }
-            }
-
-            uint32_t best[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
-
-            const uint32_t* ids = A.ids;
-            const int64_t n = f1 - f0;
-            const int64_t step = 2 * (int64_t)F;
-            const int64_t n_pair_rounds = n / step;
-            const int64_t rem = n - n_pair_rounds * step;
-
-            // ---- full rounds: every slice has two valid features ----
-            if (n_pair_rounds > 0) {
-                int64_t ja = f0 + f;
-                uint32_t xa = __ldg(ids + ja), xb = __ldg(ids + ja + F);
-                for (int64_t r = 0; r < n_pair_rounds; ++r) {
-                    // prefetch next round (clamped to a valid address)
-                    int64_t jn = ja + step;
-                    const int64_t jna = jn < f1 ? jn : f0;
-                    const int64_t jnb = jn + F < f1 ? jn + F : f0;
-                    const uint32_t xa_n = __ldg(ids + jna), xb_n = __ldg(ids + jnb);
-                    bad |= (xa >= p) | (xb >= p);
-                    if constexpr (ITER) {
-                        const uint32_t ha = mul_add_mod(tA, tAp, tB, xa, p);
-                        const uint32_t hb = mul_add_mod(tA, tAp, tB, xb, p);
-                        const uint32_t da = reduce_once(xa + bpar, p);
-                        const uint32_t db = reduce_once(xb + bpar, p);
-                        walk2_iter<K>(best, ha, da, hb, db, p);
-                    } else {
-                        walk2_random<K, NARROW>(best, cA, cAp, cB, xa, xb, p);
-                    }
-                    xa = xa_n;
-                    xb = xb_n;
-                    ja = jn;
-                }
-            }
-            // ---- tail: rem < 2F features left ----
-            if (rem > 0) {
-                const int64_t base = f0 + n_pair_rounds * step;
-                if (rem > F) {
-                    const int64_t ja = base + f;            // always < f1 since f < F < rem
-                    const int64_t jb = base + F + f;
-                    const uint32_t xa = __ldg(ids + ja);
-                    const uint32_t xb = __ldg(ids + (jb < f1 ? jb : ja));
-                    bad |= (xa >= p) | (xb >= p);
-                    if constexpr (ITER) {
-                        const uint32_t ha = mul_add_mod(tA, tAp, tB, xa, p);
-                        const uint32_t hb = mul_add_mod(tA, tAp, tB, xb, p);
-                        const uint32_t da = reduce_once(xa + bpar, p);
-                        const uint32_t db = reduce_once(xb + bpar, p);
-                        walk2_iter<K>(best, ha, da, hb, db, p);
-                    } else {
-                        walk2_random<K, NARROW>(best, cA, cAp, cB, xa, xb, p);
-                    }
-                } else {
-                    const int64_t ja = base + f;
-                    const uint32_t xa = __ldg(ids + (ja < f1 ? ja : base));
-                    bad |= (xa >= p);
-                    if constexpr (ITER) {
-                        const uint32_t ha = mul_add_mod(tA, tAp, tB, xa, p);
-                        const uint32_t da = reduce_once(xa + bpar, p);
-                        walk1_iter<K>(best, ha, da, p);
-                    } else {
-                        walk1_random<K, NARROW>(best, cA, cAp, cB, xa, p);
-                    }
-                }
-            }
-
-            // ---- combine the F slices through the warp's smem tile ----
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const int qq = q ^ (lane & SWZ);
-                *reinterpret_cast<uint4*>(red + lane * K + qq * 4) =
-                    make_uint4(best[4 * q], best[4 * q + 1], best[4 * q + 2], best[4 * q + 3]);
-            }
-            __syncwarp();
-            const int n_chunks = L / 4;
-            const bool vec_ok = ((N & 3) == 0);
-            OutT* row = out + s * (int64_t)N;
-            for (int c = lane; c < n_chunks; c += 32) {
-                const int l = 4 * c;
-                const int gg = l / K;
-                const int qk = (l % K) / 4;
-                uint4 m = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                for (int ff = 0; ff < F; ++ff) {
-                    const int w = gg * F + ff;
-                    const int qq = qk ^ (w & SWZ);
-                    const uint4 v = *reinterpret_cast<const uint4*>(red + w * K + qq * 4);
-                    m.x = min(m.x, v.x); m.y = min(m.y, v.y);
-                    m.z = min(m.z, v.z); m.w = min(m.w, v.w);
-                }
-                const int64_t i = (int64_t)sb * L + l;
-                if (merge) {
-                    if (i + 0 < N) atomic_min_out(row + i + 0, m.x);
-                    if (i + 1 < N) atomic_min_out(row + i + 1, m.y);
-                    if (i + 2 < N) atomic_min_out(row + i + 2, m.z);
-                    if (i + 3 < N) atomic_min_out(row + i + 3, m.w);
-                } else if (vec_ok && i + 3 < N) {
-                    store4(row + i, invert_lane(A, i, m.x), invert_lane(A, i + 1, m.y),
-                           invert_lane(A, i + 2, m.z), invert_lane(A, i + 3, m.w));
-                } else {
-                    if (i + 0 < N) row[i + 0] = (OutT)invert_lane(A, i + 0, m.x);
-                    if (i + 1 < N) row[i + 1] = (OutT)invert_lane(A, i + 1, m.y);
-                    if (i + 2 < N) row[i + 2] = (OutT)invert_lane(A, i + 2, m.z);
-                    if (i + 3 < N) row[i + 3] = (OutT)invert_lane(A, i + 3, m.w);
-                }
-            }
-            __syncwarp();
-        }
-        item = __shfl_sync(0xffffffffu, nxt, 0);
+    // Item pipeline: the next item's ids are staged (cp.async) while the current runs.
+    int slot = 0;
+    ItemDesc cur = next_item(A, src, ws, lane, n_extra, n_primary, n_batches);
+    stage_ids(A, cur, ws->ids[0], lane);
+    cp_async_commit();
+    while (src.phase != 2 || cur.n > 0) {
+        const ItemDesc nxt = next_item(A, src, ws, lane, n_extra, n_primary, n_batches);
+        stage_ids(A, nxt, ws->ids[slot ^ 1], lane);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        if (cur.n > 0)
+            run_item<K, ITER, NARROW, OutT>(A, cur, ws->ids[slot], ls, cur_sb, maxid, epi_s, epi_smem, lane, g, f, F);
+        cur = nxt;
+        slot ^= 1;
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
+    cp_async_wait<0>();
+    if (__any_sync(0xffffffffu, maxid >= A.p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
 }
 
 // Long sets: rows hold min hash values after the main kernel; invert in place.
@@ -490,21 +715,28 @@ static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K) {
     return i64 ? pick_kernel<false, false, long long>(K) : pick_kernel<false, false, uint32_t>(K);
 }
 
-// Occupancy (CTAs per SM) per kernel function; computed once per device.
-static int blocks_per_sm(SignKernelFn fn, size_t smem, int device) {
+// Occupancy (CTAs per SM) per (kernel, device, dynamic smem); computed once.  The
+// dynamic-smem limit is raised to the device maximum the first time a kernel is seen.
+static int blocks_per_sm(SignKernelFn fn, size_t smem, const DeviceInfo& dev) {
     static std::mutex mu;
-    struct Entry { const void* fn; int dev; int occ; };
-    static Entry cache[256];
+    struct Entry { const void* fn; int dev; size_t smem; int occ; };
+    static Entry cache[512];
     static int n_cache = 0;
     std::lock_guard<std::mutex> lock(mu);
-    for (int i = 0; i < n_cache; ++i)
-        if (cache[i].fn == (const void*)fn && cache[i].dev == device) return cache[i].occ;
-    cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    bool seen = false;
+    for (int i = 0; i < n_cache; ++i) {
+        if (cache[i].fn == (const void*)fn && cache[i].dev == dev.device) {
+            seen = true;
+            if (cache[i].smem == smem) return cache[i].occ;
+        }
+    }
+    if (!seen)
+        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dev.smem_optin);
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kBlock, smem) != cudaSuccess)
         occ = 1;
     if (occ < 1) occ = 1;
-    if (n_cache < 256) cache[n_cache++] = Entry{(const void*)fn, device, occ};
+    if (n_cache < 512) cache[n_cache++] = Entry{(const void*)fn, dev.device, smem, occ};
     return occ;
 }
 
@@ -596,9 +828,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool narrow = (3ull * prime) < (1ull << 32);
     SignKernelFn fn = select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
-    const size_t smem = (size_t)(kBlock / 32) * 32 * geo.K * sizeof(uint32_t);
-    const int occ = blocks_per_sm(fn, smem, dev.device);
-    const int64_t items_ub = n_sets * geo.n_super + (nnz / kChunk) * geo.n_super;
+    const size_t smem = (size_t)(kBlock / 32) * sizeof(WarpSmem) +
+                        (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
+    const int occ = blocks_per_sm(fn, smem, dev);
+    const int64_t items_ub = (n_sets * geo.n_super + kBatch - 1) / kBatch + (nnz / kChunk) * geo.n_super;
     int64_t blocks = (items_ub + (kBlock / 32) - 1) / (kBlock / 32);
     const int64_t cap = (int64_t)occ * dev.sms;
     if (blocks > cap) blocks = cap;

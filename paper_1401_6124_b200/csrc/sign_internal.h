@@ -11,14 +11,17 @@ enum { KIND_ITERATIVE = 0, KIND_RANDOM = 1 };
 
 constexpr int kChunk = 1024;  // features per work item; longer sets are split
 constexpr int kBlock = 256;   // threads per CTA of the main kernel
+constexpr int kEpiSmemLanes = 2048;  // epilogue table staged in shared memory up to this many lanes
+constexpr int kBatch = 8;     // consecutive sets a warp claims per atomic (must be <= 32)
 
 // Per hash lane i: h_i(x) = (A*x + B) mod p, Ap = floor(A*2^32/p) (Shoup companion).
 struct LaneTab {
     uint32_t A, Ap, B, pad;
 };
-// Per hash lane i: inv = A^{-1} mod p and its Shoup companion (argmin recovery).
+// Per hash lane i, for the argmin recovery x = (h - B) * inv mod p:
+// B (the lane offset), inv = A^{-1} mod p and its Shoup companion.
 struct InvTab {
-    uint32_t inv, invp;
+    uint32_t B, inv, invp, pad;
 };
 // One extra chunk (index >= 1) of a set longer than kChunk.
 struct Extra {
@@ -27,10 +30,10 @@ struct Extra {
     int32_t chunk;
 };
 struct Sched {
-    unsigned long long next;     // dynamic work-item counter
+    unsigned long long next;     // dynamic counter over batches of primary items
     unsigned long long n_extra;  // extra chunks planned
     unsigned long long n_big;    // (set, lane pass) pairs in merge mode
-    unsigned long long pad;
+    unsigned long long next_extra;  // dynamic counter over extra chunks
 };
 
 struct Geometry {

@@ -1,0 +1,120 @@
+// visit_probe.cu -- microbenchmark of the iterative visit sequence (registers only).
+//
+// Measures visits/clk/SM for walk shapes the signature kernel could use:
+//   lanes per thread K, independent feature chains C per thread, and
+//   lookahead L (lanes advanced per chain step: L=2 derives h_{i+1}, h_{i+2}
+//   both from h_i, halving the dependent chain length).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o visit_probe visit_probe.cu
+#include <cstdint>
+#include <cstdio>
+
+__device__ uint32_t g_sink;
+
+__device__ __forceinline__ uint32_t red(uint32_t t, uint32_t p) { return __viaddmin_u32(t, 0u - p, t); }
+
+template <int K, int C, int L>
+__global__ void __launch_bounds__(256) walk(int rounds, uint32_t p, uint32_t seed, long long* cyc) {
+    uint32_t best[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
+    uint32_t h0[C], d[C], d2[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        h0[c] = (threadIdx.x * 2654435761u + seed * (c + 1)) % p;
+        d[c] = (blockIdx.x * 40503u + 17u * c + seed) % p;
+        d2[c] = (2 * d[c]) % p;
+    }
+    long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r) {
+        uint32_t h[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) h[c] = h0[c];
+        if (L == 1) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (C == 1) best[k] = min(best[k], h[0]);
+                if (C >= 2) best[k] = __vimin3_u32(best[k], h[0], h[1]);
+                if (C >= 4) best[k] = __vimin3_u32(best[k], h[2], h[3]);
+#pragma unroll
+                for (int c = 0; c < C; ++c) h[c] = red(h[c] + d[c], p);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; k += 2) {
+                uint32_t g[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) g[c] = red(h[c] + d[c], p);
+                if (C == 1) { best[k] = min(best[k], h[0]); best[k + 1] = min(best[k + 1], g[0]); }
+                if (C >= 2) {
+                    best[k] = __vimin3_u32(best[k], h[0], h[1]);
+                    best[k + 1] = __vimin3_u32(best[k + 1], g[0], g[1]);
+                }
+                if (C >= 4) {
+                    best[k] = __vimin3_u32(best[k], h[2], h[3]);
+                    best[k + 1] = __vimin3_u32(best[k + 1], g[2], g[3]);
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) h[c] = red(h[c] + d2[c], p);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) h0[c] = red(h0[c] + (uint32_t)r, p);
+    }
+    long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_sink = acc;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int K, int C, int L>
+void run(const char* name, int sms) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, walk<K, C, L>, 256, 0);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, walk<K, C, L>);
+    int blocks = occ * sms;
+    long long* cyc;
+    cudaMalloc(&cyc, blocks * sizeof(long long));
+    int rounds = 2000;
+    walk<K, C, L><<<blocks, 256>>>(rounds / 10, 16777259u, 1u, cyc);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    walk<K, C, L><<<blocks, 256>>>(rounds, 16777259u, 2u, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long* h = new long long[blocks];
+    cudaMemcpy(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long mx = 0;
+    for (int i = 0; i < blocks; ++i) mx = h[i] > mx ? h[i] : mx;
+    double visits = (double)blocks * 256 * rounds * K * C;
+    double per_sm_clk = visits / sms / (double)mx;
+    printf("%-22s K=%3d C=%d L=%d regs=%3d occ=%d warps/SM=%2d  %.2f Tvisit/s  %.2f visits/clk/SM  clk=%.0f MHz\n", name, K,
+           C, L, fa.numRegs, occ, occ * 8, visits / (ms * 1e-3) / 1e12, per_sm_clk, mx / (ms * 1e3));
+    delete[] h;
+    cudaFree(cyc);
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    printf("SMs=%d (ALU-pipe ceiling at 1.5 ALU instr/visit = 42.7 visits/clk/SM)\n", sms);
+    run<64, 2, 1>("base", sms);
+    run<64, 2, 2>("lookahead", sms);
+    run<64, 4, 1>("4 chains", sms);
+    run<64, 4, 2>("4 chains lookahead", sms);
+    run<32, 2, 1>("base", sms);
+    run<32, 2, 2>("lookahead", sms);
+    run<32, 4, 1>("4 chains", sms);
+    run<32, 4, 2>("4 chains lookahead", sms);
+    run<128, 2, 1>("base", sms);
+    run<128, 2, 2>("lookahead", sms);
+    run<64, 1, 1>("1 chain", sms);
+    run<64, 1, 2>("1 chain lookahead", sms);
+    return 0;
+}
