@@ -1,28 +1,29 @@
 // sign.cu -- MinHash signatures over CSR sets on sm_100a (both hash families).
 //
-// Reference semantics (arXiv 1401.6124 reference package):
+// Reference semantics (arXiv 1401.6124 reference package `minhashlab`):
 //   sign_iterative  kernels.py:44-73   h_i(x) = ((a+i)x + i*b) mod p, walked as
 //                                      h <- h + (x+b) mod p with one conditional subtract
 //   sign_random     kernels.py:21-41   h_i(x) = (a_i x + b_i) mod p
 //   output          minhash.py:91-110  argmin feature id per hash index
 //
-// Design:
-//  * A warp owns one work item = (set, feature chunk <= kChunk, lane pass).  Its
-//    32 threads form G lane groups x F feature slices (G*F = 32).  Thread (g,f)
-//    keeps K running minima in registers for hash lanes i0 .. i0+K-1 and walks
-//    features f, f+F, ... of the item, two at a time.
-//  * Per (thread, feature) setup is one Shoup multiply: h_{i0}(x) = A_{i0} x + B_{i0}
-//    with per-lane constants from a table built once per call.  Per visit the
-//    iterative family costs IADD + VIADDMNMX + 1/2 VIMNMX3 (2.5 instructions);
-//    the random family costs IMAD.HI + 2 IMAD + 2 VIADDMNMX + 1/2 VIMNMX3.
-//  * Only the min HASH VALUE is tracked.  Every family member is a bijection on
-//    [0,p) (families.py:82,141; reference test test_families.py:178-186), so the
-//    argmin is recovered exactly once per entry: x = (h - B_i) * A_i^{-1} mod p.
-//  * Slices are combined through a swizzled per-warp shared-memory tile; the
-//    epilogue inverts and stores.  Sets longer than kChunk are split into chunks
-//    that merge with atomicMin on the output row; a finalize pass inverts them.
-//  * Work items are handed out by a global atomic counter (persistent grid),
-//    long-set chunks first.
+// Design (DESIGN.md has the numbers):
+//  * Plan (3 small kernels): sets are cut into virtual sets of <= kChunk features
+//    and counting-sorted by size, largest first.
+//  * Main kernel (persistent, dynamic work counter): a warp takes a group of F
+//    consecutive virtual sets -- equal sizes, thanks to the sort -- one per slice.
+//    Its 32 threads are G lane groups x F slices (G*F = 32): thread (g,f) keeps the
+//    running minima of hash lanes i0..i0+K-1 (i0 = g*K) of set f in registers and
+//    walks that set's features two at a time.  No cross-thread combine is needed
+//    and a group wastes almost nothing at its end.
+//  * Per (thread, feature): one Shoup multiply gives h_{i0}(x) = A_{i0} x + B_{i0};
+//    then the iterative walk costs IADD + VIADDMNMX + 1/2 VIMNMX3 per visit, with a
+//    two-lane lookahead that halves the dependent chain (tools/visit_probe.cu).
+//    The random family costs IMAD.HI + 2 IMAD + 2 VIADDMNMX + 1/2 VIMNMX3 per visit.
+//  * Only the min HASH VALUE is tracked.  Every member is a bijection on [0,p)
+//    (families.py:82,141; test_families.py:178-186), so the argmin is recovered
+//    exactly once per entry: x = (h - B_i) * A_i^{-1} mod p.
+//  * Sets longer than kChunk merge their chunks with atomicMin on the output row;
+//    a finalize pass inverts those rows.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -35,7 +36,7 @@
 namespace mhb {
 
 // ----------------------------------------------------------------------------
-// Geometry
+// Geometry and workspace
 // ----------------------------------------------------------------------------
 
 static int next_pow2(int v) {
@@ -76,30 +77,33 @@ WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
     Geometry gi = choose_geometry(KIND_ITERATIVE, n_hash);
     Geometry gr = choose_geometry(KIND_RANDOM, n_hash);
     int64_t n_tot = gi.n_tot > gr.n_tot ? gi.n_tot : gr.n_tot;
-    int n_super = gi.n_super > gr.n_super ? gi.n_super : gr.n_super;
     int64_t nnz_pos = nnz > 0 ? nnz : 0;
-    int64_t max_big_sets = nnz_pos / (kChunk + 1);
-    if (max_big_sets > n_sets) max_big_sets = n_sets;
-    int64_t max_big = max_big_sets * n_super;
-    int64_t max_extra = (nnz_pos / kChunk) * n_super;
+    int64_t sets = n_sets > 0 ? n_sets : 0;
+    int64_t max_big = nnz_pos / (kChunk + 1);
+    if (max_big > sets) max_big = sets;
+    int64_t max_vsets = sets + nnz_pos / kChunk;
 
     WorkspaceLayout w{};
     size_t off = 0;
     w.sched = off;  off = align_up(off + sizeof(Sched), 256);
+    w.hist = off;   off = align_up(off + 2 * kChunk * sizeof(unsigned), 256);
     w.tab = off;    off = align_up(off + (size_t)n_tot * sizeof(LaneTab), 256);
     w.inv = off;    off = align_up(off + (size_t)n_tot * sizeof(InvTab), 256);
     w.big = off;    off = align_up(off + (size_t)(max_big > 0 ? max_big : 1) * sizeof(int64_t), 256);
-    w.extra = off;  off = align_up(off + (size_t)(max_extra > 0 ? max_extra : 1) * sizeof(Extra), 256);
+    w.vsets = off;  off = align_up(off + (size_t)(max_vsets > 0 ? max_vsets : 1) * sizeof(VSet), 256);
     w.total = off;
     return w;
 }
 
 // ----------------------------------------------------------------------------
-// Setup: lane tables + long-set plan
+// Plan: lane tables, size histogram of virtual sets, long-set bookkeeping
 // ----------------------------------------------------------------------------
 
 template <typename OutT>
-__global__ void setup_kernel(SignArgs A) {
+__global__ void plan_count_kernel(SignArgs A) {
+    __shared__ unsigned sh[kChunk];
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const uint32_t p = A.p;
@@ -137,49 +141,118 @@ __global__ void setup_kernel(SignArgs A) {
         A.inv[i] = v;
     }
 
-    OutT* out = reinterpret_cast<OutT*>(A.out);
     for (int64_t s = tid; s < A.n_sets; s += stride) {
-        const int64_t lo = A.indptr[s], hi = A.indptr[s + 1];
-        const int64_t n = hi - lo;
+        const int64_t n = A.indptr[s + 1] - A.indptr[s];
         if (n <= 0) {
             if (A.status) atomicOr(A.status, MHB_STATUS_EMPTY_SET);
             continue;
         }
-        if (n > kChunk) {
-            const int64_t nch = (n + kChunk - 1) / kChunk;
-            unsigned long long eb = atomicAdd(&A.sched->n_extra,
-                                              (unsigned long long)((nch - 1) * A.n_super));
-            unsigned long long bb = atomicAdd(&A.sched->n_big, (unsigned long long)A.n_super);
-            for (int sb = 0; sb < A.n_super; ++sb) {
-                A.big[bb + sb] = s * A.n_super + sb;
-                for (int64_t c = 1; c < nch; ++c) {
-                    Extra e;
-                    e.set = s;
-                    e.sb = sb;
-                    e.chunk = (int32_t)c;
-                    A.extra[eb++] = e;
-                }
-            }
-            OutT* row = out + s * (int64_t)A.n_hash;
-            for (int32_t i = 0; i < A.n_hash; ++i) row[i] = (OutT)(~0u);
+        const int64_t nch = (n + kChunk - 1) / kChunk;
+        const int last = (int)(n - (nch - 1) * kChunk);
+        atomicAdd(&sh[last - 1], 1u);
+        if (nch > 1) {
+            atomicAdd(&sh[kChunk - 1], (unsigned)(nch - 1));
+            const unsigned long long k = atomicAdd(&A.sched->n_big, 1ull);
+            A.big[k] = s;
         }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x)
+        if (sh[i]) atomicAdd(&A.hist[i], sh[i]);
+}
+
+// One block of kChunk threads: cursor[size-1] = number of virtual sets larger than
+// `size` (descending order), total -> sched->n_vsets.
+__global__ void plan_scan_kernel(SignArgs A) {
+    __shared__ unsigned warp_tot[kChunk / 32];
+    const int t = threadIdx.x;               // t-th largest size: size = kChunk - t
+    const int bin = kChunk - 1 - t;
+    const unsigned v = A.hist[bin];
+    unsigned incl = v;
+    const int lane = t & 31, w = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        unsigned x = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        warp_tot[lane] = x;  // inclusive prefix of warp totals
+    }
+    __syncthreads();
+    const unsigned base = w > 0 ? warp_tot[w - 1] : 0u;
+    A.hist[kChunk + bin] = base + incl - v;  // exclusive start of this size's run
+    if (t == kChunk - 1) A.sched->n_vsets = base + incl;
+}
+
+// Place every virtual set at its sorted position.  Each block owns a contiguous
+// range of sets: it counts its virtual sets per size in shared memory, reserves
+// one run per size with a single global atomic, then places them (hot size bins
+// see one global atomic per block instead of one per set).  Afterwards the blocks
+// initialise the output rows of long sets (merged with atomicMin) to UINT_MAX.
+template <typename OutT>
+__global__ void plan_scatter_kernel(SignArgs A) {
+    __shared__ unsigned cnt[kChunk];
+    __shared__ unsigned base[kChunk];
+    unsigned* cursor = A.hist + kChunk;
+    const int64_t per = (A.n_sets + gridDim.x - 1) / gridDim.x;
+    const int64_t s_begin = (int64_t)blockIdx.x * per;
+    const int64_t s_end = min(A.n_sets, s_begin + per);
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t s = s_begin + threadIdx.x; s < s_end; s += blockDim.x) {
+        const int64_t n = A.indptr[s + 1] - A.indptr[s];
+        if (n <= 0) continue;
+        const int64_t nch = (n + kChunk - 1) / kChunk;
+        atomicAdd(&cnt[(int)(n - (nch - 1) * kChunk) - 1], 1u);
+        if (nch > 1) atomicAdd(&cnt[kChunk - 1], (unsigned)(nch - 1));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+        base[i] = cnt[i] ? atomicAdd(&cursor[i], cnt[i]) : 0u;
+        cnt[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t s = s_begin + threadIdx.x; s < s_end; s += blockDim.x) {
+        const int64_t lo = A.indptr[s];
+        const int64_t n = A.indptr[s + 1] - lo;
+        if (n <= 0) continue;
+        const int64_t nch = (n + kChunk - 1) / kChunk;
+        const long long merge = nch > 1 ? 1 : 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            const int size = (int)((c + 1 < nch) ? kChunk : n - c * kChunk);
+            const unsigned pos = base[size - 1] + atomicAdd(&cnt[size - 1], 1u);
+            VSet v;
+            v.f0 = lo + c * kChunk;
+            v.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
+            A.vsets[pos] = v;
+        }
+    }
+    // rows of long sets start at UINT_MAX (their chunks merge with atomicMin)
+    const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
+    OutT* out = reinterpret_cast<OutT*>(A.out);
+    for (unsigned long long e = blockIdx.x; e < n_big; e += gridDim.x) {
+        OutT* row = out + A.big[e] * (int64_t)A.n_hash;
+        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x) row[i] = (OutT)(~0u);
     }
 }
 
 // ----------------------------------------------------------------------------
-// Main kernel
+// Walks
 // ----------------------------------------------------------------------------
 
-// Argmin recovery: x = (h - B_i) * A_i^{-1} mod p, from a staged epilogue table entry.
+// Argmin recovery: x = (h - B_i) * A_i^{-1} mod p.
 __device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, uint32_t p) {
     uint32_t d = h - v.B;
     d = __viaddmin_u32(d, p, d);  // d in [0,p)
     return reduce_once(shoup_lazy(v.inv, v.invp, d, p), p);
-}
-
-__device__ __forceinline__ uint32_t invert_lane(const SignArgs& A, int64_t i, uint32_t h) {
-    const InvTab v = A.inv[i];
-    return invert_entry(v, h, A.p);
 }
 
 __device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) { atomicMin(p, v); }
@@ -200,7 +273,7 @@ __device__ __forceinline__ void store4(long long* dst, uint32_t a, uint32_t b, u
 // h_{k+2} are both derived from h_k (steps dh and 2dh mod p), which halves the
 // dependent chain and keeps the ALU pipe (VIADDMNMX + VIMNMX3) saturated
 // (tools/visit_probe.cu: 41.9 visits/clk/SM vs 36.3 for the plain chain).
-// FIRST: the item's first round initialises best instead of folding into it.
+// FIRST: the group's first round initialises best instead of folding into it.
 template <int K, bool FIRST>
 __device__ __forceinline__ void walk2_iter(uint32_t (&best)[K], uint32_t ha, uint32_t da,
                                            uint32_t hb, uint32_t db, uint32_t p) {
@@ -222,19 +295,13 @@ __device__ __forceinline__ void walk2_iter(uint32_t (&best)[K], uint32_t ha, uin
     }
 }
 
-template <int K, bool FIRST>
+template <int K>
 __device__ __forceinline__ void walk1_iter(uint32_t (&best)[K], uint32_t ha, uint32_t da, uint32_t p) {
     const uint32_t da2 = reduce_once(da + da, p);
 #pragma unroll
     for (int k = 0; k < K; k += 2) {
-        const uint32_t ga = reduce_once(ha + da, p);
-        if (FIRST) {
-            best[k] = ha;
-            best[k + 1] = ga;
-        } else {
-            best[k] = min(best[k], ha);
-            best[k + 1] = min(best[k + 1], ga);
-        }
+        best[k] = min(best[k], ha);
+        best[k + 1] = min(best[k + 1], reduce_once(ha + da, p));
         if (k + 2 < K) ha = reduce_once(ha + da2, p);
     }
 }
@@ -257,7 +324,7 @@ __device__ __forceinline__ void walk2_random(uint32_t (&best)[K], const uint32_t
     }
 }
 
-template <int K, bool NARROW, bool FIRST>
+template <int K, bool NARROW>
 __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t (&cA)[K],
                                              const uint32_t (&cAp)[K], const uint32_t (&cB)[K],
                                              uint32_t xa, uint32_t p) {
@@ -265,93 +332,8 @@ __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t
     for (int k = 0; k < K; ++k) {
         uint32_t ra = NARROW ? mul_add_mod_narrow(cA[k], cAp[k], cB[k], xa, p)
                              : mul_add_mod(cA[k], cAp[k], cB[k], xa, p);
-        best[k] = FIRST ? ra : min(best[k], ra);
+        best[k] = min(best[k], ra);
     }
-}
-
-// ---- asynchronous global->shared copies (cp.async / LDGSTS) ----
-__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(long long* dst, const int64_t* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int NPEND>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
-
-// Per-warp shared memory: a two-slot ring of item ids (the slot of the item being
-// processed doubles as the slice-combine scratch once its rounds are done) and the
-// CSR bounds of the current and next batch.
-struct WarpSmem {
-    uint32_t ids[2][kChunk];
-    long long ip[2][kBatch + 2];
-};
-
-// Warp-uniform description of one work item.
-struct ItemDesc {
-    int64_t f0;    // first feature (index into ids)
-    int64_t s;     // set index
-    int32_t n;     // features in the item (0: skip / no item)
-    int32_t sb;    // lane pass
-    int32_t merge; // long set: merge with atomicMin, finalize later
-};
-
-__device__ __forceinline__ ItemDesc make_item(int64_t s, int sb, int64_t f0, int64_t hi, bool long_set) {
-    ItemDesc d;
-    const int64_t n = hi - f0;
-    d.f0 = f0;
-    d.s = s;
-    d.sb = sb;
-    d.n = n <= 0 ? 0 : (n > kChunk ? kChunk : (int32_t)n);
-    d.merge = long_set;
-    return d;
-}
-
-__device__ __forceinline__ ItemDesc no_item() {
-    ItemDesc d;
-    d.f0 = 0; d.s = 0; d.n = 0; d.sb = 0; d.merge = 0;
-    return d;
-}
-
-// Stage an item's ids into a ring slot: lane-strided 4-byte async copies.
-__device__ __forceinline__ void stage_ids(const SignArgs& A, const ItemDesc& d, uint32_t* slot, int lane) {
-    const uint32_t* src = A.ids + d.f0;
-    for (int o = lane; o < d.n; o += 32) cp_async4(slot + o, src + o);
-}
-
-// Batch b covers primary items [b*kBatch, b*kBatch + kBatch).  Their sets span
-// [s_first, s_first + cnt); stage indptr[s_first .. s_first + cnt] (cnt+1 values).
-__device__ __forceinline__ int64_t batch_first_set(const SignArgs& A, unsigned long long b) {
-    const unsigned long long item = b * kBatch;
-    return A.n_super == 1 ? (int64_t)item : (int64_t)(item / (unsigned)A.n_super);
-}
-
-__device__ __forceinline__ void stage_bounds(const SignArgs& A, unsigned long long b, unsigned long long n_batches,
-                                             long long* ip, int lane) {
-    if (b >= n_batches) return;
-    const int64_t s0 = batch_first_set(A, b);
-    const unsigned long long last_item = min(b * kBatch + kBatch, (unsigned long long)A.n_sets * A.n_super) - 1;
-    const int64_t s1 = A.n_super == 1 ? (int64_t)last_item : (int64_t)(last_item / (unsigned)A.n_super);
-    const int cnt = (int)(s1 - s0) + 2;  // indptr values needed
-    if (lane < cnt) cp_async8(ip + lane, A.indptr + s0 + lane);
-}
-
-__device__ __forceinline__ ItemDesc batch_item(const SignArgs& A, unsigned long long b, int j, const long long* ip) {
-    const unsigned long long item = b * kBatch + j;
-    int64_t s;
-    int sb = 0;
-    if (A.n_super == 1) {
-        s = (int64_t)item;
-    } else {
-        s = (int64_t)(item / (unsigned)A.n_super);
-        sb = (int)(item - (unsigned long long)s * A.n_super);
-    }
-    const int64_t k = s - batch_first_set(A, b);
-    const int64_t lo = ip[k], hi = ip[k + 1];
-    return make_item(s, sb, lo, hi, (hi - lo) > kChunk);
 }
 
 // Per-thread hashing state: iterative start constants, or the K random-family lane constants.
@@ -373,96 +355,71 @@ __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, I
     }
 }
 
-template <int K, bool ITER, bool NARROW, bool FIRST>
+template <int K, bool ITER, bool NARROW>
 __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
         const uint32_t ha = mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
-        walk1_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), p);
+        walk1_iter<K>(best, ha, reduce_once(xa + bpar, p), p);
     } else {
-        walk1_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, p);
+        walk1_random<K, NARROW>(best, ls.cA, ls.cAp, ls.cB, xa, p);
     }
 }
 
-template <int K, bool ITER, bool NARROW, bool FIRST>
-__device__ __forceinline__ void last_round(uint32_t (&best)[K], const LaneState<K, ITER>& ls, bool single,
-                                           uint32_t xa, uint32_t xb, uint32_t p, uint32_t bpar, uint32_t& maxid) {
-    if (single) {
-        maxid = max(maxid, xa);
-        round1<K, ITER, NARROW, FIRST>(best, ls, xa, p, bpar);
-    } else {
-        maxid = __vimax3_u32(maxid, xa, xb);
-        round2<K, ITER, NARROW, FIRST>(best, ls, xa, xb, p, bpar);
-    }
+// ----------------------------------------------------------------------------
+// Main kernel
+// ----------------------------------------------------------------------------
+
+// The slice's virtual set for work item `it` (group = it / n_super), or an
+// invalid entry (meta = -1) past the end.
+__device__ __forceinline__ VSet load_vset(const SignArgs& A, unsigned long long it, unsigned long long n_vsets,
+                                          int f) {
+    VSet v;
+    v.f0 = 0;
+    v.meta = -1;
+    const unsigned long long group = A.n_super == 1 ? it : it / (unsigned)A.n_super;
+    const unsigned long long k = (group << A.log2F) + f;
+    if (k < n_vsets) v = A.vsets[k];
+    return v;
 }
 
-// Stage KP of each thread's minima (lanes k0..k0+KP) into the warp scratch `red`
-// with a 16-byte-chunk XOR swizzle (conflict-free writes and reads).
-template <int K, int K0>
-__device__ __forceinline__ void store_slice(const uint32_t (&best)[K], uint32_t* red, int lane) {
-    constexpr int KP = K < 32 ? K : 32;
-    constexpr int NQ = KP / 4;
+// Dump a thread's K minima into its (swizzled) smem row, then invert and store them
+// four lanes at a time.  EPI_SMEM: epilogue table staged in shared memory.
+template <int K>
+__device__ __forceinline__ void dump_best(const uint32_t (&best)[K], uint32_t* row, int lane) {
+    constexpr int NQ = K / 4;
     constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int qq = q ^ (lane & SWZ);
-        *reinterpret_cast<uint4*>(red + lane * KP + qq * 4) =
-            make_uint4(best[K0 + 4 * q], best[K0 + 4 * q + 1], best[K0 + 4 * q + 2], best[K0 + 4 * q + 3]);
-    }
+    for (int q = 0; q < NQ; ++q)
+        *reinterpret_cast<uint4*>(row + ((q ^ (lane & SWZ)) << 2)) =
+            make_uint4(best[4 * q], best[4 * q + 1], best[4 * q + 2], best[4 * q + 3]);
 }
 
-// Combine the F slices for lanes k0..k0+KP of every lane group, recover the argmin
-// ids and store them (or atomicMin the min hashes of a long set).
-template <int K, typename OutT>
-__device__ __forceinline__ void combine_emit(const SignArgs& A, const ItemDesc& cur, int k0, const uint32_t* red,
-                                             const InvTab* epi_s, bool epi_smem, int lane, int F) {
-    constexpr int KP = K < 32 ? K : 32;
-    constexpr int NQ = KP / 4;
+template <int K, typename OutT, bool EPI_SMEM>
+__device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
+                                           bool merge, int64_t i0, const InvTab* epi_s) {
+    constexpr int NQ = K / 4;
     constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
     const uint32_t p = A.p;
     const int32_t N = A.n_hash;
-    const int G = 32 / F;
-    const int n_chunks = G * KP / 4;
-    const bool vec_ok = ((N & 3) == 0);
-    OutT* row = reinterpret_cast<OutT*>(A.out) + cur.s * (int64_t)N;
-    for (int c = lane; c < n_chunks; c += 32) {
-        const int l4 = 4 * c;
-        const int gg = l4 / KP;
-        const int kk = l4 - gg * KP;
-        const int qk = kk / 4;
-        const uint32_t* src = red + gg * F * KP;
-        uint4 m = *reinterpret_cast<const uint4*>(src + (qk ^ ((gg * F) & SWZ)) * 4);
-        int ff = 1;
-        for (; ff + 1 < F; ff += 2) {
-            const int w0 = gg * F + ff, w1 = w0 + 1;
-            const uint4 v0 = *reinterpret_cast<const uint4*>(src + ff * KP + (qk ^ (w0 & SWZ)) * 4);
-            const uint4 v1 = *reinterpret_cast<const uint4*>(src + (ff + 1) * KP + (qk ^ (w1 & SWZ)) * 4);
-            m.x = __vimin3_u32(m.x, v0.x, v1.x); m.y = __vimin3_u32(m.y, v0.y, v1.y);
-            m.z = __vimin3_u32(m.z, v0.z, v1.z); m.w = __vimin3_u32(m.w, v0.w, v1.w);
-        }
-        if (ff < F) {
-            const int w0 = gg * F + ff;
-            const uint4 v0 = *reinterpret_cast<const uint4*>(src + ff * KP + (qk ^ (w0 & SWZ)) * 4);
-            m.x = min(m.x, v0.x); m.y = min(m.y, v0.y); m.z = min(m.z, v0.z); m.w = min(m.w, v0.w);
-        }
-        const int64_t i = (int64_t)cur.sb * A.L + (int64_t)gg * K + k0 + kk;
-        if (cur.merge) {
-            if (i + 0 < N) atomic_min_out(row + i + 0, m.x);
-            if (i + 1 < N) atomic_min_out(row + i + 1, m.y);
-            if (i + 2 < N) atomic_min_out(row + i + 2, m.z);
-            if (i + 3 < N) atomic_min_out(row + i + 3, m.w);
+    const bool vec_ok = (N & 3) == 0;
+    OutT* row = reinterpret_cast<OutT*>(A.out) + set * (int64_t)N;
+#pragma unroll 1
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t i = i0 + 4 * q;
+        if (i >= N) break;
+        const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
+        const uint32_t h[4] = {m.x, m.y, m.z, m.w};
+        if (merge) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (i + e < N) atomic_min_out(row + i + e, h[e]);
             continue;
         }
         uint32_t x[4];
-        const uint32_t h[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            InvTab t;
-            if (epi_smem) {
-                t = epi_s[i + e];
-            } else {
-                t = A.inv[min(i + e, (int64_t)A.n_tot - 1)];
-            }
+            const InvTab t = EPI_SMEM ? epi_s[i + e] : A.inv[min(i + e, A.n_tot - 1)];
             x[e] = invert_entry(t, h[e], p);
         }
         if (vec_ok && i + 3 < N) {
@@ -475,149 +432,19 @@ __device__ __forceinline__ void combine_emit(const SignArgs& A, const ItemDesc& 
     }
 }
 
-// One work item whose ids are staged in `slot`: rounds (the first initialises the
-// minima; a last round with <= F features walks one feature per slice), then the
-// slice combine in `slot` (the ids are consumed by then) and the epilogue.
-template <int K, bool ITER, bool NARROW, typename OutT>
-__device__ __forceinline__ void run_item(const SignArgs& A, const ItemDesc& cur, uint32_t* slot,
-                                         LaneState<K, ITER>& ls, int& cur_sb, uint32_t& maxid,
-                                         const InvTab* epi_s, bool epi_smem, int lane, int g, int f, int F) {
-    const uint32_t p = A.p;
-    const uint32_t bpar = A.b;
-    if (cur.sb != cur_sb) {  // lane constants change only with the lane pass
-        const int64_t i0 = (int64_t)cur.sb * A.L + (int64_t)g * K;
-        if constexpr (ITER) {
-            const LaneTab t = A.tab[i0];
-            ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
-        } else {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const LaneTab t = A.tab[i0 + k];
-                ls.cA[k] = t.A; ls.cAp[k] = t.Ap; ls.cB[k] = t.B;
-            }
-        }
-        cur_sb = cur.sb;
-    }
-
-    // rounds of 2F features; F is a power of two
-    uint32_t best[K];
-    const int n = cur.n;
-    const int last = n - 1;
-    const int sh = A.log2F + 1;
-    const int rounds = (n + (1 << sh) - 1) >> sh;
-    const bool single = rounds > 1 && (n - ((rounds - 1) << sh)) <= F;
-    {
-        const uint32_t xa = slot[min(f, last)], xb = slot[min(F + f, last)];
-        maxid = __vimax3_u32(maxid, xa, xb);
-        round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
-    }
-    // middle rounds are always full: no clamping, no branches
-    const int full_end = (rounds - 1) << sh;
-    int o = 2 * F + f;
-#pragma unroll 1
-    for (; o < full_end; o += 2 * F) {
-        const uint32_t xa = slot[o], xb = slot[o + F];
-        maxid = __vimax3_u32(maxid, xa, xb);
-        round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
-    }
-    if (rounds > 1) {
-        const uint32_t xa = slot[min(o, last)], xb = slot[min(o + F, last)];
-        if (single) {
-            maxid = max(maxid, xa);
-            round1<K, ITER, NARROW, false>(best, ls, xa, p, bpar);
-        } else {
-            maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
-        }
-    }
-    __syncwarp();  // every lane is done reading ids before the slot becomes scratch
-    constexpr int KP = K < 32 ? K : 32;
-    static_assert(K / KP <= 2, "at most two combine passes");
-#pragma unroll 1
-    for (int h = 0; h < K / KP; ++h) {
-        if (h == 0) store_slice<K, 0>(best, slot, lane);
-        else store_slice<K, (K > KP ? KP : 0)>(best, slot, lane);
-        __syncwarp();
-        combine_emit<K, OutT>(A, cur, h * KP, slot, epi_s, epi_smem, lane, F);
-        __syncwarp();
-    }
-}
-
-// Where the next work item comes from: first the extra chunks of long sets (one
-// atomic each), then batches of kBatch consecutive primary items whose CSR bounds
-// are staged in shared memory one batch ahead.
-struct ItemSource {
-    int phase;                   // 0 extras, 1 batches, 2 done
-    int j, slot_b, in_batch;
-    unsigned long long b_cur, b_nxt, b_nxt2;
-};
-
-__device__ __forceinline__ ItemDesc next_item(const SignArgs& A, ItemSource& src, WarpSmem* ws, int lane,
-                                              unsigned long long n_extra, unsigned long long n_primary,
-                                              unsigned long long n_batches) {
-    if (src.phase == 0) {
-        unsigned long long e = 0;
-        if (lane == 0) e = atomicAdd(&A.sched->next_extra, 1ull);
-        e = __shfl_sync(0xffffffffu, e, 0);
-        if (e < n_extra) {
-            const Extra x = A.extra[e];
-            const int64_t lo = A.indptr[x.set], hi = A.indptr[x.set + 1];
-            return make_item(x.set, x.sb, lo + (int64_t)x.chunk * kChunk, hi, true);
-        }
-        // enter the batch phase: claim three batches, stage two batches of bounds
-        src.phase = 1;
-        if (lane == 0) {
-            src.b_cur = atomicAdd(&A.sched->next, 1ull);
-            src.b_nxt = atomicAdd(&A.sched->next, 1ull);
-            src.b_nxt2 = atomicAdd(&A.sched->next, 1ull);
-        }
-        src.b_cur = __shfl_sync(0xffffffffu, src.b_cur, 0);
-        src.b_nxt = __shfl_sync(0xffffffffu, src.b_nxt, 0);
-        if (src.b_cur >= n_batches) {
-            src.phase = 2;
-            return no_item();
-        }
-        src.slot_b = 0;
-        stage_bounds(A, src.b_cur, n_batches, ws->ip[0], lane);
-        stage_bounds(A, src.b_nxt, n_batches, ws->ip[1], lane);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-        src.j = 0;
-        src.in_batch = (int)min((unsigned long long)kBatch, n_primary - src.b_cur * kBatch);
-        return batch_item(A, src.b_cur, 0, ws->ip[0]);
-    }
-    if (src.phase == 2) return no_item();
-    if (++src.j == src.in_batch) {
-        src.j = 0;
-        src.b_cur = src.b_nxt;
-        src.slot_b ^= 1;
-        src.b_nxt = __shfl_sync(0xffffffffu, src.b_nxt2, 0);
-        if (src.b_cur >= n_batches) {
-            src.phase = 2;
-            return no_item();
-        }
-        // The new current batch's bounds were staged a batch ago; make sure they landed.
-        cp_async_wait<0>();
-        __syncwarp();
-        stage_bounds(A, src.b_nxt, n_batches, ws->ip[src.slot_b ^ 1], lane);
-        if (lane == 0) src.b_nxt2 = atomicAdd(&A.sched->next, 1ull);
-        src.in_batch = (int)min((unsigned long long)kBatch, n_primary - src.b_cur * kBatch);
-    }
-    return batch_item(A, src.b_cur, src.j, ws->ip[src.slot_b]);
-}
-
 template <int K, bool ITER, bool NARROW, typename OutT>
 __global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw) + warp;
-    InvTab* epi_s = reinterpret_cast<InvTab*>(reinterpret_cast<WarpSmem*>(smem_raw) + kBlock / 32);
+    uint32_t* dump_row = reinterpret_cast<uint32_t*>(smem_raw) + (warp * 32 + lane) * K;
+    InvTab* epi_s = reinterpret_cast<InvTab*>(reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K);
 
     const int F = A.F;
     const int g = lane >> A.log2F;
     const int f = lane & (F - 1);
+    const uint32_t p = A.p;
+    const uint32_t bpar = A.b;
 
     // Stage the epilogue table (B_i, A_i^{-1}, companion) in shared memory.
     const bool epi_smem = A.n_tot <= kEpiSmemLanes;
@@ -626,56 +453,128 @@ __global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) 
         __syncthreads();
     }
 
+    const unsigned long long n_vsets = *((volatile unsigned long long*)&A.sched->n_vsets);
+    const unsigned long long n_groups = (n_vsets + F - 1) >> A.log2F;
+    const unsigned long long n_items = n_groups * (unsigned)A.n_super;
+
+    // Work items flow through a 3-deep pipeline: the id of the item after next is
+    // claimed while the current one runs, the next item's set entry is loaded, and
+    // the last round of the current item prefetches the next item's first features.
+    unsigned long long it = 0, itn = 0, itnn = 0;
+    if (lane == 0) {
+        it = atomicAdd(&A.sched->next, 1ull);
+        itn = atomicAdd(&A.sched->next, 1ull);
+    }
+    it = __shfl_sync(0xffffffffu, it, 0);
+    itn = __shfl_sync(0xffffffffu, itn, 0);
+    VSet ec = load_vset(A, it, n_vsets, f);
+    VSet en = load_vset(A, itn, n_vsets, f);
+
     LaneState<K, ITER> ls;
     int cur_sb = -1;
     uint32_t maxid = 0;
 
-    const unsigned long long n_extra = *((volatile unsigned long long*)&A.sched->n_extra);
-    const unsigned long long n_primary = (unsigned long long)A.n_sets * A.n_super;
-    const unsigned long long n_batches = (n_primary + kBatch - 1) / kBatch;
-    ItemSource src;
-    src.phase = 0;
-    src.j = src.slot_b = src.in_batch = 0;
-    src.b_cur = src.b_nxt = src.b_nxt2 = 0;
-
-    // Item pipeline: the next item's ids are staged (cp.async) while the current runs.
-    int slot = 0;
-    ItemDesc cur = next_item(A, src, ws, lane, n_extra, n_primary, n_batches);
-    stage_ids(A, cur, ws->ids[0], lane);
-    cp_async_commit();
-    while (src.phase != 2 || cur.n > 0) {
-        const ItemDesc nxt = next_item(A, src, ws, lane, n_extra, n_primary, n_batches);
-        stage_ids(A, nxt, ws->ids[slot ^ 1], lane);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        if (cur.n > 0)
-            run_item<K, ITER, NARROW, OutT>(A, cur, ws->ids[slot], ls, cur_sb, maxid, epi_s, epi_smem, lane, g, f, F);
-        cur = nxt;
-        slot ^= 1;
+    uint32_t xa = 0, xb = 0;
+    {
+        const int n = ec.meta >= 0 ? (int)(ec.meta & 2047) + 1 : 1;
+        const uint32_t* base = A.ids + (ec.meta >= 0 ? ec.f0 : 0);
+        xa = __ldg(base);
+        xb = __ldg(base + min(1, n - 1));
     }
-    cp_async_wait<0>();
-    if (__any_sync(0xffffffffu, maxid >= A.p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
+
+    while (it < n_items) {
+        if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
+        int sb = 0;
+        if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
+        if (sb != cur_sb) {  // lane constants change only with the lane pass
+            const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+            if constexpr (ITER) {
+                const LaneTab t = A.tab[i0];
+                ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const LaneTab t = A.tab[i0 + k];
+                    ls.cA[k] = t.A; ls.cAp[k] = t.Ap; ls.cB[k] = t.B;
+                }
+            }
+            cur_sb = sb;
+        }
+
+        const bool valid = ec.meta >= 0;
+        const int n = valid ? (int)(ec.meta & 2047) + 1 : 1;
+        const int last = n - 1;
+        const uint32_t* base = A.ids + (valid ? ec.f0 : 0);
+        // the group's first set is its largest (descending sort)
+        const int n_max = __shfl_sync(0xffffffffu, n, 0);
+        const int rounds = (n_max + 1) >> 1;
+        const bool odd = n_max & 1;
+        // next item's first features (cross-item prefetch)
+        const bool nvalid = en.meta >= 0;
+        const uint32_t* nbase = A.ids + (nvalid ? en.f0 : 0);
+        const int nlast = nvalid ? (int)(en.meta & 2047) : 0;
+
+        uint32_t best[K];
+        uint32_t pa, pb;
+        if (rounds > 1) {
+            pa = __ldg(base + min(2, last));
+            pb = __ldg(base + min(3, last));
+        } else {
+            pa = __ldg(nbase);
+            pb = __ldg(nbase + min(1, nlast));
+        }
+        maxid = __vimax3_u32(maxid, xa, xb);
+        round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
+        xa = pa; xb = pb;
+        int o = 4;
+#pragma unroll 1
+        for (int r = 1; r + 1 < rounds; ++r, o += 2) {
+            pa = __ldg(base + min(o, last));
+            pb = __ldg(base + min(o + 1, last));
+            maxid = __vimax3_u32(maxid, xa, xb);
+            round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+            xa = pa; xb = pb;
+        }
+        if (rounds > 1) {
+            pa = __ldg(nbase);
+            pb = __ldg(nbase + min(1, nlast));
+            if (odd) {
+                maxid = max(maxid, xa);
+                round1<K, ITER, NARROW>(best, ls, xa, p, bpar);
+            } else {
+                maxid = __vimax3_u32(maxid, xa, xb);
+                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+            }
+            xa = pa; xb = pb;
+        }
+
+        if (valid) {
+            const int64_t set = ec.meta >> 12;
+            const bool merge = (ec.meta >> 11) & 1;
+            const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+            dump_best<K>(best, dump_row, lane);
+            if (epi_smem) emit_lanes<K, OutT, true>(A, dump_row, lane, set, merge, i0, epi_s);
+            else emit_lanes<K, OutT, false>(A, dump_row, lane, set, merge, i0, epi_s);
+        }
+
+        it = itn;
+        ec = en;
+        itn = __shfl_sync(0xffffffffu, itnn, 0);
+        en = load_vset(A, itn, n_vsets, f);
+    }
+    if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
 }
 
-// Long sets: rows hold min hash values after the main kernel; invert in place.
+// Long sets: rows hold min hash values after the main kernel; invert in place
+// (one block per row, threads over hash lanes).
 template <typename OutT>
 __global__ void finalize_kernel(SignArgs A) {
     const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
-    const unsigned long long total = n_big * (unsigned long long)A.L;
     OutT* out = reinterpret_cast<OutT*>(A.out);
-    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long e = t / (unsigned)A.L;
-        const int l = (int)(t - e * A.L);
-        const int64_t key = A.big[e];
-        const int64_t s = key / A.n_super;
-        const int sb = (int)(key - s * A.n_super);
-        const int64_t i = (int64_t)sb * A.L + l;
-        if (i < A.n_hash) {
-            OutT* cell = out + s * (int64_t)A.n_hash + i;
-            *cell = (OutT)invert_lane(A, i, (uint32_t)*cell);
-        }
+    for (unsigned long long e = blockIdx.x; e < n_big; e += gridDim.x) {
+        OutT* row = out + A.big[e] * (int64_t)A.n_hash;
+        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x)
+            row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
     }
 }
 
@@ -767,6 +666,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (n_sets > 0 && (indptr == nullptr || out == nullptr))
         return set_error(MHB_ERR_INVALID, "null indptr/out");
     if (nnz > 0 && ids == nullptr) return set_error(MHB_ERR_INVALID, "null ids");
+    if (n_sets >= (1ll << 51)) return set_error(MHB_ERR_INVALID, "too many sets");
 
     const WorkspaceLayout wl = workspace_layout(n_sets, nnz, n_hash);
     if (workspace == nullptr || workspace_bytes < wl.total)
@@ -787,19 +687,22 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.log2F = geo.log2F;
     A.n_super = geo.n_super;
     A.L = geo.L;
+    A.K = geo.K;
     A.n_tot = geo.n_tot;
     A.kind = kind;
     A.tab = reinterpret_cast<LaneTab*>(ws + wl.tab);
     A.inv = reinterpret_cast<InvTab*>(ws + wl.inv);
     A.sched = reinterpret_cast<Sched*>(ws + wl.sched);
+    A.hist = reinterpret_cast<unsigned*>(ws + wl.hist);
     A.big = reinterpret_cast<int64_t*>(ws + wl.big);
-    A.extra = reinterpret_cast<Extra*>(ws + wl.extra);
+    A.vsets = reinterpret_cast<VSet*>(ws + wl.vsets);
     A.status = status;
     A.out = out;
     A.ra = ra;
     A.rb = rb;
 
-    int rc = cuda_check(cudaMemsetAsync(A.sched, 0, sizeof(Sched), st), "memset sched");
+    // sched and hist are contiguous at the start of the workspace
+    int rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
     if (rc) return rc;
     if (status) {
         rc = cuda_check(cudaMemsetAsync(status, 0, sizeof(int32_t), st), "memset status");
@@ -814,24 +717,33 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     {
         int64_t work = n_sets > geo.n_tot ? n_sets : geo.n_tot;
         int64_t blocks = (work + 255) / 256;
-        int64_t cap = (int64_t)dev.sms * 8;
+        int64_t cap = (int64_t)dev.sms * 4;
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
         if (out_dtype == MHB_OUT_I64)
-            setup_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(A);
+            plan_count_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(A);
         else
-            setup_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(A);
-        rc = cuda_check(cudaGetLastError(), "setup_kernel launch");
+            plan_count_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(A);
+        plan_scan_kernel<<<1, kChunk, 0, st>>>(A);
+        int64_t sblocks = (n_sets + 1023) / 1024;
+        if (sblocks > (int64_t)dev.sms * 4) sblocks = (int64_t)dev.sms * 4;
+        if (sblocks < 1) sblocks = 1;
+        if (out_dtype == MHB_OUT_I64)
+            plan_scatter_kernel<long long><<<(unsigned)sblocks, 256, 0, st>>>(A);
+        else
+            plan_scatter_kernel<uint32_t><<<(unsigned)sblocks, 256, 0, st>>>(A);
+        rc = cuda_check(cudaGetLastError(), "plan kernels launch");
         if (rc) return rc;
     }
 
     const bool narrow = (3ull * prime) < (1ull << 32);
     SignKernelFn fn = select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
-    const size_t smem = (size_t)(kBlock / 32) * sizeof(WarpSmem) +
+    const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
     const int occ = blocks_per_sm(fn, smem, dev);
-    const int64_t items_ub = (n_sets * geo.n_super + kBatch - 1) / kBatch + (nnz / kChunk) * geo.n_super;
+    const int64_t max_vsets = n_sets + nnz / kChunk;
+    const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
     int64_t blocks = (items_ub + (kBlock / 32) - 1) / (kBlock / 32);
     const int64_t cap = (int64_t)occ * dev.sms;
     if (blocks > cap) blocks = cap;
@@ -848,7 +760,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (rc) return rc;
 
     {
-        int64_t fb = (int64_t)dev.sms * 2;
+        // one block per long-set row (latency-bound: a wide grid hides the row loads)
+        int64_t fb = nnz / (kChunk + 1);
+        if (fb > 65535) fb = 65535;
+        if (fb < (int64_t)dev.sms) fb = dev.sms;
         if (out_dtype == MHB_OUT_I64)
             finalize_kernel<long long><<<(unsigned)fb, 256, 0, st>>>(A);
         else

@@ -9,10 +9,9 @@ namespace mhb {
 
 enum { KIND_ITERATIVE = 0, KIND_RANDOM = 1 };
 
-constexpr int kChunk = 1024;  // features per work item; longer sets are split
-constexpr int kBlock = 256;   // threads per CTA of the main kernel
+constexpr int kChunk = 1024;         // max features per virtual set; longer sets are split
+constexpr int kBlock = 256;          // threads per CTA of the main kernel
 constexpr int kEpiSmemLanes = 2048;  // epilogue table staged in shared memory up to this many lanes
-constexpr int kBatch = 8;     // consecutive sets a warp claims per atomic (must be <= 32)
 
 // Per hash lane i: h_i(x) = (A*x + B) mod p, Ap = floor(A*2^32/p) (Shoup companion).
 struct LaneTab {
@@ -23,23 +22,24 @@ struct LaneTab {
 struct InvTab {
     uint32_t B, inv, invp, pad;
 };
-// One extra chunk (index >= 1) of a set longer than kChunk.
-struct Extra {
-    int64_t set;
-    int32_t sb;
-    int32_t chunk;
+// A virtual set: up to kChunk consecutive features of one set.
+//   f0   : index of its first feature in ids
+//   meta : set << 12 | merge << 11 | (n - 1); merge = the set has several chunks
+struct VSet {
+    long long f0;
+    long long meta;
 };
 struct Sched {
-    unsigned long long next;     // dynamic counter over batches of primary items
-    unsigned long long n_extra;  // extra chunks planned
-    unsigned long long n_big;    // (set, lane pass) pairs in merge mode
-    unsigned long long next_extra;  // dynamic counter over extra chunks
+    unsigned long long next;     // dynamic counter over work items (group, lane pass)
+    unsigned long long n_vsets;  // virtual sets planned
+    unsigned long long n_big;    // sets in merge mode (finalize list)
+    unsigned long long pad;
 };
 
 struct Geometry {
     int K;         // hash lanes per thread
     int G;         // lane groups per warp
-    int F;         // feature slices per warp (G*F = 32)
+    int F;         // sets per warp group (one per slice; G*F = 32)
     int log2F;
     int n_super;   // lane passes per set (n_hash > 32*K)
     int L;         // lanes per pass = G*K
@@ -47,7 +47,7 @@ struct Geometry {
 };
 
 struct WorkspaceLayout {
-    size_t sched, tab, inv, big, extra, total;
+    size_t sched, hist, tab, inv, big, vsets, total;
 };
 
 struct SignArgs {
@@ -58,14 +58,15 @@ struct SignArgs {
     uint32_t b;
     uint64_t ia;
     int32_t n_hash;
-    int32_t F, log2F, n_super, L;
+    int32_t F, log2F, n_super, L, K;
     int64_t n_tot;
     int32_t kind;
     LaneTab* tab;
     InvTab* inv;
     Sched* sched;
+    unsigned* hist;   // [2*kChunk]: virtual-set size histogram, then scatter cursors
     int64_t* big;
-    Extra* extra;
+    VSet* vsets;
     int32_t* status;
     void* out;
     const uint32_t* ra;
