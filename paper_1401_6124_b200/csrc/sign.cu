@@ -255,9 +255,14 @@ __device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, ui
     return reduce_once(shoup_lazy(v.inv, v.invp, d, p), p);
 }
 
-__device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) { atomicMin(p, v); }
+// Long-set chunks merge with a fire-and-forget `red.global.min`.  Written as PTX:
+// the C++ atomicMin in this loop makes ptxas move p out of the uniform datapath
+// (every VIADDMNMX then reads -p from a vector register: -10% visit rate).
+__device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) {
+    asm volatile("red.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void atomic_min_out(long long* p, uint32_t v) {
-    atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    asm volatile("red.global.min.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");
 }
 
 __device__ __forceinline__ void store4(uint32_t* dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -432,8 +437,11 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
     }
 }
 
+// p and b arrive as separate scalar parameters so ptxas keeps them in uniform
+// registers: VIADDMNMX t, -UR, t reads one vector register instead of two
+// (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
 template <int K, bool ITER, bool NARROW, typename OutT>
-__global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) {
+__global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -443,8 +451,6 @@ __global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) 
     const int F = A.F;
     const int g = lane >> A.log2F;
     const int f = lane & (F - 1);
-    const uint32_t p = A.p;
-    const uint32_t bpar = A.b;
 
     // Stage the epilogue table (B_i, A_i^{-1}, companion) in shared memory.
     const bool epi_smem = A.n_tot <= kEpiSmemLanes;
@@ -514,30 +520,43 @@ __global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A) 
         const uint32_t* nbase = A.ids + (nvalid ? en.f0 : 0);
         const int nlast = nvalid ? (int)(en.meta & 2047) : 0;
 
+        // Rounds of two features.  Ids are prefetched two rounds ahead inside the
+        // item; the item's second-to-last round fetches the next item's first round.
         uint32_t best[K];
-        uint32_t pa, pb;
-        if (rounds > 1) {
-            pa = __ldg(base + min(2, last));
-            pb = __ldg(base + min(3, last));
-        } else {
-            pa = __ldg(nbase);
-            pb = __ldg(nbase + min(1, nlast));
-        }
-        maxid = __vimax3_u32(maxid, xa, xb);
-        round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
-        xa = pa; xb = pb;
-        int o = 4;
-#pragma unroll 1
-        for (int r = 1; r + 1 < rounds; ++r, o += 2) {
-            pa = __ldg(base + min(o, last));
-            pb = __ldg(base + min(o + 1, last));
+        if (rounds == 1) {
+            const uint32_t pa = __ldg(nbase), pb = __ldg(nbase + min(1, nlast));
             maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+            round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
             xa = pa; xb = pb;
-        }
-        if (rounds > 1) {
-            pa = __ldg(nbase);
-            pb = __ldg(nbase + min(1, nlast));
+        } else {
+            uint32_t pa = __ldg(base + min(2, last)), pb = __ldg(base + min(3, last));  // round 1
+            uint32_t qa, qb;                                                    // round 2 / next item's 0
+            if (rounds > 2) {
+                qa = __ldg(base + min(4, last));
+                qb = __ldg(base + min(5, last));
+            } else {
+                qa = __ldg(nbase);
+                qb = __ldg(nbase + min(1, nlast));
+            }
+            maxid = __vimax3_u32(maxid, xa, xb);
+            round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
+            xa = pa; xb = pb; pa = qa; pb = qb;
+            int o = 6;
+#pragma unroll 1
+            for (int r = 1; r + 2 < rounds; ++r, o += 2) {
+                qa = __ldg(base + min(o, last));  // smaller sets of the group clamp to their last id
+                qb = __ldg(base + min(o + 1, last));
+                maxid = __vimax3_u32(maxid, xa, xb);
+                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+                xa = pa; xb = pb; pa = qa; pb = qb;
+            }
+            if (rounds > 2) {
+                qa = __ldg(nbase);
+                qb = __ldg(nbase + min(1, nlast));
+                maxid = __vimax3_u32(maxid, xa, xb);
+                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+                xa = pa; xb = pb; pa = qa; pb = qb;
+            }
             if (odd) {
                 maxid = max(maxid, xa);
                 round1<K, ITER, NARROW>(best, ls, xa, p, bpar);
@@ -591,7 +610,7 @@ int g_prof_cap = 0, g_prof_n = 0, g_prof_dev = -1;
 cudaEvent_t* g_prof_ev = nullptr;
 }  // namespace
 
-using SignKernelFn = void (*)(SignArgs);
+using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t);
 
 template <bool ITER, bool NARROW, typename OutT>
 static SignKernelFn pick_kernel(int K) {
@@ -754,7 +773,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
     }
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A);
+    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b);
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
     rc = cuda_check(cudaGetLastError(), "sign_kernel launch");
     if (rc) return rc;

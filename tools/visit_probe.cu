@@ -12,8 +12,9 @@ __device__ uint32_t g_sink;
 
 __device__ __forceinline__ uint32_t red(uint32_t t, uint32_t p) { return __viaddmin_u32(t, 0u - p, t); }
 
-template <int K, int C, int L>
-__global__ void __launch_bounds__(256) walk(int rounds, uint32_t p, uint32_t seed, long long* cyc) {
+template <int K, int C, int L, bool VECP = false>
+__global__ void __launch_bounds__(256) walk(int rounds, uint32_t p_arg, uint32_t seed, long long* cyc, const uint32_t* pv = nullptr) {
+    const uint32_t p = VECP ? pv[threadIdx.x] : p_arg;  // VECP: p in a vector register
     uint32_t best[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
@@ -37,6 +38,26 @@ __global__ void __launch_bounds__(256) walk(int rounds, uint32_t p, uint32_t see
                 if (C >= 4) best[k] = __vimin3_u32(best[k], h[2], h[3]);
 #pragma unroll
                 for (int c = 0; c < C; ++c) h[c] = red(h[c] + d[c], p);
+            }
+        } else if (L == 4) {
+            uint32_t d3[C], d4[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) { d3[c] = red(d2[c] + d[c], p); d4[c] = red(d2[c] + d2[c], p); }
+#pragma unroll
+            for (int k = 0; k < K; k += 4) {
+                uint32_t g1[C], g2[C], g3[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    g1[c] = red(h[c] + d[c], p); g2[c] = red(h[c] + d2[c], p); g3[c] = red(h[c] + d3[c], p);
+                }
+                if (C >= 2) {
+                    best[k] = __vimin3_u32(best[k], h[0], h[1]);
+                    best[k + 1] = __vimin3_u32(best[k + 1], g1[0], g1[1]);
+                    best[k + 2] = __vimin3_u32(best[k + 2], g2[0], g2[1]);
+                    best[k + 3] = __vimin3_u32(best[k + 3], g3[0], g3[1]);
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) h[c] = red(h[c] + d4[c], p);
             }
         } else {
 #pragma unroll
@@ -68,22 +89,28 @@ __global__ void __launch_bounds__(256) walk(int rounds, uint32_t p, uint32_t see
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int K, int C, int L>
-void run(const char* name, int sms) {
+template <int K, int C, int L, bool VECP = false>
+void run(const char* name, int sms, int occ_cap = 99) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, walk<K, C, L>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, walk<K, C, L, VECP>, 256, 0);
+    if (occ > occ_cap) occ = occ_cap;
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, walk<K, C, L>);
+    cudaFuncGetAttributes(&fa, walk<K, C, L, VECP>);
+    uint32_t* pv;
+    cudaMalloc(&pv, 256 * 4);
+    uint32_t ph[256];
+    for (int i = 0; i < 256; ++i) ph[i] = 16777259u;
+    cudaMemcpy(pv, ph, sizeof(ph), cudaMemcpyHostToDevice);
     int blocks = occ * sms;
     long long* cyc;
     cudaMalloc(&cyc, blocks * sizeof(long long));
     int rounds = 2000;
-    walk<K, C, L><<<blocks, 256>>>(rounds / 10, 16777259u, 1u, cyc);
+    walk<K, C, L, VECP><<<blocks, 256>>>(rounds / 10, 16777259u, 1u, cyc, pv);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    walk<K, C, L><<<blocks, 256>>>(rounds, 16777259u, 2u, cyc);
+    walk<K, C, L, VECP><<<blocks, 256>>>(rounds, 16777259u, 2u, cyc, pv);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -104,6 +131,12 @@ int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     printf("SMs=%d (ALU-pipe ceiling at 1.5 ALU instr/visit = 42.7 visits/clk/SM)\n", sms);
+    run<64, 2, 2>("lookahead occ2", sms, 2);
+    run<64, 2, 2, true>("lookahead occ2 vec-p", sms, 2);
+    run<64, 2, 4>("lookahead4 occ2", sms, 2);
+    run<64, 2, 4>("lookahead4", sms);
+    run<32, 2, 2>("lookahead occ3", sms, 3);
+    run<32, 2, 4>("lookahead4 occ3", sms, 3);
     run<64, 2, 1>("base", sms);
     run<64, 2, 2>("lookahead", sms);
     run<64, 4, 1>("4 chains", sms);
