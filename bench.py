@@ -49,6 +49,8 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of signatures (N>1)")
+    ap.add_argument("--aux", action="store_true",
+                    help="also time the pairwise-Jaccard and bucket-histogram kernels (cfg3: planted pairs)")
     return ap.parse_args()
 
 
@@ -198,6 +200,56 @@ def _workload_name(cfg, family):
     return f"{cfg.n_sets} sets, {sizes}, {ids} ids over 2^{cfg.vocab_log2}, N={cfg.n_hash}, {family}"
 
 
+def _time_cuda(fn, reps=5):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def _aux_kernels(cfg, fam, indptr, ids, out, exact_j, dev):
+    """Pairwise Jaccard estimates over planted pairs (or consecutive sets) and the
+    4096-bin (64x64) bucket histogram of h_i(x) over the workload's distinct ids."""
+    import numpy as np
+    import torch
+
+    from paper_1401_6124_b200 import bucket_histogram, estimate_pairs, jaccard_block
+
+    res = {}
+    n_sets = indptr.numel() - 1
+    n_pairs = n_sets // 2
+    pi = torch.arange(0, 2 * n_pairs, 2, device=dev)
+    pj = pi + 1
+    ms = _time_cuda(lambda: estimate_pairs(out, pi, pj))
+    counts, est = estimate_pairs(out, pi, pj)
+    res["jaccard_pairs"] = {"pairs": n_pairs, "ms": ms, "pairs_per_s": n_pairs / (ms / 1e3),
+                            "gbs": 2 * 4 * fam.size * n_pairs / (ms / 1e3) / 1e9}
+    if exact_j is not None:
+        err = (est - exact_j).abs()
+        res["jaccard_pairs"]["mae_vs_exact"] = float(err.mean())
+        res["jaccard_pairs"]["max_err"] = float(err.max())
+    blk = min(4096, n_sets)
+    ms_b = _time_cuda(lambda: jaccard_block(out[:blk], out[:blk]), reps=3)
+    res["jaccard_block"] = {"rows": blk, "cols": blk, "ms": ms_b,
+                            "compares_per_s": blk * blk * fam.size / (ms_b / 1e3)}
+    xs = torch.unique(ids.to(torch.int64)).to(torch.uint32)
+    ms_h = _time_cuda(lambda: bucket_histogram(xs, fam, 4096), reps=3)
+    h = bucket_histogram(xs, fam, 4096)
+    tot = int(h.sum())
+    chi2 = float((((h.double() - tot / 4096) ** 2) / (tot / 4096)).sum())
+    res["bucket_hist"] = {"distinct_ids": int(xs.numel()), "bins": 4096, "ms": ms_h,
+                          "evals_per_s": xs.numel() * fam.size / (ms_h / 1e3), "chi2_dof4095": chi2}
+    return res
+
+
 def main():
     args = _args()
     if args.impl == "reference":
@@ -222,7 +274,14 @@ def main():
     cfg = gen.CONFIGS[args.config]
     n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
     t0 = time.perf_counter()
-    indptr, ids = gen.make_csr(cfg, device=dev, n_sets=n_sets, seed=cfg.data_seed() + rank)
+    exact_j = None
+    if cfg.name == "cfg3":
+        # planted near-duplicate pairs: n_sets/2 base sets, each followed by its mutant
+        indptr, ids, exact_j = gen.planted_pairs(cfg, device=dev, n_base=n_sets // 2 if args.n_sets else None,
+                                                 seed=cfg.data_seed() + rank)
+        n_sets = indptr.numel() - 1
+    else:
+        indptr, ids = gen.make_csr(cfg, device=dev, n_sets=n_sets, seed=cfg.data_seed() + rank)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     nnz = int(ids.numel())
@@ -353,6 +412,10 @@ def main():
                "ms_per_step": float(e2e_s.item()) * 1e3,
                "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 3 streams)"}
 
+    aux = None
+    if args.aux:
+        aux = _aux_kernels(cfg, fam, indptr, ids, out, exact_j, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -380,6 +443,8 @@ def main():
         }
         if gather_ms is not None:
             line["gather_ms"] = gather_ms
+        if aux is not None:
+            line["aux"] = aux
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -38,6 +38,16 @@ __device__ __forceinline__ uint32_t mul_add_mod_narrow(uint32_t w, uint32_t wp, 
     return reduce_once(r, p);
 }
 
+// (w*x + c) mod p with one ALU instruction, needs 3p < 2^32: r = w*x + c - q*p lies in
+// [0, 3p); the two subtractions run on the FMA pipe and a single 3-way unsigned min
+// (VIMNMX3) picks the residue (the wrapped candidates are >= 2^32 - 2p).
+__device__ __forceinline__ uint32_t mul_add_mod_min3(uint32_t w, uint32_t wp, uint32_t c,
+                                                     uint32_t x, uint32_t p) {
+    uint32_t q = __umulhi(wp, x);
+    uint32_t r = w * x + c - q * p;
+    return __vimin3_u32(r, r - p, r - 2u * p);
+}
+
 // Host/device helpers on 64-bit integers (setup only, never per visit).
 __host__ __device__ __forceinline__ uint32_t shoup_companion(uint32_t w, uint32_t p) {
     return (uint32_t)(((uint64_t)w << 32) / p);

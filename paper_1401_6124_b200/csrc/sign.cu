@@ -51,7 +51,7 @@ Geometry choose_geometry(int kind, int32_t n_hash) {
     if (kind == KIND_ITERATIVE) {
         K = n_hash >= 128 ? 64 : n_hash >= 32 ? 32 : n_hash >= 16 ? 16 : 8;
     } else {
-        K = n_hash >= 64 ? 32 : n_hash >= 16 ? 16 : 8;
+        K = n_hash >= 16 ? 16 : 8;  // 3 constants + 1 minimum per lane in registers
     }
     int lg = (n_hash + K - 1) / K;
     if (lg <= 32) {
@@ -352,8 +352,9 @@ template <int K, bool ITER, bool NARROW, bool FIRST>
 __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa, uint32_t xb,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
-        const uint32_t ha = mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
-        const uint32_t hb = mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
+        // NARROW (3p < 2^32): the start hashes reduce with one VIMNMX3 each
+        const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        const uint32_t hb = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xb, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
         walk2_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), hb, reduce_once(xb + bpar, p), p);
     } else {
         walk2_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p);
@@ -364,7 +365,7 @@ template <int K, bool ITER, bool NARROW>
 __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
-        const uint32_t ha = mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
         walk1_iter<K>(best, ha, reduce_once(xa + bpar, p), p);
     } else {
         walk1_random<K, NARROW>(best, ls.cA, ls.cAp, ls.cB, xa, p);
@@ -441,7 +442,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
 template <int K, bool ITER, bool NARROW, typename OutT>
-__global__ void __launch_bounds__(kBlock, ITER ? 2 : 1) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar) {
+__global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -627,6 +628,7 @@ static SignKernelFn pick_kernel(int K) {
 static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K) {
     const bool i64 = out_dtype == MHB_OUT_I64;
     if (kind == KIND_ITERATIVE) {
+        if (narrow) return i64 ? pick_kernel<true, true, long long>(K) : pick_kernel<true, true, uint32_t>(K);
         return i64 ? pick_kernel<true, false, long long>(K) : pick_kernel<true, false, uint32_t>(K);
     }
     if (narrow) return i64 ? pick_kernel<false, true, long long>(K) : pick_kernel<false, true, uint32_t>(K);

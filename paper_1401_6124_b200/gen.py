@@ -166,3 +166,67 @@ def make_csr(cfg: Config | str, device="cuda", n_sets: int | None = None, seed: 
     torch.cumsum(sizes, 0, out=indptr[1:])
     ids = (keys & 0xFFFFFFFF).to(torch.uint32)
     return indptr, ids
+
+
+def planted_pairs(cfg: Config | str = "cfg3", device="cuda", n_base: int | None = None, seed: int | None = None,
+                  j_lo: float = 0.1, j_hi: float = 0.95, max_rounds: int = 100):
+    """cfg3: base sets (Poisson(300) over 2^22) each followed by a mutated copy.
+
+    For base set k of size n the mutant keeps c = round(2nJ/(1+J)) base ids (a
+    random subset) and adds n - c fresh ids absent from the base, so the pair's
+    exact Jaccard is c / (2n - c) (the construction of corpus.synth_pair,
+    corpus.py:83-111, with a per-pair target J ~ U[j_lo, j_hi]).  Sets 2k and 2k+1
+    form pair k, so nnz-balanced sharding with align=2 never splits a pair.
+    Returns (indptr int64[2B+1], ids uint32, exact_jaccard float64[B]).
+    """
+    import torch
+
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    n_base = cfg.n_sets if n_base is None else int(n_base)
+    device = torch.device(device)
+    seed = cfg.data_seed() if seed is None else int(seed)
+    b_ip, b_ids = make_csr(cfg, device=device, n_sets=n_base, seed=seed)
+    gen = torch.Generator(device=device)
+    gen.manual_seed((seed + 1) & ((1 << 63) - 1))
+    sizes = b_ip[1:] - b_ip[:-1]
+    j = j_lo + (j_hi - j_lo) * torch.rand(n_base, dtype=torch.float64, device=device, generator=gen)
+    keep = torch.round(2.0 * sizes.double() * j / (1.0 + j)).to(torch.int64).clamp_(min=1)
+    keep = torch.minimum(keep, sizes)
+    set_idx = torch.arange(n_base, dtype=torch.int64, device=device)
+    owner = torch.repeat_interleave(set_idx, sizes)
+    base_keys = (owner << 32) | b_ids.to(torch.int64)
+    # random subset of size keep[k] of each base set: rank elements by a random key
+    r = torch.rand(owner.numel(), device=device, generator=gen)
+    order = torch.argsort(owner.double() * 2.0 + r)  # stable grouping by set, random inside
+    pos = torch.arange(owner.numel(), device=device) - torch.repeat_interleave(b_ip[:-1], sizes)
+    kept = base_keys[order][pos < keep[owner]]
+    # fresh ids: uniform over the vocabulary, not in the base set, no repeats
+    need = sizes - keep
+    fresh = torch.empty(0, dtype=torch.int64, device=device)
+    sorted_base = torch.sort(base_keys).values
+    for _ in range(max_rounds):
+        have = torch.bincount(fresh >> 32, minlength=n_base) if fresh.numel() else torch.zeros_like(need)
+        deficit = need - have
+        missing = int(deficit.sum())
+        if missing == 0:
+            break
+        cand = (torch.repeat_interleave(set_idx, deficit) << 32) | torch.randint(
+            0, cfg.vocab, (missing,), dtype=torch.int64, device=device, generator=gen)
+        pos_b = torch.searchsorted(sorted_base, cand).clamp_(max=sorted_base.numel() - 1)
+        cand = cand[sorted_base[pos_b] != cand]
+        fresh = torch.unique(torch.cat([fresh, cand]))
+    else:
+        raise RuntimeError("fresh-id redraw did not converge")
+    mut_keys = torch.sort(torch.cat([kept, fresh])).values
+    # interleave: base k -> set 2k, mutant k -> set 2k+1
+    b_sorted = torch.sort(base_keys).values
+    all_keys = torch.cat([((b_sorted >> 32) * 2) << 32 | (b_sorted & 0xFFFFFFFF),
+                          ((mut_keys >> 32) * 2 + 1) << 32 | (mut_keys & 0xFFFFFFFF)])
+    all_keys = torch.sort(all_keys).values
+    counts = torch.bincount(all_keys >> 32, minlength=2 * n_base)
+    indptr = torch.zeros(2 * n_base + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=indptr[1:])
+    ids = (all_keys & 0xFFFFFFFF).to(torch.uint32)
+    exact = keep.double() / (2.0 * sizes.double() - keep.double())
+    return indptr, ids, exact

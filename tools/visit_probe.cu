@@ -11,6 +11,79 @@
 __device__ uint32_t g_sink;
 
 __device__ __forceinline__ uint32_t red(uint32_t t, uint32_t p) { return __viaddmin_u32(t, 0u - p, t); }
+// FMA-pipe-only step: h' = (h + d) mod p from u = h + (d - p): c = umulhi(u, two) is u's
+// sign bit (two = 2 passed opaquely so it stays an IMAD.HI), h' = u + c*p.
+__device__ __forceinline__ uint32_t step_fma(uint32_t h, uint32_t dm, uint32_t p, uint32_t two) {
+    const uint32_t u = h + dm;
+    const uint32_t c = __umulhi(u, two);
+    return u + c * p;
+}
+
+// Lookahead walk where reductions with (j % M == 0) on chain A and (j % M == M/2) on
+// chain B go through step_fma; M = 0 disables.
+template <int K, int M>
+__global__ void __launch_bounds__(256) walk_mixed(int rounds, uint32_t p, uint32_t seed, uint32_t two, long long* cyc) {
+    uint32_t best[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
+    uint32_t h0a = (threadIdx.x * 2654435761u + seed) % p, h0b = (threadIdx.x * 40503u + 7u * seed) % p;
+    const uint32_t da = (blockIdx.x * 40503u + 17u + seed) % p, db = (blockIdx.x * 977u + 5u) % p;
+    const uint32_t da2 = (2 * da) % p, db2 = (2 * db) % p;
+    const uint32_t dam = da - p, dbm = db - p;
+    long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r) {
+        uint32_t ha = h0a, hb = h0b;
+#pragma unroll
+        for (int k = 0; k < K; k += 2) {
+            const int j = k / 2;
+            const bool fa = M > 0 && (j % M == 0), fb = M > 0 && (j % M == M / 2);
+            const uint32_t ga = fa ? step_fma(ha, dam, p, two) : red(ha + da, p);
+            const uint32_t gb = fb ? step_fma(hb, dbm, p, two) : red(hb + db, p);
+            best[k] = __vimin3_u32(best[k], ha, hb);
+            best[k + 1] = __vimin3_u32(best[k + 1], ga, gb);
+            ha = red(ha + da2, p);
+            hb = red(hb + db2, p);
+        }
+        h0a = red(h0a + (uint32_t)r, p);
+        h0b = red(h0b + 3u, p);
+    }
+    long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_sink = acc;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int K, int M>
+void run_mixed(const char* name, int sms, int occ_cap) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, walk_mixed<K, M>, 256, 0);
+    if (occ > occ_cap) occ = occ_cap;
+    int blocks = occ * sms;
+    long long* cyc;
+    cudaMalloc(&cyc, blocks * sizeof(long long));
+    int rounds = 2000;
+    walk_mixed<K, M><<<blocks, 256>>>(rounds / 10, 16777259u, 1u, 2u, cyc);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    walk_mixed<K, M><<<blocks, 256>>>(rounds, 16777259u, 2u, 2u, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long* h = new long long[blocks];
+    cudaMemcpy(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long mx = 0;
+    for (int i = 0; i < blocks; ++i) mx = h[i] > mx ? h[i] : mx;
+    double visits = (double)blocks * 256 * rounds * K * 2;
+    printf("%-22s K=%3d M=%d occ=%d  %.2f Tvisit/s  %.2f visits/clk/SM\n", name, K, M, occ,
+           visits / (ms * 1e-3) / 1e12, visits / sms / (double)mx);
+    delete[] h;
+    cudaFree(cyc);
+}
 
 template <int K, int C, int L, bool VECP = false>
 __global__ void __launch_bounds__(256) walk(int rounds, uint32_t p_arg, uint32_t seed, long long* cyc, const uint32_t* pv = nullptr) {
@@ -132,6 +205,11 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     printf("SMs=%d (ALU-pipe ceiling at 1.5 ALU instr/visit = 42.7 visits/clk/SM)\n", sms);
     run<64, 2, 2>("lookahead occ2", sms, 2);
+    run_mixed<64, 0>("mixed off", sms, 2);
+    run_mixed<64, 2>("mixed 1/4", sms, 2);
+    run_mixed<64, 3>("mixed 1/6", sms, 2);
+    run_mixed<64, 4>("mixed 1/8", sms, 2);
+    run_mixed<64, 6>("mixed 1/12", sms, 2);
     run<64, 2, 2, true>("lookahead occ2 vec-p", sms, 2);
     run<64, 2, 4>("lookahead4 occ2", sms, 2);
     run<64, 2, 4>("lookahead4", sms);
