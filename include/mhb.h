@@ -31,7 +31,8 @@
  *  - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t, or
  *    NULL for the legacy default stream).  No host synchronisation happens inside.
  *  - CSR: indptr is int64[n_sets+1] (indptr[0] need not be 0: ids are addressed
- *    as ids[indptr[s] .. indptr[s+1])), ids is uint32[>= indptr[n_sets]].
+ *    as ids[indptr[s] .. indptr[s+1])), ids is uint32[>= indptr[n_sets]] and all of
+ *    ids[0 .. indptr[n_sets]) must be readable (idle warp lanes read ids[0]).
  *    Ids may be in any order and may repeat inside a set (min is idempotent).
  *  - Data errors found on the device are OR-ed into *status (reset to 0 by the
  *    call): MHB_STATUS_EMPTY_SET mirrors minhash.py:97-98, MHB_STATUS_ID_GE_PRIME

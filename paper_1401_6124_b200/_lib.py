@@ -10,7 +10,10 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmhb.so"
+import os
+
+# MHB_LIB overrides the library path (A/B experiments with variant builds).
+LIB_PATH = Path(os.environ.get("MHB_LIB") or Path(__file__).resolve().parent / "lib" / "libmhb.so")
 
 MHB_OK = 0
 MHB_ERR_INVALID = 1

@@ -49,6 +49,12 @@ struct DeviceCache {
 std::mutex g_mu;
 DeviceCache g_cache[64];
 
+// indptr[i] -= base: a chunk's CSR offsets become relative to its own ids buffer.
+__global__ void rebase_indptr_kernel(int64_t* indptr, int64_t n, int64_t base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        indptr[i] -= base;
+}
+
 int grow(void** ptr, size_t* cap, size_t need) {
     if (*cap >= need && *ptr) return MHB_OK;
     if (*ptr) cudaFree(*ptr);
@@ -165,10 +171,13 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
             (rc = cuda_check(cudaMemcpyAsync(ln.ids, ids + id0, (size_t)cnnz * sizeof(uint32_t),
                                              cudaMemcpyHostToDevice, ln.stream), "H2D ids")))
             return rc;
-        // The chunk's indptr keeps global offsets; shift the ids base so ids[indptr[s]] lands in the chunk buffer.
-        const uint32_t* ids_base = reinterpret_cast<const uint32_t*>(
-            reinterpret_cast<uintptr_t>(ln.ids) - (uintptr_t)id0 * sizeof(uint32_t));
-        rc = launch_sign(kind, ln.indptr, ids_base, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
+        // Rebase the chunk's offsets onto its own ids buffer (ids[0..cnnz) is what the kernels may read).
+        if (id0 != 0) {
+            const int64_t nb = std::min<int64_t>((rows + 1 + 255) / 256, 1024);
+            rebase_indptr_kernel<<<(unsigned)nb, 256, 0, ln.stream>>>(ln.indptr, rows + 1, id0);
+            if ((rc = cuda_check(cudaGetLastError(), "rebase_indptr launch"))) return rc;
+        }
+        rc = launch_sign(kind, ln.indptr, ln.ids, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
                          out_dtype, ln.status, ln.ws, ln.ws_cap, ln.stream);
         if (rc) return rc;
         if ((rc = cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)s0 * n_hash * out_bytes, ln.out,

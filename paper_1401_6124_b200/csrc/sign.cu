@@ -781,10 +781,11 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (rc) return rc;
 
     {
-        // one block per long-set row (latency-bound: a wide grid hides the row loads)
+        // blocks loop over long-set rows; 16 per SM hide the row loads without paying
+        // for tens of thousands of empty blocks
         int64_t fb = nnz / (kChunk + 1);
-        if (fb > 65535) fb = 65535;
-        if (fb < (int64_t)dev.sms) fb = dev.sms;
+        if (fb > (int64_t)dev.sms * 16) fb = (int64_t)dev.sms * 16;
+        if (fb < 1) fb = 1;
         if (out_dtype == MHB_OUT_I64)
             finalize_kernel<long long><<<(unsigned)fb, 256, 0, st>>>(A);
         else

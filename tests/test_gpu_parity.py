@@ -210,3 +210,17 @@ def test_cfg2_subsample_vs_oracle(cuda_device):
     got = signatures_csr(ip, di, fam, out_dtype="uint32").cpu().numpy().astype(np.int64)
     indptr, ids = ip.cpu().numpy(), di.cpu().numpy()
     assert np.array_equal(got, oracle.sign_family_csr(indptr, ids, fam))
+
+
+def test_host_pipeline_chunked_cfg2(cuda_device):
+    """Host entry on a batch large enough to be cut into several chunks (rebased ids)."""
+    cfg = gen.CONFIGS["cfg2"]
+    ip, di = gen.make_csr(cfg, device=cuda_device, n_sets=60_000)
+    fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+    dev_out = signatures_csr(ip, di, fam, out_dtype="uint32").cpu().numpy()
+    host_out = signatures_csr(ip.cpu().numpy(), di.cpu().numpy().view(np.uint32), fam, out_dtype="uint32")
+    assert np.array_equal(dev_out, host_out)
+    k = 2000
+    ip_h = ip[:k + 1].cpu().numpy()
+    want = oracle.sign_family_csr(ip_h, di[:int(ip_h[-1])].cpu().numpy().view(np.uint32), fam)
+    assert np.array_equal(host_out[:k].astype(np.int64), want)
