@@ -136,6 +136,16 @@ int mhb_jaccard_block(const void* sig_a, int64_t n_rows, const void* sig_b, int6
                       int32_t sig_dtype, int32_t n_hash, uint32_t* counts, void* stream);
 
 /*
+ * LSH band keys (the reference has no banding): the N
+ * signature positions form N/rows_per_band bands of consecutive rows, and
+ *   keys[s*n_bands + band] = splitmix64(h), h = FNV-1a-64 over the band's argmin ids
+ *   (as uint32 words), seeded with 0xCBF29CE484222325 ^ band.
+ * sig: [n_sets, n_hash] of sig_dtype; rows_per_band must divide n_hash.
+ */
+int mhb_band_keys(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,
+                  int32_t rows_per_band, unsigned long long* keys, void* stream);
+
+/*
  * Bucket-uniformity histogram (generalises stats.py:221-224 from one x to a
  * batch): counts[m] += #{(x, i) : x in xs, 0 <= i < n_hash, h_i(x) mod buckets == m}.
  * counts is uint64[buckets], accumulated into (not cleared).  xs must be < prime.
@@ -146,6 +156,24 @@ int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x,
 int mhb_bucket_hist_random(const uint32_t* xs, int64_t n_x,
                            const uint32_t* a, const uint32_t* b, uint64_t prime, int32_t n_hash,
                            uint32_t buckets, unsigned long long* counts, void* stream);
+
+/*
+ * Signature-file records from a device signature block (the reference's formats,
+ * minhash.py:140-206).  obj_ids (device int64[n_sets]) may be NULL: ids are then
+ * first_id, first_id+1, ...
+ *   binary: out is uint64[n_sets*(n_hash+2)]: per record id, n_hash, then the ids
+ *           (little-endian, byte-identical to write_signatures_binary).
+ *   text  : lens[r] = byte length of record r's line "id N x0 ... xN-1\n"; after an
+ *           exclusive scan of lens into offsets, format_text writes the lines into
+ *           out (byte-identical to write_signatures_text).
+ */
+int mhb_format_binary_records(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,
+                              const int64_t* obj_ids, int64_t first_id, unsigned long long* out, void* stream);
+int mhb_text_record_lengths(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,
+                            const int64_t* obj_ids, int64_t first_id, int64_t* lens, void* stream);
+int mhb_format_text_records(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,
+                            const int64_t* obj_ids, int64_t first_id, const int64_t* offsets, char* out,
+                            void* stream);
 
 /*
  * Instruction-rate probe for the roofline: runs the iterative visit sequence

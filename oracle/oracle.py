@@ -122,6 +122,23 @@ def jaccard_estimate(m1: np.ndarray, m2: np.ndarray) -> float:
     return float(np.mean(np.asarray(m1) == np.asarray(m2)))
 
 
+def band_keys(sig: np.ndarray, rows_per_band: int) -> np.ndarray:
+    """LSH band keys as defined in include/mhb.h: splitmix64(FNV-1a-64 over the band's
+    argmin ids as uint32 words, seeded with 0xCBF29CE484222325 ^ band)."""
+    sig = np.asarray(sig).astype(np.uint64) & np.uint64(0xFFFFFFFF)
+    n_sets, n_hash = sig.shape
+    nb = n_hash // rows_per_band
+    with np.errstate(over="ignore"):
+        h = np.uint64(0xCBF29CE484222325) ^ np.arange(nb, dtype=np.uint64)[None, :].repeat(n_sets, 0)
+        blocks = sig.reshape(n_sets, nb, rows_per_band)
+        for j in range(rows_per_band):
+            h = (h ^ blocks[:, :, j]) * np.uint64(0x100000001B3)
+        z = h + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
 def brute_force_row(ids, family) -> np.ndarray:
     """Per hash index, scan ascending ids, strict '<' (tests/test_minhash.py:27-39)."""
     ids = sorted(set(int(v) for v in ids))

@@ -47,6 +47,10 @@ SIGNATURES = {
     "mhb_host_release": (None, []),
     "mhb_jaccard_pairs": (C.c_int, [_P, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
     "mhb_jaccard_block": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, _P, _P]),
+    "mhb_band_keys": (C.c_int, [_P, _I32, _I64, _I32, _I32, _P, _P]),
+    "mhb_format_binary_records": (C.c_int, [_P, _I32, _I64, _I32, _P, _I64, _P, _P]),
+    "mhb_text_record_lengths": (C.c_int, [_P, _I32, _I64, _I32, _P, _I64, _P, _P]),
+    "mhb_format_text_records": (C.c_int, [_P, _I32, _I64, _I32, _P, _I64, _P, _P, _P]),
     "mhb_bucket_hist_iterative": (C.c_int, [_P, _I64, _U64, _U64, _U64, _I32, _U32, _P, _P]),
     "mhb_bucket_hist_random": (C.c_int, [_P, _I64, _P, _P, _U64, _I32, _U32, _P, _P]),
     "mhb_probe_visit_rate": (C.c_int, [_I64, _I32, C.POINTER(C.c_double), C.POINTER(C.c_float), _P]),

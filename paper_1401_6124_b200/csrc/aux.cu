@@ -172,6 +172,35 @@ static int launch_hist(HistArgs H, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
+// LSH band keys: key(s, band) = splitmix64(FNV-1a-64 over the band's argmin ids,
+// seeded with the band index).  One thread per (set, band).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void band_keys_kernel(const T* __restrict__ sig, int64_t n_sets, int32_t n_hash, int32_t rows,
+                                 int32_t n_bands, unsigned long long* __restrict__ keys) {
+    const int64_t total = n_sets * (int64_t)n_bands;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / n_bands;
+        const int band = (int)(t - s * n_bands);
+        const T* row = sig + s * (int64_t)n_hash + (int64_t)band * rows;
+        unsigned long long h = 0xCBF29CE484222325ull ^ (unsigned long long)band;
+        for (int j = 0; j < rows; ++j) {
+            h ^= (unsigned long long)(uint32_t)__ldg(row + j);
+            h *= 0x100000001B3ull;
+        }
+        keys[t] = splitmix64(h);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Visit-rate probe: the iterative inner loop from registers only.
 // ---------------------------------------------------------------------------
 __device__ uint32_t g_probe_sink;
@@ -269,6 +298,30 @@ extern "C" int mhb_jaccard_block(const void* sig_a, int64_t n_rows, const void* 
     else
         return set_error(MHB_ERR_INVALID, "unknown sig_dtype %d", sig_dtype);
     return cuda_check(cudaGetLastError(), "jaccard_block launch");
+}
+
+extern "C" int mhb_band_keys(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,
+                             int32_t rows_per_band, unsigned long long* keys, void* stream) {
+    clear_error();
+    if (n_hash < 1 || rows_per_band < 1 || n_hash % rows_per_band != 0)
+        return set_error(MHB_ERR_INVALID, "rows_per_band must divide n_hash (got %d, %d)", rows_per_band, n_hash);
+    if (n_sets <= 0) return MHB_OK;
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    const int32_t n_bands = n_hash / rows_per_band;
+    int64_t blocks = (n_sets * n_bands + 255) / 256;
+    if (blocks > (int64_t)dev.sms * 16) blocks = (int64_t)dev.sms * 16;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (sig_dtype == MHB_OUT_I64)
+        band_keys_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const long long*>(sig), n_sets, n_hash,
+                                                                      rows_per_band, n_bands, keys);
+    else if (sig_dtype == MHB_OUT_U32)
+        band_keys_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const uint32_t*>(sig), n_sets, n_hash,
+                                                                     rows_per_band, n_bands, keys);
+    else
+        return set_error(MHB_ERR_INVALID, "unknown sig_dtype %d", sig_dtype);
+    return cuda_check(cudaGetLastError(), "band_keys launch");
 }
 
 extern "C" int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x, uint64_t a, uint64_t b,

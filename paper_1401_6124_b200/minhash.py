@@ -305,6 +305,26 @@ def jaccard_block(sig_a, sig_b):
     return counts
 
 
+def band_keys(sig, rows_per_band: int):
+    """LSH band keys: uint64 [S, N/rows] from a device signature matrix [S, N].
+
+    Bands are runs of `rows_per_band` consecutive hash positions; each key is
+    splitmix64 of FNV-1a-64 over the band's argmin ids (include/mhb.h).  Equal keys
+    mean the two sets agree on every row of the band (the LSH candidate test)."""
+    torch = _torch()
+    lib = _lib.load()
+    n_sets, n_hash = sig.shape
+    if n_hash % rows_per_band:
+        raise ValueError(f"rows_per_band {rows_per_band} must divide the signature length {n_hash}")
+    keys = torch.empty((n_sets, n_hash // rows_per_band), dtype=torch.uint64, device=sig.device)
+    dt = _lib.OUT_I64 if sig.dtype == torch.int64 else _lib.OUT_U32
+    with torch.cuda.device(sig.device):
+        rc = lib.mhb_band_keys(sig.contiguous().data_ptr(), dt, n_sets, n_hash, rows_per_band, keys.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc)
+    return keys
+
+
 # ---------------------------------------------------------------------------
 # Signature files (reference minhash.py:140-206): "id N ids..." text lines and
 # little-endian u64 binary records.

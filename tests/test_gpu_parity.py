@@ -15,6 +15,7 @@ import pytest
 from oracle import oracle
 from paper_1401_6124_b200 import (
     FeatureSet,
+    band_keys,
     IterativeFamily,
     RandomFamily,
     bucket_histogram,
@@ -224,3 +225,39 @@ def test_host_pipeline_chunked_cfg2(cuda_device):
     ip_h = ip[:k + 1].cpu().numpy()
     want = oracle.sign_family_csr(ip_h, di[:int(ip_h[-1])].cpu().numpy().view(np.uint32), fam)
     assert np.array_equal(host_out[:k].astype(np.int64), want)
+
+
+def test_band_keys_match_oracle(cuda_device):
+    """cfg4 layout: N=2048 as 128 bands x 16 rows; keys equal the numpy restatement."""
+    indptr, ids = gen.cfg1_numpy(n_sets=300, seed=21)
+    fam = make_family("iterative", 3, 2048, 1_048_583)
+    ip, di = _dev(indptr, ids, cuda_device)
+    for dt in ("uint32", "int64"):
+        sig = signatures_csr(ip, di, fam, out_dtype=dt)
+        keys = band_keys(sig, 16).cpu().numpy()
+        assert keys.shape == (300, 128)
+        assert np.array_equal(keys.view(np.uint64), oracle.band_keys(sig.cpu().numpy(), 16))
+    # identical sets share every band; the planted-pair mutant shares some
+    ip2 = np.array([0, 50, 100], dtype=np.int64)
+    row = ids[:50]
+    sig2 = signatures_csr(*_dev(ip2, np.concatenate([row, row]), cuda_device), fam)
+    k2 = band_keys(sig2, 16).cpu().numpy()
+    assert np.array_equal(k2[0], k2[1])
+
+
+@pytest.mark.parametrize("fmt", ["binary", "text"])
+def test_signature_files_from_gpu(tmp_path, cuda_device, fmt):
+    """GPU-formatted record files are byte-identical to the reference-format writers."""
+    from paper_1401_6124_b200 import write_signatures_binary, write_signatures_text
+    from paper_1401_6124_b200.records import write_signatures_csr
+
+    indptr, ids = gen.cfg1_numpy(n_sets=777, seed=4)
+    for kind, n in (("iterative", 128), ("random", 37)):
+        fam = make_family(kind, 12, n, 1_048_583)
+        mins = oracle.sign_family_csr(indptr, ids, fam)
+        obj = np.arange(777, dtype=np.int64) * 3 - 5  # includes negative ids
+        ref = tmp_path / f"ref.{fmt}"
+        (write_signatures_binary if fmt == "binary" else write_signatures_text)(ref, zip(obj.tolist(), mins))
+        got = tmp_path / f"gpu.{fmt}"
+        assert write_signatures_csr(got, indptr, ids, fam, fmt=fmt, obj_ids=obj, chunk_bytes=64 << 10) == 777
+        assert got.read_bytes() == ref.read_bytes(), (kind, fmt)
