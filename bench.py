@@ -273,6 +273,8 @@ def main():
 
     cfg = gen.CONFIGS[args.config]
     n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
+    if cfg.name == "cfg5" and args.n_sets is None:
+        n_sets = cfg.n_sets // 8  # box scale: one rank's 1/8 shard of the 100M-set batch
     t0 = time.perf_counter()
     exact_j = None
     if cfg.name == "cfg3":

@@ -18,6 +18,17 @@ namespace mhb {
 // Jaccard: listed pairs, one warp per pair
 // ---------------------------------------------------------------------------
 template <typename T>
+__device__ __forceinline__ uint32_t eq_count16(const uint4& a, const uint4& b) {
+    if constexpr (sizeof(T) == 4) {
+        return (a.x == b.x) + (a.y == b.y) + (a.z == b.z) + (a.w == b.w);
+    } else {  // two int64 entries per 16 bytes
+        return ((a.x == b.x) & (a.y == b.y)) + ((a.z == b.z) & (a.w == b.w));
+    }
+}
+
+// VEC: rows are 16-byte aligned and a whole number of 16-byte words (n_hash*sizeof(T) % 16 == 0):
+// each lane compares 16-byte words, four in flight per iteration.
+template <typename T, bool VEC>
 __global__ void jaccard_pairs_kernel(const T* __restrict__ sig, int32_t n_hash,
                                      const int64_t* __restrict__ pi, const int64_t* __restrict__ pj,
                                      int64_t n_pairs, uint32_t* __restrict__ counts,
@@ -29,7 +40,20 @@ __global__ void jaccard_pairs_kernel(const T* __restrict__ sig, int32_t n_hash,
         const T* r1 = sig + pi[k] * (int64_t)n_hash;
         const T* r2 = sig + pj[k] * (int64_t)n_hash;
         uint32_t c = 0;
-        for (int32_t i = lane; i < n_hash; i += 32) c += (__ldg(r1 + i) == __ldg(r2 + i));
+        if constexpr (VEC) {
+            const uint4* v1 = reinterpret_cast<const uint4*>(r1);
+            const uint4* v2 = reinterpret_cast<const uint4*>(r2);
+            const int nw = (int)((int64_t)n_hash * sizeof(T) / 16);
+            int w = lane;
+            for (; w + 96 < nw; w += 128) {
+                const uint4 a0 = __ldg(v1 + w), a1 = __ldg(v1 + w + 32), a2 = __ldg(v1 + w + 64), a3 = __ldg(v1 + w + 96);
+                const uint4 b0 = __ldg(v2 + w), b1 = __ldg(v2 + w + 32), b2 = __ldg(v2 + w + 64), b3 = __ldg(v2 + w + 96);
+                c += eq_count16<T>(a0, b0) + eq_count16<T>(a1, b1) + eq_count16<T>(a2, b2) + eq_count16<T>(a3, b3);
+            }
+            for (; w < nw; w += 32) c += eq_count16<T>(__ldg(v1 + w), __ldg(v2 + w));
+        } else {
+            for (int32_t i = lane; i < n_hash; i += 32) c += (__ldg(r1 + i) == __ldg(r2 + i));
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) {
@@ -268,14 +292,19 @@ extern "C" int mhb_jaccard_pairs(const void* sig, int32_t sig_dtype, int32_t n_h
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int64_t blocks = (n_pairs * 32 + 255) / 256;
     if (blocks > (int64_t)dev.sms * 16) blocks = (int64_t)dev.sms * 16;
-    if (sig_dtype == MHB_OUT_I64)
-        jaccard_pairs_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(
-            static_cast<const long long*>(sig), n_hash, pi, pj, n_pairs, counts, est);
-    else if (sig_dtype == MHB_OUT_U32)
-        jaccard_pairs_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(
-            static_cast<const uint32_t*>(sig), n_hash, pi, pj, n_pairs, counts, est);
-    else
+    const size_t esz = sig_dtype == MHB_OUT_I64 ? 8 : 4;
+    const bool vec = ((uintptr_t)sig % 16 == 0) && (((size_t)n_hash * esz) % 16 == 0);
+    if (sig_dtype == MHB_OUT_I64) {
+        const long long* s = static_cast<const long long*>(sig);
+        if (vec) jaccard_pairs_kernel<long long, true><<<(unsigned)blocks, 256, 0, st>>>(s, n_hash, pi, pj, n_pairs, counts, est);
+        else jaccard_pairs_kernel<long long, false><<<(unsigned)blocks, 256, 0, st>>>(s, n_hash, pi, pj, n_pairs, counts, est);
+    } else if (sig_dtype == MHB_OUT_U32) {
+        const uint32_t* s = static_cast<const uint32_t*>(sig);
+        if (vec) jaccard_pairs_kernel<uint32_t, true><<<(unsigned)blocks, 256, 0, st>>>(s, n_hash, pi, pj, n_pairs, counts, est);
+        else jaccard_pairs_kernel<uint32_t, false><<<(unsigned)blocks, 256, 0, st>>>(s, n_hash, pi, pj, n_pairs, counts, est);
+    } else {
         return set_error(MHB_ERR_INVALID, "unknown sig_dtype %d", sig_dtype);
+    }
     return cuda_check(cudaGetLastError(), "jaccard_pairs launch");
 }
 

@@ -98,23 +98,46 @@ def cfg1_numpy(n_sets: int = 10_000, seed: int | None = None, mean: float = 50.0
 # ---------------------------------------------------------------------------
 
 class _ZipfSampler:
-    """Inverse-CDF sampler for Zipf(s) truncated to ranks 1..V (exact table)."""
+    """Zipf(s) truncated to ranks 1..V, drawn by inverse CDF.
+
+    Ranks <= H (H = min(V, 2^22)) come from an exact float64 CDF table.  For V > H
+    the tail k in (H, V] is drawn by inverting the continuous power law
+    x^-s on [H+1/2, V+1/2] (Euler-Maclaurin midpoint approximation of the discrete
+    tail, relative error ~ s/(24 k^2) per rank), weighted by its approximate mass.
+    """
+
+    HEAD = 1 << 22
 
     def __init__(self, s: float, vocab: int, device):
         import torch
 
-        if vocab > (1 << 26):
-            raise NotImplementedError("exact Zipf table limited to V <= 2^26 in this round")
-        k = torch.arange(1, vocab + 1, dtype=torch.float64, device=device)
-        cdf = torch.cumsum(k.pow(-s), 0)
-        self.cdf = cdf / cdf[-1]
-        self.vocab = vocab
+        self.s, self.vocab = float(s), int(vocab)
+        self.h = min(self.vocab, self.HEAD)
+        k = torch.arange(1, self.h + 1, dtype=torch.float64, device=device)
+        head = torch.cumsum(k.pow(-self.s), 0)
+        head_mass = float(head[-1])
+        if self.vocab > self.h:
+            one_m = 1.0 - self.s
+            self.lo = (self.h + 0.5) ** one_m
+            self.hi = (self.vocab + 0.5) ** one_m
+            tail_mass = (self.hi - self.lo) / one_m
+        else:
+            tail_mass = 0.0
+        self.p_tail = tail_mass / (head_mass + tail_mass)
+        self.cdf = head / head_mass
 
     def sample(self, n: int, gen):
         import torch
 
-        u = torch.rand(n, dtype=torch.float64, device=self.cdf.device, generator=gen)
-        rank0 = torch.searchsorted(self.cdf, u).clamp_(max=self.vocab - 1)
+        dev = self.cdf.device
+        u = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        rank0 = torch.searchsorted(self.cdf, u).clamp_(max=self.h - 1)
+        if self.p_tail > 0:
+            v = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+            in_tail = torch.rand(n, dtype=torch.float64, device=dev, generator=gen) < self.p_tail
+            x = (self.lo + v * (self.hi - self.lo)).pow(1.0 / (1.0 - self.s))
+            tail0 = torch.floor(x + 0.5).to(torch.int64).clamp_(self.h + 1, self.vocab) - 1
+            rank0 = torch.where(in_tail, tail0, rank0)
         return (rank0 * ZIPF_SCRAMBLE) & (self.vocab - 1)
 
 

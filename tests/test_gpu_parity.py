@@ -261,3 +261,21 @@ def test_signature_files_from_gpu(tmp_path, cuda_device, fmt):
         got = tmp_path / f"gpu.{fmt}"
         assert write_signatures_csr(got, indptr, ids, fam, fmt=fmt, obj_ids=obj, chunk_bytes=64 << 10) == 777
         assert got.read_bytes() == ref.read_bytes(), (kind, fmt)
+
+
+@pytest.mark.parametrize("n_hash", [37, 512])
+@pytest.mark.parametrize("dt", ["uint32", "int64"])
+def test_pair_counts_vector_and_scalar_paths(cuda_device, n_hash, dt):
+    import torch
+
+    indptr, ids = gen.cfg1_numpy(n_sets=400, seed=n_hash)
+    fam = make_family("iterative", 2, n_hash, 1_048_583)
+    sig = signatures_csr(*_dev(indptr, ids, cuda_device), fam, out_dtype=dt)
+    rng = np.random.default_rng(1)
+    pi = rng.integers(0, 400, 1000)
+    pj = rng.integers(0, 400, 1000)
+    counts, est = estimate_pairs(sig, torch.as_tensor(pi, device=cuda_device), torch.as_tensor(pj, device=cuda_device))
+    host = sig.cpu().numpy().astype(np.int64)
+    want = (host[pi] == host[pj]).sum(1)
+    assert np.array_equal(counts.cpu().numpy().astype(np.int64), want)
+    assert est.cpu().tolist() == [float(np.mean(host[a] == host[b])) for a, b in zip(pi, pj)]
