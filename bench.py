@@ -412,7 +412,8 @@ def main():
         e2e = {"value": world * n_sets * N / float(e2e_s.item()), "unit": "entries/s",
                "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
                "ms_per_step": float(e2e_s.item()) * 1e3,
-               "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 3 streams)"}
+               "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 4 streams)",
+               "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
 
     aux = None
     if args.aux:

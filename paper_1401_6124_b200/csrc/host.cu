@@ -22,10 +22,12 @@ namespace mhb {
 
 namespace {
 
-constexpr int kLanes = 3;
+constexpr int kLanes = 4;
+constexpr int kMaxChunks = 4096;
 
 struct Lane {
     cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;  // recorded after the lane's last D2H
     int64_t* indptr = nullptr;
     size_t indptr_cap = 0;
     uint32_t* ids = nullptr;
@@ -34,12 +36,12 @@ struct Lane {
     size_t out_cap = 0;
     void* ws = nullptr;
     size_t ws_cap = 0;
-    int32_t* status = nullptr;
 };
 
 struct DeviceCache {
     bool init = false;
     Lane lanes[kLanes];
+    int32_t* status = nullptr;  // one word per chunk, read once at the end
     uint32_t* ra = nullptr;
     uint32_t* rb = nullptr;
     size_t ra_cap = 0;
@@ -124,9 +126,11 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         for (auto& ln : dc.lanes) {
             rc = cuda_check(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking), "stream create");
             if (rc) return rc;
-            rc = cuda_check(cudaMalloc((void**)&ln.status, sizeof(int32_t)), "cudaMalloc status");
+            rc = cuda_check(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming), "event create");
             if (rc) return rc;
         }
+        rc = cuda_check(cudaMalloc((void**)&dc.status, kMaxChunks * sizeof(int32_t)), "cudaMalloc status");
+        if (rc) return rc;
         dc.init = true;
     }
     if (kind == KIND_RANDOM) {
@@ -142,6 +146,7 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     }
 
     const std::vector<Chunk> chunks = plan_chunks(indptr, n_sets, n_hash, out_bytes);
+    if (chunks.size() > (size_t)kMaxChunks) return set_error(MHB_ERR_INVALID, "batch needs more than %d chunks", kMaxChunks);
     int32_t status_acc = 0;
 
     for (size_t c = 0; c < chunks.size(); ++c) {
@@ -150,12 +155,8 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         const int64_t id0 = indptr[s0], id1 = indptr[s1];
         const int64_t cnnz = id1 - id0;
         if (c >= (size_t)kLanes) {
-            // The lane's previous chunk must be fully drained before its buffers are reused;
-            // collect its device status at the same time.
-            if ((rc = cuda_check(cudaStreamSynchronize(ln.stream), "lane sync"))) return rc;
-            int32_t st = 0;
-            cudaMemcpy(&st, ln.status, sizeof(int32_t), cudaMemcpyDeviceToHost);
-            status_acc |= st;
+            // the lane's previous chunk must have drained before its buffers are reused
+            if ((rc = cuda_check(cudaEventSynchronize(ln.done), "lane sync"))) return rc;
         }
         if ((rc = grow((void**)&ln.indptr, &ln.indptr_cap, (size_t)(rows + 1) * sizeof(int64_t)))) return rc;
         if ((rc = grow((void**)&ln.ids, &ln.ids_cap, (size_t)std::max<int64_t>(cnnz, 1) * sizeof(uint32_t))))
@@ -178,20 +179,22 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
             if ((rc = cuda_check(cudaGetLastError(), "rebase_indptr launch"))) return rc;
         }
         rc = launch_sign(kind, ln.indptr, ln.ids, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
-                         out_dtype, ln.status, ln.ws, ln.ws_cap, ln.stream);
+                         out_dtype, dc.status + c, ln.ws, ln.ws_cap, ln.stream);
         if (rc) return rc;
         if ((rc = cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)s0 * n_hash * out_bytes, ln.out,
                                              (size_t)rows * n_hash * out_bytes, cudaMemcpyDeviceToHost, ln.stream),
                              "D2H out")))
             return rc;
+        if ((rc = cuda_check(cudaEventRecord(ln.done, ln.stream), "event record"))) return rc;
     }
     for (int l = 0; l < kLanes && (size_t)l < chunks.size(); ++l) {
-        Lane& ln = dc.lanes[l];
-        if ((rc = cuda_check(cudaStreamSynchronize(ln.stream), "final sync"))) return rc;
-        int32_t st = 0;
-        cudaMemcpy(&st, ln.status, sizeof(int32_t), cudaMemcpyDeviceToHost);
-        status_acc |= st;
+        if ((rc = cuda_check(cudaStreamSynchronize(dc.lanes[l].stream), "final sync"))) return rc;
     }
+    std::vector<int32_t> st(chunks.size());
+    if ((rc = cuda_check(cudaMemcpy(st.data(), dc.status, chunks.size() * sizeof(int32_t), cudaMemcpyDeviceToHost),
+                         "status read")))
+        return rc;
+    for (int32_t v : st) status_acc |= v;
     if (status_host) *status_host = status_acc;
     cudaSetDevice(prev);
     return MHB_OK;
@@ -209,12 +212,13 @@ extern "C" void mhb_host_release(void) {
             cudaFree(ln.ids);
             cudaFree(ln.out);
             cudaFree(ln.ws);
-            cudaFree(ln.status);
+            cudaEventDestroy(ln.done);
             cudaStreamDestroy(ln.stream);
             ln = Lane{};
         }
         cudaFree(dc.ra);
         cudaFree(dc.rb);
+        cudaFree(dc.status);
         dc = DeviceCache{};
     }
 }
