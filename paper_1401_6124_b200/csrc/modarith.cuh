@@ -48,6 +48,28 @@ __device__ __forceinline__ uint32_t mul_add_mod_min3(uint32_t w, uint32_t wp, ui
     return __vimin3_u32(r, r - p, r - 2u * p);
 }
 
+// Variants taking negp = 2^32 - p from an opaque (kernel-parameter) register:
+// r = w*x + c + q*negp is one IMAD per term, where the "- q*p" spelling costs an
+// extra negation of q (IMAD.MOV/IADD3) on the per-visit path.
+__device__ __forceinline__ uint32_t mul_add_mod_narrow_n(uint32_t w, uint32_t wp, uint32_t c, uint32_t x,
+                                                         uint32_t p, uint32_t negp) {
+    const uint32_t q = __umulhi(wp, x);
+    const uint32_t r = w * x + c + q * negp;  // in [0, 3p)
+    return reduce_once(reduce_once(r, p), p);
+}
+__device__ __forceinline__ uint32_t mul_add_mod_n(uint32_t w, uint32_t wp, uint32_t c, uint32_t x, uint32_t p,
+                                                  uint32_t negp) {
+    const uint32_t q = __umulhi(wp, x);
+    const uint32_t r = reduce_once(w * x + q * negp, p);
+    return reduce_once(r + c, p);
+}
+__device__ __forceinline__ uint32_t mul_add_mod_min3_n(uint32_t w, uint32_t wp, uint32_t c, uint32_t x, uint32_t p,
+                                                       uint32_t negp) {
+    const uint32_t q = __umulhi(wp, x);
+    const uint32_t r = w * x + c + q * negp;
+    return __vimin3_u32(r, r + negp, r + 2u * negp);
+}
+
 // Host/device helpers on 64-bit integers (setup only, never per visit).
 __host__ __device__ __forceinline__ uint32_t shoup_companion(uint32_t w, uint32_t p) {
     return (uint32_t)(((uint64_t)w << 32) / p);

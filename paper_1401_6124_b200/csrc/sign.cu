@@ -314,16 +314,16 @@ __device__ __forceinline__ void walk1_iter(uint32_t (&best)[K], uint32_t ha, uin
 template <int K, bool NARROW, bool FIRST>
 __device__ __forceinline__ void walk2_random(uint32_t (&best)[K], const uint32_t (&cA)[K],
                                              const uint32_t (&cAp)[K], const uint32_t (&cB)[K],
-                                             uint32_t xa, uint32_t xb, uint32_t p) {
+                                             uint32_t xa, uint32_t xb, uint32_t p, uint32_t negp) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         uint32_t ra, rb;
         if (NARROW) {
-            ra = mul_add_mod_narrow(cA[k], cAp[k], cB[k], xa, p);
-            rb = mul_add_mod_narrow(cA[k], cAp[k], cB[k], xb, p);
+            ra = mul_add_mod_narrow_n(cA[k], cAp[k], cB[k], xa, p, negp);
+            rb = mul_add_mod_narrow_n(cA[k], cAp[k], cB[k], xb, p, negp);
         } else {
-            ra = mul_add_mod(cA[k], cAp[k], cB[k], xa, p);
-            rb = mul_add_mod(cA[k], cAp[k], cB[k], xb, p);
+            ra = mul_add_mod_n(cA[k], cAp[k], cB[k], xa, p, negp);
+            rb = mul_add_mod_n(cA[k], cAp[k], cB[k], xb, p, negp);
         }
         best[k] = FIRST ? min(ra, rb) : __vimin3_u32(best[k], ra, rb);
     }
@@ -332,11 +332,11 @@ __device__ __forceinline__ void walk2_random(uint32_t (&best)[K], const uint32_t
 template <int K, bool NARROW>
 __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t (&cA)[K],
                                              const uint32_t (&cAp)[K], const uint32_t (&cB)[K],
-                                             uint32_t xa, uint32_t p) {
+                                             uint32_t xa, uint32_t p, uint32_t negp) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        uint32_t ra = NARROW ? mul_add_mod_narrow(cA[k], cAp[k], cB[k], xa, p)
-                             : mul_add_mod(cA[k], cAp[k], cB[k], xa, p);
+        uint32_t ra = NARROW ? mul_add_mod_narrow_n(cA[k], cAp[k], cB[k], xa, p, negp)
+                             : mul_add_mod_n(cA[k], cAp[k], cB[k], xa, p, negp);
         best[k] = min(best[k], ra);
     }
 }
@@ -345,6 +345,7 @@ __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t
 template <int K, bool ITER>
 struct LaneState {
     uint32_t tA, tAp, tB;
+    uint32_t negp;  // 2^32 - p (kernel parameter; random family only)
     uint32_t cA[ITER ? 1 : K], cAp[ITER ? 1 : K], cB[ITER ? 1 : K];
 };
 
@@ -357,7 +358,7 @@ __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, I
         const uint32_t hb = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xb, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
         walk2_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), hb, reduce_once(xb + bpar, p), p);
     } else {
-        walk2_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p);
+        walk2_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p, ls.negp);
     }
 }
 
@@ -368,7 +369,7 @@ __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, I
         const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
         walk1_iter<K>(best, ha, reduce_once(xa + bpar, p), p);
     } else {
-        walk1_random<K, NARROW>(best, ls.cA, ls.cAp, ls.cB, xa, p);
+        walk1_random<K, NARROW>(best, ls.cA, ls.cAp, ls.cB, xa, p, ls.negp);
     }
 }
 
@@ -442,7 +443,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
 template <int K, bool ITER, bool NARROW, typename OutT>
-__global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar) {
+__global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -478,6 +479,7 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
     VSet en = load_vset(A, itn, n_vsets, f);
 
     LaneState<K, ITER> ls;
+    ls.negp = negp;
     int cur_sb = -1;
     uint32_t maxid = 0;
 
@@ -611,7 +613,7 @@ int g_prof_cap = 0, g_prof_n = 0, g_prof_dev = -1;
 cudaEvent_t* g_prof_ev = nullptr;
 }  // namespace
 
-using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t);
+using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t);
 
 template <bool ITER, bool NARROW, typename OutT>
 static SignKernelFn pick_kernel(int K) {
@@ -775,7 +777,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
     }
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b);
+    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p);
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
     rc = cuda_check(cudaGetLastError(), "sign_kernel launch");
     if (rc) return rc;

@@ -5,7 +5,7 @@ set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 OUT=$ROOT/tools/variants; mkdir -p $OUT/obj_$1
 NV="nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -I$ROOT/include -I$ROOT/paper_1401_6124_b200/csrc"
-for f in common aux host; do $NV -c $ROOT/paper_1401_6124_b200/csrc/$f.cu -o $OUT/obj_$1/$f.o & done
+for src in $ROOT/paper_1401_6124_b200/csrc/*.cu; do f=$(basename $src .cu); [ $f = sign ] && continue; $NV -c $src -o $OUT/obj_$1/$f.o & done
 cp "$2" $OUT/obj_$1/sign.cu
 $NV -c $OUT/obj_$1/sign.cu -o $OUT/obj_$1/sign.o &
 wait
