@@ -39,8 +39,10 @@
  *    mirrors minhash.py:99-101.  Rows with a flagged error hold unspecified ids.
  *  - Return value: MHB_OK or an MHB_ERR_* code; mhb_last_error() gives the text
  *    (thread-local).  Argument errors are detected before any launch.
- *  - Supported modulus: 3 <= prime < 2^31, prime must be prime.  (Every BASELINE
- *    configuration qualifies: the largest prime used is 1,073,741,827.)
+ *  - Supported modulus: 3 <= prime < 2^63, prime must be prime.  Primes < 2^31 (every
+ *    BASELINE configuration: the largest is 1,073,741,827) run the tuned u32 kernels;
+ *    2^31 <= p < 2^63 runs a correctness-first 64-bit path (wide.cu), the analogue of
+ *    the reference's int64 / exact fallback paths (minhash.py:102-127).
  */
 #ifndef MHB_H_
 #define MHB_H_
@@ -101,6 +103,15 @@ int mhb_sign_random_csr(const int64_t* indptr, const uint32_t* ids,
                         const uint32_t* a, const uint32_t* b, uint64_t prime, int32_t n_hash,
                         void* out, int32_t out_dtype, int32_t* status,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Random family with 64-bit parameters (a, b: device uint64[n_hash]), required for
+ * primes >= 2^31; any prime < 2^63.  No workspace.
+ */
+int mhb_sign_random_csr_u64(const int64_t* indptr, const uint32_t* ids,
+                            int64_t n_sets, int64_t nnz,
+                            const uint64_t* a, const uint64_t* b, uint64_t prime, int32_t n_hash,
+                            void* out, int32_t out_dtype, int32_t* status, void* stream);
 
 /*
  * Host-buffer entry (the end-to-end path an FFI caller uses): indptr/ids/out are

@@ -671,11 +671,15 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
     if (prime < 3 || !is_prime_u64(prime)) return set_error(MHB_ERR_INVALID, "modulus %llu is not prime",
                                                              (unsigned long long)prime);
-    if (prime >= (1ull << 31))
-        return set_error(MHB_ERR_UNSUPPORTED, "prime %llu >= 2^31 is outside the u32 kernels' range",
-                         (unsigned long long)prime);
+    if (prime >= (1ull << 63))
+        return set_error(MHB_ERR_UNSUPPORTED, "prime %llu >= 2^63 is out of range", (unsigned long long)prime);
     if (out_dtype != MHB_OUT_U32 && out_dtype != MHB_OUT_I64)
         return set_error(MHB_ERR_INVALID, "unknown out_dtype %d", out_dtype);
+    const bool wide = prime >= (1ull << 31);
+    if (wide && kind == KIND_RANDOM)
+        return set_error(MHB_ERR_UNSUPPORTED,
+                         "prime %llu >= 2^31: random-family parameters need 64 bits, use mhb_sign_random_csr_u64",
+                         (unsigned long long)prime);
     if (kind == KIND_ITERATIVE) {
         if (a < 1 || a >= prime || b >= prime)
             return set_error(MHB_ERR_INVALID, "need 1 <= a < p and 0 <= b < p");
@@ -690,6 +694,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         return set_error(MHB_ERR_INVALID, "null indptr/out");
     if (nnz > 0 && ids == nullptr) return set_error(MHB_ERR_INVALID, "null ids");
     if (n_sets >= (1ll << 51)) return set_error(MHB_ERR_INVALID, "too many sets");
+
+    if (wide)  // 64-bit residues; no workspace needed
+        return launch_sign_wide(true, indptr, ids, n_sets, a, b, nullptr, nullptr, prime, n_hash, out, out_dtype,
+                                status, st);
 
     const WorkspaceLayout wl = workspace_layout(n_sets, nnz, n_hash);
     if (workspace == nullptr || workspace_bytes < wl.total)

@@ -74,6 +74,11 @@ struct SignArgs {
 };
 
 Geometry choose_geometry(int kind, int32_t n_hash);
+
+// 64-bit-residue path for primes 2^31 <= p < 2^63 (wide.cu).
+int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, uint64_t a, uint64_t b,
+                     const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash, void* out,
+                     int32_t out_dtype, int32_t* status, cudaStream_t st);
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash);
 
 int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,

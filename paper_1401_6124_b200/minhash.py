@@ -98,13 +98,14 @@ def _torch():
     return torch
 
 
+MAX_ID = 2**32 - 1  # CSR feature ids are uint32
+
+
 def _check_family(family: Family) -> None:
     if not isinstance(family, (IterativeFamily, RandomFamily)):
         raise TypeError(f"unsupported family type {type(family).__name__}")
-    if family.prime > MAX_KERNEL_PRIME:
-        raise NotImplementedError(
-            f"prime {family.prime} >= 2^31: the u32 CUDA kernels cover every prime < 2^31 "
-            f"(all BASELINE configurations); wider moduli are not implemented")
+    if family.prime >= 2**63:
+        raise NotImplementedError(f"prime {family.prime} >= 2^63 is outside the reference's range too")
 
 
 def _raise_status(status: int, family: Family) -> None:
@@ -137,6 +138,11 @@ def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) 
                                             family.base.a, family.base.b, family.prime, n_hash,
                                             out.data_ptr(), out_dtype, status_ptr,
                                             ws.data_ptr(), ws_bytes, sptr)
+        elif family.prime > MAX_KERNEL_PRIME:
+            a, b = family.device_params(dev, wide=True)
+            rc = lib.mhb_sign_random_csr_u64(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
+                                             a.data_ptr(), b.data_ptr(), family.prime, n_hash,
+                                             out.data_ptr(), out_dtype, status_ptr, sptr)
         else:
             a, b = family.device_params(dev)
             rc = lib.mhb_sign_random_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
@@ -167,11 +173,14 @@ def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
     if not (ids.is_cuda and indptr.is_cuda):
         raise ValueError("signatures_csr needs CUDA tensors (or numpy arrays for the host pipeline)")
     if ids.dtype != torch.uint32:
-        if ids.dtype in (torch.int64, torch.int32) and validate:
-            if ids.numel() and int(ids.min()) < 0:
+        if ids.dtype in (torch.int64, torch.int32) and ids.numel():
+            lo, hi = int(ids.min()), int(ids.max())
+            if lo < 0:
                 raise ValueError("feature ids must be non-negative")
-            if ids.numel() and int(ids.max()) >= family.prime:
-                raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+            if hi >= family.prime:
+                raise ValueError(f"feature id {hi} >= family prime {family.prime}")
+            if hi > MAX_ID:
+                raise NotImplementedError(f"feature id {hi} >= 2^32: CSR ids are uint32")
         ids = ids.to(torch.uint32)
     ids = ids.contiguous()
     indptr = indptr.to(torch.int64).contiguous()
@@ -193,11 +202,16 @@ def _signatures_csr_host(indptr, ids, family, out_dtype, out, device):
     lib = _lib.load()
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     if ids.dtype != np.uint32:
-        if ids.size and (ids.min() < 0 or ids.max() >= family.prime):
+        if ids.size and (ids.min() < 0 or ids.max() >= family.prime or ids.max() > MAX_ID):
             if ids.min() < 0:
                 raise ValueError("feature ids must be non-negative")
-            raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+            if ids.max() >= family.prime:
+                raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
+            raise NotImplementedError(f"feature id {int(ids.max())} >= 2^32: CSR ids are uint32")
         ids = ids.astype(np.uint32)
+    if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:
+        raise NotImplementedError("host pipeline with primes >= 2^31 supports the iterative family; "
+                                  "pass device tensors for the random family")
     ids = np.ascontiguousarray(ids)
     n_sets = indptr.size - 1
     ndt = np.int64 if out_dtype == "int64" else np.uint32
@@ -231,6 +245,8 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         raise ValueError("cannot build a signature for an empty feature set")
     if s.max_id >= family.prime:
         raise ValueError(f"feature id {s.max_id} >= family prime {family.prime}")
+    if s.max_id > MAX_ID:
+        raise NotImplementedError(f"feature id {s.max_id} >= 2^32: CSR ids are uint32")
     torch = _torch()
     _check_family(family)
     dev = torch.device("cuda", torch.cuda.current_device())

@@ -197,7 +197,30 @@ def jaccard_fixture():
     (HERE / "jaccard.json").write_text(json.dumps({"families": meta, "estimates": est, "exact": exact}))
 
 
+def wide_fixture():
+    """Primes >= 2^31: the reference's int64 numba path (p <= MAX_VECTOR_PRIME) and its
+    exact `_signature_by_rows` fallback beyond (minhash.py:102-127)."""
+    rng = np.random.default_rng(31)
+    rows = [np.sort(rng.choice(1 << 31, size=int(k), replace=False)) for k in rng.integers(1, 40, 24)]
+    indptr, ids = csr_from_rows(rows)
+    arrays = {"indptr": indptr, "ids": ids}
+    meta = []
+    primes = (ref.next_prime(2**31), ref.next_prime(3_000_000_000), ref.next_prime(3_037_000_500),
+              ref.next_prime(2**62))
+    n = 0
+    for p in primes:
+        for kind, hashes in (("iterative", 37), ("random", 19)):
+            seed = int(rng.integers(0, 2**62))
+            fam = ref.make_family(kind, seed, hashes, p)
+            arrays[f"out{n}"] = ref_sign_csr(indptr, ids, fam)
+            meta.append({"kind": kind, "seed": seed, "n": hashes, "p": p})
+            n += 1
+    np.savez_compressed(HERE / "wide.npz", **arrays)
+    (HERE / "wide.json").write_text(json.dumps(meta))
+
+
 if __name__ == "__main__":
+    wide_fixture()
     families_fixture()
     known_answers()
     fuzz_fixture()

@@ -58,13 +58,19 @@ def test_argument_errors_before_launch(prime, a, n, err):
         _lib.check(rc)
 
 
-def test_unsupported_wide_prime():
+def test_prime_range_limits():
     lib = _lib.load()
-    p = 2_147_483_659  # smallest prime above 2^31
-    rc = lib.mhb_sign_iterative_csr(None, None, 0, 0, 5, 3, p, 4, None, 0, None, None, 0, None)
+    p63 = 2**63 + 29  # first prime above 2^63: beyond the reference's 64-bit range too
+    rc = lib.mhb_sign_iterative_csr(None, None, 0, 0, 5, 3, p63, 4, None, 0, None, None, 0, None)
     assert rc == _lib.MHB_ERR_UNSUPPORTED
     with pytest.raises(NotImplementedError):
         _lib.check(rc)
+    wide = 2_147_483_659  # smallest prime above 2^31: supported (64-bit path), no work for n_sets=0
+    assert lib.mhb_sign_iterative_csr(None, None, 0, 0, 5, 3, wide, 4, None, 0, None, None, 0, None) == _lib.MHB_OK
+    dummy = C.c_int64(0)
+    rc = lib.mhb_sign_random_csr(None, None, 0, 0, C.addressof(dummy), C.addressof(dummy), wide, 4,
+                                 None, 0, None, None, 0, None)
+    assert rc == _lib.MHB_ERR_UNSUPPORTED and "u64" in _lib.last_error()
 
 
 def test_workspace_too_small_rejected():

@@ -81,7 +81,10 @@ def test_no_cpu_fallback_for_signing():
         signatures_csr(torch.tensor([0, 2]), torch.tensor([1, 2], dtype=torch.int64), fam)
 
 
-def test_wide_primes_rejected_explicitly():
-    fam = make_family("iterative", 1, 8, 2_147_483_659)
-    with pytest.raises(NotImplementedError):
-        signatures_csr(np.array([0, 1]), np.array([5], dtype=np.uint32), fam)
+def test_out_of_range_inputs_rejected_before_cuda():
+    """Checked on the host before any device work (so this runs on CPU)."""
+    fam = make_family("iterative", 1, 8, 2**61 - 1)  # a wide prime: supported on the device
+    with pytest.raises(NotImplementedError, match="2\\^32"):
+        signatures_csr(np.array([0, 1]), np.array([2**33], dtype=np.int64), fam)
+    with pytest.raises(ValueError):
+        signatures_csr(np.array([0, 1]), np.array([-1], dtype=np.int64), fam)

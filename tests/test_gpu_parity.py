@@ -279,3 +279,15 @@ def test_pair_counts_vector_and_scalar_paths(cuda_device, n_hash, dt):
     want = (host[pi] == host[pj]).sum(1)
     assert np.array_equal(counts.cpu().numpy().astype(np.int64), want)
     assert est.cpu().tolist() == [float(np.mean(host[a] == host[b])) for a, b in zip(pi, pj)]
+
+
+def test_wide_primes_match_reference(golden, cuda_device):
+    """Primes 2^31 .. 2^62: the 64-bit path equals the reference's outputs."""
+    z = np.load(golden / "wide.npz")
+    meta = json.loads((golden / "wide.json").read_text())
+    ip, di = _dev(z["indptr"], z["ids"].astype(np.int64), cuda_device)
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        for dt in ("int64", "uint32"):
+            got = signatures_csr(ip, di, fam, out_dtype=dt).cpu().numpy().astype(np.int64)
+            assert np.array_equal(got, z[f"out{k}"]), (m, dt)

@@ -99,3 +99,15 @@ def test_oracle_thread_count_invariant(threads):
     a = oracle.sign_family_csr(indptr, ids, fam, threads=threads)
     b = oracle.sign_family_csr(indptr, ids, fam, threads=1)
     assert np.array_equal(a, b)
+
+
+def test_wide_primes_restatement(golden):
+    """Reference outputs for primes >= 2^31 (incl. its exact fallback beyond 3.04e9)
+    equal the Python-int brute force (test_minhash.py:27-39)."""
+    z = np.load(golden / "wide.npz")
+    meta = json.loads((golden / "wide.json").read_text())
+    ip, ids = z["indptr"], z["ids"]
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        for s in range(ip.size - 1):
+            assert np.array_equal(oracle.brute_force_row(ids[ip[s]:ip[s + 1]], fam), z[f"out{k}"][s]), m
