@@ -442,7 +442,7 @@ def main():
                        "parallelism": f"dp{world} (row shards, no collective in the step)",
                        "gen_seconds": round(gen_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 3 * args.steps, "clocks": clocks,
+            "gpu_launches": 5 * args.steps, "clocks": clocks,  # plan_count, plan_scan, plan_scatter, sign, finalize
         }
         if gather_ms is not None:
             line["gather_ms"] = gather_ms

@@ -291,3 +291,23 @@ def test_wide_primes_match_reference(golden, cuda_device):
         for dt in ("int64", "uint32"):
             got = signatures_csr(ip, di, fam, out_dtype=dt).cpu().numpy().astype(np.int64)
             assert np.array_equal(got, z[f"out{k}"]), (m, dt)
+
+
+def test_plain_c_consumer_of_the_abi(cuda_device):
+    """tests/c/abi_smoke.c: a C program (no Python/torch) linking libmhb through include/mhb.h."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    src = root / "tests" / "c" / "abi_smoke.c"
+    exe = root / "tests" / "c" / "abi_smoke"
+    gcc = shutil.which("gcc")
+    if gcc:
+        cmd = [gcc, "-O2", str(src), f"-I{root / 'include'}", "-I/usr/local/cuda/include",
+               f"-L{root / 'paper_1401_6124_b200' / 'lib'}", "-lmhb", "-L/usr/local/cuda/lib64", "-lcudart",
+               f"-Wl,-rpath,{root / 'paper_1401_6124_b200' / 'lib'}", "-o", str(exe)]
+        subprocess.run(cmd, check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "abi_smoke ok" in r.stdout
