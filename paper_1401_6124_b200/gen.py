@@ -93,6 +93,37 @@ def cfg1_numpy(n_sets: int = 10_000, seed: int | None = None, mean: float = 50.0
     return indptr, ids
 
 
+def synth_corpus_numpy(n_docs: int, doc_size: int, seed: int, id_space: int | None = None):
+    """The reference's synthetic timing corpus as CSR (restates corpus.synth_corpus,
+    corpus.py:114-130): sizes uniform in [round(0.8 s), round(1.2 s)], distinct ids drawn
+    with Generator.choice over id_space = max(1024, n_docs*doc_size//5), sorted like
+    FeatureSet.  The same numpy calls in the same order, so the sets are identical."""
+    if n_docs < 1 or doc_size < 1:
+        raise ValueError("need positive document count and size")
+    if id_space is None:
+        id_space = max(1024, n_docs * doc_size // 5)
+    lo = max(1, round(0.8 * doc_size))
+    hi = max(lo, round(1.2 * doc_size))
+    if id_space < hi:
+        raise ValueError(f"id space {id_space} too small for documents of ~{doc_size}")
+    rng = np.random.default_rng(int(seed))
+    rows = []
+    for _ in range(n_docs):
+        sz = int(rng.integers(lo, hi + 1))
+        rows.append(np.sort(rng.choice(id_space, size=sz, replace=False)))
+    indptr = np.zeros(n_docs + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in rows], out=indptr[1:])
+    return indptr, np.concatenate(rows).astype(np.uint32)
+
+
+def c6_workload():
+    """Acceptance criterion C6 / the paper's Table 3 timing shape (tests/test_acceptance.py:134-149):
+    500 documents of ~100 ids, N = 100,000 hashes, prime = choose_prime(max id, N)."""
+    indptr, ids = synth_corpus_numpy(500, 100, derive_seed(MASTER_SEED, 6, 0))
+    prime = choose_prime(int(ids.max()), 100_000)
+    return indptr, ids, prime, derive_seed(MASTER_SEED, 6, 1)
+
+
 # ---------------------------------------------------------------------------
 # torch: full-size workloads (GPU) with the same distributions
 # ---------------------------------------------------------------------------

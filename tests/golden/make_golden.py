@@ -219,7 +219,18 @@ def wide_fixture():
     (HERE / "wide.json").write_text(json.dumps(meta))
 
 
+def synth_corpus_fixture():
+    """The reference's synth_corpus for the C6 timing workload: checksum of its sets."""
+    docs = ref_corpus.synth_corpus(500, 100, ref.derive_seed(20260810, 6, 0))
+    blob = b"".join(np.asarray(d.ids, dtype=np.int64).tobytes() + b"|" for d in docs)
+    meta = {"n_docs": 500, "doc_size": 100, "seed": ref.derive_seed(20260810, 6, 0),
+            "sha256": hashlib.sha256(blob).hexdigest(),
+            "prime": ref.choose_prime(max(d.max_id for d in docs), 100_000)}
+    (HERE / "c6.json").write_text(json.dumps(meta, indent=1))
+
+
 if __name__ == "__main__":
+    synth_corpus_fixture()
     wide_fixture()
     families_fixture()
     known_answers()

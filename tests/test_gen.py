@@ -50,3 +50,13 @@ def test_poisson_configs():
         ip, ids = gen.make_csr(cfg, device="cpu", n_sets=500)
         ip, _ = _check_csr(ip, ids, cfg.vocab)
         assert abs(np.diff(ip).mean() - cfg.size_a) < 0.1 * cfg.size_a
+
+
+def test_synth_corpus_matches_reference(golden):
+    """gen.synth_corpus_numpy reproduces the reference's synth_corpus sets exactly."""
+    meta = json.loads((golden / "c6.json").read_text())
+    indptr, ids = gen.synth_corpus_numpy(meta["n_docs"], meta["doc_size"], meta["seed"])
+    blob = b"".join(ids[indptr[s]:indptr[s + 1]].astype(np.int64).tobytes() + b"|" for s in range(indptr.size - 1))
+    assert hashlib.sha256(blob).hexdigest() == meta["sha256"]
+    _, _, prime, _ = gen.c6_workload()
+    assert prime == meta["prime"]

@@ -55,6 +55,79 @@ __global__ void __launch_bounds__(256) walk_mixed(int rounds, uint32_t p, uint32
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// Lookahead walk where odd lanes skip the reduction: best = min3(min3(best, t, t-p), u, u-p)
+// with t = hA + da, u = hB + db unreduced.  PHI: 1 = every odd lane, 2 = every other odd lane.
+__device__ __forceinline__ uint32_t mad1(uint32_t h, uint32_t one, uint32_t d) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(h), "r"(one), "r"(d));
+    return r;
+}
+
+template <int K, int PHI>
+__global__ void __launch_bounds__(256) walk_unred(int rounds, uint32_t p, uint32_t seed, long long* cyc, uint32_t one) {
+    uint32_t best[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
+    uint32_t h0a = (threadIdx.x * 2654435761u + seed) % p, h0b = (threadIdx.x * 40503u + 7u * seed) % p;
+    const uint32_t da = (blockIdx.x * 40503u + 17u + seed) % p, db = (blockIdx.x * 977u + 5u) % p;
+    const uint32_t da2 = (2 * da) % p, db2 = (2 * db) % p;
+    const uint32_t dam = da - p, dbm = db - p;
+    long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r) {
+        uint32_t ha = h0a, hb = h0b;
+#pragma unroll
+        for (int k = 0; k < K; k += 2) {
+            best[k] = __vimin3_u32(best[k], ha, hb);
+            if (PHI > 0 && ((k / 2) % PHI == 0)) {
+                best[k + 1] = __vimin3_u32(__vimin3_u32(best[k + 1], mad1(ha, one, da), mad1(ha, one, dam)),
+                                           mad1(hb, one, db), mad1(hb, one, dbm));
+            } else {
+                best[k + 1] = __vimin3_u32(best[k + 1], red(ha + da, p), red(hb + db, p));
+            }
+            ha = red(ha + da2, p);
+            hb = red(hb + db2, p);
+        }
+        h0a = red(h0a + (uint32_t)r, p);
+        h0b = red(h0b + 3u, p);
+    }
+    long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_sink = acc;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int K, int PHI>
+void run_unred(const char* name, int sms, int occ_cap) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, walk_unred<K, PHI>, 256, 0);
+    if (occ > occ_cap) occ = occ_cap;
+    int blocks = occ * sms;
+    long long* cyc;
+    cudaMalloc(&cyc, blocks * sizeof(long long));
+    int rounds = 2000;
+    walk_unred<K, PHI><<<blocks, 256>>>(rounds / 10, 16777259u, 1u, cyc, 1u);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    walk_unred<K, PHI><<<blocks, 256>>>(rounds, 16777259u, 2u, cyc, 1u);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long* h = new long long[blocks];
+    cudaMemcpy(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long mx = 0;
+    for (int i = 0; i < blocks; ++i) mx = h[i] > mx ? h[i] : mx;
+    double visits = (double)blocks * 256 * rounds * K * 2;
+    printf("%-22s K=%3d PHI=%d occ=%d  %.2f Tvisit/s  %.2f visits/clk/SM\n", name, K, PHI, occ,
+           visits / (ms * 1e-3) / 1e12, visits / sms / (double)mx);
+    delete[] h;
+    cudaFree(cyc);
+}
+
 template <int K, int M>
 void run_mixed(const char* name, int sms, int occ_cap) {
     int occ = 0;
@@ -205,6 +278,10 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     printf("SMs=%d (ALU-pipe ceiling at 1.5 ALU instr/visit = 42.7 visits/clk/SM)\n", sms);
     run<64, 2, 2>("lookahead occ2", sms, 2);
+    run_unred<64, 0>("unred off", sms, 2);
+    run_unred<64, 1>("unred all odd", sms, 2);
+    run_unred<64, 2>("unred 1/2 odd", sms, 2);
+    run_unred<64, 3>("unred 1/3 odd", sms, 2);
     run_mixed<64, 0>("mixed off", sms, 2);
     run_mixed<64, 2>("mixed 1/4", sms, 2);
     run_mixed<64, 3>("mixed 1/6", sms, 2);
