@@ -221,7 +221,8 @@ def _aux_kernels(cfg, fam, indptr, ids, out, exact_j, dev):
     import numpy as np
     import torch
 
-    from paper_1401_6124_b200 import bucket_histogram, estimate_pairs, jaccard_block
+    from paper_1401_6124_b200 import (IterativeFamily, band_keys, bucket_histogram, estimate_pairs,
+                                      jaccard_block, signatures_band_keys, signatures_csr)
 
     res = {}
     n_sets = indptr.numel() - 1
@@ -247,6 +248,21 @@ def _aux_kernels(cfg, fam, indptr, ids, out, exact_j, dev):
     chi2 = float((((h.double() - tot / 4096) ** 2) / (tot / 4096)).sum())
     res["bucket_hist"] = {"distinct_ids": int(xs.numel()), "bins": 4096, "ms": ms_h,
                           "evals_per_s": xs.numel() * fam.size / (ms_h / 1e3), "chi2_dof4095": chi2}
+    # LSH band keys (16 rows per band): from the stored matrix vs fused into the signing epilogue
+    if fam.size % 16 == 0:
+        rows = 16
+        ms_k = _time_cuda(lambda: band_keys(out, rows), reps=5)
+        res["band_keys"] = {"rows_per_band": rows, "bands": fam.size // rows, "ms": ms_k,
+                            "sig_gbs": out.numel() * out.element_size() / (ms_k / 1e3) / 1e9}
+        if isinstance(fam, IterativeFamily):
+            sep = _time_cuda(lambda: band_keys(signatures_csr(indptr, ids, fam, out_dtype="uint32",
+                                                              validate=False), rows), reps=5)
+            fused = _time_cuda(lambda: signatures_band_keys(indptr, ids, fam, rows, validate=False), reps=5)
+            keys_only = _time_cuda(lambda: signatures_band_keys(indptr, ids, fam, rows, write_signatures=False,
+                                                                validate=False), reps=5)
+            _, k_f = signatures_band_keys(indptr, ids, fam, rows, validate=False)
+            res["band_keys"].update({"sign_then_keys_ms": sep, "fused_ms": fused, "fused_keys_only_ms": keys_only,
+                                     "fused_equal": bool(torch.equal(k_f.view(torch.int64), band_keys(out, rows).view(torch.int64)))})
     return res
 
 

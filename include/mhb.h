@@ -105,6 +105,21 @@ int mhb_sign_random_csr(const int64_t* indptr, const uint32_t* ids,
                         void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * Iterative signatures with the LSH band keys of mhb_band_keys computed in the
+ * signing epilogue (no re-read of the signature matrix).  keys: device uint64
+ * [n_sets * n_hash/rows_per_band].  write_signatures = 0 skips storing the
+ * signatures (out is still required: long sets use their rows as merge scratch).
+ * Needs the K = 32/64 lane geometry (n_hash >= 32), rows_per_band a multiple of 4
+ * dividing both K and n_hash, and prime < 2^31; else MHB_ERR_UNSUPPORTED.
+ */
+int mhb_sign_iterative_csr_bands(const int64_t* indptr, const uint32_t* ids,
+                                 int64_t n_sets, int64_t nnz,
+                                 uint64_t a, uint64_t b, uint64_t prime, int32_t n_hash,
+                                 int32_t rows_per_band, unsigned long long* keys,
+                                 void* out, int32_t out_dtype, int32_t write_signatures, int32_t* status,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Random family with 64-bit parameters (a, b: device uint64[n_hash]), required for
  * primes >= 2^31; any prime < 2^63.  No workspace.
  */

@@ -22,6 +22,7 @@ from .minhash import (
     FeatureSet,
     Signature,
     band_keys,
+    signatures_band_keys,
     estimate_jaccard,
     estimate_pairs,
     exact_jaccard,
@@ -43,7 +44,7 @@ __version__ = "0.1.0"
 __all__ = [
     "FAMILY_KINDS", "HashParams", "IterativeFamily", "RandomFamily", "derive_seed", "family_from_json",
     "family_to_json", "make_family", "make_iterative_family", "sample_random_family", "FeatureSet",
-    "Signature", "band_keys", "estimate_jaccard", "estimate_pairs", "exact_jaccard", "jaccard_block",
+    "Signature", "band_keys", "signatures_band_keys", "estimate_jaccard", "estimate_pairs", "exact_jaccard", "jaccard_block",
     "read_signatures_binary", "read_signatures_text", "sign_csr_device", "signature", "signatures",
     "signatures_csr", "write_signatures_binary", "write_signatures_text", "MAX_KERNEL_PRIME",
     "MAX_VECTOR_PRIME", "choose_prime", "is_prime", "mulmod", "next_prime", "bucket_histogram",

@@ -258,6 +258,15 @@ __device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, ui
 // Long-set chunks merge with a fire-and-forget `red.global.min`.  Written as PTX:
 // the C++ atomicMin in this loop makes ptxas move p out of the uniform datapath
 // (every VIADDMNMX then reads -p from a vector register: -10% visit rate).
+// LSH band keys (include/mhb.h): splitmix64(FNV-1a-64 over the band's argmin ids,
+// seeded with 0xCBF29CE484222325 ^ band).
+__device__ __forceinline__ unsigned long long band_mix(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 __device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) {
     asm volatile("red.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -402,7 +411,7 @@ __device__ __forceinline__ void dump_best(const uint32_t (&best)[K], uint32_t* r
             make_uint4(best[4 * q], best[4 * q + 1], best[4 * q + 2], best[4 * q + 3]);
 }
 
-template <int K, typename OutT, bool EPI_SMEM>
+template <int K, typename OutT, bool EPI_SMEM, bool BANDS>
 __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
                                            bool merge, int64_t i0, const InvTab* epi_s) {
     constexpr int NQ = K / 4;
@@ -411,6 +420,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
     const int32_t N = A.n_hash;
     const bool vec_ok = (N & 3) == 0;
     OutT* row = reinterpret_cast<OutT*>(A.out) + set * (int64_t)N;
+    unsigned long long hk = 0;  // running band hash (BANDS)
 #pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
         const int64_t i = i0 + 4 * q;
@@ -429,6 +439,16 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
             const InvTab t = EPI_SMEM ? epi_s[i + e] : A.inv[min(i + e, A.n_tot - 1)];
             x[e] = invert_entry(t, h[e], p);
         }
+        if constexpr (BANDS) {
+            // bands are runs of A.rows lanes; rows divides K and n_hash, so a band never
+            // straddles threads or the row end
+            const int64_t band = i / A.rows;
+            if (i - band * A.rows == 0) hk = 0xCBF29CE484222325ull ^ (unsigned long long)band;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hk = (hk ^ (unsigned long long)x[e]) * 0x100000001B3ull;
+            if (i + 4 - band * A.rows == A.rows) A.keys[set * (int64_t)(N / A.rows) + band] = band_mix(hk);
+            if (!A.write_sig) continue;
+        }
         if (vec_ok && i + 3 < N) {
             store4(row + i, x[0], x[1], x[2], x[3]);
         } else {
@@ -442,7 +462,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
-template <int K, bool ITER, bool NARROW, typename OutT>
+template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false>
 __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -575,8 +595,8 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
             const bool merge = (ec.meta >> 11) & 1;
             const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
             dump_best<K>(best, dump_row, lane);
-            if (epi_smem) emit_lanes<K, OutT, true>(A, dump_row, lane, set, merge, i0, epi_s);
-            else emit_lanes<K, OutT, false>(A, dump_row, lane, set, merge, i0, epi_s);
+            if (epi_smem) emit_lanes<K, OutT, true, BANDS>(A, dump_row, lane, set, merge, i0, epi_s);
+            else emit_lanes<K, OutT, false, BANDS>(A, dump_row, lane, set, merge, i0, epi_s);
         }
 
         it = itn;
@@ -594,9 +614,20 @@ __global__ void finalize_kernel(SignArgs A) {
     const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
     OutT* out = reinterpret_cast<OutT*>(A.out);
     for (unsigned long long e = blockIdx.x; e < n_big; e += gridDim.x) {
-        OutT* row = out + A.big[e] * (int64_t)A.n_hash;
+        const int64_t s = A.big[e];
+        OutT* row = out + s * (int64_t)A.n_hash;
         for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x)
             row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
+        if (A.keys) {  // band keys of long sets (their chunks merged in `out`)
+            __syncthreads();
+            const int n_bands = A.n_hash / A.rows;
+            for (int band = threadIdx.x; band < n_bands; band += blockDim.x) {
+                unsigned long long hk = 0xCBF29CE484222325ull ^ (unsigned long long)band;
+                for (int j = 0; j < A.rows; ++j) hk = (hk ^ (unsigned long long)(uint32_t)row[band * A.rows + j]) * 0x100000001B3ull;
+                A.keys[s * (int64_t)n_bands + band] = band_mix(hk);
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -624,6 +655,19 @@ static SignKernelFn pick_kernel(int K) {
         default: break;
     }
     if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT>;
+    return nullptr;
+}
+
+static SignKernelFn select_bands_kernel(bool narrow, int out_dtype, int K) {
+    const bool i64 = out_dtype == MHB_OUT_I64;
+    if (K == 64) {
+        if (narrow) return i64 ? sign_kernel<64, true, true, long long, true> : sign_kernel<64, true, true, uint32_t, true>;
+        return i64 ? sign_kernel<64, true, false, long long, true> : sign_kernel<64, true, false, uint32_t, true>;
+    }
+    if (K == 32) {
+        if (narrow) return i64 ? sign_kernel<32, true, true, long long, true> : sign_kernel<32, true, true, uint32_t, true>;
+        return i64 ? sign_kernel<32, true, false, long long, true> : sign_kernel<32, true, false, uint32_t, true>;
+    }
     return nullptr;
 }
 
@@ -665,7 +709,8 @@ static int blocks_per_sm(SignKernelFn fn, size_t smem, const DeviceInfo& dev) {
 int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
                 uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
                 int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,
-                size_t workspace_bytes, cudaStream_t st) {
+                size_t workspace_bytes, cudaStream_t st, unsigned long long* keys, int32_t rows_per_band,
+                int32_t write_sig) {
     clear_error();
     if (n_sets < 0 || nnz < 0) return set_error(MHB_ERR_INVALID, "n_sets and nnz must be >= 0");
     if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
@@ -731,6 +776,9 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.out = out;
     A.ra = ra;
     A.rb = rb;
+    A.keys = keys;
+    A.rows = rows_per_band;
+    A.write_sig = write_sig;
 
     // sched and hist are contiguous at the start of the workspace
     int rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
@@ -768,7 +816,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     }
 
     const bool narrow = (3ull * prime) < (1ull << 32);
-    SignKernelFn fn = select_kernel(kind, narrow, out_dtype, geo.K);
+    SignKernelFn fn = keys ? select_bands_kernel(narrow, out_dtype, geo.K) : select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
@@ -867,6 +915,28 @@ extern "C" int mhb_sign_iterative_csr(const int64_t* indptr, const uint32_t* ids
     return mhb::launch_sign(mhb::KIND_ITERATIVE, indptr, ids, n_sets, nnz, a, b, nullptr, nullptr,
                             prime, n_hash, out, out_dtype, status, workspace, workspace_bytes,
                             static_cast<cudaStream_t>(stream));
+}
+
+// Iterative signatures with LSH band keys fused into the epilogue.
+extern "C" int mhb_sign_iterative_csr_bands(const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
+                                            uint64_t a, uint64_t b, uint64_t prime, int32_t n_hash,
+                                            int32_t rows_per_band, unsigned long long* keys, void* out,
+                                            int32_t out_dtype, int32_t write_signatures, int32_t* status,
+                                            void* workspace, size_t workspace_bytes, void* stream) {
+    using namespace mhb;
+    clear_error();
+    if (!keys) return set_error(MHB_ERR_INVALID, "keys output is required");
+    if (rows_per_band < 4 || rows_per_band % 4 != 0 || n_hash % rows_per_band != 0)
+        return set_error(MHB_ERR_INVALID, "rows_per_band must be a multiple of 4 dividing n_hash (got %d, %d)",
+                         rows_per_band, n_hash);
+    const Geometry geo = choose_geometry(KIND_ITERATIVE, n_hash);
+    if ((geo.K != 64 && geo.K != 32) || geo.K % rows_per_band != 0 || prime >= (1ull << 31))
+        return set_error(MHB_ERR_UNSUPPORTED,
+                         "fused band keys need 32 <= n_hash, rows_per_band dividing %d and prime < 2^31; "
+                         "use mhb_sign_iterative_csr + mhb_band_keys", geo.K);
+    return launch_sign(KIND_ITERATIVE, indptr, ids, n_sets, nnz, a, b, nullptr, nullptr, prime, n_hash, out,
+                       out_dtype, status, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), keys,
+                       rows_per_band, write_signatures ? 1 : 0);
 }
 
 extern "C" int mhb_sign_random_csr(const int64_t* indptr, const uint32_t* ids, int64_t n_sets,

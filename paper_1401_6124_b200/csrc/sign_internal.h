@@ -71,6 +71,10 @@ struct SignArgs {
     void* out;
     const uint32_t* ra;
     const uint32_t* rb;
+    // fused LSH band keys (mhb_sign_iterative_csr_bands); keys == nullptr: off
+    unsigned long long* keys;
+    int32_t rows;       // rows per band (divides K and n_hash)
+    int32_t write_sig;  // 0: keys only (out still serves long-set rows as scratch)
 };
 
 Geometry choose_geometry(int kind, int32_t n_hash);
@@ -84,6 +88,7 @@ WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash);
 int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
                 uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
                 int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,
-                size_t workspace_bytes, cudaStream_t st);
+                size_t workspace_bytes, cudaStream_t st, unsigned long long* keys = nullptr,
+                int32_t rows_per_band = 0, int32_t write_sig = 1);
 
 }  // namespace mhb

@@ -341,6 +341,57 @@ def band_keys(sig, rows_per_band: int):
     return keys
 
 
+def signatures_band_keys(indptr, ids, family: Family, rows_per_band: int, *, write_signatures: bool = True,
+                         out_dtype: str = "uint32", validate: bool = True):
+    """Signatures and their LSH band keys in one pass (device tensors).
+
+    For the iterative family on the u32 kernels, the keys are computed in the
+    signing epilogue (mhb_sign_iterative_csr_bands), so the signature matrix is
+    not read back.  ``write_signatures=False`` also skips storing it; the result
+    is then (None, keys).  Other families and geometries run signatures_csr and
+    then band_keys.  The keys are equal to ``band_keys(signatures_csr(...), rows)``.
+    """
+    _check_family(family)
+    torch = _torch()
+    if rows_per_band <= 0 or family.size % rows_per_band:
+        raise ValueError(f"rows_per_band {rows_per_band} must divide the signature length {family.size}")
+    lanes = 64 if family.size >= 128 else 32  # the kernel's per-thread lane count K (sign.cu choose_geometry)
+    fused = (isinstance(family, IterativeFamily) and family.prime <= MAX_KERNEL_PRIME and family.size >= 32
+             and rows_per_band % 4 == 0 and lanes % rows_per_band == 0)
+    if not fused or not (torch.is_tensor(ids) and ids.is_cuda):
+        sig = signatures_csr(indptr, ids, family, out_dtype=out_dtype, validate=validate)
+        if not torch.is_tensor(sig):
+            sig = torch.from_numpy(sig).cuda()
+        keys = band_keys(sig, rows_per_band)
+        return (sig if write_signatures else None), keys
+    if ids.dtype != torch.uint32:
+        if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= family.prime):
+            raise ValueError("feature ids must be in [0, family.prime)")
+        ids = ids.to(torch.uint32)
+    ids = ids.contiguous()
+    indptr = indptr.to(torch.int64).contiguous()
+    n_sets = indptr.numel() - 1
+    tdt = torch.int64 if out_dtype == "int64" else torch.uint32
+    lib = _lib.load()
+    dev = ids.device
+    sig = torch.empty((n_sets, family.size), dtype=tdt, device=dev)
+    keys = torch.empty((n_sets, family.size // rows_per_band), dtype=torch.uint64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev) if validate else None
+    ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, ids.numel(), family.size)
+    with torch.cuda.device(dev):
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        rc = lib.mhb_sign_iterative_csr_bands(
+            indptr.data_ptr(), ids.data_ptr(), n_sets, ids.numel(), family.base.a, family.base.b, family.prime,
+            family.size, rows_per_band, keys.data_ptr(), sig.data_ptr(),
+            _lib.OUT_I64 if tdt == torch.int64 else _lib.OUT_U32, 1 if write_signatures else 0,
+            status.data_ptr() if status is not None else None, ws.data_ptr(), ws_bytes,
+            torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(rc)
+    if validate:
+        _raise_status(int(status.item()), family)
+    return (sig if write_signatures else None), keys
+
+
 # ---------------------------------------------------------------------------
 # Signature files (reference minhash.py:140-206): "id N ids..." text lines and
 # little-endian u64 binary records.

@@ -26,6 +26,7 @@ from paper_1401_6124_b200 import (
     make_family,
     signature,
     signatures,
+    signatures_band_keys,
     signatures_csr,
 )
 
@@ -243,6 +244,65 @@ def test_band_keys_match_oracle(cuda_device):
     sig2 = signatures_csr(*_dev(ip2, np.concatenate([row, row]), cuda_device), fam)
     k2 = band_keys(sig2, 16).cpu().numpy()
     assert np.array_equal(k2[0], k2[1])
+
+
+def _mixed_csr(seed):
+    """cfg1-like short sets plus long sets that take the merged (> kChunk) path."""
+    rng = np.random.default_rng(seed)
+    indptr, ids = gen.cfg1_numpy(n_sets=200, seed=seed)
+    rows = [ids[indptr[s]:indptr[s + 1]] for s in range(200)]
+    for n in (1025, 1500, 4096, 9000):
+        rows.insert(int(rng.integers(0, len(rows))), rng.choice(1 << 20, size=n, replace=False).astype(np.uint32))
+    ip = np.zeros(len(rows) + 1, dtype=np.int64)
+    ip[1:] = np.cumsum([r.size for r in rows])
+    return ip, np.concatenate(rows).astype(np.uint32)
+
+
+@pytest.mark.parametrize("n_hash,rows", [(2048, 16), (256, 8), (200, 8), (64, 32), (4096, 64), (128, 4)])
+def test_fused_band_keys(cuda_device, n_hash, rows):
+    """Keys fused into the signing epilogue equal the oracle's band keys of the
+    oracle's signatures (short sets in the epilogue, long sets in finalize)."""
+    indptr, ids = _mixed_csr(n_hash)
+    fam = make_family("iterative", 11, n_hash, 1_048_583)
+    want_sig = oracle.sign_family_csr(indptr, ids, fam)
+    want = oracle.band_keys(want_sig, rows)
+    ip, di = _dev(indptr, ids, cuda_device)
+    for dt in ("uint32", "int64"):
+        sig, keys = signatures_band_keys(ip, di, fam, rows, out_dtype=dt)
+        assert np.array_equal(sig.cpu().numpy().astype(np.int64), want_sig)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), want)
+    none, keys = signatures_band_keys(ip, di, fam, rows, write_signatures=False)
+    assert none is None
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), want)
+
+
+def test_fused_band_keys_fallbacks(cuda_device):
+    """Random family / rows not dividing the lane count: unfused path, same keys."""
+    indptr, ids = gen.cfg1_numpy(n_sets=100, seed=4)
+    ip, di = _dev(indptr, ids, cuda_device)
+    for fam, rows in ((make_family("random", 2, 256, 1_048_583), 16),
+                      (make_family("iterative", 2, 240, 1_048_583), 48),
+                      (make_family("iterative", 2, 24, 1_048_583), 4)):
+        sig, keys = signatures_band_keys(ip, di, fam, rows)
+        want = oracle.band_keys(oracle.sign_family_csr(indptr, ids, fam), rows)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), want)
+    with pytest.raises(ValueError):
+        signatures_band_keys(ip, di, make_family("iterative", 2, 256, 1_048_583), 24)
+
+
+def test_fused_band_keys_abi_errors(cuda_device):
+    import torch
+
+    from paper_1401_6124_b200 import _lib
+
+    lib = _lib.load()
+    keys = torch.empty(64, dtype=torch.uint64, device=cuda_device)
+    # rows not dividing n_hash -> INVALID; rows not dividing the lane count -> UNSUPPORTED
+    assert lib.mhb_sign_iterative_csr_bands(None, None, 0, 0, 1, 1, 101, 256, 12, keys.data_ptr(), None, 0, 1,
+                                            None, None, 0, None) == 1
+    assert lib.mhb_sign_iterative_csr_bands(None, None, 0, 0, 1, 1, 101, 256, 128, keys.data_ptr(), None, 0, 1,
+                                            None, None, 0, None) == 3
+    assert b"rows_per_band" in lib.mhb_last_error()
 
 
 @pytest.mark.parametrize("fmt", ["binary", "text"])
