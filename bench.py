@@ -49,6 +49,7 @@ def _args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of signatures (N>1)")
+    ap.add_argument("--corpus-lines", type=int, default=400_000, help="--config corpus: text lines")
     ap.add_argument("--aux", action="store_true",
                     help="also time the pairwise-Jaccard and bucket-histogram kernels (cfg3: planted pairs)")
     return ap.parse_args()
@@ -330,8 +331,128 @@ def run_c6(args):
     print(json.dumps(line), flush=True)
 
 
+def _python_ingest(lines_bytes):
+    """The reference's build_corpus loop (corpus.py:67-80) over decoded lines, as pure
+    Python (tokenize + Vocabulary.add per line) -- the CPU arm of --config corpus."""
+    import io
+
+    from paper_1401_6124_b200.corpus import Vocabulary, tokenize
+
+    vocab = Vocabulary()
+    docs = []
+    for line in io.TextIOWrapper(io.BytesIO(lines_bytes), encoding="utf-8"):  # text-mode file iteration
+        docs.append(sorted(vocab.add(t) for t in tokenize(line)))
+    return vocab, docs
+
+
+def run_corpus(args):
+    """SURVEY §8f #4 and the reference CLI `sign` (cli.py:205-230): one-document-per-line
+    text -> native ingest (CSR + vocabulary) -> GPU signatures (iterative, N=128, the
+    CLI default length) -> GPU-formatted text records -> host file.  A step is the
+    whole `sign_corpus` call on a host file; the ingest alone is timed beside it."""
+    import tempfile
+
+    import numpy as np
+    import torch
+
+    from paper_1401_6124_b200 import derive_seed, gen
+    from paper_1401_6124_b200.corpus import build_corpus_csr, sign_corpus
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    text = gen.synth_text_corpus(args.corpus_lines, derive_seed(gen.MASTER_SEED, 40), unicode_frac=0.01)
+    mb = len(text) / 1e6
+    tmpdir = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+    src = os.path.join(tmpdir, f"mhb_corpus_{os.getpid()}.txt")
+    dst = os.path.join(tmpdir, f"mhb_sigs_{os.getpid()}.txt")
+    with open(src, "wb") as fh:
+        fh.write(text)
+    threads = os.cpu_count() or 1
+    workload = (f"synth_text_corpus({args.corpus_lines} lines, Poisson(40) Zipf(1.1) words of 200k, 1% lines "
+                f"non-ASCII) = {mb:.1f} MB; sign --family iterative --hashes 128 --format text")
+    try:
+        if args.impl == "reference":
+            # bounded sample: the pure-Python build_corpus loop + the C port of the signing kernels
+            from oracle import oracle
+            from paper_1401_6124_b200 import make_family
+            from paper_1401_6124_b200.modmath import choose_prime
+
+            cut = text.find(b"\n", min(len(text), 8 << 20) - 1) + 1 or len(text)
+            sample = text[:cut]
+            times = []
+            for r in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                vocab, docs = _python_ingest(sample)
+                rows = [d for d in docs if d]
+                ip = np.zeros(len(rows) + 1, dtype=np.int64)
+                ip[1:] = np.cumsum([len(d) for d in rows])
+                ids = np.fromiter((x for d in rows for x in d), dtype=np.uint32, count=int(ip[-1]))
+                fam = make_family("iterative", 0, 128, choose_prime(len(vocab) - 1, 128))
+                oracle.sign_family_csr(ip, ids, fam, threads=threads)
+                if r >= args.warmup:
+                    times.append(time.perf_counter() - t0)
+            step = statistics.mean(times)
+            value = len(sample) / 1e6 / step
+            line = {"impl": "reference", "metric": "corpus_sign_mb_per_s", "value": value, "unit": "MB/s",
+                    "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
+                    "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+                    "data": "synthetic", "config": {"workload": workload},
+                    "cpu_baseline": {"value": value, "unit": "MB/s", "cores": threads, "kind": "port",
+                                     "sample": f"first {len(sample) / 1e6:.1f} MB; pure-Python build_corpus loop "
+                                               "(1 core) + C/OpenMP port of kernels.py signing"},
+                    "e2e": {"value": value, "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+            return
+        for _ in range(args.warmup):
+            sign_corpus(src, dst, family="iterative", hashes=128, seed=0, fmt="text", log=None)
+        ingest, e2e = [], []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            c = build_corpus_csr(src)
+            ingest.append(time.perf_counter() - t0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            n, prime = sign_corpus(src, dst, family="iterative", hashes=128, seed=0, fmt="text", log=None)
+            torch.cuda.synchronize()
+            e2e.append(time.perf_counter() - t0)
+        out_bytes = os.path.getsize(dst)
+        # Python build_corpus loop on a bounded sample for the CPU baseline
+        cut = text.find(b"\n", min(len(text), 4 << 20) - 1) + 1 or len(text)
+        t0 = time.perf_counter()
+        _python_ingest(text[:cut])
+        py_mbs = cut / 1e6 / (time.perf_counter() - t0)
+        step = statistics.mean(e2e)
+        value = mb / step
+        nnz = int(c.ids.size)
+        line = {"metric": "corpus_sign_mb_per_s", "value": value, "unit": "MB/s", "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": workload, "docs": int(c.indptr.size - 1), "nnz": nnz,
+                           "vocabulary": len(c.vocabulary), "prime": prime, "records": n,
+                           "output_bytes": out_bytes, "host_threads": threads},
+                "ingest": {"mb_per_s": mb / statistics.mean(ingest), "ms": statistics.mean(ingest) * 1e3,
+                           "share_of_step": statistics.mean(ingest) / step},
+                "roofline": None,
+                "roofline_note": "host-bound pipeline (native ingest + file I/O); the signing kernel's roofline "
+                                 "is reported by the cfg* lines",
+                "cpu_baseline": {"value": py_mbs, "unit": "MB/s", "cores": 1, "kind": "port",
+                                 "sample": f"first {cut / 1e6:.1f} MB, pure-Python build_corpus loop (ingest only)"},
+                "e2e": {"value": value, "unit": "MB/s", "h2d_bytes_per_step": 8 * (c.indptr.size) + 4 * nnz,
+                        "d2h_bytes_per_step": out_bytes},
+                "gpu_launches": None}
+        print(json.dumps(line), flush=True)
+    finally:
+        for f in (src, dst):
+            if os.path.exists(f):
+                os.unlink(f)
+
+
 def main():
     args = _args()
+    if args.config == "corpus":
+        run_corpus(args)
+        return
     if args.config == "c6":
         run_c6(args)
         return

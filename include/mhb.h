@@ -202,6 +202,35 @@ int mhb_format_text_records(const void* sig, int32_t sig_dtype, int64_t n_sets, 
                             void* stream);
 
 /*
+ * Corpus ingest (reference corpus.py:18-80: build_corpus, tokenize, Vocabulary):
+ * a one-document-per-line UTF-8 buffer -> CSR feature ids + vocabulary.
+ *   lines   : "\n", "\r\n" or a lone "\r" end a line (Python universal newlines);
+ *   terms   : lowercase maximal alphanumeric runs ([^\W_]), deduplicated, sorted;
+ *   ids     : vocabulary ids in first-occurrence order (document order, then the
+ *             document's sorted terms); each document is its sorted id set.
+ * Host-only, multi-threaded (n_threads <= 0: all hardware threads).  Pure-ASCII lines
+ * are tokenized natively.  Lines holding a byte >= 0x80 are deferred: the caller
+ * tokenizes them with the Unicode rules (Python str.lower / str.isalnum) and passes
+ * the sorted UTF-8 terms to mhb_corpus_set_terms before mhb_corpus_intern.  `text`
+ * must stay alive and unchanged until mhb_corpus_free.
+ */
+typedef struct mhb_corpus mhb_corpus;
+int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_threads, mhb_corpus** corpus);
+int mhb_corpus_info(const mhb_corpus* corpus, int64_t* n_docs, int64_t* n_deferred);
+/* per deferred line k: its document index, byte offset and byte length in `text` */
+int mhb_corpus_deferred(const mhb_corpus* corpus, int64_t* lines, int64_t* starts, int64_t* lens);
+/* terms of deferred line lines[k] are term_offsets[line_ptr[k] .. line_ptr[k+1]] slices of blob */
+int mhb_corpus_set_terms(mhb_corpus* corpus, int64_t n_lines, const int64_t* lines, const int64_t* line_ptr,
+                         const char* blob, const int64_t* term_offsets);
+int mhb_corpus_intern(mhb_corpus* corpus, int64_t* nnz, int64_t* n_terms, int64_t* term_bytes,
+                      int64_t* empty_docs);
+/* indptr int64[n_docs+1], ids uint32[nnz], term_offsets int64[n_terms+1], term_blob char[term_bytes];
+   any pointer may be NULL */
+int mhb_corpus_export(const mhb_corpus* corpus, int64_t* indptr, uint32_t* ids, int64_t* term_offsets,
+                      char* term_blob);
+void mhb_corpus_free(mhb_corpus* corpus);
+
+/*
  * Instruction-rate probe for the roofline: runs the iterative visit sequence
  * (add, conditional subtract, 3-way min) from registers only, `visits_per_thread`
  * visits per thread on a persistent grid, and reports visits and device ms.

@@ -32,7 +32,7 @@ def _nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    return sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.cpp")])
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:

@@ -56,6 +56,13 @@ SIGNATURES = {
     "mhb_format_text_records": (C.c_int, [_P, _I32, _I64, _I32, _P, _I64, _P, _P, _P]),
     "mhb_bucket_hist_iterative": (C.c_int, [_P, _I64, _U64, _U64, _U64, _I32, _U32, _P, _P]),
     "mhb_bucket_hist_random": (C.c_int, [_P, _I64, _P, _P, _U64, _I32, _U32, _P, _P]),
+    "mhb_corpus_scan": (C.c_int, [_P, _I64, _I32, _P]),
+    "mhb_corpus_info": (C.c_int, [_P, _P, _P]),
+    "mhb_corpus_deferred": (C.c_int, [_P, _P, _P, _P]),
+    "mhb_corpus_set_terms": (C.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "mhb_corpus_intern": (C.c_int, [_P, _P, _P, _P, _P]),
+    "mhb_corpus_export": (C.c_int, [_P, _P, _P, _P, _P]),
+    "mhb_corpus_free": (None, [_P]),
     "mhb_probe_visit_rate": (C.c_int, [_I64, _I32, C.POINTER(C.c_double), C.POINTER(C.c_float), _P]),
     "mhb_profile_begin": (C.c_int, [_I32]),
     "mhb_profile_end": (C.c_int, [C.POINTER(C.c_float), C.POINTER(C.c_int32)]),

@@ -124,6 +124,75 @@ def c6_workload():
     return indptr, ids, prime, derive_seed(MASTER_SEED, 6, 1)
 
 
+_TEXT_SEPS = (b" ", b" ", b" ", b"  ", b", ", b". ", b"-", b"_", b"\t", b"!? ", b" (", b") ", b"; ", b"'")
+_UNICODE_WORDS = ("caf\u00e9", "CAF\u00c9", "na\u00efve", "\u00fcber", "Stra\u00dfe", "\u0130stanbul",
+                  "\u212akelvin", "\u03a3\u03bf\u03c6\u03af\u03b1", "\u65e5\u672c\u8a9e", "x\u00b2y",
+                  "\u0663\u0664", "\u00e9t\u00e9", "\ufb01ne", "\u1e9e", "\u0441\u043b\u043e\u0432\u043e")
+
+
+def synth_text_corpus(n_lines: int, seed: int, *, words_per_line: float = 40.0, vocab: int = 200_000,
+                      zipf_s: float = 1.1, unicode_frac: float = 0.0, empty_frac: float = 0.01,
+                      crlf: bool = False) -> bytes:
+    """Seeded one-document-per-line text for the corpus-ingest path.
+
+    The reference ingests real text (corpus.py:67-80) and ships none, so this stands
+    in: Poisson(words_per_line) words per line drawn Zipf(zipf_s) from `vocab` random
+    mixed-case ASCII words (1-14 chars of [A-Za-z0-9]), joined by separators that
+    include punctuation, tabs and underscores; a fraction `empty_frac` of lines is
+    empty and a fraction `unicode_frac` of lines gets one non-ASCII word (accents,
+    sharp s, dotted I, Kelvin sign, Greek, CJK, ligatures, superscripts, Arabic-Indic
+    digits).  Vectorised numpy, assembled in chunks."""
+    rng = np.random.default_rng(int(seed))
+    alpha = np.frombuffer(b"abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789", dtype=np.uint8)
+    wlen = rng.integers(1, 15, size=vocab)
+    wbytes = alpha[rng.integers(0, alpha.size, size=int(wlen.sum()))]
+    # lowercase-heavy: most letters lowered, so case folding merges some words
+    low = (wbytes >= 65) & (wbytes <= 90) & (rng.random(wbytes.size) < 0.8)
+    wbytes = np.where(low, wbytes + 32, wbytes).astype(np.uint8)
+    uni = [w.encode("utf-8") for w in _UNICODE_WORDS]
+    seps = list(_TEXT_SEPS)
+    nl = b"\r\n" if crlf else b"\n"
+    # token table: [vocab words][unicode words][separators][newline]
+    table = [wbytes.tobytes()] + uni + seps + [nl]
+    tlen = np.concatenate([wlen, [len(u) for u in uni], [len(x) for x in seps], [len(nl)]]).astype(np.int64)
+    tstart = np.zeros(tlen.size, dtype=np.int64)
+    tstart[1:] = np.cumsum(tlen)[:-1]
+    blob = np.frombuffer(b"".join(table), dtype=np.uint8)
+    U0, S0, NL = vocab, vocab + len(uni), vocab + len(uni) + len(seps)
+    k = np.arange(1, vocab + 1, dtype=np.float64)
+    cdf = np.cumsum(k ** -zipf_s)
+    cdf /= cdf[-1]
+    out = []
+    for l0 in range(0, n_lines, 1 << 16):
+        nl_ = min(n_lines - l0, 1 << 16)
+        nw = rng.poisson(words_per_line, size=nl_)
+        nw[rng.random(nl_) < empty_frac] = 0
+        tot = int(nw.sum())
+        words = np.minimum(np.searchsorted(cdf, rng.random(tot)), vocab - 1)
+        has_uni = (rng.random(nl_) < unicode_frac) & (nw > 0)
+        first = np.zeros(nl_, dtype=np.int64)
+        first[1:] = np.cumsum(nw)[:-1]
+        pick = first[has_uni] + rng.integers(0, np.maximum(nw[has_uni], 1))
+        words[pick] = U0 + rng.integers(0, len(uni), size=pick.size)
+        sep = S0 + rng.integers(0, len(seps), size=tot)
+        # per line: w0 s0 w1 s1 ... w_{n-1} NL  (an empty line is just NL)
+        cnt = np.where(nw > 0, 2 * nw, 1)
+        base = np.cumsum(cnt) - cnt
+        tok = np.empty(int(cnt.sum()), dtype=np.int64)
+        lw = np.repeat(np.arange(nl_), nw)
+        j = np.arange(tot) - first[lw]
+        wpos = base[lw] + 2 * j
+        tok[wpos] = words
+        inner = j < nw[lw] - 1
+        tok[wpos[inner] + 1] = sep[inner]
+        tok[base + cnt - 1] = NL
+        L = tlen[tok]
+        offs = np.cumsum(L) - L
+        idx = np.repeat(tstart[tok] - offs, L) + np.arange(int(L.sum()))
+        out.append(blob[idx].tobytes())
+    return b"".join(out)
+
+
 # ---------------------------------------------------------------------------
 # torch: full-size workloads (GPU) with the same distributions
 # ---------------------------------------------------------------------------

@@ -229,7 +229,81 @@ def synth_corpus_fixture():
     (HERE / "c6.json").write_text(json.dumps(meta, indent=1))
 
 
+CORPUS_EDGE_CASES = [
+    "",
+    "\n",
+    "a",
+    "a\n",
+    "The cat ate the mouse\nThe mouse ate the cheese\n",
+    "A-B, a_b; 12ab!\r\nDog dog DOG\rx\r\r\ny\n\n...\nZ",
+    "\n\n\n",
+    "trailing cr\r",
+    "x\ty\x0bz\x0cw\x1cq\u2028r\x00s\n",
+    "Stra\u00dfe STRASSE \u0130stanbul \u212a kelvin caf\u00e9 CAF\u00c9 \u00b2 x\u00b2y \u0663\u0664 _a_\n"
+    " plain ascii line\n\ufeffbom sep line\n",
+    "na\u00efve\nNA\u00cfVE naive\n\u65e5\u672c\u8a9e \u30c6\u30b9\u30c8\n\u0391\u03b2\u03b3 abc\n",
+    "\ufb01ne fine FINE\n\u1e9e \u00df ss\nABCDEFGHIJKLMNOPQRSTUVWXYZ abcdefghijklmnopqrstuvwxyz0123456789\n",
+]
+
+CORPUS_SYNTH = [  # gen.synth_text_corpus arguments
+    {"n_lines": 3000, "seed": 11, "words_per_line": 30.0, "vocab": 5000, "unicode_frac": 0.05},
+    {"n_lines": 2000, "seed": 12, "words_per_line": 12.0, "vocab": 800, "unicode_frac": 0.0, "crlf": True},
+    {"n_lines": 1500, "seed": 13, "words_per_line": 60.0, "vocab": 20000, "unicode_frac": 0.3,
+     "empty_frac": 0.1},
+]
+
+
+def corpus_fixture():
+    """Reference build_corpus (corpus.py:67-80) on edge-case texts and seeded synthetic
+    corpora, plus the bytes of the reference CLI `sign` output (cli.py:205-230)."""
+    import tempfile
+
+    import types
+
+    # the reference CLI imports plots.py -> matplotlib (absent here); `sign` never plots
+    if "matplotlib" not in sys.modules:
+        mpl = types.ModuleType("matplotlib")
+        mpl.use = lambda *a, **k: None
+        mpl.pyplot = types.ModuleType("matplotlib.pyplot")
+        sys.modules["matplotlib"] = mpl
+        sys.modules["matplotlib.pyplot"] = mpl.pyplot
+    from minhashlab.cli import main as ref_cli
+
+    cases, arrays = [], {}
+    texts = [t.encode("utf-8") for t in CORPUS_EDGE_CASES]
+    texts += [gen.synth_text_corpus(**kw) for kw in CORPUS_SYNTH]
+    with tempfile.TemporaryDirectory() as tmp:
+        for k, data in enumerate(texts):
+            path = Path(tmp) / f"c{k}.txt"
+            path.write_bytes(data)
+            vocab, docs, empty = ref_corpus.build_corpus(path)
+            indptr = np.zeros(len(docs) + 1, dtype=np.int64)
+            indptr[1:] = np.cumsum([len(d) for d in docs])
+            ids = np.concatenate([d.ids for d in docs]) if docs else np.zeros(0, dtype=np.int64)
+            arrays[f"indptr{k}"] = indptr
+            arrays[f"ids{k}"] = ids.astype(np.int64)
+            case = {"sha256": hashlib.sha256(data).hexdigest(), "terms": list(vocab.terms), "empty": empty}
+            if k >= len(CORPUS_EDGE_CASES):
+                case["synth"] = CORPUS_SYNTH[k - len(CORPUS_EDGE_CASES)]
+                sign = {}
+                for fam in ("random", "iterative"):
+                    for fmt in ("text", "binary"):
+                        out = Path(tmp) / f"s{k}_{fam}_{fmt}"
+                        rc = ref_cli(["sign", "--corpus", str(path), "--family", fam, "--hashes", "16",
+                                      "--seed", "3", "--out", str(out), "--format", fmt])
+                        assert rc == 0
+                        sign[f"{fam}_{fmt}"] = hashlib.sha256(out.read_bytes()).hexdigest()
+                case["sign_hashes16_seed3"] = sign
+                case["sign_prime"] = ref.choose_prime(len(vocab) - 1, 16)
+            else:
+                case["text"] = CORPUS_EDGE_CASES[k]
+            cases.append(case)
+    np.savez_compressed(HERE / "corpus.npz", **arrays)
+    (HERE / "corpus.json").write_text(json.dumps(cases, indent=1, ensure_ascii=True))
+
+
 if __name__ == "__main__":
+    corpus_fixture()
     synth_corpus_fixture()
     wide_fixture()
     families_fixture()

@@ -371,3 +371,23 @@ def test_plain_c_consumer_of_the_abi(cuda_device):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "abi_smoke ok" in r.stdout
+
+
+def test_sign_corpus_matches_reference_cli(golden, tmp_path, cuda_device):
+    """Text corpus -> native ingest -> GPU signatures -> GPU-formatted records: the file
+    is byte-identical to the reference CLI's `sign` output (cli.py:205-230) for both
+    families and formats, including the skipped empty documents' ids."""
+    from paper_1401_6124_b200.corpus import sign_corpus
+
+    cases = json.loads((golden / "corpus.json").read_text())
+    for case in cases:
+        if "synth" not in case:
+            continue
+        path = tmp_path / "corpus.txt"
+        path.write_bytes(gen.synth_text_corpus(**case["synth"]))
+        for key, want in case["sign_hashes16_seed3"].items():
+            fam, fmt = key.split("_")
+            out = tmp_path / f"sig_{key}"
+            n, prime = sign_corpus(path, out, family=fam, hashes=16, seed=3, fmt=fmt, log=None)
+            assert prime == case["sign_prime"]
+            assert hashlib.sha256(out.read_bytes()).hexdigest() == want, (case["synth"], key)

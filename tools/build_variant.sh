@@ -7,7 +7,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 OUT=$ROOT/tools/variants; mkdir -p $OUT/obj_$1
 if [ -d "$2" ]; then SRC=$(cd "$2" && pwd); else SRC=$ROOT/paper_1401_6124_b200/csrc; fi
 NV="nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr -I$ROOT/include -I$SRC"
-for src in $SRC/*.cu; do f=$(basename $src .cu); [ $f = sign ] && [ ! -d "$2" ] && continue; $NV -c $src -o $OUT/obj_$1/$f.o & done
+for src in $SRC/*.cu $SRC/*.cpp; do [ -e $src ] || continue; f=$(basename ${src%.*}); [ $f = sign ] && [ ! -d "$2" ] && continue; $NV -c $src -o $OUT/obj_$1/$f.o & done
 if [ ! -d "$2" ]; then
   cp "$2" $OUT/obj_$1/sign.cu
   $NV -c $OUT/obj_$1/sign.cu -o $OUT/obj_$1/sign.o &
