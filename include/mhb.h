@@ -224,7 +224,8 @@ int mhb_corpus_set_terms(mhb_corpus* corpus, int64_t n_lines, const int64_t* lin
                          const char* blob, const int64_t* term_offsets);
 int mhb_corpus_intern(mhb_corpus* corpus, int64_t* nnz, int64_t* n_terms, int64_t* term_bytes,
                       int64_t* empty_docs);
-/* indptr int64[n_docs+1], ids uint32[nnz], term_offsets int64[n_terms+1], term_blob char[term_bytes];
+/* indptr int64[n_docs+1], ids uint32[nnz]; the vocabulary in id order as term_blob char[term_bytes]
+   (each term followed by '\n') with term_offsets int64[n_terms+1] (term starts, then term_bytes);
    any pointer may be NULL */
 int mhb_corpus_export(const mhb_corpus* corpus, int64_t* indptr, uint32_t* ids, int64_t* term_offsets,
                       char* term_blob);

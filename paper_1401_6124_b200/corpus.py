@@ -16,7 +16,6 @@ GPU and stream the records to the signature file.
 from __future__ import annotations
 
 import ctypes as C
-import os
 import re
 import sys
 from fractions import Fraction
@@ -48,7 +47,7 @@ class Vocabulary:
     def _from_terms(cls, terms: list[str]) -> "Vocabulary":
         v = cls()
         v._id_to_term = list(terms)
-        v._term_to_id = {t: i for i, t in enumerate(v._id_to_term)}
+        v._term_to_id = dict(zip(v._id_to_term, range(len(v._id_to_term))))
         return v
 
     def add(self, term: str) -> int:
@@ -104,19 +103,21 @@ def _ingest(text: bytes, threads: int | None) -> CorpusCSR:
             lens = np.empty_like(lines)
             _lib.check(lib.mhb_corpus_deferred(h, lines.ctypes.data, starts.ctypes.data, lens.ctypes.data))
             line_ptr = np.zeros(n_def.value + 1, dtype=np.int64)
-            chunks, offs, off = [], [0], 0
+            all_terms = []
             for k in range(n_def.value):
                 s = int(starts[k])
                 # strict UTF-8, as open(path, encoding="utf-8") in the reference
                 terms = tokenize(text[s:s + int(lens[k])].decode("utf-8"))
-                for t in terms:
-                    b = t.encode("utf-8")
-                    chunks.append(b)
-                    off += len(b)
-                    offs.append(off)
+                all_terms.extend(terms)
                 line_ptr[k + 1] = line_ptr[k] + len(terms)
-            blob = np.frombuffer(b"".join(chunks) or b"\0", dtype=np.uint8)
-            term_off = np.asarray(offs, dtype=np.int64)
+            # terms never contain "\n": join, encode once, split by the separators in numpy
+            joined = np.frombuffer(("\n".join(all_terms) + "\n").encode("utf-8"), dtype=np.uint8)
+            nl = np.flatnonzero(joined == 10)
+            term_off = np.zeros(nl.size + 1, dtype=np.int64)
+            term_off[1:] = nl + 1 - np.arange(1, nl.size + 1)  # starts in the separator-free blob
+            blob = joined[joined != 10]
+            if not blob.size:
+                blob = np.zeros(1, dtype=np.uint8)
             _lib.check(lib.mhb_corpus_set_terms(h, n_def.value, lines.ctypes.data, line_ptr.ctypes.data,
                                                 blob.ctypes.data, term_off.ctypes.data))
         nnz, n_terms, tbytes, empty = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
@@ -129,8 +130,7 @@ def _ingest(text: bytes, threads: int | None) -> CorpusCSR:
                                          tblob.ctypes.data))
     finally:
         lib.mhb_corpus_free(h)
-    raw = tblob.tobytes()
-    terms = [raw[toff[i]:toff[i + 1]].decode("utf-8") for i in range(n_terms.value)]
+    terms = tblob[:tbytes.value].tobytes().decode("utf-8").split("\n")[:-1] if n_terms.value else []
     return CorpusCSR(Vocabulary._from_terms(terms), indptr, ids, int(empty.value))
 
 

@@ -298,7 +298,7 @@ void scan_parts(mhb_corpus* c) {
         const int64_t d0 = c->range[t], d1 = c->range[t + 1];
         const int64_t bytes = d1 > d0 ? c->line_end[d1 - 1] - c->line_start[d0] : 0;
         Table& tab = c->local[t];
-        tab.init((size_t)std::max<int64_t>(1024, bytes / 256));
+        tab.init(4096);
         auto& dt = c->doc_terms[t];
         dt.reserve(bytes / 8 + 16);
         std::vector<Tok> toks;
@@ -483,7 +483,7 @@ extern "C" int mhb_corpus_intern(mhb_corpus* c, int64_t* nnz, int64_t* n_terms, 
                     const uint64_t below = bits[o >> 6].load(std::memory_order_relaxed) & ((1ull << (o & 63)) - 1);
                     e.first = (uint64_t)(pre[o >> 6] + __builtin_popcountll(below));  // now the id
                     c->vocab[e.first] = &e;
-                    vb[s] += e.len;
+                    vb[s] += e.len + 1;  // + the '\n' separator of the export
                 }
             });
             c->vocab_bytes = 0;
@@ -537,8 +537,11 @@ extern "C" int mhb_corpus_export(const mhb_corpus* c, int64_t* indptr, uint32_t*
         int64_t off = 0;
         for (size_t v = 0; v < c->vocab.size(); ++v) {
             if (term_offsets) term_offsets[v] = off;
-            if (term_blob) std::memcpy(term_blob + off, c->vocab[v]->p, c->vocab[v]->len);
-            off += c->vocab[v]->len;
+            if (term_blob) {
+                std::memcpy(term_blob + off, c->vocab[v]->p, c->vocab[v]->len);
+                term_blob[off + c->vocab[v]->len] = '\n';
+            }
+            off += c->vocab[v]->len + 1;
         }
         if (term_offsets) term_offsets[c->vocab.size()] = off;
     }

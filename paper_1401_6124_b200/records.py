@@ -70,38 +70,68 @@ def format_text(sig, obj_ids=None, first_id: int = 0):
     return out
 
 
+_PINNED: dict = {}  # slot -> pinned uint8 host buffer, reused across calls
+
+
+def _pinned(slot: int, nbytes: int):
+    import torch
+
+    buf = _PINNED.get(slot)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _PINNED[slot] = buf
+    return buf[:nbytes]
+
+
 def write_signatures_csr(path, indptr, ids, family: Family, fmt: str = "binary", obj_ids=None,
-                         first_id: int = 0, chunk_bytes: int = 256 << 20) -> int:
+                         first_id: int = 0, chunk_bytes: int = 64 << 20) -> int:
     """Sign every set of a CSR batch and write the records to `path`.
 
     fmt: "binary" (LE u64 records) or "text" ("id N ids..." lines).  obj_ids: one id per
-    set (default first_id + row).  Works on device tensors or numpy arrays; the batch
-    is processed in chunks of about `chunk_bytes` of formatted output.  Returns the
-    number of records written."""
+    set (default first_id + row).  Works on device tensors or numpy arrays.  The batch
+    is processed in chunks of about `chunk_bytes` of formatted output; each chunk's
+    bytes land in one of two pinned host buffers while the previous chunk is written
+    to the file.  Returns the number of records written."""
     import torch
 
     if fmt not in ("binary", "text"):
         raise ValueError(f"fmt must be 'binary' or 'text', got {fmt!r}")
     dev = torch.device("cuda", torch.cuda.current_device())
     ip = torch.as_tensor(np.asarray(indptr) if not torch.is_tensor(indptr) else indptr, dtype=torch.int64)
-    x = ids if torch.is_tensor(ids) else torch.from_numpy(np.asarray(ids).astype(np.int64))
+    x = ids if torch.is_tensor(ids) else torch.from_numpy(np.asarray(ids))
     n_sets = ip.numel() - 1
     oids = None if obj_ids is None else np.asarray(obj_ids, dtype=np.int64)
     per_record = (family.size + 2) * 8 if fmt == "binary" else family.size * 11 + 24
     step = max(1, chunk_bytes // per_record)
+    ip_h = ip.cpu().numpy()
     written = 0
+    pending = None  # (pinned host view, event) of the chunk in flight
+    slot = 0
     with open(path, "wb") as fh:
         for s0 in range(0, n_sets, step):
             s1 = min(n_sets, s0 + step)
-            lo, hi = int(ip[s0]), int(ip[s1])
-            cip = (ip[s0:s1 + 1] - lo).to(dev)
-            cx = x[lo:hi].to(dev).to(torch.uint32) if x.dtype != torch.uint32 else x[lo:hi].to(dev)
+            lo, hi = int(ip_h[s0]), int(ip_h[s1])
+            cip = torch.as_tensor(ip_h[s0:s1 + 1] - lo).to(dev, non_blocking=True)
+            cx = x[lo:hi]
+            if cx.dtype != torch.uint32:
+                cx = cx.to(torch.int64).to(torch.uint32) if cx.dtype != torch.int64 else cx.to(torch.uint32)
+            cx = cx.to(dev, non_blocking=True)
             sig = signatures_csr(cip, cx, family, out_dtype="uint32")
             chunk_ids = None if oids is None else oids[s0:s1]
-            if fmt == "binary":
-                buf = format_binary(sig, chunk_ids, first_id + s0)
-            else:
-                buf = format_text(sig, chunk_ids, first_id + s0)
-            fh.write(buf.cpu().numpy().tobytes())
+            buf = format_binary(sig, chunk_ids, first_id + s0) if fmt == "binary" else \
+                format_text(sig, chunk_ids, first_id + s0)
+            raw = buf.view(torch.uint8)
+            host = _pinned(slot, raw.numel())
+            host.copy_(raw, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            if pending is not None:
+                pending[1].synchronize()
+                fh.write(memoryview(pending[0].numpy()))
+            pending = (host, ev)
+            slot ^= 1
             written += s1 - s0
+        if pending is not None:
+            pending[1].synchronize()
+            fh.write(memoryview(pending[0].numpy()))
     return written
