@@ -48,7 +48,10 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
-    ap.add_argument("--gather", action="store_true", help="also time the NCCL gather of signatures (N>1)")
+    ap.add_argument("--gather", nargs="?", const="nccl", choices=["nccl", "peer"], default=None,
+                    help="also time gathering every rank's signatures on rank 0: 'nccl' (sign, then "
+                         "torch.distributed.gather) or 'peer' (fused: kernels store into rank 0's matrix "
+                         "over CUDA IPC / NVLink)")
     ap.add_argument("--corpus-lines", type=int, default=400_000, help="--config corpus: text lines")
     ap.add_argument("--aux", action="store_true",
                     help="also time the pairwise-Jaccard and bucket-histogram kernels (cfg3: planted pairs)")
@@ -547,7 +550,50 @@ def main():
     value = world * n_sets * N * args.steps / (max_ms / 1e3)
 
     gather_ms = None
-    if world > 1 and args.gather:
+    gather_peer = None
+    if args.gather == "peer":
+        # fused sign + gather: every step signs straight into rank 0's [world*S, N] matrix
+        from paper_1401_6124_b200.dist import PeerMatrix
+        from paper_1401_6124_b200.minhash import sign_csr_to_ptr
+
+        owner = PeerMatrix.allocate(world * n_sets, N, 4, local) if rank == 0 else None
+        box = [owner.handle if owner is not None else None]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
+        view = owner if rank == 0 else PeerMatrix.open(box[0], world * n_sets, N, 4, local)
+        dst_ptr = view.ptr(rank * n_sets)
+        for _ in range(args.warmup):
+            sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        tp = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        if rank == 0:  # this rank's rows landed where they belong
+            mine = owner.tensor()[:n_sets]
+            if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
+                raise SystemExit("peer gather: rank 0 rows differ from the local signatures")
+        if world > 1:
+            dist.barrier()
+        if rank != 0:
+            view.close()
+        if world > 1:
+            dist.barrier()
+        if owner is not None:
+            owner.close()
+        pms = float(tp.item()) / args.steps
+        gather_peer = {"ms_per_step": pms, "entries_per_s": world * n_sets * N / (pms / 1e3),
+                       "bytes_to_rank0_per_step": world * n_sets * N * 4,
+                       "path": "mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC (csrc/peer.cu)"}
+    if world > 1 and args.gather == "nccl":
         from paper_1401_6124_b200.dist import gather_blocks
 
         torch.cuda.synchronize()
@@ -650,6 +696,8 @@ def main():
         }
         if gather_ms is not None:
             line["gather_ms"] = gather_ms
+        if gather_peer is not None:
+            line["gather_peer"] = gather_peer
         if aux is not None:
             line["aux"] = aux
         print(json.dumps(line), flush=True)

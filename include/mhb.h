@@ -232,6 +232,19 @@ int mhb_corpus_export(const mhb_corpus* corpus, int64_t* indptr, uint32_t* ids, 
 void mhb_corpus_free(mhb_corpus* corpus);
 
 /*
+ * Peer-memory gather target (fused sign + gather across ranks, one process per GPU).
+ * mhb_peer_alloc: cudaMalloc `bytes` on `device` and export its 64-byte CUDA IPC handle.
+ * mhb_peer_open: map another process's buffer (NVLink peer mapping across GPUs); any
+ * mhb_sign_* entry may then take out = mapped + row0 * n_hash * elem_size and its
+ * stores land directly in the owner's matrix.  Close / free when every writer's
+ * stream has completed (a barrier after the sign calls).
+ */
+int mhb_peer_alloc(size_t bytes, int32_t device, void** ptr, unsigned char handle[64]);
+int mhb_peer_open(const unsigned char handle[64], int32_t device, void** ptr);
+int mhb_peer_close(void* ptr);
+int mhb_peer_free(void* ptr);
+
+/*
  * Instruction-rate probe for the roofline: runs the iterative visit sequence
  * (add, conditional subtract, 3-way min) from registers only, `visits_per_thread`
  * visits per thread on a persistent grid, and reports visits and device ms.

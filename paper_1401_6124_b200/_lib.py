@@ -63,6 +63,10 @@ SIGNATURES = {
     "mhb_corpus_intern": (C.c_int, [_P, _P, _P, _P, _P]),
     "mhb_corpus_export": (C.c_int, [_P, _P, _P, _P, _P]),
     "mhb_corpus_free": (None, [_P]),
+    "mhb_peer_alloc": (C.c_int, [_SZ, _I32, _P, _P]),
+    "mhb_peer_open": (C.c_int, [_P, _I32, _P]),
+    "mhb_peer_close": (C.c_int, [_P]),
+    "mhb_peer_free": (C.c_int, [_P]),
     "mhb_probe_visit_rate": (C.c_int, [_I64, _I32, C.POINTER(C.c_double), C.POINTER(C.c_float), _P]),
     "mhb_profile_begin": (C.c_int, [_I32]),
     "mhb_profile_end": (C.c_int, [C.POINTER(C.c_float), C.POINTER(C.c_int32)]),

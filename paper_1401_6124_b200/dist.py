@@ -1,4 +1,4 @@
-"""Row-sharded multi-GPU signing: nnz-balanced partition + NCCL gather.
+"""Row-sharded multi-GPU signing: nnz-balanced partition + gather (NCCL, or fused over peer memory).
 
 Sets are independent (reference minhash.py:91-110 signs one set at a time), so
 the batch shards by rows with no exchange during compute.  Every rank derives
@@ -9,6 +9,12 @@ collective is the optional gather of uint32 signature blocks to one rank.
 
 One process per GPU (torchrun); ``torch.distributed`` with backend "nccl" on the
 box, "gloo" in the CPU tests (which inject the CPU oracle as ``sign_fn``).
+
+Fused sign + gather (``sign_gather_peer``): the destination rank allocates the
+full [S, N] matrix as a ``PeerMatrix`` (CUDA IPC handle, csrc/peer.cu), every rank
+maps it and signs its rows straight into it -- the kernels' epilogue stores cross
+NVLink tile by tile while the rest of the shard is still being signed, so there is
+no separate gather step.  The handle travels once over the process group.
 """
 from __future__ import annotations
 
@@ -104,3 +110,104 @@ def sign_sharded(indptr, ids, family, *, sign_fn=None, gather: bool = True, dst:
         rows = [cuts[r + 1] - cuts[r] for r in range(world)]
         full = gather_blocks(block, rows, dst=dst, group=group)
     return block, (s0, s1), full
+
+
+class PeerMatrix:
+    """A [rows, cols] uint32/int64 device matrix shared across processes (csrc/peer.cu).
+
+    The owner allocates it (``PeerMatrix.allocate``) and passes ``handle`` (64 bytes)
+    to the others, which map it (``PeerMatrix.open``).  ``ptr(row)`` is the device
+    address of a row in this process's mapping; ``tensor()`` (owner only) views the
+    buffer as a torch tensor.  ``close()`` unmaps / frees."""
+
+    def __init__(self, ptr: int, handle: bytes, rows: int, cols: int, itemsize: int, owner: bool, device: int):
+        self._ptr, self.handle, self.rows, self.cols = ptr, handle, rows, cols
+        self.itemsize, self.owner, self.device = itemsize, owner, device
+
+    @classmethod
+    def allocate(cls, rows: int, cols: int, itemsize: int = 4, device: int = 0) -> "PeerMatrix":
+        import ctypes as C
+
+        from . import _lib
+
+        lib = _lib.load()
+        ptr, h = C.c_void_p(), (C.c_ubyte * 64)()
+        _lib.check(lib.mhb_peer_alloc(rows * cols * itemsize, device, C.byref(ptr), h))
+        return cls(ptr.value, bytes(h), rows, cols, itemsize, True, device)
+
+    @classmethod
+    def open(cls, handle: bytes, rows: int, cols: int, itemsize: int = 4, device: int = 0) -> "PeerMatrix":
+        import ctypes as C
+
+        from . import _lib
+
+        lib = _lib.load()
+        ptr = C.c_void_p()
+        h = (C.c_ubyte * 64).from_buffer_copy(handle)
+        _lib.check(lib.mhb_peer_open(h, device, C.byref(ptr)))
+        return cls(ptr.value, handle, rows, cols, itemsize, False, device)
+
+    def ptr(self, row: int = 0) -> int:
+        return self._ptr + row * self.cols * self.itemsize
+
+    @property
+    def __cuda_array_interface__(self):
+        typestr = "<u4" if self.itemsize == 4 else "<i8"
+        return {"shape": (self.rows, self.cols), "typestr": typestr, "data": (self._ptr, False), "version": 3}
+
+    def tensor(self):
+        """Zero-copy torch view (owner only; keeps this object alive)."""
+        import torch
+
+        if not self.owner:
+            raise RuntimeError("only the owning rank views the matrix as a tensor")
+        return torch.as_tensor(self, device=f"cuda:{self.device}")
+
+    def close(self) -> None:
+        from . import _lib
+
+        if self._ptr:
+            lib = _lib.load()
+            _lib.check(lib.mhb_peer_free(self._ptr) if self.owner else lib.mhb_peer_close(self._ptr))
+            self._ptr = 0
+
+
+def sign_gather_peer(indptr, ids, family, *, dst: int = 0, align: int = 1, device=None, group=None):
+    """Fused sign + gather: every rank signs its nnz-balanced slice directly into the
+    destination rank's [S, N] uint32 matrix (mapped over CUDA IPC / NVLink).
+
+    Returns (matrix, (s0, s1)): on `dst` the PeerMatrix holding every signature
+    (``.tensor()`` views it; the caller closes it), elsewhere None.  Each rank's
+    kernels complete (stream sync) before the barrier that publishes the matrix."""
+    import torch
+    import torch.distributed as dist
+
+    from .minhash import sign_csr_to_ptr
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    cuts = nnz_balanced_cuts(indptr, world, align)
+    s0, s1 = cuts[rank], cuts[rank + 1]
+    n_total = cuts[-1]
+    ip = np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64)
+    lo, hi = int(ip[s0]), int(ip[s1])
+    local_ip = torch.as_tensor(ip[s0:s1 + 1] - lo).to(dev)
+    x = ids if torch.is_tensor(ids) else torch.from_numpy(np.asarray(ids))
+    local_ids = x[lo:hi].to(dev)
+    if local_ids.dtype != torch.uint32:
+        local_ids = local_ids.to(torch.int64).to(torch.uint32)
+    mat = PeerMatrix.allocate(n_total, family.size, 4, dev.index) if rank == dst else None
+    box = [mat.handle if mat is not None else None]
+    dist.broadcast_object_list(box, src=dst, group=group)
+    view = mat if rank == dst else PeerMatrix.open(box[0], n_total, family.size, 4, dev.index)
+    try:
+        if s1 > s0:
+            sign_csr_to_ptr(local_ip, local_ids, family, view.ptr(s0))
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)  # every row has landed in dst's matrix
+    finally:
+        if rank != dst:
+            view.close()
+    dist.barrier(group=group)  # every mapping is closed before dst may free the matrix
+    return (mat if rank == dst else None), (s0, s1)

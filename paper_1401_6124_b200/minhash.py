@@ -121,12 +121,21 @@ def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) 
     """Raw asynchronous device call: indptr int64[S+1], ids uint32, out uint32/int64[S,N]
     CUDA tensors on one device.  No validation beyond the library's, no sync."""
     torch = _torch()
+    sign_csr_to_ptr(indptr, ids, family, out.data_ptr(), out.dtype == torch.int64, status, stream)
+
+
+def sign_csr_to_ptr(indptr, ids, family: Family, out_ptr: int, out_int64: bool = False, status=None,
+                    stream=None) -> None:
+    """sign_csr_device with the output given as a device address: rows [S, family.size]
+    of uint32 (or int64) starting at `out_ptr` -- e.g. this rank's rows of a peer
+    rank's matrix mapped with dist.PeerMatrix (fused sign + gather)."""
+    torch = _torch()
     lib = _lib.load()
     dev = ids.device
     n_sets = indptr.numel() - 1
     nnz = ids.numel()
     n_hash = family.size
-    out_dtype = _lib.OUT_I64 if out.dtype == torch.int64 else _lib.OUT_U32
+    out_dtype = _lib.OUT_I64 if out_int64 else _lib.OUT_U32
     ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, nnz, n_hash)
     with torch.cuda.device(dev):
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
@@ -136,18 +145,18 @@ def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) 
         if isinstance(family, IterativeFamily):
             rc = lib.mhb_sign_iterative_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
                                             family.base.a, family.base.b, family.prime, n_hash,
-                                            out.data_ptr(), out_dtype, status_ptr,
+                                            out_ptr, out_dtype, status_ptr,
                                             ws.data_ptr(), ws_bytes, sptr)
         elif family.prime > MAX_KERNEL_PRIME:
             a, b = family.device_params(dev, wide=True)
             rc = lib.mhb_sign_random_csr_u64(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
                                              a.data_ptr(), b.data_ptr(), family.prime, n_hash,
-                                             out.data_ptr(), out_dtype, status_ptr, sptr)
+                                             out_ptr, out_dtype, status_ptr, sptr)
         else:
             a, b = family.device_params(dev)
             rc = lib.mhb_sign_random_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
                                          a.data_ptr(), b.data_ptr(), family.prime, n_hash,
-                                         out.data_ptr(), out_dtype, status_ptr,
+                                         out_ptr, out_dtype, status_ptr,
                                          ws.data_ptr(), ws_bytes, sptr)
     _lib.check(rc)
 

@@ -1,0 +1,98 @@
+"""Fused sign + gather over peer memory (dist.sign_gather_peer, csrc/peer.cu).
+
+Every rank maps the destination rank's [S, N] matrix through a CUDA IPC handle and
+its signing kernels store their rows straight into it.  The box has one GPU, so the
+ranks here are processes sharing cuda:0 (same-device IPC): the code path -- handle
+export/import, per-rank row offsets, long-set red.global.min merges and finalize on
+mapped memory, the publish/unmap barriers -- is the multi-GPU one; the kernels never
+wait on each other (only host barriers after completion).  Result: bit-exact
+against the single-process signatures of the whole batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _batch():
+    from paper_1401_6124_b200 import gen
+
+    indptr, ids = gen.cfg1_numpy(n_sets=3000, seed=9)
+    rng = np.random.default_rng(4)
+    rows = [ids[indptr[s]:indptr[s + 1]] for s in range(indptr.size - 1)]
+    for n in (1500, 5000):  # long sets: chunk merges into the mapped matrix
+        rows.insert(int(rng.integers(0, len(rows))), rng.choice(1 << 20, size=n, replace=False).astype(np.uint32))
+    ip = np.zeros(len(rows) + 1, dtype=np.int64)
+    ip[1:] = np.cumsum([r.size for r in rows])
+    return ip, np.concatenate(rows).astype(np.uint32)
+
+
+def _worker(rank, world, port, kind, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6124_b200 import make_family, signatures_csr
+    from paper_1401_6124_b200.dist import sign_gather_peer
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ip, ids = _batch()
+        fam = make_family(kind, 5, 256, 1_048_583)
+        mat, (s0, s1) = sign_gather_peer(ip, ids, fam, device="cuda:0")
+        if rank == 0:
+            got = mat.tensor().cpu().numpy().copy()
+            mat.close()
+            want = signatures_csr(torch.as_tensor(ip, device="cuda:0"),
+                                  torch.as_tensor(ids.astype(np.int64), device="cuda:0").to(torch.uint32),
+                                  fam, out_dtype="uint32").cpu().numpy()
+            q.put(("ok", bool(np.array_equal(got, want)), int((got != want).sum())))
+    except Exception as exc:  # surface the failure to the parent
+        q.put(("error", repr(exc), 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "iterative"), (3, "random")])
+def test_sign_gather_peer_matches_single_process(cuda_device, world, kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_worker, args=(world, _free_port(), kind, q), nprocs=world, join=True,
+                       start_method="spawn")
+    status, equal, n_diff = q.get(timeout=60)
+    assert status == "ok", equal
+    assert equal, f"{n_diff} entries differ"
+
+
+def test_peer_matrix_single_rank(cuda_device):
+    """world == 1: the owner signs into its own PeerMatrix (no mapping)."""
+    import torch
+
+    from paper_1401_6124_b200 import make_family, signatures_csr
+    from paper_1401_6124_b200.dist import PeerMatrix
+    from paper_1401_6124_b200.minhash import sign_csr_to_ptr
+
+    ip, ids = _batch()
+    fam = make_family("iterative", 2, 128, 1_048_583)
+    m = PeerMatrix.allocate(ip.size - 1, 128, 4, 0)
+    try:
+        dip = torch.as_tensor(ip, device="cuda:0")
+        dids = torch.as_tensor(ids.astype(np.int64), device="cuda:0").to(torch.uint32)
+        sign_csr_to_ptr(dip, dids, fam, m.ptr(0))
+        torch.cuda.synchronize()
+        want = signatures_csr(dip, dids, fam, out_dtype="uint32")
+        assert torch.equal(m.tensor().view(torch.int32), want.view(torch.int32))
+    finally:
+        m.close()
