@@ -208,14 +208,22 @@ int mhb_format_text_records(const void* sig, int32_t sig_dtype, int64_t n_sets, 
  *   terms   : lowercase maximal alphanumeric runs ([^\W_]), deduplicated, sorted;
  *   ids     : vocabulary ids in first-occurrence order (document order, then the
  *             document's sorted terms); each document is its sorted id set.
- * Host-only, multi-threaded (n_threads <= 0: all hardware threads).  Pure-ASCII lines
- * are tokenized natively.  Lines holding a byte >= 0x80 are deferred: the caller
- * tokenizes them with the Unicode rules (Python str.lower / str.isalnum) and passes
- * the sorted UTF-8 terms to mhb_corpus_set_terms before mhb_corpus_intern.  `text`
- * must stay alive and unchanged until mhb_corpus_free.
+ * Host backend multi-threaded (n_threads <= 0: all hardware threads); device backend:
+ * mhb_corpus_scan_device.  Lines with a byte >= 0x80 are "deferred": their pure-ASCII
+ * segments (maximal runs of [A-Za-z0-9\x80-\xff] without a byte >= 0x80) are tokenized
+ * natively, and the caller supplies, through mhb_corpus_set_terms before
+ * mhb_corpus_intern, the terms of the line's other segments -- tokenize() of those
+ * segments joined by "\n", with Python's Unicode str.lower / str.isalnum -- or of the
+ * whole line when it holds U+03A3 (bytes CE A3; Final_Sigma is the one lowercase rule
+ * that looks across separators).  `text` must stay alive and unchanged until
+ * mhb_corpus_free.
  */
 typedef struct mhb_corpus mhb_corpus;
 int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_threads, mhb_corpus** corpus);
+/* The same ingest on GPU `device` (corpus_gpu.cu): lines, tokens, vocabulary and documents are
+   computed on the device; the rest of the mhb_corpus_* API is shared.  `text` is a host buffer
+   (pinned for full PCIe speed). */
+int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, mhb_corpus** corpus);
 int mhb_corpus_info(const mhb_corpus* corpus, int64_t* n_docs, int64_t* n_deferred);
 /* per deferred line k: its document index, byte offset and byte length in `text` */
 int mhb_corpus_deferred(const mhb_corpus* corpus, int64_t* lines, int64_t* starts, int64_t* lens);
@@ -229,6 +237,8 @@ int mhb_corpus_intern(mhb_corpus* corpus, int64_t* nnz, int64_t* n_terms, int64_
    any pointer may be NULL */
 int mhb_corpus_export(const mhb_corpus* corpus, int64_t* indptr, uint32_t* ids, int64_t* term_offsets,
                       char* term_blob);
+/* device-backend handles: copy indptr / ids into device buffers on `stream` (feeds mhb_sign_*_csr) */
+int mhb_corpus_export_device(const mhb_corpus* corpus, int64_t* indptr, uint32_t* ids, void* stream);
 void mhb_corpus_free(mhb_corpus* corpus);
 
 /*

@@ -28,6 +28,7 @@ from . import _lib
 from .minhash import FeatureSet
 
 _TOKEN = re.compile(r"[^\W_]+", re.UNICODE)
+_SEGMENT = re.compile(rb"[A-Za-z0-9\x80-\xff]+")  # tokens never cross ASCII separators
 
 
 def tokenize(text: str) -> tuple[str, ...]:
@@ -46,11 +47,17 @@ class Vocabulary:
     @classmethod
     def _from_terms(cls, terms: list[str]) -> "Vocabulary":
         v = cls()
-        v._id_to_term = list(terms)
-        v._term_to_id = dict(zip(v._id_to_term, range(len(v._id_to_term))))
+        v._id_to_term = terms
+        v._term_to_id = None  # built on first lookup
         return v
 
+    def _index(self) -> dict:
+        if self._term_to_id is None:
+            self._term_to_id = dict(zip(self._id_to_term, range(len(self._id_to_term))))
+        return self._term_to_id
+
     def add(self, term: str) -> int:
+        self._index()
         tid = self._term_to_id.get(term)
         if tid is None:
             tid = len(self._id_to_term)
@@ -59,7 +66,7 @@ class Vocabulary:
         return tid
 
     def id_of(self, term: str) -> int:
-        return self._term_to_id[term]
+        return self._index()[term]
 
     def term_of(self, tid: int) -> str:
         return self._id_to_term[tid]
@@ -68,7 +75,7 @@ class Vocabulary:
         return len(self._id_to_term)
 
     def __contains__(self, term: str) -> bool:
-        return term in self._term_to_id
+        return term in self._index()
 
     @property
     def terms(self) -> tuple[str, ...]:
@@ -89,11 +96,17 @@ class CorpusCSR(NamedTuple):
     empty_documents: int
 
 
-def _ingest(text: bytes, threads: int | None) -> CorpusCSR:
+def _ingest(text, n_bytes: int, threads: int | None, device: int | None, on_device: bool = False) -> CorpusCSR:
+    """text: bytes-like host buffer (numpy uint8 / pinned tensor view) of n_bytes."""
     lib = _lib.load()
-    buf = np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(1, dtype=np.uint8)
+    buf = text if isinstance(text, np.ndarray) else np.frombuffer(text, dtype=np.uint8)
+    if buf.size == 0:
+        buf = np.zeros(1, dtype=np.uint8)
     h = C.c_void_p()
-    _lib.check(lib.mhb_corpus_scan(buf.ctypes.data, len(text), int(threads or 0), C.byref(h)))
+    if device is None:
+        _lib.check(lib.mhb_corpus_scan(buf.ctypes.data, n_bytes, int(threads or 0), C.byref(h)))
+    else:
+        _lib.check(lib.mhb_corpus_scan_device(buf.ctypes.data, n_bytes, int(device), C.byref(h)))
     try:
         n_docs, n_def = C.c_int64(), C.c_int64()
         _lib.check(lib.mhb_corpus_info(h, C.byref(n_docs), C.byref(n_def)))
@@ -106,8 +119,7 @@ def _ingest(text: bytes, threads: int | None) -> CorpusCSR:
             all_terms = []
             for k in range(n_def.value):
                 s = int(starts[k])
-                # strict UTF-8, as open(path, encoding="utf-8") in the reference
-                terms = tokenize(text[s:s + int(lens[k])].decode("utf-8"))
+                terms = _deferred_terms(buf[s:s + int(lens[k])].tobytes())
                 all_terms.extend(terms)
                 line_ptr[k + 1] = line_ptr[k] + len(terms)
             # terms never contain "\n": join, encode once, split by the separators in numpy
@@ -122,28 +134,87 @@ def _ingest(text: bytes, threads: int | None) -> CorpusCSR:
                                                 blob.ctypes.data, term_off.ctypes.data))
         nnz, n_terms, tbytes, empty = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         _lib.check(lib.mhb_corpus_intern(h, C.byref(nnz), C.byref(n_terms), C.byref(tbytes), C.byref(empty)))
-        indptr = np.empty(n_docs.value + 1, dtype=np.int64)
-        ids = np.empty(nnz.value, dtype=np.uint32)
-        toff = np.empty(n_terms.value + 1, dtype=np.int64)
         tblob = np.empty(max(1, tbytes.value), dtype=np.uint8)
-        _lib.check(lib.mhb_corpus_export(h, indptr.ctypes.data, ids.ctypes.data, toff.ctypes.data,
-                                         tblob.ctypes.data))
+        if on_device:
+            import torch
+
+            dev = torch.device("cuda", device)
+            indptr = torch.empty(n_docs.value + 1, dtype=torch.int64, device=dev)
+            ids = torch.empty(max(1, nnz.value), dtype=torch.uint32, device=dev)[:nnz.value]
+            with torch.cuda.device(dev):
+                st = torch.cuda.current_stream(dev)
+                _lib.check(lib.mhb_corpus_export_device(h, indptr.data_ptr(), ids.data_ptr(), st.cuda_stream))
+            _lib.check(lib.mhb_corpus_export(h, None, None, None, tblob.ctypes.data))
+        else:
+            indptr = np.empty(n_docs.value + 1, dtype=np.int64)
+            ids = np.empty(nnz.value, dtype=np.uint32)
+            _lib.check(lib.mhb_corpus_export(h, indptr.ctypes.data, ids.ctypes.data, None, tblob.ctypes.data))
     finally:
         lib.mhb_corpus_free(h)
     terms = tblob[:tbytes.value].tobytes().decode("utf-8").split("\n")[:-1] if n_terms.value else []
     return CorpusCSR(Vocabulary._from_terms(terms), indptr, ids, int(empty.value))
 
 
-def build_corpus_csr(path_or_bytes, threads: int | None = None) -> CorpusCSR:
+def _deferred_terms(line: bytes) -> tuple[str, ...]:
+    """The caller's share of a line holding non-ASCII bytes (include/mhb.h): the
+    reference's tokenize() over the line's segments that hold non-ASCII bytes (the
+    pure-ASCII ones are tokenized natively), or over the whole line when it holds
+    U+03A3, whose lowercase (Final_Sigma) depends on context across separators.
+    Decoding is strict UTF-8, as open(path, encoding="utf-8") in the reference: every
+    byte >= 0x80 sits in a decoded segment."""
+    if b"\xce\xa3" in line:
+        return tokenize(line.decode("utf-8"))
+    return tokenize("\n".join(seg.decode("utf-8") for seg in _SEGMENT.findall(line) if not seg.isascii()))
+
+
+def _resolve_backend(backend: str, device):
+    if backend not in ("auto", "gpu", "host"):
+        raise ValueError(f"backend must be 'auto', 'gpu' or 'host', got {backend!r}")
+    if backend == "host":
+        return None
+    import torch
+
+    if backend == "auto" and not torch.cuda.is_available():
+        return None
+    if device is None:
+        return torch.cuda.current_device()
+    return torch.device(device).index or 0
+
+
+def build_corpus_csr(path_or_bytes, threads: int | None = None, *, backend: str = "auto", device=None,
+                     on_device: bool = False) -> CorpusCSR:
     """Ingest a one-document-per-line UTF-8 file (or its bytes) into a CSR batch.
 
     Same documents, vocabulary and empty-document tally as ``build_corpus``; the
-    rows are the documents' sorted ids, ready for ``signatures_csr``."""
+    rows are the documents' sorted ids, ready for ``signatures_csr``.
+    backend: "gpu" (csrc/corpus_gpu.cu), "host" (csrc/corpus.cpp, `threads` workers)
+    or "auto" (the GPU when one is visible).  on_device (GPU backend): indptr / ids
+    come back as CUDA tensors instead of numpy arrays."""
+    dev = _resolve_backend(backend, device)
+    if on_device and dev is None:
+        raise ValueError("on_device=True needs the GPU backend")
     if isinstance(path_or_bytes, (bytes, bytearray, memoryview)):
-        text = bytes(path_or_bytes)
-    else:
-        text = Path(path_or_bytes).read_bytes()
-    return _ingest(text, threads)
+        data = np.frombuffer(bytes(path_or_bytes), dtype=np.uint8)
+        return _ingest(data, data.size, threads, dev, on_device)
+    path = Path(path_or_bytes)
+    n = path.stat().st_size
+    view = _staging(n) if dev is not None else np.empty(n, dtype=np.uint8)
+    with open(path, "rb", buffering=0) as fh:
+        got = fh.readinto(memoryview(view))
+    if got != n:
+        raise OSError(f"short read of {path}: {got} of {n} bytes")
+    return _ingest(view, n, threads, dev, on_device)
+
+
+_STAGING = []  # one pinned host buffer, grown on demand and reused (full-speed H2D of the text)
+
+
+def _staging(n: int) -> np.ndarray:
+    import torch
+
+    if not _STAGING or _STAGING[0].numel() < n:
+        _STAGING[:] = [torch.empty(max(n, 1 << 20), dtype=torch.uint8, pin_memory=True)]
+    return _STAGING[0].numpy()[:n]
 
 
 def build_corpus(path) -> CorpusData:
@@ -186,7 +257,8 @@ def synth_corpus(n_docs: int, doc_size: int, seed: int, id_space: int | None = N
 
 
 def sign_corpus(corpus, out, *, family: str, hashes: int = 128, prime: int | None = None, seed: int = 0,
-                fmt: str = "text", threads: int | None = None, log=sys.stderr) -> tuple[int, int]:
+                fmt: str = "text", threads: int | None = None, backend: str = "auto",
+                log=sys.stderr) -> tuple[int, int]:
     """The reference CLI's ``sign`` (cli.py:205-230): ingest `corpus`, build the family,
     sign every non-empty document on the GPU and write (doc_id, signature) records to
     `out` in the reference's text or binary format.  Returns (records, prime)."""
@@ -196,7 +268,8 @@ def sign_corpus(corpus, out, *, family: str, hashes: int = 128, prime: int | Non
 
     if fmt not in ("text", "binary"):
         raise ValueError(f"fmt must be 'text' or 'binary', got {fmt!r}")
-    c = build_corpus_csr(corpus, threads)
+    dev = _resolve_backend(backend, None)
+    c = build_corpus_csr(corpus, threads, backend=backend, on_device=dev is not None)
     vocab_size = len(c.vocabulary)
     if vocab_size == 0:
         raise ValueError(f"corpus {corpus} holds no tokens to sign")
@@ -205,16 +278,33 @@ def sign_corpus(corpus, out, *, family: str, hashes: int = 128, prime: int | Non
     else:
         p = choose_prime(vocab_size - 1, hashes)
     fam = make_family(family, seed, hashes, p)
-    sizes = np.diff(c.indptr)
-    keep = np.flatnonzero(sizes > 0)
-    if keep.size == sizes.size:
-        ip, ids, oids = c.indptr, c.ids, None
+    if dev is not None:  # CSR already resident: drop the empty documents on the device
+        import torch
+
+        sizes_t = c.indptr[1:] - c.indptr[:-1]
+        keep_t = torch.nonzero(sizes_t > 0).flatten()
+        if keep_t.numel() == sizes_t.numel():
+            ip, ids, oids = c.indptr, c.ids, None
+        else:
+            ks = sizes_t[keep_t]
+            ip = torch.zeros(keep_t.numel() + 1, dtype=torch.int64, device=sizes_t.device)
+            torch.cumsum(ks, 0, out=ip[1:])
+            sel = torch.repeat_interleave(keep_t, ks)
+            pos = torch.arange(int(ip[-1]), device=ip.device) - torch.repeat_interleave(ip[:-1], ks) + c.indptr[sel]
+            ids, oids = c.ids.view(torch.int32)[pos].view(torch.uint32), keep_t.cpu().numpy()
+        sizes = sizes_t.cpu().numpy()
+        keep = np.flatnonzero(sizes > 0)
     else:
-        ip = np.zeros(keep.size + 1, dtype=np.int64)
-        ip[1:] = np.cumsum(sizes[keep])
-        sel = np.repeat(keep, sizes[keep])
-        pos = np.arange(ip[-1]) - np.repeat(ip[:-1], sizes[keep]) + c.indptr[sel]
-        ids, oids = c.ids[pos], keep
+        sizes = np.diff(c.indptr)
+        keep = np.flatnonzero(sizes > 0)
+        if keep.size == sizes.size:
+            ip, ids, oids = c.indptr, c.ids, None
+        else:
+            ip = np.zeros(keep.size + 1, dtype=np.int64)
+            ip[1:] = np.cumsum(sizes[keep])
+            sel = np.repeat(keep, sizes[keep])
+            pos = np.arange(ip[-1]) - np.repeat(ip[:-1], sizes[keep]) + c.indptr[sel]
+            ids, oids = c.ids[pos], keep
     skipped = int(sizes.size - keep.size)
     n = write_signatures_csr(out, ip, ids, fam, fmt=fmt, obj_ids=oids) if keep.size else _touch(out)
     if skipped and log is not None:

@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "common.h"
+#include "corpus_device.h"
 
 namespace {
 
@@ -208,6 +209,11 @@ struct mhb_corpus {
     std::vector<Table> global;                     // [S]
     std::vector<const Entry*> vocab;               // by id
     int64_t vocab_bytes = 0, empty_docs = 0;
+    // device backend (corpus_gpu.cu); null for the host backend
+    mhb::CorpusDevice* dev = nullptr;
+    ~mhb_corpus() {
+        if (dev) mhb::corpus_device_free(dev);
+    }
 };
 
 namespace {
@@ -244,24 +250,36 @@ void split_lines(mhb_corpus* c) {
     }
 }
 
-// Tokenize one pure-ASCII line into `toks` (sorted, unique).  false: the line holds
-// a non-ASCII byte and must be deferred.
-bool tokenize_ascii(const unsigned char* p, int64_t len, Arena& ar, std::vector<Tok>& toks) {
+// Native tokens of one line into `toks` (sorted, unique): the maximal ASCII
+// alphanumeric runs whose segment (maximal run of [A-Za-z0-9\x80-\xff]) is pure
+// ASCII.  *foreign: the line holds a byte >= 0x80 (its other segments are the
+// caller's, see mhb_corpus_set_terms).  A line holding U+03A3 (bytes CE A3, Python's
+// only context-dependent lowercase) has no native tokens.
+void tokenize_native(const unsigned char* p, int64_t len, Arena& ar, std::vector<Tok>& toks, bool* foreign) {
     toks.clear();
+    *foreign = false;
+    bool sigma = false;
     for (int64_t j = 0; j < len;) {
         const uint8_t cj = kClass.c[p[j]];
         if (cj == 0) {
             ++j;
             continue;
         }
-        if (cj & 4) return false;
         int64_t k = j;
         uint8_t up = 0, ck;
         while (k < len && ((ck = kClass.c[p[k]]) & 3)) {
             up |= ck;
             ++k;
         }
-        if (k < len && (kClass.c[p[k]] & 4)) return false;
+        if (k < len && (kClass.c[p[k]] & 4)) {  // the segment holds non-ASCII bytes: not native
+            *foreign = true;
+            while (k < len && kClass.c[p[k]] != 0) {
+                sigma |= p[k] == 0xCE && k + 1 < len && p[k + 1] == 0xA3;
+                ++k;
+            }
+            j = k;
+            continue;
+        }
         const char* tp = reinterpret_cast<const char*>(p + j);
         const uint32_t n = (uint32_t)(k - j);
         if (up & 2) {
@@ -272,9 +290,9 @@ bool tokenize_ascii(const unsigned char* p, int64_t len, Arena& ar, std::vector<
         toks.push_back(Tok{tp, prefix_key(tp, n), n});
         j = k;
     }
+    if (sigma) toks.clear();
     std::sort(toks.begin(), toks.end(), tok_less);
     toks.erase(std::unique(toks.begin(), toks.end(), tok_eq), toks.end());
-    return true;
 }
 
 void scan_parts(mhb_corpus* c) {
@@ -304,7 +322,9 @@ void scan_parts(mhb_corpus* c) {
         std::vector<Tok> toks;
         for (int64_t d = d0; d < d1; ++d) {
             const unsigned char* p = reinterpret_cast<const unsigned char*>(c->text + c->line_start[d]);
-            if (!tokenize_ascii(p, c->line_end[d] - c->line_start[d], c->arenas[t], toks)) {
+            bool foreign;
+            tokenize_native(p, c->line_end[d] - c->line_start[d], c->arenas[t], toks, &foreign);
+            if (foreign) {  // interned in mhb_corpus_set_terms, with the caller's terms
                 c->deferred[d] = 1;
                 continue;
             }
@@ -348,6 +368,24 @@ extern "C" int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_thre
     }
 }
 
+extern "C" int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, mhb_corpus** out) {
+    using namespace mhb;
+    clear_error();
+    if (!out || n_bytes < 0 || (n_bytes > 0 && !text)) return set_error(MHB_ERR_INVALID, "bad corpus buffer");
+    *out = nullptr;
+    try {
+        auto c = std::make_unique<mhb_corpus>();
+        c->text = text;
+        c->n_bytes = n_bytes;
+        const int rc = corpus_device_scan(text, n_bytes, device, &c->dev, c->line_start, c->line_end, c->deferred_lines);
+        if (rc) return rc;
+        *out = c.release();
+        return MHB_OK;
+    } catch (const std::exception& e) {
+        return set_error(MHB_ERR_INVALID, "corpus scan failed: %s", e.what());
+    }
+}
+
 extern "C" int mhb_corpus_info(const mhb_corpus* c, int64_t* n_docs, int64_t* n_deferred) {
     using namespace mhb;
     clear_error();
@@ -375,31 +413,42 @@ extern "C" int mhb_corpus_set_terms(mhb_corpus* c, int64_t n_lines, const int64_
     using namespace mhb;
     clear_error();
     if (!c) return set_error(MHB_ERR_INVALID, "null corpus handle");
-    if (c->interned) return set_error(MHB_ERR_INVALID, "corpus already interned");
     if (n_lines < 0 || (n_lines > 0 && (!lines || !line_ptr || !term_offsets)))
         return set_error(MHB_ERR_INVALID, "bad deferred-term arrays");
+    if (c->dev) return corpus_device_set_terms(c->dev, n_lines, lines, line_ptr, blob, term_offsets);
+    if (c->interned) return set_error(MHB_ERR_INVALID, "corpus already interned");
     const int64_t n_docs = (int64_t)c->line_start.size();
     const int P = c->T;  // the deferred part
     Table& tab = c->local[P];
     auto& dt = c->doc_terms[P];
     Arena& ar = c->arenas[P];
+    std::vector<Tok> toks;
     for (int64_t k = 0; k < n_lines; ++k) {
         const int64_t d = lines[k];
         if (d < 0 || d >= n_docs || c->deferred[d] != 1)
             return set_error(MHB_ERR_INVALID, "line %lld is not a deferred line awaiting terms", (long long)d);
         const int64_t t0 = line_ptr[k], t1 = line_ptr[k + 1];
-        if (t1 < t0 || t1 - t0 >= (1ll << kRankBits))
-            return set_error(MHB_ERR_INVALID, "bad term count for line %lld", (long long)d);
-        c->term_off[d] = (int64_t)dt.size();
-        c->term_cnt[d] = t1 - t0;
+        if (t1 < t0) return set_error(MHB_ERR_INVALID, "bad term count for line %lld", (long long)d);
+        // the line's native tokens + the supplied terms, sorted and deduplicated
+        bool foreign;
+        const unsigned char* p = reinterpret_cast<const unsigned char*>(c->text + c->line_start[d]);
+        tokenize_native(p, c->line_end[d] - c->line_start[d], ar, toks, &foreign);
         for (int64_t j = t0; j < t1; ++j) {
             const int64_t len = term_offsets[j + 1] - term_offsets[j];
             if (len <= 0 || len > 0xFFFFFFFFll) return set_error(MHB_ERR_INVALID, "bad term length");
             char* q = ar.alloc(len);
             std::memcpy(q, blob + term_offsets[j], len);
-            dt.push_back(tab.intern(q, (uint32_t)len, hash_bytes(q, len), prefix_key(q, (uint32_t)len),
-                                    ((uint64_t)d << kRankBits) | (j - t0)));
+            toks.push_back(Tok{q, prefix_key(q, (uint32_t)len), (uint32_t)len});
         }
+        std::sort(toks.begin(), toks.end(), tok_less);
+        toks.erase(std::unique(toks.begin(), toks.end(), tok_eq), toks.end());
+        if (toks.size() >= (1u << kRankBits))
+            return set_error(MHB_ERR_INVALID, "line %lld holds 2^24 or more distinct terms", (long long)d);
+        c->term_off[d] = (int64_t)dt.size();
+        c->term_cnt[d] = (int64_t)toks.size();
+        for (size_t r = 0; r < toks.size(); ++r)
+            dt.push_back(tab.intern(toks[r].p, toks[r].len, hash_bytes(toks[r].p, toks[r].len), toks[r].key,
+                                    ((uint64_t)d << kRankBits) | r));
         c->deferred[d] = 2;
     }
     return MHB_OK;
@@ -410,6 +459,7 @@ extern "C" int mhb_corpus_intern(mhb_corpus* c, int64_t* nnz, int64_t* n_terms, 
     using namespace mhb;
     clear_error();
     if (!c) return set_error(MHB_ERR_INVALID, "null corpus handle");
+    if (c->dev) return corpus_device_intern(c->dev, nnz, n_terms, term_bytes, empty_docs);
     const int64_t n_docs = (int64_t)c->line_start.size();
     for (int64_t d : c->deferred_lines)
         if (c->deferred[d] != 2)
@@ -530,6 +580,7 @@ extern "C" int mhb_corpus_export(const mhb_corpus* c, int64_t* indptr, uint32_t*
     using namespace mhb;
     clear_error();
     if (!c) return set_error(MHB_ERR_INVALID, "null corpus handle");
+    if (c->dev) return corpus_device_export(c->dev, indptr, ids, term_offsets, term_blob);
     if (!c->interned) return set_error(MHB_ERR_INVALID, "call mhb_corpus_intern first");
     if (indptr) std::memcpy(indptr, c->indptr.data(), c->indptr.size() * sizeof(int64_t));
     if (ids && !c->ids.empty()) std::memcpy(ids, c->ids.data(), c->ids.size() * sizeof(uint32_t));
@@ -546,6 +597,14 @@ extern "C" int mhb_corpus_export(const mhb_corpus* c, int64_t* indptr, uint32_t*
         if (term_offsets) term_offsets[c->vocab.size()] = off;
     }
     return MHB_OK;
+}
+
+extern "C" int mhb_corpus_export_device(const mhb_corpus* c, int64_t* indptr, uint32_t* ids, void* stream) {
+    using namespace mhb;
+    clear_error();
+    if (!c) return set_error(MHB_ERR_INVALID, "null corpus handle");
+    if (!c->dev) return set_error(MHB_ERR_INVALID, "mhb_corpus_export_device needs a handle from mhb_corpus_scan_device");
+    return corpus_device_export_device(c->dev, indptr, ids, stream);
 }
 
 extern "C" void mhb_corpus_free(mhb_corpus* c) { delete c; }

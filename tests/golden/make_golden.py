@@ -243,6 +243,10 @@ CORPUS_EDGE_CASES = [
     " plain ascii line\n\ufeffbom sep line\n",
     "na\u00efve\nNA\u00cfVE naive\n\u65e5\u672c\u8a9e \u30c6\u30b9\u30c8\n\u0391\u03b2\u03b3 abc\n",
     "\ufb01ne fine FINE\n\u1e9e \u00df ss\nABCDEFGHIJKLMNOPQRSTUVWXYZ abcdefghijklmnopqrstuvwxyz0123456789\n",
+    # Final_Sigma looks across ASCII case-ignorables (' and .): whole-line lowercase
+    "\u039f\u0394\u039f\u03a3 \u039f\u0394\u039f\u03a3'\u0391 \u0391\u03a3.x \u03a3 x_\u0391\u03a3_y \u03a3\u0391 plain\n",
+    "\u201ccurly quotes\u201d don\u2019t \u2014 dashes\u2026 and plain words\n",
+    "x\u00a0y abc\u0301def \u212aelvin K k mixed ASCII caf\u00e9 na\u00efve end\n",
 ]
 
 CORPUS_SYNTH = [  # gen.synth_text_corpus arguments

@@ -141,3 +141,28 @@ def test_abi_deferred_protocol_errors():
         assert lib.mhb_corpus_export(h, None, None, None, None) == _lib.MHB_ERR_INVALID
     finally:
         lib.mhb_corpus_free(h)
+
+
+def test_corpus_oracle_pinned_to_reference(golden):
+    """The pure-Python restatement (oracle/corpus_oracle.py) reproduces the reference's
+    golden output before it is used as the fuzz checker."""
+    from oracle import corpus_oracle
+
+    for k, data, case, indptr, ids in _cases(golden):
+        terms, ip, x, empty = corpus_oracle.build_corpus_bytes(data)
+        assert terms == case["terms"] and empty == case["empty"], k
+        assert np.array_equal(ip, indptr) and np.array_equal(x, ids), k
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_host_backend_against_oracle(seed):
+    """Random text over separators, every line-break kind, Final_Sigma contexts and
+    case-expanding / non-alphanumeric code points: native ingest == the oracle."""
+    from oracle import corpus_oracle
+
+    data = corpus_oracle.fuzz_text(seed, 4000 + 500 * seed)
+    terms, ip, x, empty = corpus_oracle.build_corpus_bytes(data)
+    for threads in (1, 3):
+        c = build_corpus_csr(data, threads=threads, backend="host")
+        assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
+        assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)

@@ -391,3 +391,77 @@ def test_sign_corpus_matches_reference_cli(golden, tmp_path, cuda_device):
             n, prime = sign_corpus(path, out, family=fam, hashes=16, seed=3, fmt=fmt, log=None)
             assert prime == case["sign_prime"]
             assert hashlib.sha256(out.read_bytes()).hexdigest() == want, (case["synth"], key)
+
+
+def test_gpu_corpus_ingest_matches_reference(golden, cuda_device):
+    """Device ingest (csrc/corpus_gpu.cu) == the reference's build_corpus on the golden
+    corpora (edge cases + seeded synthetic text with non-ASCII lines)."""
+    from paper_1401_6124_b200.corpus import build_corpus_csr
+
+    cases = json.loads((golden / "corpus.json").read_text())
+    z = np.load(golden / "corpus.npz")
+    for k, case in enumerate(cases):
+        data = case["text"].encode("utf-8") if "text" in case else gen.synth_text_corpus(**case["synth"])
+        c = build_corpus_csr(data, backend="gpu")
+        assert list(c.vocabulary.terms) == case["terms"], k
+        assert c.empty_documents == case["empty"], k
+        assert np.array_equal(c.indptr, z[f"indptr{k}"]), k
+        assert np.array_equal(c.ids.astype(np.int64), z[f"ids{k}"]), k
+
+
+@pytest.mark.parametrize("unicode_frac,crlf", [(0.0, False), (0.02, True), (0.3, False)])
+def test_gpu_corpus_ingest_equals_host_backend(tmp_path, cuda_device, unicode_frac, crlf):
+    """Larger corpora: GPU and host (csrc/corpus.cpp) backends agree exactly, through a
+    file (pinned read) and with the CSR exported straight to device tensors."""
+    import torch
+
+    from paper_1401_6124_b200.corpus import build_corpus_csr
+
+    text = gen.synth_text_corpus(60000, 21, vocab=80000, unicode_frac=unicode_frac, crlf=crlf)
+    path = tmp_path / "c.txt"
+    path.write_bytes(text)
+    h = build_corpus_csr(path, backend="host")
+    g = build_corpus_csr(path, backend="gpu")
+    assert g.vocabulary.terms == h.vocabulary.terms and g.empty_documents == h.empty_documents
+    assert np.array_equal(g.indptr, h.indptr) and np.array_equal(g.ids, h.ids)
+    d = build_corpus_csr(path, backend="gpu", on_device=True)
+    assert d.indptr.is_cuda and d.ids.is_cuda
+    assert np.array_equal(d.indptr.cpu().numpy(), h.indptr)
+    assert np.array_equal(d.ids.cpu().numpy(), h.ids)
+    # and the CSR signs like the host copy
+    from paper_1401_6124_b200 import make_family, signatures_csr
+
+    fam = make_family("iterative", 1, 64, 1_048_583)
+    keep = np.flatnonzero(np.diff(h.indptr) > 0)[:2000]
+    rows = [h.ids[h.indptr[r]:h.indptr[r + 1]] for r in keep]
+    ip = np.zeros(len(rows) + 1, dtype=np.int64)
+    ip[1:] = np.cumsum([r.size for r in rows])
+    sig = signatures_csr(torch.as_tensor(ip, device=cuda_device),
+                         torch.as_tensor(np.concatenate(rows).astype(np.int64), device=cuda_device).to(torch.uint32),
+                         fam)
+    assert np.array_equal(sig.cpu().numpy(), oracle.sign_family_csr(ip, np.concatenate(rows), fam))
+
+
+def test_sign_corpus_host_backend_matches_reference_cli(golden, tmp_path, cuda_device):
+    from paper_1401_6124_b200.corpus import sign_corpus
+
+    case = [c for c in json.loads((golden / "corpus.json").read_text()) if "synth" in c][0]
+    path = tmp_path / "corpus.txt"
+    path.write_bytes(gen.synth_text_corpus(**case["synth"]))
+    out = tmp_path / "sig"
+    sign_corpus(path, out, family="random", hashes=16, seed=3, fmt="binary", backend="host", log=None)
+    assert hashlib.sha256(out.read_bytes()).hexdigest() == case["sign_hashes16_seed3"]["random_binary"]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_gpu_corpus_fuzz_against_oracle(cuda_device, seed):
+    """Device ingest on seeded random text (every line-break kind, Final_Sigma contexts,
+    case-expanding and non-alphanumeric code points) == the pure-Python oracle."""
+    from oracle import corpus_oracle
+    from paper_1401_6124_b200.corpus import build_corpus_csr
+
+    data = corpus_oracle.fuzz_text(100 + seed, 6000 + 700 * seed)
+    terms, ip, x, empty = corpus_oracle.build_corpus_bytes(data)
+    c = build_corpus_csr(data, backend="gpu")
+    assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
+    assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
