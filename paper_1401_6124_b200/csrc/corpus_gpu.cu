@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -435,9 +437,8 @@ int corpus_device_scan(const char* text_h, int64_t n, int device, CorpusDevice**
     try {
         Scratch sc(st);
         // count the breaks, then select their positions
-        cub::CountingInputIterator<int64_t> iota(0);
-        cub::TransformInputIterator<int64_t, BreakFlag, cub::CountingInputIterator<int64_t>> flags(iota,
-                                                                                                 BreakFlag{d->text});
+        thrust::counting_iterator<int64_t> iota(0);
+        auto flags = thrust::make_transform_iterator(iota, BreakFlag{d->text});
         int64_t* n_brk_d = sc.get<int64_t>(1);
         size_t tb = 0;
         MHB_CUDA(cub::DeviceReduce::Sum(nullptr, tb, flags, n_brk_d, n, st));
