@@ -478,11 +478,25 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MHB_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- exercises the N>1 code
+    # path (barriers, max over ranks, peer gather) on a one-GPU box; its timings mean nothing
+    shared = os.environ.get("MHB_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
+
+    def max_over_ranks(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     cfg = gen.CONFIGS[args.config]
     n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
@@ -548,10 +562,7 @@ def main():
     _lib.check(lib.mhb_profile_end(C.byref(kms), C.byref(kn)))
     clocks = clk.stop()
     elapsed_ms = e0.elapsed_time(e1)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(elapsed_ms)
     ms_per_step = max_ms / args.steps
     value = world * n_sets * N * args.steps / (max_ms / 1e3)
 
@@ -580,13 +591,13 @@ def main():
             sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
         p1.record(stream)
         torch.cuda.synchronize()
-        tp = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device=dev)
+        pms_max = max_over_ranks(p0.elapsed_time(p1))
         if world > 1:
-            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-        if rank == 0:  # this rank's rows landed where they belong
-            mine = owner.tensor()[:n_sets]
-            if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
-                raise SystemExit("peer gather: rank 0 rows differ from the local signatures")
+            dist.barrier()  # every rank's rows have landed
+        # each rank checks its rows of rank 0's matrix through its own mapping
+        mine = view.tensor()[rank * n_sets:(rank + 1) * n_sets]
+        if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
+            raise SystemExit(f"peer gather: rank {rank} rows in rank 0's matrix differ from its local signatures")
         if world > 1:
             dist.barrier()
         if rank != 0:
@@ -595,7 +606,7 @@ def main():
             dist.barrier()
         if owner is not None:
             owner.close()
-        pms = float(tp.item()) / args.steps
+        pms = pms_max / args.steps
         gather_peer = {"ms_per_step": pms, "entries_per_s": world * n_sets * N / (pms / 1e3),
                        "bytes_to_rank0_per_step": world * n_sets * N * 4,
                        "path": "mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC (csrc/peer.cu)"}
@@ -662,12 +673,10 @@ def main():
             times.append(time.perf_counter() - t0)
         if not np.array_equal(out_np[:1000], out[:1000].cpu().numpy()):
             raise SystemExit("e2e output differs from the device path")
-        e2e_s = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n_sets * N / float(e2e_s.item()), "unit": "entries/s",
+        e2e_max = max_over_ranks(statistics.mean(times))
+        e2e = {"value": world * n_sets * N / e2e_max, "unit": "entries/s",
                "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
-               "ms_per_step": float(e2e_s.item()) * 1e3,
+               "ms_per_step": e2e_max * 1e3,
                "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 4 streams)",
                "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
 

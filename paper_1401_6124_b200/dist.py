@@ -117,8 +117,8 @@ class PeerMatrix:
 
     The owner allocates it (``PeerMatrix.allocate``) and passes ``handle`` (64 bytes)
     to the others, which map it (``PeerMatrix.open``).  ``ptr(row)`` is the device
-    address of a row in this process's mapping; ``tensor()`` (owner only) views the
-    buffer as a torch tensor.  ``close()`` unmaps / frees."""
+    address of a row in this process's mapping; ``tensor()`` views the mapping as a
+    torch tensor.  ``close()`` unmaps / frees."""
 
     def __init__(self, ptr: int, handle: bytes, rows: int, cols: int, itemsize: int, owner: bool, device: int):
         self._ptr, self.handle, self.rows, self.cols = ptr, handle, rows, cols
@@ -156,11 +156,12 @@ class PeerMatrix:
         return {"shape": (self.rows, self.cols), "typestr": typestr, "data": (self._ptr, False), "version": 3}
 
     def tensor(self):
-        """Zero-copy torch view (owner only; keeps this object alive)."""
+        """Zero-copy torch view of this process's mapping (keeps this object alive;
+        invalid after close())."""
         import torch
 
-        if not self.owner:
-            raise RuntimeError("only the owning rank views the matrix as a tensor")
+        if not self._ptr:
+            raise RuntimeError("the matrix is closed")
         return torch.as_tensor(self, device=f"cuda:{self.device}")
 
     def close(self) -> None:

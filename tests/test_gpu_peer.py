@@ -96,3 +96,23 @@ def test_peer_matrix_single_rank(cuda_device):
         assert torch.equal(m.tensor().view(torch.int32), want.view(torch.int32))
     finally:
         m.close()
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N>1 path (torchrun, barriers, max over ranks, fused peer gather with
+    every rank checking its rows) with both ranks on the box's one GPU over gloo
+    (MHB_BENCH_SHARED_GPU=1).  Checks the plumbing, not the timings."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MHB_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--n-sets", "50000", "--gather", "peer", "--no-e2e", "--no-cpu-baseline"]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "weak"
+    assert line["gather_peer"]["bytes_to_rank0_per_step"] == 2 * 50000 * 256 * 4
