@@ -38,8 +38,24 @@ struct Lane {
     size_t ws_cap = 0;
 };
 
+// Small batches (the per-set reference API: signature() on one FeatureSet) skip the
+// chunk pipeline: inputs are staged in mapped pinned memory, one kernel launch reads
+// them over PCIe (ids once into shared memory), computes every (set, hash) argmin
+// exactly in 64-bit arithmetic and writes the result back into mapped memory.
+constexpr int64_t kSmallSets = 64;
+constexpr int64_t kSmallNnz = 1 << 16;
+constexpr int64_t kSmallSetMax = 8192;  // ids of one set in shared memory
+constexpr int32_t kSmallHash = 16384;
+
+struct SmallStage {
+    char* in = nullptr;    // indptr | ids | a | b   (mapped pinned)
+    char* out = nullptr;   // [sets, hashes] u32 / i64 (mapped pinned)
+    int32_t* status = nullptr;
+};
+
 struct DeviceCache {
     bool init = false;
+    SmallStage small;
     Lane lanes[kLanes];
     int32_t* status = nullptr;  // one word per chunk, read once at the end
     uint32_t* ra = nullptr;
@@ -55,6 +71,51 @@ DeviceCache g_cache[64];
 __global__ void rebase_indptr_kernel(int64_t* indptr, int64_t n, int64_t base) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         indptr[i] -= base;
+}
+
+__global__ void __launch_bounds__(256) sign_small_kernel(int kind, const int64_t* indptr, const uint32_t* ids,
+                                                        uint64_t a, uint64_t b, const uint32_t* ra,
+                                                        const uint32_t* rb, uint64_t p, int32_t n_hash, void* out,
+                                                        int32_t out_dtype, int32_t* status) {
+    __shared__ uint32_t xs[kSmallSetMax];
+    __shared__ int block_flags;
+    if (threadIdx.x == 0) block_flags = 0;
+    const int64_t set = blockIdx.x;
+    const int64_t f0 = indptr[set] - indptr[0];
+    const int n = (int)(indptr[set + 1] - indptr[set]);
+    int flags = n == 0 ? MHB_STATUS_EMPTY_SET : 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t x = ids[f0 + k];
+        xs[k] = x;
+        if (x >= p) flags |= MHB_STATUS_ID_GE_PRIME;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_hash; i += blockDim.x) {
+        uint64_t A, B;
+        if (kind == KIND_ITERATIVE) {  // h_i(x) = ((a + i) x + i b) mod p, families.py:170-176
+            A = a + (uint64_t)i;
+            B = ((uint64_t)i * b) % p;
+        } else {  // h_i(x) = (a_i x + b_i) mod p, kernels.py:21-41
+            A = ra[i];
+            B = rb[i];
+            if (A < 1 || A >= p || B >= p) flags |= MHB_STATUS_BAD_PARAM;
+        }
+        uint64_t best = ~0ull;
+        uint32_t arg = 0;
+        for (int k = 0; k < n; ++k) {  // p < 2^32: A x + B < 2^64
+            const uint32_t x = xs[k];
+            const uint64_t h = (A * x + B) % p;
+            if (h < best) {  // bijection on [0, p): the minimum is unique
+                best = h;
+                arg = x;
+            }
+        }
+        if (out_dtype == MHB_OUT_I64) reinterpret_cast<long long*>(out)[set * n_hash + i] = (long long)arg;
+        else reinterpret_cast<uint32_t*>(out)[set * n_hash + i] = arg;
+    }
+    if (flags) atomicOr(&block_flags, flags);  // (__syncthreads_or would only say "some flag")
+    __syncthreads();
+    if (threadIdx.x == 0) status[set] = block_flags;
 }
 
 int grow(void** ptr, size_t* cap, size_t need) {
@@ -97,6 +158,60 @@ std::vector<Chunk> plan_chunks(const int64_t* indptr, int64_t n_sets, int32_t n_
 
 }  // namespace mhb
 
+namespace mhb {
+namespace {
+
+bool small_batch(const int64_t* indptr, int64_t n_sets, int32_t n_hash, uint64_t prime) {
+    if (n_sets > kSmallSets || n_hash > kSmallHash || prime >= (1ull << 32)) return false;
+    if (indptr[n_sets] - indptr[0] > kSmallNnz) return false;
+    for (int64_t s = 0; s < n_sets; ++s)
+        if (indptr[s + 1] - indptr[s] > kSmallSetMax || indptr[s + 1] < indptr[s]) return false;
+    return true;
+}
+
+int sign_small(DeviceCache& dc, int32_t kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets,
+               uint64_t a, uint64_t b, const uint32_t* a_host, const uint32_t* b_host, uint64_t prime,
+               int32_t n_hash, void* out, int32_t out_dtype, int32_t* status_host) {
+    SmallStage& sm = dc.small;
+    const size_t in_bytes = (kSmallSets + 1) * 8 + kSmallNnz * 4 + 2 * (size_t)kSmallHash * 4;
+    const size_t out_cap = kSmallSets * (size_t)kSmallHash * 8;
+    if (!sm.in) {
+        int rc = cuda_check(cudaHostAlloc((void**)&sm.in, in_bytes, cudaHostAllocMapped), "cudaHostAlloc (small in)");
+        if (rc) return rc;
+        rc = cuda_check(cudaHostAlloc((void**)&sm.out, out_cap, cudaHostAllocMapped), "cudaHostAlloc (small out)");
+        if (rc) return rc;
+        rc = cuda_check(cudaHostAlloc((void**)&sm.status, kSmallSets * 4, cudaHostAllocMapped),
+                        "cudaHostAlloc (small status)");
+        if (rc) return rc;
+    }
+    int64_t* ip = reinterpret_cast<int64_t*>(sm.in);
+    uint32_t* x = reinterpret_cast<uint32_t*>(sm.in + (kSmallSets + 1) * 8);
+    uint32_t* ra = x + kSmallNnz;
+    uint32_t* rb = ra + kSmallHash;
+    const int64_t nnz = indptr[n_sets] - indptr[0];
+    std::memcpy(ip, indptr, (n_sets + 1) * 8);
+    if (nnz) std::memcpy(x, ids + indptr[0], nnz * 4);
+    if (kind == KIND_RANDOM) {
+        std::memcpy(ra, a_host, n_hash * 4);
+        std::memcpy(rb, b_host, n_hash * 4);
+    }
+    cudaStream_t st = dc.lanes[0].stream;
+    sign_small_kernel<<<(unsigned)n_sets, 256, 0, st>>>(kind, ip, x, a, b, ra, rb, prime, n_hash, sm.out, out_dtype,
+                                                      sm.status);
+    int rc = cuda_check(cudaGetLastError(), "sign_small_kernel launch");
+    if (rc) return rc;
+    rc = cuda_check(cudaStreamSynchronize(st), "sign_small_kernel");
+    if (rc) return rc;
+    std::memcpy(out, sm.out, (size_t)n_sets * n_hash * (out_dtype == MHB_OUT_I64 ? 8 : 4));
+    int32_t st_or = 0;
+    for (int64_t s = 0; s < n_sets; ++s) st_or |= sm.status[s];
+    if (status_host) *status_host = st_or;
+    return MHB_OK;
+}
+
+}  // namespace
+}  // namespace mhb
+
 using namespace mhb;
 
 extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets,
@@ -132,6 +247,14 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         rc = cuda_check(cudaMalloc((void**)&dc.status, kMaxChunks * sizeof(int32_t)), "cudaMalloc status");
         if (rc) return rc;
         dc.init = true;
+    }
+    if (small_batch(indptr, n_sets, n_hash, prime)) {
+        if (kind == KIND_RANDOM && (!a_host || !b_host)) return set_error(MHB_ERR_INVALID, "random family needs a and b");
+        if ((rc = check_sign_params(kind, a, b, true, prime, n_hash))) return rc;
+        rc = sign_small(dc, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out, out_dtype,
+                        status_host);
+        cudaSetDevice(prev);
+        return rc;
     }
     if (kind == KIND_RANDOM) {
         if (!a_host || !b_host) return set_error(MHB_ERR_INVALID, "random family needs a and b");
@@ -219,6 +342,9 @@ extern "C" void mhb_host_release(void) {
         cudaFree(dc.ra);
         cudaFree(dc.rb);
         cudaFree(dc.status);
+        if (dc.small.in) cudaFreeHost(dc.small.in);
+        if (dc.small.out) cudaFreeHost(dc.small.out);
+        if (dc.small.status) cudaFreeHost(dc.small.status);
         dc = DeviceCache{};
     }
 }

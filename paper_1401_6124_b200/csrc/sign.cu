@@ -706,22 +706,13 @@ static int blocks_per_sm(SignKernelFn fn, size_t smem, const DeviceInfo& dev) {
     return occ;
 }
 
-int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
-                uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
-                int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,
-                size_t workspace_bytes, cudaStream_t st, unsigned long long* keys, int32_t rows_per_band,
-                int32_t write_sig) {
-    clear_error();
-    if (n_sets < 0 || nnz < 0) return set_error(MHB_ERR_INVALID, "n_sets and nnz must be >= 0");
+int check_sign_params(int kind, uint64_t a, uint64_t b, bool have_random_arrays, uint64_t prime, int32_t n_hash) {
     if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
     if (prime < 3 || !is_prime_u64(prime)) return set_error(MHB_ERR_INVALID, "modulus %llu is not prime",
                                                              (unsigned long long)prime);
     if (prime >= (1ull << 63))
         return set_error(MHB_ERR_UNSUPPORTED, "prime %llu >= 2^63 is out of range", (unsigned long long)prime);
-    if (out_dtype != MHB_OUT_U32 && out_dtype != MHB_OUT_I64)
-        return set_error(MHB_ERR_INVALID, "unknown out_dtype %d", out_dtype);
-    const bool wide = prime >= (1ull << 31);
-    if (wide && kind == KIND_RANDOM)
+    if (prime >= (1ull << 31) && kind == KIND_RANDOM)
         return set_error(MHB_ERR_UNSUPPORTED,
                          "prime %llu >= 2^31: random-family parameters need 64 bits, use mhb_sign_random_csr_u64",
                          (unsigned long long)prime);
@@ -732,9 +723,23 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
             return set_error(MHB_ERR_INVALID,
                              "need a + size < prime to keep every member invertible; got a=%llu, size=%d, "
                              "prime=%llu", (unsigned long long)a, n_hash, (unsigned long long)prime);
-    } else if (ra == nullptr || rb == nullptr) {
+    } else if (!have_random_arrays) {
         return set_error(MHB_ERR_INVALID, "random family needs device arrays a and b");
     }
+    return MHB_OK;
+}
+
+int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
+                uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
+                int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,
+                size_t workspace_bytes, cudaStream_t st, unsigned long long* keys, int32_t rows_per_band,
+                int32_t write_sig) {
+    clear_error();
+    if (n_sets < 0 || nnz < 0) return set_error(MHB_ERR_INVALID, "n_sets and nnz must be >= 0");
+    if (out_dtype != MHB_OUT_U32 && out_dtype != MHB_OUT_I64)
+        return set_error(MHB_ERR_INVALID, "unknown out_dtype %d", out_dtype);
+    if (int rc = check_sign_params(kind, a, b, ra != nullptr && rb != nullptr, prime, n_hash)) return rc;
+    const bool wide = prime >= (1ull << 31);
     if (n_sets > 0 && (indptr == nullptr || out == nullptr))
         return set_error(MHB_ERR_INVALID, "null indptr/out");
     if (nnz > 0 && ids == nullptr) return set_error(MHB_ERR_INVALID, "null ids");

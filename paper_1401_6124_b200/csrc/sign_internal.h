@@ -85,6 +85,9 @@ int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int6
                      int32_t out_dtype, int32_t* status, cudaStream_t st);
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash);
 
+// Host-side parameter checks shared by every signing entry (errors as in launch_sign).
+int check_sign_params(int kind, uint64_t a, uint64_t b, bool have_random_arrays, uint64_t prime, int32_t n_hash);
+
 int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, int64_t nnz,
                 uint64_t a, uint64_t b, const uint32_t* ra, const uint32_t* rb, uint64_t prime,
                 int32_t n_hash, void* out, int32_t out_dtype, int32_t* status, void* workspace,

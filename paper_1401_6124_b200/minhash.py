@@ -256,13 +256,18 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         raise ValueError(f"feature id {s.max_id} >= family prime {family.prime}")
     if s.max_id > MAX_ID:
         raise NotImplementedError(f"feature id {s.max_id} >= 2^32: CSR ids are uint32")
-    torch = _torch()
     _check_family(family)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    ids = torch.from_numpy(s.ids.astype(np.uint32)).to(dev, non_blocking=False)
-    indptr = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
-    out = signatures_csr(indptr, ids, family, out_dtype="int64", validate=False)
-    return Signature(out[0].cpu().numpy(), family.key)
+    if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:  # 64-bit a, b: device entry
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ids = torch.from_numpy(s.ids.astype(np.uint32)).to(dev, non_blocking=False)
+        indptr = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
+        out = signatures_csr(indptr, ids, family, out_dtype="int64", validate=False)
+        return Signature(out[0].cpu().numpy(), family.key)
+    # host buffers -> mhb_sign_csr_host, whose small-batch path is one launch (csrc/host.cu)
+    out = _signatures_csr_host(np.array([0, len(s)], dtype=np.int64), s.ids.astype(np.uint32), family, "int64",
+                               None, None)
+    return Signature(out[0], family.key)
 
 
 def signatures(sets, family: Family) -> list[Signature]:

@@ -465,3 +465,60 @@ def test_gpu_corpus_fuzz_against_oracle(cuda_device, seed):
     c = build_corpus_csr(data, backend="gpu")
     assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
     assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
+
+
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_small_batch_host_path(cuda_device, kind):
+    """mhb_sign_csr_host's one-launch small-batch path (<= 64 sets, <= 8192 ids per set,
+    N <= 16384, p < 2^32) against the oracle, at and across its limits, both dtypes."""
+    from paper_1401_6124_b200.minhash import _signatures_csr_host
+
+    rng = np.random.default_rng(17 if kind == "iterative" else 18)
+    primes = [1_048_583, 16_777_259] + ([2_147_483_659, 4_294_967_291] if kind == "iterative" else [])
+    for p in primes:
+        for n_hash in (1, 7, 128, 1000, 16384):
+            if kind == "iterative" and n_hash * 2 + 3 >= p:
+                continue
+            fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
+            for sizes in ([1], [50], [8192], [8193], [3, 1, 9, 40] * 16, [5] * 65):
+                if n_hash >= 1000 and sum(sizes) > 9000 and len(sizes) > 1:
+                    continue
+                hi = min(p, 1 << 32)
+                rows = [np.unique(rng.integers(0, hi, size=n)).astype(np.uint32) for n in sizes]
+                ip = np.zeros(len(rows) + 1, dtype=np.int64)
+                ip[1:] = np.cumsum([r.size for r in rows])
+                ids = np.concatenate(rows)
+                want = oracle.sign_family_csr(ip, ids, fam)
+                for dt in ("int64", "uint32"):
+                    got = _signatures_csr_host(ip, ids, fam, dt, None, None)
+                    assert np.array_equal(got.astype(np.int64), want), (p, n_hash, sizes[:3], dt)
+
+
+def test_small_batch_status_flags(cuda_device):
+    """Empty sets, ids >= p and out-of-range random parameters raise as in the reference."""
+    from paper_1401_6124_b200.minhash import _signatures_csr_host
+
+    fam = make_family("iterative", 3, 64, 1_048_583)
+    with pytest.raises(ValueError):
+        _signatures_csr_host(np.array([0, 2, 2], dtype=np.int64), np.array([1, 2], dtype=np.uint32), fam, "int64",
+                             None, None)
+    with pytest.raises(ValueError):
+        signature(FeatureSet([5, 1_048_583 + 10]), fam)
+    # out-of-range random parameters (a family object would reject them): status flag from both
+    # the small-batch path (1 set) and the chunked pipeline (100 sets)
+    import ctypes as C
+
+    from paper_1401_6124_b200 import _lib
+
+    lib = _lib.load()
+    a = np.array([0, 5], dtype=np.uint32)
+    b = np.array([1, 2], dtype=np.uint32)
+    for n_sets in (1, 100):
+        ip = np.arange(0, 2 * n_sets + 1, 2, dtype=np.int64)
+        x = np.tile(np.array([1, 2], dtype=np.uint32), n_sets)
+        out = np.empty((n_sets, 2), dtype=np.int64)
+        st = C.c_int32(0)
+        rc = lib.mhb_sign_csr_host(_lib.KIND_RANDOM, ip.ctypes.data, x.ctypes.data, n_sets, x.size, 0, 0,
+                                   a.ctypes.data, b.ctypes.data, 1_048_583, 2, out.ctypes.data, _lib.OUT_I64,
+                                   C.addressof(st), 0)
+        assert rc == 0 and st.value & _lib.STATUS_BAD_PARAM, (n_sets, st.value)

@@ -111,3 +111,26 @@ def test_wide_primes_restatement(golden):
         fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
         for s in range(ip.size - 1):
             assert np.array_equal(oracle.brute_force_row(ids[ip[s]:ip[s + 1]], fam), z[f"out{k}"][s]), m
+
+
+def test_c_oracle_wide_primes_against_reference(golden):
+    """The C oracle itself on the reference's wide-prime outputs: int64 loops up to
+    MAX_VECTOR_PRIME, the exact (_signature_by_rows) arithmetic beyond it."""
+    z = np.load(golden / "wide.npz")
+    meta = json.loads((golden / "wide.json").read_text())
+    for k, m in enumerate(meta):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        if fam.prime >= 1 << 63:
+            continue
+        assert np.array_equal(oracle.sign_family_csr(z["indptr"], z["ids"], fam), z[f"out{k}"]), m
+
+
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_c_oracle_exact_beyond_max_vector_prime(kind):
+    """p just below 2^32 (a*x overflows int64): the C oracle == Python-int brute force."""
+    rng = np.random.default_rng(5)
+    p = 4_294_967_291
+    fam = make_family(kind, 11, 9, p)
+    ids = np.unique(rng.integers(0, p, size=300)).astype(np.uint32)
+    got = oracle.sign_family_csr(np.array([0, ids.size]), ids, fam)[0]
+    assert np.array_equal(got, oracle.brute_force_row(ids, fam))

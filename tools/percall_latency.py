@@ -1,0 +1,32 @@
+"""Per-call latency of the reference-style per-set API (signature) vs the batched path."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1401_6124_b200 import FeatureSet, gen, make_family, signature, signatures_csr  # noqa: E402
+
+indptr, ids = gen.cfg1_numpy(n_sets=2000, seed=3)
+fam = make_family("iterative", 1, 128, 1_048_583)
+sets = [FeatureSet(ids[indptr[s]:indptr[s + 1]]) for s in range(2000)]
+torch.cuda.init()
+for s in sets[:50]:
+    signature(s, fam)
+t0 = time.perf_counter()
+for s in sets:
+    signature(s, fam)
+dt = (time.perf_counter() - t0) / len(sets)
+print(f"signature(): {dt * 1e6:.1f} us/call (N=128, ~50 ids)")
+one = np.array([0, len(sets[0])], dtype=np.int64)
+x = sets[0].ids.astype(np.uint32)
+for _ in range(50):
+    signatures_csr(one, x, fam)
+t0 = time.perf_counter()
+for _ in range(2000):
+    signatures_csr(one, x, fam)
+print(f"signatures_csr(numpy, S=1): {(time.perf_counter() - t0) / 2000 * 1e6:.1f} us/call")
+t0 = time.perf_counter()
+signatures_csr(indptr, ids, fam)
+print(f"signatures_csr(numpy, S=2000): {(time.perf_counter() - t0) * 1e6 / 2000:.2f} us/set")
