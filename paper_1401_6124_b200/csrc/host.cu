@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.h"
+#include "modarith.cuh"
 #include "sign_internal.h"
 
 namespace mhb {
@@ -100,14 +101,28 @@ __global__ void __launch_bounds__(256) sign_small_kernel(int kind, const int64_t
             B = rb[i];
             if (A < 1 || A >= p || B >= p) flags |= MHB_STATUS_BAD_PARAM;
         }
-        uint64_t best = ~0ull;
         uint32_t arg = 0;
-        for (int k = 0; k < n; ++k) {  // p < 2^32: A x + B < 2^64
-            const uint32_t x = xs[k];
-            const uint64_t h = (A * x + B) % p;
-            if (h < best) {  // bijection on [0, p): the minimum is unique
-                best = h;
-                arg = x;
+        if (p < (1ull << 31)) {  // u32 Shoup multiply (modarith.cuh), exact for any x < 2^32
+            const uint32_t a32 = (uint32_t)A, b32 = (uint32_t)B, p32 = (uint32_t)p;
+            const uint32_t ap = (uint32_t)((A << 32) / p);
+            uint32_t best = 0xffffffffu;
+            for (int k = 0; k < n; ++k) {
+                const uint32_t x = xs[k];
+                const uint32_t h = mul_add_mod(a32, ap, b32, x, p32);
+                if (h < best) {  // bijection on [0, p): the minimum is unique
+                    best = h;
+                    arg = x;
+                }
+            }
+        } else {  // p < 2^32: A x + B < 2^64
+            uint64_t best = ~0ull;
+            for (int k = 0; k < n; ++k) {
+                const uint32_t x = xs[k];
+                const uint64_t h = (A * x + B) % p;
+                if (h < best) {
+                    best = h;
+                    arg = x;
+                }
             }
         }
         if (out_dtype == MHB_OUT_I64) reinterpret_cast<long long*>(out)[set * n_hash + i] = (long long)arg;

@@ -264,9 +264,25 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         indptr = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
         out = signatures_csr(indptr, ids, family, out_dtype="int64", validate=False)
         return Signature(out[0].cpu().numpy(), family.key)
-    # host buffers -> mhb_sign_csr_host, whose small-batch path is one launch (csrc/host.cu)
-    out = _signatures_csr_host(np.array([0, len(s)], dtype=np.int64), s.ids.astype(np.uint32), family, "int64",
-                               None, None)
+    # host buffers -> mhb_sign_csr_host, whose small-batch path is one launch (csrc/host.cu);
+    # the FeatureSet is already canonical and checked above, so the call goes straight through
+    lib = _lib.load()
+    ids = s.ids.astype(np.uint32)
+    indptr = np.array([0, ids.size], dtype=np.int64)
+    out = np.empty((1, family.size), dtype=np.int64)
+    status = C.c_int32(0)
+    dev = _torch().cuda.current_device()
+    if isinstance(family, IterativeFamily):
+        rc = lib.mhb_sign_csr_host(_lib.KIND_ITERATIVE, indptr.ctypes.data, ids.ctypes.data, 1, ids.size,
+                                   family.base.a, family.base.b, None, None, family.prime, family.size,
+                                   out.ctypes.data, _lib.OUT_I64, C.addressof(status), dev)
+    else:
+        a, b = family.host_params()
+        rc = lib.mhb_sign_csr_host(_lib.KIND_RANDOM, indptr.ctypes.data, ids.ctypes.data, 1, ids.size, 0, 0,
+                                   a.ctypes.data, b.ctypes.data, family.prime, family.size, out.ctypes.data,
+                                   _lib.OUT_I64, C.addressof(status), dev)
+    _lib.check(rc)
+    _raise_status(status.value, family)
     return Signature(out[0], family.key)
 
 

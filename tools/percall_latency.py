@@ -30,3 +30,23 @@ print(f"signatures_csr(numpy, S=1): {(time.perf_counter() - t0) / 2000 * 1e6:.1f
 t0 = time.perf_counter()
 signatures_csr(indptr, ids, fam)
 print(f"signatures_csr(numpy, S=2000): {(time.perf_counter() - t0) * 1e6 / 2000:.2f} us/set")
+
+import ctypes as C  # noqa: E402
+
+from paper_1401_6124_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+out = np.empty(128, dtype=np.int64)
+st = C.c_int32(0)
+args = (_lib.KIND_ITERATIVE, one.ctypes.data, x.ctypes.data, 1, x.size, fam.base.a, fam.base.b, None, None,
+        fam.prime, 128, out.ctypes.data, _lib.OUT_I64, C.addressof(st), 0)
+for _ in range(100):
+    lib.mhb_sign_csr_host(*args)
+t0 = time.perf_counter()
+for _ in range(5000):
+    lib.mhb_sign_csr_host(*args)
+print(f"raw mhb_sign_csr_host (S=1): {(time.perf_counter() - t0) / 5000 * 1e6:.1f} us/call")
+import cProfile, pstats  # noqa: E402,E401
+
+cProfile.run("for s in sets[:500]: signature(s, fam)", "/tmp/sig.prof")
+pstats.Stats("/tmp/sig.prof").sort_stats("tottime").print_stats(10)
