@@ -247,8 +247,11 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     const size_t out_bytes = out_dtype == MHB_OUT_I64 ? 8 : 4;
 
     std::lock_guard<std::mutex> lock(g_mu);
-    int prev = 0;
-    cudaGetDevice(&prev);
+    struct DeviceGuard {  // restores the caller's current device on every return path
+        int prev = 0;
+        DeviceGuard() { cudaGetDevice(&prev); }
+        ~DeviceGuard() { cudaSetDevice(prev); }
+    } guard;
     int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
     if (rc) return rc;
     DeviceCache& dc = g_cache[device];
@@ -266,10 +269,8 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     if (small_batch(indptr, n_sets, n_hash, prime)) {
         if (kind == KIND_RANDOM && (!a_host || !b_host)) return set_error(MHB_ERR_INVALID, "random family needs a and b");
         if ((rc = check_sign_params(kind, a, b, true, prime, n_hash))) return rc;
-        rc = sign_small(dc, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out, out_dtype,
-                        status_host);
-        cudaSetDevice(prev);
-        return rc;
+        return sign_small(dc, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out, out_dtype,
+                          status_host);
     }
     if (kind == KIND_RANDOM) {
         if (!a_host || !b_host) return set_error(MHB_ERR_INVALID, "random family needs a and b");
@@ -334,7 +335,6 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         return rc;
     for (int32_t v : st) status_acc |= v;
     if (status_host) *status_host = status_acc;
-    cudaSetDevice(prev);
     return MHB_OK;
 }
 
