@@ -220,10 +220,23 @@ int mhb_format_text_records(const void* sig, int32_t sig_dtype, int64_t n_sets, 
  */
 typedef struct mhb_corpus mhb_corpus;
 int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_threads, mhb_corpus** corpus);
+/* Unicode tables of the caller's Python (what tokenize() uses): bit c of alnum_bits is
+   chr(c).isalnum(); lower_keys (ascending) are the code points whose str.lower() differs,
+   lower_vals[3k..3k+2] the lowercase code points of lower_keys[k] (0xFFFFFFFF padded). */
+typedef struct mhb_unicode_tables {
+    const uint32_t* alnum_bits;   /* [0x110000 / 32] */
+    const uint32_t* lower_keys;   /* [n_lower] */
+    const uint32_t* lower_vals;   /* [3 * n_lower] */
+    int32_t n_lower;
+} mhb_unicode_tables;
 /* The same ingest on GPU `device` (corpus_gpu.cu): lines, tokens, vocabulary and documents are
    computed on the device; the rest of the mhb_corpus_* API is shared.  `text` is a host buffer
-   (pinned for full PCIe speed). */
-int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, mhb_corpus** corpus);
+   (pinned for full PCIe speed).  With `tables`, lines holding non-ASCII bytes are tokenized on the
+   device too (strict UTF-8, full lowercase mapping, isalnum), except lines with invalid UTF-8 or
+   U+03A3, which stay deferred to the caller under the rule above; tables == NULL defers every
+   non-ASCII segment as the host backend does. */
+int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, const mhb_unicode_tables* tables,
+                           mhb_corpus** corpus);
 int mhb_corpus_info(const mhb_corpus* corpus, int64_t* n_docs, int64_t* n_deferred);
 /* per deferred line k: its document index, byte offset and byte length in `text` */
 int mhb_corpus_deferred(const mhb_corpus* corpus, int64_t* lines, int64_t* starts, int64_t* lens);

@@ -96,6 +96,37 @@ class CorpusCSR(NamedTuple):
     empty_documents: int
 
 
+class _UnicodeTables(C.Structure):  # include/mhb.h mhb_unicode_tables
+    _fields_ = [("alnum_bits", C.c_void_p), ("lower_keys", C.c_void_p), ("lower_vals", C.c_void_p),
+                ("n_lower", C.c_int32)]
+
+
+_UNI: list = []  # (struct, arrays) built once per process
+
+
+def unicode_tables():
+    """str.isalnum / str.lower of THIS Python over every code point -- the rules
+    tokenize() applies -- packed for mhb_corpus_scan_device (about 0.4 s, once)."""
+    if not _UNI:
+        alnum = np.zeros(0x110000 // 32, dtype=np.uint32)
+        bits = np.fromiter((chr(c).isalnum() for c in range(0x110000)), dtype=bool, count=0x110000)
+        alnum[:] = np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").ravel()
+        keys, vals = [], []
+        for c in range(0x80, 0x110000):
+            low = chr(c).lower()
+            if low != chr(c):
+                if len(low) > 3:
+                    raise NotImplementedError(f"lowercase of U+{c:04X} has {len(low)} code points")
+                keys.append(c)
+                vals.extend([ord(x) for x in low] + [0xFFFFFFFF] * (3 - len(low)))
+        k = np.asarray(keys, dtype=np.uint32)
+        v = np.asarray(vals, dtype=np.uint32)
+        st = _UnicodeTables(alnum.ctypes.data, k.ctypes.data if k.size else None, v.ctypes.data if v.size else None,
+                            int(k.size))
+        _UNI[:] = [st, (alnum, k, v)]
+    return _UNI[0]
+
+
 def _ingest(text, n_bytes: int, threads: int | None, device: int | None, on_device: bool = False) -> CorpusCSR:
     """text: bytes-like host buffer (numpy uint8 / pinned tensor view) of n_bytes."""
     lib = _lib.load()
@@ -106,7 +137,8 @@ def _ingest(text, n_bytes: int, threads: int | None, device: int | None, on_devi
     if device is None:
         _lib.check(lib.mhb_corpus_scan(buf.ctypes.data, n_bytes, int(threads or 0), C.byref(h)))
     else:
-        _lib.check(lib.mhb_corpus_scan_device(buf.ctypes.data, n_bytes, int(device), C.byref(h)))
+        _lib.check(lib.mhb_corpus_scan_device(buf.ctypes.data, n_bytes, int(device), C.byref(unicode_tables()),
+                                              C.byref(h)))
     try:
         n_docs, n_def = C.c_int64(), C.c_int64()
         _lib.check(lib.mhb_corpus_info(h, C.byref(n_docs), C.byref(n_def)))

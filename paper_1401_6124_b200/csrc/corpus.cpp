@@ -368,7 +368,8 @@ extern "C" int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_thre
     }
 }
 
-extern "C" int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, mhb_corpus** out) {
+extern "C" int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device,
+                                      const mhb_unicode_tables* tables, mhb_corpus** out) {
     using namespace mhb;
     clear_error();
     if (!out || n_bytes < 0 || (n_bytes > 0 && !text)) return set_error(MHB_ERR_INVALID, "bad corpus buffer");
@@ -377,7 +378,8 @@ extern "C" int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t
         auto c = std::make_unique<mhb_corpus>();
         c->text = text;
         c->n_bytes = n_bytes;
-        const int rc = corpus_device_scan(text, n_bytes, device, &c->dev, c->line_start, c->line_end, c->deferred_lines);
+        const int rc = corpus_device_scan(text, n_bytes, device, tables, &c->dev, c->line_start, c->line_end,
+                                          c->deferred_lines);
         if (rc) return rc;
         *out = c.release();
         return MHB_OK;

@@ -4,13 +4,16 @@
 #include <cstdint>
 #include <vector>
 
+#include "mhb.h"
+
 namespace mhb {
 
 struct CorpusDevice;  // device buffers + results of one ingest
 
 // Lines + per-line token counts + non-ASCII detection on the GPU.  Fills the host
 // line arrays and the list of deferred (non-ASCII) lines.  Synchronous.
-int corpus_device_scan(const char* text, int64_t n_bytes, int device, CorpusDevice** out,
+int corpus_device_scan(const char* text, int64_t n_bytes, int device, const mhb_unicode_tables* tables,
+                       CorpusDevice** out,
                        std::vector<int64_t>& line_start, std::vector<int64_t>& line_end,
                        std::vector<int64_t>& deferred_lines);
 int corpus_device_set_terms(CorpusDevice* d, int64_t n_lines, const int64_t* lines, const int64_t* line_ptr,

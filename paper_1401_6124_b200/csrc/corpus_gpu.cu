@@ -98,7 +98,7 @@ __device__ __forceinline__ bool native_start(const uint8_t* s, int64_t j, int64_
 
 // One warp per line: native token count, non-ASCII and U+03A3 detection.
 __global__ void scan_lines(const uint8_t* s, const int64_t* line_start, const int64_t* line_end, int64_t n_docs,
-                           int64_t* ncount, uint8_t* deferred) {
+                           int64_t* ncount, uint8_t* deferred, bool uni) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -116,7 +116,7 @@ __global__ void scan_lines(const uint8_t* s, const int64_t* line_start, const in
         }
         if (lane == 0) {
             deferred[d] = foreign ? 1 : 0;
-            ncount[d] = sigma ? 0 : cnt;
+            ncount[d] = (sigma || (uni && foreign)) ? 0 : cnt;  // uni: uni_lines tokenizes the whole line
         }
     }
 }
@@ -130,16 +130,17 @@ __global__ void scatter_deferred(const int64_t* lines, const int64_t* cnt, const
     }
 }
 
-__global__ void add_counts(const int64_t* a, const int64_t* b, int64_t n, int64_t* out) {
+__global__ void add_counts(const int64_t* a, const int64_t* b, const int64_t* c, int64_t n, int64_t* out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < n) out[k] = a[k] + b[k];
+    if (k < n) out[k] = a[k] + b[k] + c[k];
 }
 
 // One warp per line: token (start, len, line) in document order -- the line's native
 // tokens, then (deferred lines) the caller-supplied terms.
 __global__ void write_tokens(const uint8_t* s, int64_t n_bytes, const int64_t* line_start, const int64_t* line_end,
-                             int64_t n_docs, const int64_t* ncount, const int64_t* tok_off, const int64_t* dfirst,
-                             const int64_t* dterm_off, int64_t* tok_start, uint32_t* tok_len, uint32_t* tok_line) {
+                             int64_t n_docs, const int64_t* ncount, const uint8_t* code, const int64_t* tok_off,
+                             const int64_t* dfirst, const int64_t* dterm_off, int64_t* tok_start, uint32_t* tok_len,
+                             uint32_t* tok_line) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -162,7 +163,7 @@ __global__ void write_tokens(const uint8_t* s, int64_t n_bytes, const int64_t* l
                 rank += __popc(m);
             }
         }
-        const int64_t ns = tok_off[d + 1] - t0 - nn;  // supplied terms (deferred lines)
+        const int64_t ns = code[d] == 1 ? tok_off[d + 1] - t0 - nn : 0;  // caller-supplied terms
         if (ns > 0) {
             const int64_t k0 = dfirst[d];
             for (int64_t r = lane; r < ns; r += 32) {
@@ -328,6 +329,159 @@ __global__ void compact_csr(const uint32_t* sorted, const int64_t* keep, const i
     }
 }
 
+// ---- Unicode lines on the device ---------------------------------------------------
+// With the caller's tables (str.isalnum / str.lower of the running Python), a line
+// holding non-ASCII bytes is tokenized here exactly as tokenize() does it: strict
+// UTF-8 decode, lowercase each code point (full mapping, 1..3 code points), tokens =
+// maximal runs of alphanumeric lowered code points, re-encoded as UTF-8.  Lines with
+// invalid UTF-8 (the reference raises) or U+03A3 (Final_Sigma, context-dependent)
+// stay deferred to the caller.
+struct UniTab {
+    const uint32_t* alnum;  // bitmap over code points
+    const uint32_t* keys;   // ascending code points whose lowercase differs
+    const uint32_t* vals;   // [n * 3] lowercase code points, 0xFFFFFFFF padded
+    int n;
+};
+
+__device__ __forceinline__ bool uni_alnum(const UniTab& t, uint32_t c) { return (t.alnum[c >> 5] >> (c & 31)) & 1u; }
+
+__device__ __forceinline__ int uni_lower(const UniTab& t, uint32_t cp, uint32_t* out) {
+    if (cp < 0x80) {
+        out[0] = (cp - 'A' < 26u) ? cp + 32 : cp;
+        return 1;
+    }
+    int lo = 0, hi = t.n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (t.keys[mid] < cp) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < t.n && t.keys[lo] == cp) {
+        int k = 0;
+        for (; k < 3 && t.vals[3 * lo + k] != 0xFFFFFFFFu; ++k) out[k] = t.vals[3 * lo + k];
+        return k;
+    }
+    out[0] = cp;
+    return 1;
+}
+
+// Strict UTF-8 (Python's decoder): no overlongs, surrogates or code points > U+10FFFF.
+__device__ __forceinline__ int utf8_decode(const uint8_t* s, int64_t i, int64_t end, uint32_t* cp) {
+    const uint32_t b0 = s[i];
+    if (b0 < 0x80) {
+        *cp = b0;
+        return 1;
+    }
+    int n;
+    uint32_t lo = 0x80, hi = 0xBF, c;
+    if (b0 >= 0xC2 && b0 <= 0xDF) {
+        n = 2;
+        c = b0 & 0x1F;
+    } else if (b0 >= 0xE0 && b0 <= 0xEF) {
+        n = 3;
+        c = b0 & 0x0F;
+        if (b0 == 0xE0) lo = 0xA0;
+        if (b0 == 0xED) hi = 0x9F;
+    } else if (b0 >= 0xF0 && b0 <= 0xF4) {
+        n = 4;
+        c = b0 & 0x07;
+        if (b0 == 0xF0) lo = 0x90;
+        if (b0 == 0xF4) hi = 0x8F;
+    } else {
+        return 0;
+    }
+    if (i + n > end) return 0;
+    for (int k = 1; k < n; ++k) {
+        const uint32_t b = s[i + k];
+        if (k == 1 ? (b < lo || b > hi) : (b < 0x80 || b > 0xBF)) return 0;
+        c = (c << 6) | (b & 0x3F);
+    }
+    *cp = c;
+    return n;
+}
+
+__device__ __forceinline__ int utf8_len(uint32_t c) { return c < 0x80 ? 1 : c < 0x800 ? 2 : c < 0x10000 ? 3 : 4; }
+
+__device__ __forceinline__ void utf8_put(uint8_t* o, uint32_t c) {
+    if (c < 0x80) {
+        o[0] = (uint8_t)c;
+    } else if (c < 0x800) {
+        o[0] = (uint8_t)(0xC0 | (c >> 6));
+        o[1] = (uint8_t)(0x80 | (c & 0x3F));
+    } else if (c < 0x10000) {
+        o[0] = (uint8_t)(0xE0 | (c >> 12));
+        o[1] = (uint8_t)(0x80 | ((c >> 6) & 0x3F));
+        o[2] = (uint8_t)(0x80 | (c & 0x3F));
+    } else {
+        o[0] = (uint8_t)(0xF0 | (c >> 18));
+        o[1] = (uint8_t)(0x80 | ((c >> 12) & 0x3F));
+        o[2] = (uint8_t)(0x80 | ((c >> 6) & 0x3F));
+        o[3] = (uint8_t)(0x80 | (c & 0x3F));
+    }
+}
+
+// Thread per non-ASCII line.  COUNT: tokens and lowered token bytes, or "stay deferred"
+// (code 1) for invalid UTF-8 / U+03A3; handled lines become code 3.  WRITE: the tokens
+// (start into the blob region, length, line) and their lowered bytes.
+template <bool WRITE>
+__global__ void uni_lines(const uint8_t* s, const int64_t* line_start, const int64_t* line_end, int64_t n_docs,
+                          UniTab tab, uint8_t* code, int64_t* ucount, int64_t* ubytes, const int64_t* tok_off,
+                          const int64_t* uoff, int64_t blob_base, uint8_t* ubuf, int64_t* tok_start,
+                          uint32_t* tok_len, uint32_t* tok_line) {
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n_docs;
+         d += (int64_t)gridDim.x * blockDim.x) {
+        if (code[d] != (WRITE ? 3 : 1)) continue;
+        const int64_t s0 = line_start[d], s1 = line_end[d];
+        int64_t cnt = 0, nb = 0, tok0 = 0;
+        bool in_tok = false, bad = false;
+        const int64_t t0 = WRITE ? tok_off[d] : 0;
+        uint8_t* o = WRITE ? ubuf + uoff[d] : nullptr;
+        for (int64_t i = s0; i < s1;) {
+            uint32_t cp;
+            const int len = utf8_decode(s, i, s1, &cp);
+            if (!len || cp == 0x3A3) {
+                bad = true;
+                break;
+            }
+            i += len;
+            uint32_t lc[3];
+            const int m = uni_lower(tab, cp, lc);
+            for (int k = 0; k < m; ++k) {
+                if (uni_alnum(tab, lc[k])) {
+                    if (!in_tok) {
+                        in_tok = true;
+                        tok0 = nb;
+                    }
+                    if (WRITE) utf8_put(o + nb, lc[k]);
+                    nb += utf8_len(lc[k]);
+                } else if (in_tok) {
+                    in_tok = false;
+                    if (WRITE) {
+                        tok_start[t0 + cnt] = blob_base + uoff[d] + tok0;
+                        tok_len[t0 + cnt] = (uint32_t)(nb - tok0);
+                        tok_line[t0 + cnt] = (uint32_t)d;
+                    }
+                    ++cnt;
+                }
+            }
+        }
+        if (!WRITE && bad) continue;  // stays deferred (code 1)
+        if (in_tok) {
+            if (WRITE) {
+                tok_start[t0 + cnt] = blob_base + uoff[d] + tok0;
+                tok_len[t0 + cnt] = (uint32_t)(nb - tok0);
+                tok_line[t0 + cnt] = (uint32_t)d;
+            }
+            ++cnt;
+        }
+        if (!WRITE) {
+            code[d] = 3;
+            ucount[d] = cnt;
+            ubytes[d] = nb;
+        }
+    }
+}
+
 inline unsigned blocks_for(int64_t n, int threads = 256) { return (unsigned)((n + threads - 1) / threads + 1); }
 inline unsigned warp_blocks(int64_t n_docs) {
     const int64_t b = (n_docs + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -386,8 +540,14 @@ struct CorpusDevice {
     int64_t* line_start = nullptr;  // [n_docs + 1]
     int64_t* line_end = nullptr;
     int64_t* count = nullptr;       // [n_docs + 1] native tokens per line
-    uint8_t* deferred = nullptr;    // [n_docs]
+    uint8_t* deferred = nullptr;    // [n_docs] 0 ASCII, 1 deferred to the caller, 3 Unicode on the device
     std::vector<uint8_t> deferred_h;
+    // Unicode tables (device copies) and per-line Unicode token counts / lowered bytes
+    bool uni = false;
+    UniTab tab{};
+    uint32_t* tab_buf = nullptr;
+    int64_t* ucount = nullptr;      // [n_docs + 1]
+    int64_t* ubytes = nullptr;      // [n_docs + 1]
     // supplied terms of the deferred lines (host until intern)
     std::vector<int64_t> dl_line, dl_cnt, dl_first, dterm_off{0};
     std::vector<char> dblob;
@@ -407,15 +567,16 @@ struct CorpusDevice {
         if (!st) return;
         cudaSetDevice(device);
         for (void* p : {(void*)text, (void*)line_start, (void*)line_end, (void*)count, (void*)deferred,
-                        (void*)indptr, (void*)ids, (void*)voff, (void*)vblob})
+                        (void*)indptr, (void*)ids, (void*)voff, (void*)vblob, (void*)tab_buf, (void*)ucount,
+                        (void*)ubytes})
             if (p) cudaFreeAsync(p, st);
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
     }
 };
 
-int corpus_device_scan(const char* text_h, int64_t n, int device, CorpusDevice** out,
-                       std::vector<int64_t>& line_start, std::vector<int64_t>& line_end,
+int corpus_device_scan(const char* text_h, int64_t n, int device, const mhb_unicode_tables* tables,
+                       CorpusDevice** out, std::vector<int64_t>& line_start, std::vector<int64_t>& line_end,
                        std::vector<int64_t>& deferred_lines) {
     MHB_CUDA(cudaSetDevice(device));
     auto d = std::make_unique<CorpusDevice>();
@@ -433,6 +594,19 @@ int corpus_device_scan(const char* text_h, int64_t n, int device, CorpusDevice**
     StageTimer tm(st);
     MHB_CUDA(d->alloc(&d->text, n + 1));
     if (n) MHB_CUDA(cudaMemcpyAsync(d->text, text_h, n, cudaMemcpyHostToDevice, st));
+    if (tables) {  // isalnum bitmap | lowercase keys | lowercase values
+        if (tables->n_lower < 0 || !tables->alnum_bits || (tables->n_lower && (!tables->lower_keys || !tables->lower_vals)))
+            return set_error(MHB_ERR_INVALID, "bad Unicode tables");
+        const size_t words = 0x110000 / 32, nl = (size_t)tables->n_lower;
+        MHB_CUDA(d->alloc(&d->tab_buf, words + nl * 4 + 1));
+        MHB_CUDA(cudaMemcpyAsync(d->tab_buf, tables->alnum_bits, words * 4, cudaMemcpyHostToDevice, st));
+        if (nl) {
+            MHB_CUDA(cudaMemcpyAsync(d->tab_buf + words, tables->lower_keys, nl * 4, cudaMemcpyHostToDevice, st));
+            MHB_CUDA(cudaMemcpyAsync(d->tab_buf + words + nl, tables->lower_vals, nl * 12, cudaMemcpyHostToDevice, st));
+        }
+        d->uni = true;
+        d->tab = UniTab{d->tab_buf, d->tab_buf + words, d->tab_buf + words + nl, (int)nl};
+    }
     tm.mark("scan: H2D text");
     try {
         Scratch sc(st);
@@ -464,10 +638,18 @@ int corpus_device_scan(const char* text_h, int64_t n, int device, CorpusDevice**
         const int64_t nd = d->n_docs;
         MHB_CUDA(d->alloc(&d->count, nd + 1));
         MHB_CUDA(d->alloc(&d->deferred, nd));
+        MHB_CUDA(d->alloc(&d->ucount, nd + 1));
+        MHB_CUDA(d->alloc(&d->ubytes, nd + 1));
         MHB_CUDA(cudaMemsetAsync(d->count, 0, (nd + 1) * sizeof(int64_t), st));
+        MHB_CUDA(cudaMemsetAsync(d->ucount, 0, (nd + 1) * sizeof(int64_t), st));
+        MHB_CUDA(cudaMemsetAsync(d->ubytes, 0, (nd + 1) * sizeof(int64_t), st));
         if (nd) {
             scan_lines<<<warp_blocks(nd), 32 * kWarpsPerBlock, 0, st>>>(d->text, d->line_start, d->line_end, nd,
-                                                                        d->count, d->deferred);
+                                                                        d->count, d->deferred, d->uni);
+            if (d->uni)
+                uni_lines<false><<<blocks_for(nd, 128), 128, 0, st>>>(
+                    d->text, d->line_start, d->line_end, nd, d->tab, d->deferred, d->ucount, d->ubytes, nullptr,
+                    nullptr, 0, nullptr, nullptr, nullptr, nullptr);
         }
         line_start.resize(nd);
         line_end.resize(nd);
@@ -485,7 +667,7 @@ int corpus_device_scan(const char* text_h, int64_t n, int device, CorpusDevice**
     MHB_CUDA(cudaGetLastError());
     deferred_lines.clear();
     for (int64_t k = 0; k < d->n_docs; ++k)
-        if (d->deferred_h[k]) deferred_lines.push_back(k);
+        if (d->deferred_h[k] == 1) deferred_lines.push_back(k);
     *out = d.release();
     return MHB_OK;
 }
@@ -533,7 +715,17 @@ int corpus_device_intern(CorpusDevice* d, int64_t* nnz, int64_t* n_terms, int64_
             int64_t* count = sc.get<int64_t>(nd + 1);
             MHB_CUDA(cudaMemsetAsync(scount, 0, (nd + 1) * sizeof(int64_t), st));
             int64_t* dterm_off = sc.get<int64_t>(d->dterm_off.size());
-            uint8_t* dblob = sc.get<uint8_t>(d->dblob.size() + 1);
+            // blob region: caller-supplied terms, then the lowered bytes of device-tokenized Unicode lines
+            int64_t* uoff = sc.get<int64_t>(nd + 1);
+            size_t tbu = 0;
+            MHB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tbu, d->ubytes, uoff, nd + 1, st));
+            void* tmpu = sc.get<char>(tbu);
+            MHB_CUDA(cub::DeviceScan::ExclusiveSum(tmpu, tbu, d->ubytes, uoff, nd + 1, st));
+            int64_t UB = 0;
+            MHB_CUDA(cudaMemcpyAsync(&UB, uoff + nd, 8, cudaMemcpyDeviceToHost, st));
+            MHB_CUDA(cudaStreamSynchronize(st));
+            const int64_t D = (int64_t)d->dblob.size();
+            uint8_t* dblob = sc.get<uint8_t>(D + UB + 1);
             if (ndl) {
                 int64_t* a = sc.get<int64_t>(ndl);
                 int64_t* b = sc.get<int64_t>(ndl);
@@ -550,7 +742,7 @@ int corpus_device_intern(CorpusDevice* d, int64_t* nnz, int64_t* n_terms, int64_
             // token offsets per line
             int64_t* tok_off = sc.get<int64_t>(nd + 1);
             size_t tb = 0;
-            add_counts<<<blocks_for(nd + 1), 256, 0, st>>>(d->count, scount, nd + 1, count);
+            add_counts<<<blocks_for(nd + 1), 256, 0, st>>>(d->count, scount, d->ucount, nd + 1, count);
             MHB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, count, tok_off, nd + 1, st));
             void* tmp = sc.get<char>(tb);
             MHB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, count, tok_off, nd + 1, st));
@@ -564,8 +756,12 @@ int corpus_device_intern(CorpusDevice* d, int64_t* nnz, int64_t* n_terms, int64_
             uint32_t* tok_line = sc.get<uint32_t>(T);
             if (nd)
                 write_tokens<<<warp_blocks(nd), 32 * kWarpsPerBlock, 0, st>>>(
-                    d->text, d->n_bytes, d->line_start, d->line_end, nd, d->count, tok_off, dfirst, dterm_off,
-                    tok_start, tok_len, tok_line);
+                    d->text, d->n_bytes, d->line_start, d->line_end, nd, d->count, d->deferred, tok_off, dfirst,
+                    dterm_off, tok_start, tok_len, tok_line);
+            if (nd && d->uni)
+                uni_lines<true><<<blocks_for(nd, 128), 128, 0, st>>>(
+                    d->text, d->line_start, d->line_end, nd, d->tab, d->deferred, nullptr, nullptr, tok_off, uoff,
+                    d->n_bytes + D, dblob + D, tok_start, tok_len, tok_line);
             // hash, sort, verify runs (re-hash with another seed on a collision)
             tm.mark("intern: write tokens");
             unsigned long long* h = sc.get<unsigned long long>(T);

@@ -522,3 +522,65 @@ def test_small_batch_status_flags(cuda_device):
                                    a.ctypes.data, b.ctypes.data, 1_048_583, 2, out.ctypes.data, _lib.OUT_I64,
                                    C.addressof(st), 0)
         assert rc == 0 and st.value & _lib.STATUS_BAD_PARAM, (n_sets, st.value)
+
+
+def _random_unicode_text(seed, n_chars):
+    """Random code points from every plane (no surrogates) mixed with ASCII words,
+    separators and line breaks."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_chars):
+        r = rng.random()
+        if r < 0.45:
+            out.append(chr(int(rng.integers(0x61, 0x7B))) if rng.random() < 0.7 else chr(int(rng.integers(0x41, 0x5B))))
+        elif r < 0.6:
+            out.append(" \t.,'-_"[int(rng.integers(0, 7))])
+        elif r < 0.63:
+            out.append(["\n", "\r\n", "\r"][int(rng.integers(0, 3))])
+        else:
+            while True:
+                c = int(rng.integers(0x80, 0x110000)) if rng.random() < 0.3 else int(rng.integers(0x80, 0x3000))
+                if not 0xD800 <= c <= 0xDFFF:
+                    break
+            out.append(chr(c))
+    return "".join(out).encode("utf-8")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_corpus_unicode_on_device(cuda_device, seed):
+    """Non-ASCII lines tokenized on the device (Python's own isalnum / lower tables)
+    == the pure-Python oracle; only U+03A3 lines stay deferred to the caller."""
+    import ctypes as C
+
+    from oracle import corpus_oracle
+    from paper_1401_6124_b200 import _lib
+    from paper_1401_6124_b200.corpus import build_corpus_csr, unicode_tables
+
+    data = _random_unicode_text(seed, 20000 + 5000 * seed)
+    terms, ip, x, empty = corpus_oracle.build_corpus_bytes(data)
+    c = build_corpus_csr(data, backend="gpu")
+    assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
+    assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
+    # which lines went back to Python: exactly those holding U+03A3
+    lib = _lib.load()
+    buf = np.frombuffer(data, dtype=np.uint8)
+    h = C.c_void_p()
+    _lib.check(lib.mhb_corpus_scan_device(buf.ctypes.data, buf.size, 0, C.byref(unicode_tables()), C.byref(h)))
+    try:
+        nd, nf = C.c_int64(), C.c_int64()
+        lib.mhb_corpus_info(h, C.byref(nd), C.byref(nf))
+        lines = data.decode("utf-8").replace("\r\n", "\n").replace("\r", "\n").split("\n")
+        if lines and lines[-1] == "":
+            lines = lines[:-1]
+        assert nf.value == sum("Σ" in ln for ln in lines)
+    finally:
+        lib.mhb_corpus_free(h)
+
+
+def test_gpu_corpus_invalid_utf8_raises(cuda_device):
+    from paper_1401_6124_b200.corpus import build_corpus_csr
+
+    for bad in (b"ok line\nbad \xc3\x28 x\n", b"a\xed\xa0\x80b\n", b"\xf4\x90\x80\x80\n", b"x\xe2\x82\n",
+                b"\xc0\xaf overlong\n"):
+        with pytest.raises(UnicodeDecodeError):
+            build_corpus_csr(bad, backend="gpu")
