@@ -437,7 +437,7 @@ def run_corpus(args):
                 "config": {"workload": workload, "docs": int(c.indptr.size - 1), "nnz": nnz,
                            "vocabulary": len(c.vocabulary), "prime": prime, "records": n,
                            "output_bytes": out_bytes, "host_threads": threads},
-                "ingest": {"backend": "gpu (csrc/corpus_gpu.cu; Unicode lines on the device with the running Python's isalnum/lower tables; U+03A3 lines in Python)",
+                "ingest": {"backend": "gpu (csrc/corpus_gpu.cu; Unicode lines on the device with the running Python's isalnum/lower/Cased/Case_Ignorable tables)",
                            "mb_per_s": mb / statistics.mean(ingest), "ms": statistics.mean(ingest) * 1e3,
                            "share_of_step": statistics.mean(ingest) / step},
                 "ingest_host": {"backend": f"host (csrc/corpus.cpp, {threads} threads)",

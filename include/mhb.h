@@ -222,19 +222,24 @@ typedef struct mhb_corpus mhb_corpus;
 int mhb_corpus_scan(const char* text, int64_t n_bytes, int32_t n_threads, mhb_corpus** corpus);
 /* Unicode tables of the caller's Python (what tokenize() uses): bit c of alnum_bits is
    chr(c).isalnum(); lower_keys (ascending) are the code points whose str.lower() differs,
-   lower_vals[3k..3k+2] the lowercase code points of lower_keys[k] (0xFFFFFFFF padded). */
+   lower_vals[3k..3k+2] the lowercase code points of lower_keys[k] (0xFFFFFFFF padded);
+   cased_bits / ignorable_bits (optional) are the Cased and Case_Ignorable properties that
+   str.lower() consults for U+03A3 (Final_Sigma). */
 typedef struct mhb_unicode_tables {
-    const uint32_t* alnum_bits;   /* [0x110000 / 32] */
-    const uint32_t* lower_keys;   /* [n_lower] */
-    const uint32_t* lower_vals;   /* [3 * n_lower] */
+    const uint32_t* alnum_bits;      /* [0x110000 / 32] */
+    const uint32_t* lower_keys;      /* [n_lower] */
+    const uint32_t* lower_vals;      /* [3 * n_lower] */
     int32_t n_lower;
+    const uint32_t* cased_bits;      /* [0x110000 / 32] or NULL */
+    const uint32_t* ignorable_bits;  /* [0x110000 / 32] or NULL */
 } mhb_unicode_tables;
 /* The same ingest on GPU `device` (corpus_gpu.cu): lines, tokens, vocabulary and documents are
    computed on the device; the rest of the mhb_corpus_* API is shared.  `text` is a host buffer
    (pinned for full PCIe speed).  With `tables`, lines holding non-ASCII bytes are tokenized on the
-   device too (strict UTF-8, full lowercase mapping, isalnum), except lines with invalid UTF-8 or
-   U+03A3, which stay deferred to the caller under the rule above; tables == NULL defers every
-   non-ASCII segment as the host backend does. */
+   device too (strict UTF-8, full lowercase mapping incl. Final_Sigma, isalnum), except lines with
+   invalid UTF-8 (and, without cased/ignorable bits, lines with U+03A3), which stay deferred to the
+   caller under the rule above; tables == NULL defers every non-ASCII segment as the host backend
+   does. */
 int mhb_corpus_scan_device(const char* text, int64_t n_bytes, int32_t device, const mhb_unicode_tables* tables,
                            mhb_corpus** corpus);
 int mhb_corpus_info(const mhb_corpus* corpus, int64_t* n_docs, int64_t* n_deferred);

@@ -98,23 +98,40 @@ class CorpusCSR(NamedTuple):
 
 class _UnicodeTables(C.Structure):  # include/mhb.h mhb_unicode_tables
     _fields_ = [("alnum_bits", C.c_void_p), ("lower_keys", C.c_void_p), ("lower_vals", C.c_void_p),
-                ("n_lower", C.c_int32)]
+                ("n_lower", C.c_int32), ("cased_bits", C.c_void_p), ("ignorable_bits", C.c_void_p)]
 
 
 _UNI: list = []  # (struct, arrays) built once per process
 
 
+def _bitmap(flags) -> np.ndarray:
+    bits = np.fromiter(flags, dtype=bool, count=0x110000)
+    return np.ascontiguousarray(np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").ravel(),
+                                dtype=np.uint32)
+
+
+def _case_ignorable(c: str, cased: bool) -> bool:
+    """Case_Ignorable as THIS Python's str.lower() sees it (its Final_Sigma rule skips such
+    code points): probed through the rule itself rather than re-derived."""
+    if cased:  # backward scan from a final U+03A3 stops at a cased c unless c is ignorable
+        return ("1" + c + "\u03a3").lower()[-1] == "\u03c3"
+    return ("A\u03a3" + c + "A").lower()[1] == "\u03c3"
+
+
 def unicode_tables():
-    """str.isalnum / str.lower of THIS Python over every code point -- the rules
-    tokenize() applies -- packed for mhb_corpus_scan_device (about 0.4 s, once)."""
+    """str.isalnum / str.lower (and the Cased / Case_Ignorable sets its Final_Sigma rule
+    uses) of THIS Python over every code point -- the rules tokenize() applies -- packed
+    for mhb_corpus_scan_device (about 1 s, once per process)."""
     if not _UNI:
-        alnum = np.zeros(0x110000 // 32, dtype=np.uint32)
-        bits = np.fromiter((chr(c).isalnum() for c in range(0x110000)), dtype=bool, count=0x110000)
-        alnum[:] = np.packbits(bits.reshape(-1, 32)[:, ::-1], axis=1).view(">u4").ravel()
+        chars = [chr(c) for c in range(0x110000)]
+        alnum = _bitmap(c.isalnum() for c in chars)
+        cased_l = [c.islower() or c.isupper() or c.istitle() for c in chars]
+        cased = _bitmap(cased_l)
+        ign = _bitmap(_case_ignorable(c, k) for c, k in zip(chars, cased_l))
         keys, vals = [], []
         for c in range(0x80, 0x110000):
-            low = chr(c).lower()
-            if low != chr(c):
+            low = chars[c].lower()
+            if low != chars[c]:
                 if len(low) > 3:
                     raise NotImplementedError(f"lowercase of U+{c:04X} has {len(low)} code points")
                 keys.append(c)
@@ -122,8 +139,8 @@ def unicode_tables():
         k = np.asarray(keys, dtype=np.uint32)
         v = np.asarray(vals, dtype=np.uint32)
         st = _UnicodeTables(alnum.ctypes.data, k.ctypes.data if k.size else None, v.ctypes.data if v.size else None,
-                            int(k.size))
-        _UNI[:] = [st, (alnum, k, v)]
+                            int(k.size), cased.ctypes.data, ign.ctypes.data)
+        _UNI[:] = [st, (alnum, k, v, cased, ign)]
     return _UNI[0]
 
 

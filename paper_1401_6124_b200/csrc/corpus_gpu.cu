@@ -341,7 +341,11 @@ struct UniTab {
     const uint32_t* keys;   // ascending code points whose lowercase differs
     const uint32_t* vals;   // [n * 3] lowercase code points, 0xFFFFFFFF padded
     int n;
+    const uint32_t* cased;      // Final_Sigma context (nullptr: U+03A3 lines stay deferred)
+    const uint32_t* ignorable;
 };
+
+__device__ __forceinline__ bool uni_bit(const uint32_t* b, uint32_t c) { return (b[c >> 5] >> (c & 31)) & 1u; }
 
 __device__ __forceinline__ bool uni_alnum(const UniTab& t, uint32_t c) { return (t.alnum[c >> 5] >> (c & 31)) & 1u; }
 
@@ -400,6 +404,39 @@ __device__ __forceinline__ int utf8_decode(const uint8_t* s, int64_t i, int64_t 
     return n;
 }
 
+// Python's handle_capital_sigma (Objects/unicodeobject.c): U+03A3 lowercases to U+03C2
+// when a cased letter precedes it and none follows, skipping case-ignorable code points,
+// within the string being lowered -- here the line.  `at` is the byte offset of the
+// U+03A3; earlier code points of the line are already validated.  Returns 0 on invalid
+// UTF-8 after it.
+__device__ __forceinline__ uint32_t final_sigma(const UniTab& t, const uint8_t* s, int64_t s0, int64_t s1, int64_t at) {
+    bool fin = false;
+    for (int64_t j = at; j > s0;) {  // backward
+        int64_t k = j - 1;
+        while (k > s0 && (s[k] & 0xC0) == 0x80) --k;
+        uint32_t c;
+        utf8_decode(s, k, s1, &c);
+        if (!uni_bit(t.ignorable, c)) {
+            fin = uni_bit(t.cased, c);
+            break;
+        }
+        j = k;
+    }
+    if (fin) {  // forward
+        for (int64_t k = at + 2; k < s1;) {
+            uint32_t c;
+            const int len = utf8_decode(s, k, s1, &c);
+            if (!len) return 0;
+            if (!uni_bit(t.ignorable, c)) {
+                fin = !uni_bit(t.cased, c);
+                break;
+            }
+            k += len;
+        }
+    }
+    return fin ? 0x3C2u : 0x3C3u;
+}
+
 __device__ __forceinline__ int utf8_len(uint32_t c) { return c < 0x80 ? 1 : c < 0x800 ? 2 : c < 0x10000 ? 3 : 4; }
 
 __device__ __forceinline__ void utf8_put(uint8_t* o, uint32_t c) {
@@ -421,7 +458,8 @@ __device__ __forceinline__ void utf8_put(uint8_t* o, uint32_t c) {
 }
 
 // Thread per non-ASCII line.  COUNT: tokens and lowered token bytes, or "stay deferred"
-// (code 1) for invalid UTF-8 / U+03A3; handled lines become code 3.  WRITE: the tokens
+// (code 1) for invalid UTF-8 (or U+03A3 without the Final_Sigma tables); handled lines
+// become code 3.  WRITE: the tokens
 // (start into the blob region, length, line) and their lowered bytes.
 template <bool WRITE>
 __global__ void uni_lines(const uint8_t* s, const int64_t* line_start, const int64_t* line_end, int64_t n_docs,
@@ -439,13 +477,23 @@ __global__ void uni_lines(const uint8_t* s, const int64_t* line_start, const int
         for (int64_t i = s0; i < s1;) {
             uint32_t cp;
             const int len = utf8_decode(s, i, s1, &cp);
-            if (!len || cp == 0x3A3) {
+            if (!len || (cp == 0x3A3 && !tab.cased)) {
                 bad = true;
                 break;
             }
-            i += len;
             uint32_t lc[3];
-            const int m = uni_lower(tab, cp, lc);
+            int m;
+            if (cp == 0x3A3) {
+                lc[0] = final_sigma(tab, s, s0, s1, i);
+                m = 1;
+                if (!lc[0]) {
+                    bad = true;
+                    break;
+                }
+            } else {
+                m = uni_lower(tab, cp, lc);
+            }
+            i += len;
             for (int k = 0; k < m; ++k) {
                 if (uni_alnum(tab, lc[k])) {
                     if (!in_tok) {
@@ -598,14 +646,22 @@ int corpus_device_scan(const char* text_h, int64_t n, int device, const mhb_unic
         if (tables->n_lower < 0 || !tables->alnum_bits || (tables->n_lower && (!tables->lower_keys || !tables->lower_vals)))
             return set_error(MHB_ERR_INVALID, "bad Unicode tables");
         const size_t words = 0x110000 / 32, nl = (size_t)tables->n_lower;
-        MHB_CUDA(d->alloc(&d->tab_buf, words + nl * 4 + 1));
-        MHB_CUDA(cudaMemcpyAsync(d->tab_buf, tables->alnum_bits, words * 4, cudaMemcpyHostToDevice, st));
+        const bool sig = tables->cased_bits && tables->ignorable_bits;
+        // alnum | keys | vals | cased | ignorable
+        MHB_CUDA(d->alloc(&d->tab_buf, words + nl * 4 + 2 * words + 1));
+        uint32_t* tb = d->tab_buf;
+        MHB_CUDA(cudaMemcpyAsync(tb, tables->alnum_bits, words * 4, cudaMemcpyHostToDevice, st));
         if (nl) {
-            MHB_CUDA(cudaMemcpyAsync(d->tab_buf + words, tables->lower_keys, nl * 4, cudaMemcpyHostToDevice, st));
-            MHB_CUDA(cudaMemcpyAsync(d->tab_buf + words + nl, tables->lower_vals, nl * 12, cudaMemcpyHostToDevice, st));
+            MHB_CUDA(cudaMemcpyAsync(tb + words, tables->lower_keys, nl * 4, cudaMemcpyHostToDevice, st));
+            MHB_CUDA(cudaMemcpyAsync(tb + words + nl, tables->lower_vals, nl * 12, cudaMemcpyHostToDevice, st));
+        }
+        uint32_t* cased = tb + words + 4 * nl;
+        if (sig) {
+            MHB_CUDA(cudaMemcpyAsync(cased, tables->cased_bits, words * 4, cudaMemcpyHostToDevice, st));
+            MHB_CUDA(cudaMemcpyAsync(cased + words, tables->ignorable_bits, words * 4, cudaMemcpyHostToDevice, st));
         }
         d->uni = true;
-        d->tab = UniTab{d->tab_buf, d->tab_buf + words, d->tab_buf + words + nl, (int)nl};
+        d->tab = UniTab{tb, tb + words, tb + words + nl, (int)nl, sig ? cased : nullptr, sig ? cased + words : nullptr};
     }
     tm.mark("scan: H2D text");
     try {

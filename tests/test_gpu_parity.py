@@ -548,8 +548,9 @@ def _random_unicode_text(seed, n_chars):
 
 @pytest.mark.parametrize("seed", range(6))
 def test_gpu_corpus_unicode_on_device(cuda_device, seed):
-    """Non-ASCII lines tokenized on the device (Python's own isalnum / lower tables)
-    == the pure-Python oracle; only U+03A3 lines stay deferred to the caller."""
+    """Non-ASCII lines tokenized on the device (Python's own isalnum / lower tables,
+    Final_Sigma included) == the pure-Python oracle; valid UTF-8 leaves nothing for
+    the caller."""
     import ctypes as C
 
     from oracle import corpus_oracle
@@ -561,7 +562,7 @@ def test_gpu_corpus_unicode_on_device(cuda_device, seed):
     c = build_corpus_csr(data, backend="gpu")
     assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
     assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
-    # which lines went back to Python: exactly those holding U+03A3
+    # nothing goes back to Python for valid UTF-8
     lib = _lib.load()
     buf = np.frombuffer(data, dtype=np.uint8)
     h = C.c_void_p()
@@ -569,10 +570,7 @@ def test_gpu_corpus_unicode_on_device(cuda_device, seed):
     try:
         nd, nf = C.c_int64(), C.c_int64()
         lib.mhb_corpus_info(h, C.byref(nd), C.byref(nf))
-        lines = data.decode("utf-8").replace("\r\n", "\n").replace("\r", "\n").split("\n")
-        if lines and lines[-1] == "":
-            lines = lines[:-1]
-        assert nf.value == sum("Σ" in ln for ln in lines)
+        assert nf.value == 0
     finally:
         lib.mhb_corpus_free(h)
 
@@ -584,3 +582,23 @@ def test_gpu_corpus_invalid_utf8_raises(cuda_device):
                 b"\xc0\xaf overlong\n"):
         with pytest.raises(UnicodeDecodeError):
             build_corpus_csr(bad, backend="gpu")
+
+
+def test_gpu_corpus_final_sigma(cuda_device):
+    """U+03A3 in every Final_Sigma context str.lower() distinguishes: cased / uncased
+    neighbours, case-ignorable runs (' . : ^ ` U+0301 U+00AD) on either side, line
+    start / end, CRLF -- device ingest == the pure-Python oracle."""
+    from oracle import corpus_oracle
+    from paper_1401_6124_b200.corpus import build_corpus_csr
+
+    ctx = ["", "A", "α", "1", " ", "'", ".", ":", "^", "`", "\u0301", "\u00ad", "A'", "A.", "1'", "ΑΒ", "_", "\u2019"]
+    lines = []
+    for left in ctx:
+        for right in ctx:
+            lines.append(f"{left}Σ{right}")
+            lines.append(f"x {left}ΣΣ{right} y")
+    data = ("\n".join(lines) + "\r\nΣ\rΑΣ").encode("utf-8")
+    terms, ip, x, empty = corpus_oracle.build_corpus_bytes(data)
+    c = build_corpus_csr(data, backend="gpu")
+    assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
+    assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
