@@ -129,6 +129,16 @@ int mhb_sign_random_csr_u64(const int64_t* indptr, const uint32_t* ids,
                             void* out, int32_t out_dtype, int32_t* status, void* stream);
 
 /*
+ * 64-bit feature ids (the reference's FeatureSet ids are int64: with a prime >= 2^32
+ * they may reach p - 1, minhash.py:99-127).  kind 0 iterative (a, b), 1 random
+ * (ra, rb: device uint64[n_hash]); any prime < 2^63; ids: device uint64[nnz];
+ * out: device int64[n_sets * n_hash].  Runs the 64-bit-residue path (wide.cu).
+ */
+int mhb_sign_csr_ids64(int32_t kind, const int64_t* indptr, const uint64_t* ids, int64_t n_sets, int64_t nnz,
+                       uint64_t a, uint64_t b, const uint64_t* ra, const uint64_t* rb, uint64_t prime,
+                       int32_t n_hash, long long* out, int32_t* status, void* stream);
+
+/*
  * Host-buffer entry (the end-to-end path an FFI caller uses): indptr/ids/out are
  * HOST pointers (page-locked for full copy bandwidth; pageable also works).  The
  * library stages chunks through its own device buffers on `device` with copy/

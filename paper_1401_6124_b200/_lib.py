@@ -46,6 +46,7 @@ SIGNATURES = {
     "mhb_sign_iterative_csr_bands": (C.c_int, [_P, _P, _I64, _I64, _U64, _U64, _U64, _I32, _I32, _P, _P, _I32,
                                                _I32, _P, _P, _SZ, _P]),
     "mhb_sign_random_csr_u64": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _U64, _I32, _P, _I32, _P, _P]),
+    "mhb_sign_csr_ids64": (C.c_int, [_I32, _P, _P, _I64, _I64, _U64, _U64, _P, _P, _U64, _I32, _P, _P, _P]),
     "mhb_sign_csr_host": (C.c_int, [_I32, _P, _P, _I64, _I64, _U64, _U64, _P, _P, _U64, _I32, _P, _I32, _P, _I32]),
     "mhb_host_release": (None, []),
     "mhb_jaccard_pairs": (C.c_int, [_P, _I32, _I32, _P, _P, _I64, _P, _P, _P]),

@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "common.h"
+#include "sign_internal.h"
 
 namespace mhb {
 
@@ -26,8 +27,8 @@ __device__ __forceinline__ uint64_t addmod64(uint64_t a, uint64_t b, uint64_t p)
     return t >= p ? t - p : t;
 }
 
-template <bool ITER, typename OutT>
-__global__ void sign_wide_kernel(const int64_t* __restrict__ indptr, const uint32_t* __restrict__ ids,
+template <bool ITER, typename OutT, typename IdT>
+__global__ void sign_wide_kernel(const int64_t* __restrict__ indptr, const IdT* __restrict__ ids,
                                  int64_t n_sets, uint64_t a, uint64_t b, const uint64_t* __restrict__ ra,
                                  const uint64_t* __restrict__ rb, uint64_t p, int32_t n_hash, OutT* __restrict__ out,
                                  int32_t* status) {
@@ -92,9 +93,10 @@ __global__ void wide_check_kernel(const int64_t* __restrict__ indptr, int64_t n_
             if ((ra[i] == 0 || ra[i] >= p || rb[i] >= p) && status) atomicOr(status, MHB_STATUS_BAD_PARAM);
 }
 
-int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, uint64_t a, uint64_t b,
-                     const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash, void* out,
-                     int32_t out_dtype, int32_t* status, cudaStream_t st) {
+template <typename IdT>
+int launch_sign_wide_t(bool iter, const int64_t* indptr, const IdT* ids, int64_t n_sets, uint64_t a, uint64_t b,
+                       const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash, void* out,
+                       int32_t out_dtype, int32_t* status, cudaStream_t st) {
     if (status) {
         int rc = cuda_check(cudaMemsetAsync(status, 0, sizeof(int32_t), st), "memset status");
         if (rc) return rc;
@@ -110,18 +112,25 @@ int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int6
     if (blocks < 1) blocks = 1;
     const bool i64 = out_dtype == MHB_OUT_I64;
     if (iter && i64)
-        sign_wide_kernel<true, long long><<<(unsigned)blocks, 128, 0, st>>>(
+        sign_wide_kernel<true, long long, IdT><<<(unsigned)blocks, 128, 0, st>>>(
             indptr, ids, n_sets, a, b, ra, rb, prime, n_hash, static_cast<long long*>(out), status);
     else if (iter)
-        sign_wide_kernel<true, uint32_t><<<(unsigned)blocks, 128, 0, st>>>(
+        sign_wide_kernel<true, uint32_t, IdT><<<(unsigned)blocks, 128, 0, st>>>(
             indptr, ids, n_sets, a, b, ra, rb, prime, n_hash, static_cast<uint32_t*>(out), status);
     else if (i64)
-        sign_wide_kernel<false, long long><<<(unsigned)blocks, 128, 0, st>>>(
+        sign_wide_kernel<false, long long, IdT><<<(unsigned)blocks, 128, 0, st>>>(
             indptr, ids, n_sets, a, b, ra, rb, prime, n_hash, static_cast<long long*>(out), status);
     else
-        sign_wide_kernel<false, uint32_t><<<(unsigned)blocks, 128, 0, st>>>(
+        sign_wide_kernel<false, uint32_t, IdT><<<(unsigned)blocks, 128, 0, st>>>(
             indptr, ids, n_sets, a, b, ra, rb, prime, n_hash, static_cast<uint32_t*>(out), status);
     return cuda_check(cudaGetLastError(), "sign_wide launch");
+}
+
+int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, uint64_t a, uint64_t b,
+                     const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash, void* out,
+                     int32_t out_dtype, int32_t* status, cudaStream_t st) {
+    return launch_sign_wide_t<uint32_t>(iter, indptr, ids, n_sets, a, b, ra, rb, prime, n_hash, out, out_dtype,
+                                        status, st);
 }
 
 }  // namespace mhb
@@ -141,4 +150,30 @@ extern "C" int mhb_sign_random_csr_u64(const int64_t* indptr, const uint32_t* id
     if (!a || !b) return set_error(MHB_ERR_INVALID, "random family needs device arrays a and b");
     return launch_sign_wide(false, indptr, ids, n_sets, 0, 0, a, b, prime, n_hash, out, out_dtype, status,
                             static_cast<cudaStream_t>(stream));
+}
+
+// 64-bit feature ids (the reference's int64 FeatureSet ids; with primes >= 2^32 they
+// may exceed 2^32): any prime < 2^63, int64 output.
+extern "C" int mhb_sign_csr_ids64(int32_t kind, const int64_t* indptr, const uint64_t* ids, int64_t n_sets,
+                                  int64_t nnz, uint64_t a, uint64_t b, const uint64_t* ra, const uint64_t* rb,
+                                  uint64_t prime, int32_t n_hash, long long* out, int32_t* status, void* stream) {
+    using namespace mhb;
+    clear_error();
+    if (kind != KIND_ITERATIVE && kind != KIND_RANDOM) return set_error(MHB_ERR_INVALID, "unknown kind %d", kind);
+    if (n_sets < 0 || nnz < 0) return set_error(MHB_ERR_INVALID, "n_sets and nnz must be >= 0");
+    if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
+    if (prime < 3 || !is_prime_u64(prime)) return set_error(MHB_ERR_INVALID, "modulus %llu is not prime",
+                                                             (unsigned long long)prime);
+    if (prime >= (1ull << 63)) return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^63 is out of range");
+    if (kind == KIND_ITERATIVE) {
+        if (a < 1 || a >= prime || b >= prime) return set_error(MHB_ERR_INVALID, "need 1 <= a < p and 0 <= b < p");
+        if (a + (uint64_t)n_hash >= prime)
+            return set_error(MHB_ERR_INVALID, "need a + size < prime to keep every member invertible");
+    } else if (!ra || !rb) {
+        return set_error(MHB_ERR_INVALID, "random family needs device arrays a and b");
+    }
+    if (n_sets > 0 && (!indptr || !out)) return set_error(MHB_ERR_INVALID, "null indptr/out");
+    if (nnz > 0 && !ids) return set_error(MHB_ERR_INVALID, "null ids");
+    return launch_sign_wide_t<uint64_t>(kind == KIND_ITERATIVE, indptr, ids, n_sets, a, b, ra, rb, prime, n_hash,
+                                        out, MHB_OUT_I64, status, static_cast<cudaStream_t>(stream));
 }

@@ -188,8 +188,8 @@ def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
                 raise ValueError("feature ids must be non-negative")
             if hi >= family.prime:
                 raise ValueError(f"feature id {hi} >= family prime {family.prime}")
-            if hi > MAX_ID:
-                raise NotImplementedError(f"feature id {hi} >= 2^32: CSR ids are uint32")
+            if hi > MAX_ID:  # the reference's int64 ids beyond 2^32 (primes >= 2^32)
+                return _signatures_ids64(indptr, ids.to(torch.int64), family, out_dtype, out, validate)
         ids = ids.to(torch.uint32)
     ids = ids.contiguous()
     indptr = indptr.to(torch.int64).contiguous()
@@ -206,6 +206,36 @@ def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
     return out
 
 
+def _signatures_ids64(indptr, ids, family: Family, out_dtype, out, validate):
+    """Device CSR batch with int64 feature ids >= 2^32 (mhb_sign_csr_ids64, wide.cu)."""
+    torch = _torch()
+    if out_dtype != "int64":
+        raise ValueError("feature ids >= 2^32 need out_dtype='int64'")
+    lib = _lib.load()
+    dev = ids.device
+    indptr = indptr.to(torch.int64).contiguous()
+    ids = ids.contiguous()
+    n_sets = indptr.numel() - 1
+    if out is None:
+        out = torch.empty((n_sets, family.size), dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        sptr = torch.cuda.current_stream(dev).cuda_stream
+        if isinstance(family, IterativeFamily):
+            rc = lib.mhb_sign_csr_ids64(_lib.KIND_ITERATIVE, indptr.data_ptr(), ids.data_ptr(), n_sets, ids.numel(),
+                                        family.base.a, family.base.b, None, None, family.prime, family.size,
+                                        out.data_ptr(), status.data_ptr(), sptr)
+        else:
+            a, b = family.device_params(dev, wide=True)
+            rc = lib.mhb_sign_csr_ids64(_lib.KIND_RANDOM, indptr.data_ptr(), ids.data_ptr(), n_sets, ids.numel(), 0, 0,
+                                        a.data_ptr(), b.data_ptr(), family.prime, family.size, out.data_ptr(),
+                                        status.data_ptr(), sptr)
+    _lib.check(rc)
+    if validate:
+        _raise_status(int(status.item()), family)
+    return out
+
+
 def _signatures_csr_host(indptr, ids, family, out_dtype, out, device):
     torch = _torch()
     lib = _lib.load()
@@ -216,11 +246,24 @@ def _signatures_csr_host(indptr, ids, family, out_dtype, out, device):
                 raise ValueError("feature ids must be non-negative")
             if ids.max() >= family.prime:
                 raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
-            raise NotImplementedError(f"feature id {int(ids.max())} >= 2^32: CSR ids are uint32")
+            # ids beyond 2^32 (primes >= 2^32): the 64-bit-id device entry
+            dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+            res = _signatures_ids64(torch.as_tensor(indptr, device=dev), torch.as_tensor(ids.astype(np.int64), device=dev),
+                                    family, out_dtype, None, True).cpu().numpy()
+            if out is None:
+                return res
+            out[...] = res
+            return out
         ids = ids.astype(np.uint32)
     if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:
-        raise NotImplementedError("host pipeline with primes >= 2^31 supports the iterative family; "
-                                  "pass device tensors for the random family")
+        # 64-bit random-family parameters: the device entry (mhb_sign_random_csr_u64)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+        res = signatures_csr(torch.as_tensor(indptr, device=dev), torch.as_tensor(ids.astype(np.int64), device=dev),
+                             family, out_dtype=out_dtype).cpu().numpy()
+        if out is None:
+            return res
+        out[...] = res
+        return out
     ids = np.ascontiguousarray(ids)
     n_sets = indptr.size - 1
     ndt = np.int64 if out_dtype == "int64" else np.uint32
@@ -254,8 +297,12 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         raise ValueError("cannot build a signature for an empty feature set")
     if s.max_id >= family.prime:
         raise ValueError(f"feature id {s.max_id} >= family prime {family.prime}")
-    if s.max_id > MAX_ID:
-        raise NotImplementedError(f"feature id {s.max_id} >= 2^32: CSR ids are uint32")
+    if s.max_id > MAX_ID:  # int64 ids beyond 2^32: the 64-bit-id device entry
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ip = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
+        out = _signatures_ids64(ip, torch.as_tensor(s.ids, device=dev), family, "int64", None, True)
+        return Signature(out[0].cpu().numpy(), family.key)
     _check_family(family)
     if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:  # 64-bit a, b: device entry
         torch = _torch()

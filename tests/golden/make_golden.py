@@ -305,8 +305,33 @@ def corpus_fixture():
     np.savez_compressed(HERE / "corpus.npz", **arrays)
     (HERE / "corpus.json").write_text(json.dumps(cases, indent=1, ensure_ascii=True))
 
+def wide_ids_fixture():
+    """int64 feature ids beyond 2^32 under primes >= 2^32 (the reference's FeatureSet
+    is int64; signature() takes _signature_by_rows there, minhash.py:102-127)."""
+    rng = np.random.default_rng(2026)
+    cases, arrays = [], {}
+    for k, (kind, p, n) in enumerate([("iterative", 4_294_967_311, 16), ("random", 4_294_967_311, 12),
+                                       ("iterative", 2**62 + 135, 16), ("random", 2**62 + 135, 9)]):
+        seed = int(rng.integers(1 << 30))
+        fam = ref.make_family(kind, seed, n, p)
+        sizes = [1, 2, 7, 40, 13]
+        rows = [np.unique(rng.integers(0, p, size=m, dtype=np.int64)) for m in sizes]
+        # every case reaches past 2^32: 2^32 itself and the largest ids below p
+        rows[1] = np.unique(np.concatenate([rows[1], [2**32, p - 1]]))
+        rows[3] = np.unique(np.concatenate([rows[3], [2**32 + 1, p - 2, 7]]))
+        indptr = np.zeros(len(rows) + 1, dtype=np.int64)
+        indptr[1:] = np.cumsum([r.size for r in rows])
+        out = np.stack([ref.signature(ref.FeatureSet(r), fam).mins for r in rows])
+        arrays[f"indptr{k}"] = indptr
+        arrays[f"ids{k}"] = np.concatenate(rows)
+        arrays[f"out{k}"] = out
+        cases.append({"kind": kind, "p": p, "n": n, "seed": seed})
+    np.savez_compressed(HERE / "wide_ids.npz", **arrays)
+    (HERE / "wide_ids.json").write_text(json.dumps(cases, indent=1))
+
 
 if __name__ == "__main__":
+    wide_ids_fixture()
     corpus_fixture()
     synth_corpus_fixture()
     wide_fixture()

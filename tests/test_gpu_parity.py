@@ -602,3 +602,33 @@ def test_gpu_corpus_final_sigma(cuda_device):
     c = build_corpus_csr(data, backend="gpu")
     assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
     assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
+
+
+def test_wide_ids_beyond_2_32(golden, cuda_device):
+    """The reference's int64 feature ids beyond 2^32 (primes >= 2^32): device tensors,
+    numpy batches and the per-set API all equal the reference (mhb_sign_csr_ids64)."""
+    import torch
+
+    z = np.load(golden / "wide_ids.npz")
+    for k, m in enumerate(json.loads((golden / "wide_ids.json").read_text())):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        ip, ids, want = z[f"indptr{k}"], z[f"ids{k}"], z[f"out{k}"]
+        dev = signatures_csr(torch.as_tensor(ip, device=cuda_device), torch.as_tensor(ids, device=cuda_device), fam)
+        assert np.array_equal(dev.cpu().numpy(), want), m
+        assert np.array_equal(signatures_csr(ip, ids, fam), want), m
+        for s in range(ip.size - 1):
+            assert np.array_equal(signature(FeatureSet(ids[ip[s]:ip[s + 1]]), fam).mins, want[s]), m
+        with pytest.raises(ValueError, match="int64"):
+            signatures_csr(ip, ids, fam, out_dtype="uint32")
+
+
+def test_random_wide_prime_host_arrays(cuda_device):
+    """numpy batches with a random family over a prime >= 2^31 (64-bit a, b) run on the device."""
+    rng = np.random.default_rng(8)
+    fam = make_family("random", 5, 24, 3_000_000_019)
+    rows = [np.unique(rng.integers(0, 2**31, size=m)) for m in (1, 9, 30)]
+    ip = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int64)
+    ids = np.concatenate(rows)
+    got = signatures_csr(ip, ids, fam)
+    for s, r in enumerate(rows):
+        assert np.array_equal(got[s], oracle.brute_force_row(r, fam))

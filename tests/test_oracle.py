@@ -134,3 +134,14 @@ def test_c_oracle_exact_beyond_max_vector_prime(kind):
     ids = np.unique(rng.integers(0, p, size=300)).astype(np.uint32)
     got = oracle.sign_family_csr(np.array([0, ids.size]), ids, fam)[0]
     assert np.array_equal(got, oracle.brute_force_row(ids, fam))
+
+
+def test_wide_ids_restatement(golden):
+    """int64 ids beyond 2^32 (primes >= 2^32): the reference's outputs == brute force."""
+    z = np.load(golden / "wide_ids.npz")
+    for k, m in enumerate(json.loads((golden / "wide_ids.json").read_text())):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        ip, ids = z[f"indptr{k}"], z[f"ids{k}"]
+        assert ids.max() > 2**32
+        for s in range(ip.size - 1):
+            assert np.array_equal(oracle.brute_force_row(ids[ip[s]:ip[s + 1]], fam), z[f"out{k}"][s]), m
