@@ -632,3 +632,26 @@ def test_random_wide_prime_host_arrays(cuda_device):
     got = signatures_csr(ip, ids, fam)
     for s, r in enumerate(rows):
         assert np.array_equal(got[s], oracle.brute_force_row(r, fam))
+
+
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_extreme_sets(cuda_device, kind):
+    """A 5M-id set (about 4,900 merged chunks through red.global.min + finalize), a set
+    of one id repeated 3000 times, ids 0 and p-1, next to ordinary sets."""
+    import torch
+
+    p = 16_777_259
+    fam = make_family(kind, 9, 64, p)
+    rng = np.random.default_rng(3)
+    rows = [rng.integers(0, p, size=5_000_000).astype(np.uint32),  # repeats allowed: still a set
+            np.full(3000, 12345, dtype=np.uint32),
+            np.array([0, p - 1], dtype=np.uint32),
+            np.array([p - 1], dtype=np.uint32),
+            rng.integers(0, p, size=300).astype(np.uint32)]
+    ip = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int64)
+    ids = np.concatenate(rows)
+    want = oracle.sign_family_csr(ip, ids, fam)
+    got = signatures_csr(torch.as_tensor(ip, device=cuda_device),
+                         torch.as_tensor(ids.astype(np.int64), device=cuda_device).to(torch.uint32), fam)
+    assert np.array_equal(got.cpu().numpy(), want)
+    assert np.array_equal(signatures_csr(ip, ids, fam), want)  # host pipeline, chunked
