@@ -301,7 +301,7 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         torch = _torch()
         dev = torch.device("cuda", torch.cuda.current_device())
         ip = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
-        out = _signatures_ids64(ip, torch.as_tensor(s.ids, device=dev), family, "int64", None, True)
+        out = _signatures_ids64(ip, torch.tensor(s.ids, device=dev), family, "int64", None, True)
         return Signature(out[0].cpu().numpy(), family.key)
     _check_family(family)
     if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:  # 64-bit a, b: device entry
