@@ -634,8 +634,9 @@ def main():
     alg_bytes = 4 * nnz + 8 * (n_sets + 1) + 4 * n_sets * N
     traffic, traffic_src = _ncu_traffic(args.config, args.family)
     probe_v, probe_ms = C.c_double(0), C.c_float(0)
-    _lib.check(lib.mhb_probe_visit_rate(1 << 20, 0 if args.family == "iterative" else 1,
-                                        C.byref(probe_v), C.byref(probe_ms), stream.cuda_stream))
+    probe_kind = 0 if args.family == "iterative" else (2 if fam.prime <= (1 << 23) else 1)
+    _lib.check(lib.mhb_probe_visit_rate(1 << 20, probe_kind, C.byref(probe_v), C.byref(probe_ms),
+                                        stream.cuda_stream))
     probe_rate = probe_v.value / (probe_ms.value / 1e3)
     roofline = {
         "bound": "int", "unit": "Gvisit/s",

@@ -283,9 +283,10 @@ int mhb_peer_close(void* ptr);
 int mhb_peer_free(void* ptr);
 
 /*
- * Instruction-rate probe for the roofline: runs the iterative visit sequence
- * (add, conditional subtract, 3-way min) from registers only, `visits_per_thread`
- * visits per thread on a persistent grid, and reports visits and device ms.
+ * Instruction-rate probe for the roofline: runs a visit sequence from registers only,
+ * `visits_per_thread` visits per thread on a persistent grid, and reports visits and
+ * device ms.  kind 0: iterative (add, conditional subtract, 3-way min); 1: random family,
+ * Shoup lanes; 2: random family, float-quotient lanes (the kernel's path for p <= 2^23).
  */
 int mhb_probe_visit_rate(int64_t visits_per_thread, int32_t kind,
                          double* visits_out, float* ms_out, void* stream);

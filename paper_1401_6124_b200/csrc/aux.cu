@@ -276,6 +276,39 @@ __global__ void __launch_bounds__(256) probe_random_kernel(int64_t rounds, uint3
     if (acc == 0x9e3779b9u) g_probe_sink = acc;
 }
 
+// The random family's float-quotient visit (sign.cu walk2_random_fpq, p <= 2^23), K lanes.
+template <int K>
+__global__ void __launch_bounds__(256) probe_random_fpq_kernel(int64_t rounds, uint32_t p, uint32_t seed) {
+    uint32_t best[K], cA[K], cW[K], cC[K];
+    const uint32_t negp = 0u - p;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        best[k] = 0xffffffffu;
+        cA[k] = (seed + 977u * k + threadIdx.x) % (p - 1) + 1;
+        cW[k] = __float_as_uint(__double2float_rd((double)cA[k] / (double)p));
+        cC[k] = (seed * 31u + k) % p + 0x4B000000u * p;
+    }
+    uint32_t xa = (threadIdx.x * 2654435761u + seed) % p, xb = (xa * 7u + 13u) % p;
+    for (int64_t r = 0; r < rounds; ++r) {
+        const float fa = __uint2float_rn(xa), fb = __uint2float_rn(xb);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float wf = __uint_as_float(cW[k]);
+            const uint32_t qa = __float_as_uint(__fmaf_rz(fa, wf, 8388608.0f));
+            const uint32_t qb = __float_as_uint(__fmaf_rz(fb, wf, 8388608.0f));
+            const uint32_t ra = reduce_once(reduce_once(cA[k] * xa + cC[k] + qa * negp, p), p);
+            const uint32_t rb = reduce_once(reduce_once(cA[k] * xb + cC[k] + qb * negp, p), p);
+            best[k] = __vimin3_u32(best[k], ra, rb);
+        }
+        xa = reduce_once(xa + 1u, p);
+        xb = reduce_once(xb + 3u, p);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc ^= best[k];
+    if (acc == 0x9e3779b9u) g_probe_sink = acc;
+}
+
 }  // namespace mhb
 
 using namespace mhb;
@@ -382,22 +415,27 @@ extern "C" int mhb_probe_visit_rate(int64_t visits_per_thread, int32_t kind, dou
     int rc = current_device_info(&dev);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    constexpr int K = 64;
+    // kind 0: iterative walk (K=64); 1: random family, Shoup lanes (K=64); 2: random family,
+    // float-quotient lanes as the kernel runs them for p <= 2^23 (K=16, p = 4,194,319)
+    const int K = kind == 2 ? 16 : 64;
     const int64_t rounds = visits_per_thread / (2 * K) > 0 ? visits_per_thread / (2 * K) : 1;
     int occ = 0;
-    const void* fn = kind == 0 ? (const void*)probe_iter_kernel<K> : (const void*)probe_random_kernel<K>;
+    const void* fn = kind == 0 ? (const void*)probe_iter_kernel<64>
+                               : kind == 1 ? (const void*)probe_random_kernel<64> : (const void*)probe_random_fpq_kernel<16>;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
     if (occ < 1) occ = 1;
     const int blocks = occ * dev.sms;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    // warm-up
-    if (kind == 0) probe_iter_kernel<K><<<blocks, 256, 0, st>>>(rounds / 10 + 1, 16777259u, 1u);
-    else probe_random_kernel<K><<<blocks, 256, 0, st>>>(rounds / 10 + 1, 16777259u, 1u);
+    auto launch = [&](int64_t r, uint32_t seed) {
+        if (kind == 0) probe_iter_kernel<64><<<blocks, 256, 0, st>>>(r, 16777259u, seed);
+        else if (kind == 1) probe_random_kernel<64><<<blocks, 256, 0, st>>>(r, 16777259u, seed);
+        else probe_random_fpq_kernel<16><<<blocks, 256, 0, st>>>(r, 4194319u, seed);
+    };
+    launch(rounds / 10 + 1, 1u);  // warm-up
     cudaEventRecord(e0, st);
-    if (kind == 0) probe_iter_kernel<K><<<blocks, 256, 0, st>>>(rounds, 16777259u, 2u);
-    else probe_random_kernel<K><<<blocks, 256, 0, st>>>(rounds, 16777259u, 2u);
+    launch(rounds, 2u);
     cudaEventRecord(e1, st);
     rc = cuda_check(cudaEventSynchronize(e1), "probe sync");
     float ms = 0.f;

@@ -131,6 +131,10 @@ __global__ void plan_count_kernel(SignArgs A) {
         t.A = w;
         t.Ap = shoup_companion(w, p);
         t.B = c;
+        if (A.fpq) {  // float-quotient lanes (walk2_random_fpq): rd(w/p) and c + 2^23-magic * p
+            t.Ap = __float_as_uint(__double2float_rd((double)w / (double)p));
+            t.B = c + 0x4B000000u * p;
+        }
         t.pad = 0;
         A.tab[i] = t;
         InvTab v;
@@ -350,6 +354,39 @@ __device__ __forceinline__ void walk1_random(uint32_t (&best)[K], const uint32_t
     }
 }
 
+// Random family, p <= 2^23: the Shoup quotient (IMAD.HI, two FMA-heavy issue slots)
+// comes from the FP32 pipe instead.  With x < 2^23 exact in float and wf = rd(w/p),
+// q = rz(x*wf + 2^23) - 2^23 = floor(x*wf) lies in {floor(x*w/p) - 1, floor(x*w/p)},
+// so r = w*x + c - q*p lies in [0, 3p): two conditional subtracts.  The magic 2^23 is
+// folded into the lane offset (cC = c + 0x4B000000 * p), q*p is added as bits*(2^32-p).
+template <int K, bool FIRST>
+__device__ __forceinline__ void walk2_random_fpq(uint32_t (&best)[K], const uint32_t (&cA)[K],
+                                                 const uint32_t (&cW)[K], const uint32_t (&cC)[K],
+                                                 uint32_t xa, uint32_t xb, uint32_t p, uint32_t negp) {
+    const float fa = __uint2float_rn(xa), fb = __uint2float_rn(xb);  // exact: x < 2^24
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float wf = __uint_as_float(cW[k]);
+        const uint32_t qa = __float_as_uint(__fmaf_rz(fa, wf, 8388608.0f));
+        const uint32_t qb = __float_as_uint(__fmaf_rz(fb, wf, 8388608.0f));
+        const uint32_t ra = reduce_once(reduce_once(cA[k] * xa + cC[k] + qa * negp, p), p);
+        const uint32_t rb = reduce_once(reduce_once(cA[k] * xb + cC[k] + qb * negp, p), p);
+        best[k] = FIRST ? min(ra, rb) : __vimin3_u32(best[k], ra, rb);
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void walk1_random_fpq(uint32_t (&best)[K], const uint32_t (&cA)[K],
+                                                 const uint32_t (&cW)[K], const uint32_t (&cC)[K], uint32_t xa,
+                                                 uint32_t p, uint32_t negp) {
+    const float fa = __uint2float_rn(xa);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t qa = __float_as_uint(__fmaf_rz(fa, __uint_as_float(cW[k]), 8388608.0f));
+        best[k] = min(best[k], reduce_once(reduce_once(cA[k] * xa + cC[k] + qa * negp, p), p));
+    }
+}
+
 // Per-thread hashing state: iterative start constants, or the K random-family lane constants.
 template <int K, bool ITER>
 struct LaneState {
@@ -358,7 +395,7 @@ struct LaneState {
     uint32_t cA[ITER ? 1 : K], cAp[ITER ? 1 : K], cB[ITER ? 1 : K];
 };
 
-template <int K, bool ITER, bool NARROW, bool FIRST>
+template <int K, bool ITER, bool NARROW, bool FIRST, bool FPQ = false>
 __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa, uint32_t xb,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
@@ -366,17 +403,21 @@ __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, I
         const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
         const uint32_t hb = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xb, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
         walk2_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), hb, reduce_once(xb + bpar, p), p);
+    } else if constexpr (FPQ) {
+        walk2_random_fpq<K, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p, ls.negp);
     } else {
         walk2_random<K, NARROW, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p, ls.negp);
     }
 }
 
-template <int K, bool ITER, bool NARROW>
+template <int K, bool ITER, bool NARROW, bool FPQ = false>
 __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
         const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
         walk1_iter<K>(best, ha, reduce_once(xa + bpar, p), p);
+    } else if constexpr (FPQ) {
+        walk1_random_fpq<K>(best, ls.cA, ls.cAp, ls.cB, xa, p, ls.negp);
     } else {
         walk1_random<K, NARROW>(best, ls.cA, ls.cAp, ls.cB, xa, p, ls.negp);
     }
@@ -462,7 +503,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
-template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false>
+template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false>
 __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -549,7 +590,7 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
         if (rounds == 1) {
             const uint32_t pa = __ldg(nbase), pb = __ldg(nbase + min(1, nlast));
             maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
+            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
             xa = pa; xb = pb;
         } else {
             uint32_t pa = __ldg(base + min(2, last)), pb = __ldg(base + min(3, last));  // round 1
@@ -562,7 +603,7 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
                 qb = __ldg(nbase + min(1, nlast));
             }
             maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, true>(best, ls, xa, xb, p, bpar);
+            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
             xa = pa; xb = pb; pa = qa; pb = qb;
             int o = 6;
 #pragma unroll 1
@@ -570,22 +611,22 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
                 qa = __ldg(base + min(o, last));  // smaller sets of the group clamp to their last id
                 qb = __ldg(base + min(o + 1, last));
                 maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
                 xa = pa; xb = pb; pa = qa; pb = qb;
             }
             if (rounds > 2) {
                 qa = __ldg(nbase);
                 qb = __ldg(nbase + min(1, nlast));
                 maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
                 xa = pa; xb = pb; pa = qa; pb = qb;
             }
             if (odd) {
                 maxid = max(maxid, xa);
-                round1<K, ITER, NARROW>(best, ls, xa, p, bpar);
+                round1<K, ITER, NARROW, FPQ>(best, ls, xa, p, bpar);
             } else {
                 maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false>(best, ls, xa, xb, p, bpar);
+                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
             }
             xa = pa; xb = pb;
         }
@@ -655,6 +696,15 @@ static SignKernelFn pick_kernel(int K) {
         default: break;
     }
     if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT>;
+    return nullptr;
+}
+
+static SignKernelFn select_fpq_kernel(int out_dtype, int K) {
+    const bool i64 = out_dtype == MHB_OUT_I64;
+    if (K == 16) return i64 ? sign_kernel<16, false, true, long long, false, true>
+                            : sign_kernel<16, false, true, uint32_t, false, true>;
+    if (K == 8) return i64 ? sign_kernel<8, false, true, long long, false, true>
+                           : sign_kernel<8, false, true, uint32_t, false, true>;
     return nullptr;
 }
 
@@ -797,6 +847,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     DeviceInfo dev;
     rc = current_device_info(&dev);
     if (rc) return rc;
+    // random family with p <= 2^23: float-quotient lanes (walk2_random_fpq); the plan
+    // kernels build their lane tables, so the flag is set before they launch
+    const bool fpq = !keys && kind == KIND_RANDOM && prime <= (1ull << 23) && (geo.K == 16 || geo.K == 8);
+    A.fpq = fpq ? 1 : 0;
 
     {
         int64_t work = n_sets > geo.n_tot ? n_sets : geo.n_tot;
@@ -821,7 +875,8 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     }
 
     const bool narrow = (3ull * prime) < (1ull << 32);
-    SignKernelFn fn = keys ? select_bands_kernel(narrow, out_dtype, geo.K) : select_kernel(kind, narrow, out_dtype, geo.K);
+    SignKernelFn fn = keys ? select_bands_kernel(narrow, out_dtype, geo.K)
+                           : fpq ? select_fpq_kernel(out_dtype, geo.K) : select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);

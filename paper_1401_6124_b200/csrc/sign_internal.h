@@ -75,6 +75,7 @@ struct SignArgs {
     unsigned long long* keys;
     int32_t rows;       // rows per band (divides K and n_hash)
     int32_t write_sig;  // 0: keys only (out still serves long-set rows as scratch)
+    int32_t fpq;        // random family, p <= 2^23: lane tables hold rd(w/p) and the folded offset
 };
 
 Geometry choose_geometry(int kind, int32_t n_hash);
