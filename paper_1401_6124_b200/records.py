@@ -108,6 +108,13 @@ def write_signatures_csr(path, indptr, ids, family: Family, fmt: str = "binary",
     pending = None  # (pinned host view, event) of the chunk in flight
     slot = 0
     with open(path, "wb") as fh:
+        fd, pos = fh.fileno(), 0
+
+        def flush(view):  # concurrent pwrite of the chunk (page-cache copies in parallel)
+            nonlocal pos
+            _pwrite_parallel(fd, memoryview(view.numpy()), pos)
+            pos += view.numel()
+
         for s0 in range(0, n_sets, step):
             s1 = min(n_sets, s0 + step)
             lo, hi = int(ip_h[s0]), int(ip_h[s1])
@@ -127,11 +134,34 @@ def write_signatures_csr(path, indptr, ids, family: Family, fmt: str = "binary",
             ev.record()
             if pending is not None:
                 pending[1].synchronize()
-                fh.write(memoryview(pending[0].numpy()))
+                flush(pending[0])
             pending = (host, ev)
             slot ^= 1
             written += s1 - s0
         if pending is not None:
             pending[1].synchronize()
-            fh.write(memoryview(pending[0].numpy()))
+            flush(pending[0])
     return written
+
+
+_WRITERS: list = []
+
+
+def _pwrite_parallel(fd: int, mv: memoryview, offset: int, parts: int = 8, min_part: int = 4 << 20) -> None:
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = len(mv)
+    parts = max(1, min(parts, n // min_part))
+
+    def put(k):
+        lo, hi = n * k // parts, n * (k + 1) // parts
+        while lo < hi:
+            lo += os.pwritev(fd, [mv[lo:hi]], offset + lo)
+
+    if parts == 1:
+        put(0)
+        return
+    if not _WRITERS:
+        _WRITERS.append(ThreadPoolExecutor(8))
+    list(_WRITERS[0].map(put, range(parts)))
