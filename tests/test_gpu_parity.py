@@ -274,6 +274,23 @@ def test_fused_band_keys(cuda_device, n_hash, rows):
     none, keys = signatures_band_keys(ip, di, fam, rows, write_signatures=False)
     assert none is None
     assert np.array_equal(keys.cpu().numpy().view(np.uint64), want)
+    # the ABI's fused mode that also stores the signatures (write_signatures = 1)
+    import torch
+
+    from paper_1401_6124_b200 import _lib
+
+    lib = _lib.load()
+    n_sets = ip.numel() - 1
+    sig = torch.empty((n_sets, n_hash), dtype=torch.uint32, device=cuda_device)
+    k2 = torch.empty((n_sets, n_hash // rows), dtype=torch.uint64, device=cuda_device)
+    ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, di.numel(), n_hash)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=cuda_device)
+    _lib.check(lib.mhb_sign_iterative_csr_bands(ip.data_ptr(), di.data_ptr(), n_sets, di.numel(), fam.base.a,
+                                                fam.base.b, fam.prime, n_hash, rows, k2.data_ptr(), sig.data_ptr(),
+                                                _lib.OUT_U32, 1, None, ws.data_ptr(), ws_bytes,
+                                                torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(sig.cpu().numpy().astype(np.int64), want_sig)
+    assert np.array_equal(k2.cpu().numpy().view(np.uint64), want)
 
 
 def test_fused_band_keys_fallbacks(cuda_device):
