@@ -452,7 +452,13 @@ __device__ __forceinline__ void dump_best(const uint32_t (&best)[K], uint32_t* r
             make_uint4(best[4 * q], best[4 * q + 1], best[4 * q + 2], best[4 * q + 3]);
 }
 
-template <int K, typename OutT, bool EPI_SMEM, bool BANDS>
+template <int K>
+__host__ __device__ constexpr int kLog2() { return K <= 1 ? 0 : 1 + kLog2<K / 2>(); }
+
+// SKEW: the shared-memory epilogue table holds lane i at i + i/K.  With large G (lane
+// blocks of the warp's threads K apart, N >= 16*K) the 8 threads of an LDS.128 phase
+// would otherwise all hit one bank group (an 8-way conflict at G = 32).
+template <int K, typename OutT, bool EPI_SMEM, bool BANDS, bool SKEW = false>
 __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
                                            bool merge, int64_t i0, const InvTab* epi_s) {
     constexpr int NQ = K / 4;
@@ -477,7 +483,8 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
         uint32_t x[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const InvTab t = EPI_SMEM ? epi_s[i + e] : A.inv[min(i + e, A.n_tot - 1)];
+            const int64_t ie = SKEW ? (i + e) + ((i + e) >> kLog2<K>()) : i + e;
+            const InvTab t = EPI_SMEM ? epi_s[ie] : A.inv[min(i + e, A.n_tot - 1)];
             x[e] = invert_entry(t, h[e], p);
         }
         if constexpr (BANDS) {
@@ -503,7 +510,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
-template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false>
+template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false>
 __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
     // Stage the epilogue table (B_i, A_i^{-1}, companion) in shared memory.
     const bool epi_smem = A.n_tot <= kEpiSmemLanes;
     if (epi_smem) {
-        for (int i = threadIdx.x; i < A.n_tot; i += blockDim.x) epi_s[i] = A.inv[i];
+        for (int i = threadIdx.x; i < A.n_tot; i += blockDim.x) epi_s[SKEW ? i + i / K : i] = A.inv[i];
         __syncthreads();
     }
 
@@ -636,8 +643,8 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
             const bool merge = (ec.meta >> 11) & 1;
             const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
             dump_best<K>(best, dump_row, lane);
-            if (epi_smem) emit_lanes<K, OutT, true, BANDS>(A, dump_row, lane, set, merge, i0, epi_s);
-            else emit_lanes<K, OutT, false, BANDS>(A, dump_row, lane, set, merge, i0, epi_s);
+            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW>(A, dump_row, lane, set, merge, i0, epi_s);
+            else emit_lanes<K, OutT, false, BANDS, SKEW>(A, dump_row, lane, set, merge, i0, epi_s);
         }
 
         it = itn;
@@ -697,6 +704,15 @@ static SignKernelFn pick_kernel(int K) {
     }
     if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT>;
     return nullptr;
+}
+
+// Iterative K = 64 with G >= 16 lane groups (N >= 1024): the skewed epilogue table.
+static SignKernelFn select_skew_kernel(bool narrow, int out_dtype) {
+    const bool i64 = out_dtype == MHB_OUT_I64;
+    if (narrow) return i64 ? sign_kernel<64, true, true, long long, false, false, true>
+                           : sign_kernel<64, true, true, uint32_t, false, false, true>;
+    return i64 ? sign_kernel<64, true, false, long long, false, false, true>
+               : sign_kernel<64, true, false, uint32_t, false, false, true>;
 }
 
 static SignKernelFn select_fpq_kernel(int out_dtype, int K) {
@@ -875,11 +891,14 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     }
 
     const bool narrow = (3ull * prime) < (1ull << 32);
-    SignKernelFn fn = keys ? select_bands_kernel(narrow, out_dtype, geo.K)
-                           : fpq ? select_fpq_kernel(out_dtype, geo.K) : select_kernel(kind, narrow, out_dtype, geo.K);
+    const bool skew = !keys && kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
+    SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K)
+                      : fpq  ? select_fpq_kernel(out_dtype, geo.K)
+                      : skew ? select_skew_kernel(narrow, out_dtype)
+                             : select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
-                        (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
+                        (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0);
     const int occ = blocks_per_sm(fn, smem, dev);
     const int64_t max_vsets = n_sets + nnz / kChunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
