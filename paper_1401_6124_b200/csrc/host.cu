@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -153,7 +154,12 @@ std::vector<Chunk> plan_chunks(const int64_t* indptr, int64_t n_sets, int32_t n_
     const int64_t nnz = indptr[n_sets] - indptr[0];
     // nnz-balanced cuts, ~16 chunks for large inputs, bounded rows so the output
     // chunk stays <= 256 MB.
-    int64_t target_nnz = std::max<int64_t>(nnz / 16, 1 << 22);
+    static const int64_t n_chunks = [] {  // MHB_HOST_CHUNKS: tuning override
+        const char* e = std::getenv("MHB_HOST_CHUNKS");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? (int64_t)v : (int64_t)16;
+    }();
+    int64_t target_nnz = std::max<int64_t>(nnz / n_chunks, 1 << 22);
     int64_t max_rows = std::max<int64_t>(1, (int64_t)((256ull << 20) / ((size_t)n_hash * out_bytes)));
     std::vector<Chunk> out;
     int64_t s = 0;

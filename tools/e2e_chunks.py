@@ -1,0 +1,29 @@
+"""e2e (host numpy in -> host numpy out) time of cfg2 for the current MHB_HOST_CHUNKS."""
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1401_6124_b200 import gen, make_family, signatures_csr  # noqa: E402
+
+cfg = gen.CONFIGS["cfg2"]
+ip, ids = gen.make_csr(cfg, device="cuda:0")
+fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+ip_pin = torch.empty(ip.numel(), dtype=torch.int64, pin_memory=True)
+ids_pin = torch.empty(ids.numel(), dtype=torch.int32, pin_memory=True)
+out_pin = torch.empty((ip.numel() - 1, fam.size), dtype=torch.int32, pin_memory=True)
+ip_pin.copy_(ip)
+ids_pin.copy_(ids.view(torch.int32))
+a, b, o = ip_pin.numpy(), ids_pin.numpy().view(np.uint32), out_pin.numpy().view(np.uint32)
+for _ in range(2):
+    signatures_csr(a, b, fam, out_dtype="uint32", out=o)
+t = []
+for _ in range(5):
+    t0 = time.perf_counter()
+    signatures_csr(a, b, fam, out_dtype="uint32", out=o)
+    t.append(time.perf_counter() - t0)
+print(os.environ.get("MHB_HOST_CHUNKS", "16"), "chunks:", round(statistics.mean(t) * 1e3, 2), "ms", round(min(t) * 1e3, 2))
