@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -38,7 +42,132 @@ struct Lane {
     size_t out_cap = 0;
     void* ws = nullptr;
     size_t ws_cap = 0;
+    // pinned staging for pageable caller buffers / int64 output (see mhb_sign_csr_host)
+    uint32_t* stage_ids = nullptr;
+    size_t stage_ids_cap = 0;
+    uint32_t* stage_out = nullptr;
+    size_t stage_out_cap = 0;
+    int64_t pend_s0 = -1, pend_rows = 0;  // chunk whose staged output awaits the host copy
 };
+
+// Persistent host worker pool for the staging copies (page-cache-speed memcpy and the
+// u32 -> int64 widening run on many cores while the GPU moves the next chunks).
+class HostPool {
+  public:
+    HostPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int n = (int)std::min(16u, hw) - 1;  // the calling thread works too
+        for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // fn(part) for part in [0, parts), spread over the pool and the caller
+    void run(int parts, const std::function<void(int)>& fn) {
+        if (parts <= 1 || th_.empty()) {
+            for (int k = 0; k < parts; ++k) fn(k);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> l(m_);
+            fn_ = &fn;
+            parts_ = parts;
+            next_.store(0);
+            left_ = parts;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [this] { return left_ == 0; });
+        fn_ = nullptr;
+    }
+    int width() const { return (int)th_.size() + 1; }
+
+  private:
+    void work() {
+        for (int k; (k = next_.fetch_add(1)) < parts_;) {
+            (*fn_)(k);
+            std::lock_guard<std::mutex> l(m_);
+            if (--left_ == 0) done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int parts_ = 0, left_ = 0;
+    std::atomic<int> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+HostPool& host_pool() {
+    static HostPool pool;
+    return pool;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int grow_pinned(void** ptr, size_t* cap, size_t need) {
+    if (*cap >= need && *ptr) return MHB_OK;
+    if (*ptr) cudaFreeHost(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    const size_t want = need + need / 4 + 256;
+    int rc = cuda_check(cudaHostAlloc(ptr, want, cudaHostAllocDefault), "cudaHostAlloc (staging)");
+    if (rc) return rc;
+    *cap = want;
+    return MHB_OK;
+}
+
+// Parallel copy (u32 -> u32, or u32 -> int64 widening) of `n` elements.
+void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen) {
+    HostPool& pool = host_pool();
+    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n >> 18));
+    pool.run(parts, [&](int k) {
+        const int64_t lo = n * k / parts, hi = n * (k + 1) / parts;
+        if (widen) {
+            long long* d = static_cast<long long*>(dst);
+            for (int64_t i = lo; i < hi; ++i) d[i] = (long long)src[i];
+        } else {
+            std::memcpy(static_cast<uint32_t*>(dst) + lo, src + lo, (size_t)(hi - lo) * 4);
+        }
+    });
+}
+
+void host_copy_in(const uint32_t* src, uint32_t* dst, int64_t n) {
+    HostPool& pool = host_pool();
+    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n >> 18));
+    pool.run(parts, [&](int k) {
+        const int64_t lo = n * k / parts, hi = n * (k + 1) / parts;
+        std::memcpy(dst + lo, src + lo, (size_t)(hi - lo) * 4);
+    });
+}
 
 // Small batches (the per-set reference API: signature() on one FeatureSet) skip the
 // chunk pipeline: inputs are staged in mapped pinned memory, one kernel launch reads
@@ -293,6 +422,24 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     const std::vector<Chunk> chunks = plan_chunks(indptr, n_sets, n_hash, out_bytes);
     if (chunks.size() > (size_t)kMaxChunks) return set_error(MHB_ERR_INVALID, "batch needs more than %d chunks", kMaxChunks);
     int32_t status_acc = 0;
+    // Pageable caller buffers would make every cudaMemcpyAsync synchronous (staged by the
+    // driver).  So: ids from pageable memory are copied into a pinned lane buffer by the
+    // host pool before their H2D; for pageable output the kernels write uint32, the D2H
+    // lands in a pinned lane buffer, and the pool copies (or widens to int64: half the
+    // PCIe bytes) into the caller's array once the lane drains -- overlapped with the
+    // transfers of the other lanes.  Pinned output keeps the direct D2H.
+    // (pinned int64 output keeps the direct int64 D2H: widening 2x the bytes on the host
+    // is no faster than the DMA writing them)
+    const bool stage_out = !is_pinned(out);
+    const bool widen = stage_out && out_dtype == MHB_OUT_I64;
+    const bool stage_in = nnz > 0 && !is_pinned(ids);
+    auto drain = [&](Lane& ln) {
+        if (ln.pend_s0 >= 0) {
+            host_copy_out(ln.stage_out, static_cast<char*>(out) + (size_t)ln.pend_s0 * n_hash * out_bytes,
+                          ln.pend_rows * (int64_t)n_hash, widen);
+            ln.pend_s0 = -1;
+        }
+    };
 
     for (size_t c = 0; c < chunks.size(); ++c) {
         Lane& ln = dc.lanes[c % kLanes];
@@ -302,19 +449,27 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         if (c >= (size_t)kLanes) {
             // the lane's previous chunk must have drained before its buffers are reused
             if ((rc = cuda_check(cudaEventSynchronize(ln.done), "lane sync"))) return rc;
+            drain(ln);
         }
         if ((rc = grow((void**)&ln.indptr, &ln.indptr_cap, (size_t)(rows + 1) * sizeof(int64_t)))) return rc;
         if ((rc = grow((void**)&ln.ids, &ln.ids_cap, (size_t)std::max<int64_t>(cnnz, 1) * sizeof(uint32_t))))
             return rc;
-        if ((rc = grow(&ln.out, &ln.out_cap, (size_t)rows * n_hash * out_bytes))) return rc;
+        const size_t dev_out_bytes = (size_t)rows * n_hash * (stage_out ? 4 : out_bytes);
+        if ((rc = grow(&ln.out, &ln.out_cap, dev_out_bytes))) return rc;
         const size_t wsb = mhb_sign_workspace_bytes(rows, cnnz, n_hash);
         if ((rc = grow(&ln.ws, &ln.ws_cap, wsb))) return rc;
 
         if ((rc = cuda_check(cudaMemcpyAsync(ln.indptr, indptr + s0, (size_t)(rows + 1) * sizeof(int64_t),
                                              cudaMemcpyHostToDevice, ln.stream), "H2D indptr")))
             return rc;
+        const uint32_t* id_src = ids + id0;
+        if (stage_in && cnnz > 0) {
+            if ((rc = grow_pinned((void**)&ln.stage_ids, &ln.stage_ids_cap, (size_t)cnnz * 4))) return rc;
+            host_copy_in(ids + id0, ln.stage_ids, cnnz);
+            id_src = ln.stage_ids;
+        }
         if (cnnz > 0 &&
-            (rc = cuda_check(cudaMemcpyAsync(ln.ids, ids + id0, (size_t)cnnz * sizeof(uint32_t),
+            (rc = cuda_check(cudaMemcpyAsync(ln.ids, id_src, (size_t)cnnz * sizeof(uint32_t),
                                              cudaMemcpyHostToDevice, ln.stream), "H2D ids")))
             return rc;
         // Rebase the chunk's offsets onto its own ids buffer (ids[0..cnnz) is what the kernels may read).
@@ -324,16 +479,25 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
             if ((rc = cuda_check(cudaGetLastError(), "rebase_indptr launch"))) return rc;
         }
         rc = launch_sign(kind, ln.indptr, ln.ids, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
-                         out_dtype, dc.status + c, ln.ws, ln.ws_cap, ln.stream);
+                         stage_out ? MHB_OUT_U32 : out_dtype, dc.status + c, ln.ws, ln.ws_cap, ln.stream);
         if (rc) return rc;
-        if ((rc = cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)s0 * n_hash * out_bytes, ln.out,
-                                             (size_t)rows * n_hash * out_bytes, cudaMemcpyDeviceToHost, ln.stream),
-                             "D2H out")))
+        if (stage_out) {
+            if ((rc = grow_pinned((void**)&ln.stage_out, &ln.stage_out_cap, dev_out_bytes))) return rc;
+            if ((rc = cuda_check(cudaMemcpyAsync(ln.stage_out, ln.out, dev_out_bytes, cudaMemcpyDeviceToHost,
+                                                 ln.stream), "D2H out (staged)")))
+                return rc;
+            ln.pend_s0 = s0;
+            ln.pend_rows = rows;
+        } else if ((rc = cuda_check(cudaMemcpyAsync(static_cast<char*>(out) + (size_t)s0 * n_hash * out_bytes, ln.out,
+                                                    dev_out_bytes, cudaMemcpyDeviceToHost, ln.stream),
+                                    "D2H out"))) {
             return rc;
+        }
         if ((rc = cuda_check(cudaEventRecord(ln.done, ln.stream), "event record"))) return rc;
     }
     for (int l = 0; l < kLanes && (size_t)l < chunks.size(); ++l) {
         if ((rc = cuda_check(cudaStreamSynchronize(dc.lanes[l].stream), "final sync"))) return rc;
+        drain(dc.lanes[l]);
     }
     std::vector<int32_t> st(chunks.size());
     if ((rc = cuda_check(cudaMemcpy(st.data(), dc.status, chunks.size() * sizeof(int32_t), cudaMemcpyDeviceToHost),
@@ -356,6 +520,8 @@ extern "C" void mhb_host_release(void) {
             cudaFree(ln.ids);
             cudaFree(ln.out);
             cudaFree(ln.ws);
+            if (ln.stage_ids) cudaFreeHost(ln.stage_ids);
+            if (ln.stage_out) cudaFreeHost(ln.stage_out);
             cudaEventDestroy(ln.done);
             cudaStreamDestroy(ln.stream);
             ln = Lane{};

@@ -15,15 +15,18 @@ ip, ids = gen.make_csr(cfg, device="cuda:0")
 fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
 ip_pin = torch.empty(ip.numel(), dtype=torch.int64, pin_memory=True)
 ids_pin = torch.empty(ids.numel(), dtype=torch.int32, pin_memory=True)
-out_pin = torch.empty((ip.numel() - 1, fam.size), dtype=torch.int32, pin_memory=True)
+DT = os.environ.get("E2E_DTYPE", "uint32")
+out_pin = torch.empty((ip.numel() - 1, fam.size), dtype=torch.int32 if DT == "uint32" else torch.int64,
+                      pin_memory=os.environ.get("E2E_PAGEABLE") != "1")
 ip_pin.copy_(ip)
 ids_pin.copy_(ids.view(torch.int32))
-a, b, o = ip_pin.numpy(), ids_pin.numpy().view(np.uint32), out_pin.numpy().view(np.uint32)
+a, b = ip_pin.numpy(), ids_pin.numpy().view(np.uint32)
+o = out_pin.numpy().view(np.uint32) if DT == "uint32" else out_pin.numpy()
 for _ in range(2):
-    signatures_csr(a, b, fam, out_dtype="uint32", out=o)
+    signatures_csr(a, b, fam, out_dtype=DT, out=o)
 t = []
 for _ in range(5):
     t0 = time.perf_counter()
-    signatures_csr(a, b, fam, out_dtype="uint32", out=o)
+    signatures_csr(a, b, fam, out_dtype=DT, out=o)
     t.append(time.perf_counter() - t0)
-print(os.environ.get("MHB_HOST_CHUNKS", "16"), "chunks:", round(statistics.mean(t) * 1e3, 2), "ms", round(min(t) * 1e3, 2))
+print(DT, os.environ.get("MHB_HOST_CHUNKS", "16"), "chunks:", round(statistics.mean(t) * 1e3, 2), "ms", round(min(t) * 1e3, 2))
