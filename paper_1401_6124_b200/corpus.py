@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes as C
 import re
 import sys
+import threading
 from fractions import Fraction
 from pathlib import Path
 from typing import NamedTuple
@@ -281,15 +282,16 @@ def _read_parallel(path, view: np.ndarray, n: int, parts: int = 8, min_part: int
         os.close(fd)
 
 
-_STAGING = []  # one pinned host buffer, grown on demand and reused (full-speed H2D of the text)
+_STAGING = threading.local()  # per-thread pinned host buffer, grown on demand (full-speed H2D of the text)
 
 
 def _staging(n: int) -> np.ndarray:
     import torch
 
-    if not _STAGING or _STAGING[0].numel() < n:
-        _STAGING[:] = [torch.empty(max(n, 1 << 20), dtype=torch.uint8, pin_memory=True)]
-    return _STAGING[0].numpy()[:n]
+    buf = getattr(_STAGING, "buf", None)
+    if buf is None or buf.numel() < n:
+        buf = _STAGING.buf = torch.empty(max(n, 1 << 20), dtype=torch.uint8, pin_memory=True)
+    return buf.numpy()[:n]
 
 
 def build_corpus(path) -> CorpusData:

@@ -10,6 +10,8 @@ reference's own readers).
 """
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -70,16 +72,19 @@ def format_text(sig, obj_ids=None, first_id: int = 0):
     return out
 
 
-_PINNED: dict = {}  # slot -> pinned uint8 host buffer, reused across calls
+_PINNED = threading.local()  # per thread: slot -> pinned uint8 host buffer, reused across calls
 
 
 def _pinned(slot: int, nbytes: int):
     import torch
 
-    buf = _PINNED.get(slot)
+    bufs = getattr(_PINNED, "bufs", None)
+    if bufs is None:
+        bufs = _PINNED.bufs = {}
+    buf = bufs.get(slot)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-        _PINNED[slot] = buf
+        bufs[slot] = buf
     return buf[:nbytes]
 
 
