@@ -691,9 +691,11 @@ def main():
         ip_h = indptr.cpu().numpy()
         ids_h = ids.cpu().numpy().view(np.uint32)
         v, n_s, nnz_s, dt = cpu_baseline_run(ip_h, ids_h, fam, args.cpu_seconds, threads)
+        v1, n1, _, dt1 = cpu_baseline_run(ip_h, ids_h, fam, min(3.0, args.cpu_seconds / 4), 1)
         cpu = {"value": v, "unit": "entries/s", "cores": threads, "kind": "port",
                "sample": f"first {n_s} of {n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
-                         f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets"}
+                         f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets",
+               "value_1core": v1, "sample_1core": f"first {n1} sets, {dt1:.1f} s, one thread"}
 
     if rank == 0:
         line = {
