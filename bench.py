@@ -457,46 +457,51 @@ def run_corpus(args):
                 os.unlink(f)
 
 
-def main():
-    args = _args()
-    if args.config == "corpus":
-        run_corpus(args)
-        return
-    if args.config == "c6":
-        run_c6(args)
-        return
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+class _Ctx:
+    """Process-group plumbing of one bench rank."""
 
-    from paper_1401_6124_b200 import _lib, gen, make_family, signatures_csr
-    from paper_1401_6124_b200.minhash import sign_csr_device
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # MHB_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- exercises the N>1 code
-    # path (barriers, max over ranks, peer gather) on a one-GPU box; its timings mean nothing
-    shared = os.environ.get("MHB_BENCH_SHARED_GPU") == "1"
-    if shared:
-        local = 0
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-    lib = _lib.load()
+        from paper_1401_6124_b200 import _lib
 
-    def max_over_ranks(x: float) -> float:
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # MHB_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- exercises the N>1 code
+        # path (barriers, max over ranks, peer gather) on a one-GPU box; its timings mean nothing
+        self.shared = os.environ.get("MHB_BENCH_SHARED_GPU") == "1"
+        if self.shared:
+            self.local = 0
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            if self.shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
+        self.lib = _lib.load()
+        self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.shared else self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+
+def _workload(args, ctx):
+    """This rank's batch of the configuration, generated on its GPU (outside any timing)."""
+    import torch
+
+    from paper_1401_6124_b200 import gen
 
     cfg = gen.CONFIGS[args.config]
     n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
@@ -506,30 +511,21 @@ def main():
     exact_j = None
     if cfg.name == "cfg3":
         # planted near-duplicate pairs: n_sets/2 base sets, each followed by its mutant
-        indptr, ids, exact_j = gen.planted_pairs(cfg, device=dev, n_base=n_sets // 2 if args.n_sets else None,
-                                                 seed=cfg.data_seed() + rank)
-        n_sets = indptr.numel() - 1
+        indptr, ids, exact_j = gen.planted_pairs(cfg, device=ctx.dev, n_base=n_sets // 2 if args.n_sets else None,
+                                                 seed=cfg.data_seed() + ctx.rank)
     else:
-        indptr, ids = gen.make_csr(cfg, device=dev, n_sets=n_sets, seed=cfg.data_seed() + rank)
+        indptr, ids = gen.make_csr(cfg, device=ctx.dev, n_sets=n_sets, seed=cfg.data_seed() + ctx.rank)
     torch.cuda.synchronize()
-    gen_s = time.perf_counter() - t0
-    nnz = int(ids.numel())
-    fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
-    N = fam.size
-    out = torch.empty((n_sets, N), dtype=torch.uint32, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    return cfg, indptr, ids, exact_j, time.perf_counter() - t0
 
-    def step():
-        sign_csr_device(indptr, ids, fam, out, status, stream)
 
-    # correctness guard on a few hundred sets (the full parity suite lives in tests/)
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
+def _guard(ctx, indptr, ids, fam, out, status):
+    """Status flags clean and a few hundred rows equal to the oracle (the parity suite is in tests/)."""
+    import numpy as np
+
     if int(status.item()) != 0:
         raise SystemExit(f"device status flags {int(status.item())}")
-    if rank == 0:
+    if ctx.rank == 0:
         from oracle import oracle
 
         k = 300
@@ -538,15 +534,25 @@ def main():
         if not np.array_equal(out[:k].cpu().numpy().astype(np.int64), want):
             raise SystemExit("bench guard: GPU signatures differ from the oracle")
 
-    clk = ClockSampler(local)
+
+def _timed_steps(args, ctx, step, stream):
+    """W warm-up steps, then K steps between a barrier + synchronize on both sides, timed
+    with CUDA events on the launch stream (main-kernel time from the library's per-launch
+    events) while nvidia-smi samples the clocks.  Returns (max-over-ranks ms, kernel ms, clocks)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1401_6124_b200 import _lib
+
+    clk = ClockSampler(ctx.local)
     clk.start()
     time.sleep(0.3)
     for _ in range(args.warmup):
         step()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
-    _lib.check(lib.mhb_profile_begin(args.steps))
+    _lib.check(ctx.lib.mhb_profile_begin(args.steps))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -554,91 +560,94 @@ def main():
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
+    kms, kn = C.c_float(0), C.c_int32(0)
+    _lib.check(ctx.lib.mhb_profile_end(C.byref(kms), C.byref(kn)))
+    clocks = clk.stop()
+    return ctx.max_over_ranks(e0.elapsed_time(e1)), kms.value / max(kn.value, 1), clocks
+
+
+def _gather_peer(args, ctx, indptr, ids, fam, out, status, stream):
+    """Fused sign + gather: every step signs straight into rank 0's [world*S, N] matrix."""
+    import torch
+
+    from paper_1401_6124_b200.dist import PeerMatrix
+    from paper_1401_6124_b200.minhash import sign_csr_to_ptr
+
+    n_sets, N = out.shape
+    owner = PeerMatrix.allocate(ctx.world * n_sets, N, 4, ctx.local) if ctx.rank == 0 else None
+    box = [owner.handle if owner is not None else None]
+    if ctx.world > 1:
+        ctx.dist.broadcast_object_list(box, src=0)
+    view = owner if ctx.rank == 0 else PeerMatrix.open(box[0], ctx.world * n_sets, N, 4, ctx.local)
+    dst_ptr = view.ptr(ctx.rank * n_sets)
+    for _ in range(args.warmup):
+        sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    pms = ctx.max_over_ranks(p0.elapsed_time(p1)) / args.steps
+    ctx.barrier()  # every rank's rows have landed
+    # each rank checks its rows of rank 0's matrix through its own mapping
+    mine = view.tensor()[ctx.rank * n_sets:(ctx.rank + 1) * n_sets]
+    if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
+        raise SystemExit(f"peer gather: rank {ctx.rank} rows in rank 0's matrix differ from its local signatures")
+    ctx.barrier()
+    if ctx.rank != 0:
+        view.close()
+    ctx.barrier()
+    if owner is not None:
+        owner.close()
+    return {"ms_per_step": pms, "entries_per_s": ctx.world * n_sets * N / (pms / 1e3),
+            "bytes_to_rank0_per_step": ctx.world * n_sets * N * 4,
+            "path": "mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC (csrc/peer.cu)"}
+
+
+def _gather_nccl(ctx, out):
+    import torch
+
+    from paper_1401_6124_b200.dist import gather_blocks
+
+    torch.cuda.synchronize()
+    ctx.barrier()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    g0.record()
+    gather_blocks(out, [out.shape[0]] * ctx.world)
+    g1.record()
+    torch.cuda.synchronize()
+    return g0.elapsed_time(g1)
+
+
+def _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, stream):
+    """Visits/s of the main kernel against the integer peak, the register-only
+    probe of the same visit sequence, and the HBM side with the ncu traffic per launch."""
     import ctypes as C
 
-    kms, kn = C.c_float(0), C.c_int32(0)
-    _lib.check(lib.mhb_profile_end(C.byref(kms), C.byref(kn)))
-    clocks = clk.stop()
-    elapsed_ms = e0.elapsed_time(e1)
-    max_ms = max_over_ranks(elapsed_ms)
-    ms_per_step = max_ms / args.steps
-    value = world * n_sets * N * args.steps / (max_ms / 1e3)
+    import torch
 
-    gather_ms = None
-    gather_peer = None
-    if args.gather == "peer":
-        # fused sign + gather: every step signs straight into rank 0's [world*S, N] matrix
-        from paper_1401_6124_b200.dist import PeerMatrix
-        from paper_1401_6124_b200.minhash import sign_csr_to_ptr
+    from paper_1401_6124_b200 import _lib
 
-        owner = PeerMatrix.allocate(world * n_sets, N, 4, local) if rank == 0 else None
-        box = [owner.handle if owner is not None else None]
-        if world > 1:
-            dist.broadcast_object_list(box, src=0)
-        view = owner if rank == 0 else PeerMatrix.open(box[0], world * n_sets, N, 4, local)
-        dst_ptr = view.ptr(rank * n_sets)
-        for _ in range(args.warmup):
-            sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        for _ in range(args.steps):
-            sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
-        p1.record(stream)
-        torch.cuda.synchronize()
-        pms_max = max_over_ranks(p0.elapsed_time(p1))
-        if world > 1:
-            dist.barrier()  # every rank's rows have landed
-        # each rank checks its rows of rank 0's matrix through its own mapping
-        mine = view.tensor()[rank * n_sets:(rank + 1) * n_sets]
-        if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
-            raise SystemExit(f"peer gather: rank {rank} rows in rank 0's matrix differ from its local signatures")
-        if world > 1:
-            dist.barrier()
-        if rank != 0:
-            view.close()
-        if world > 1:
-            dist.barrier()
-        if owner is not None:
-            owner.close()
-        pms = pms_max / args.steps
-        gather_peer = {"ms_per_step": pms, "entries_per_s": world * n_sets * N / (pms / 1e3),
-                       "bytes_to_rank0_per_step": world * n_sets * N * 4,
-                       "path": "mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC (csrc/peer.cu)"}
-    if world > 1 and args.gather == "nccl":
-        from paper_1401_6124_b200.dist import gather_blocks
-
-        torch.cuda.synchronize()
-        dist.barrier()
-        g0 = torch.cuda.Event(enable_timing=True)
-        g1 = torch.cuda.Event(enable_timing=True)
-        g0.record()
-        gather_blocks(out, [n_sets] * world)
-        g1.record()
-        torch.cuda.synchronize()
-        gather_ms = g0.elapsed_time(g1)
-
-    # ---- roofline of the main kernel ----
+    N = fam.size
     hbm_gbs, sm_max_mhz, peak_src = _peaks()
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    kernel_ms = kms.value / max(kn.value, 1)
-    visits = N * nnz
+    sms = torch.cuda.get_device_properties(ctx.dev).multi_processor_count
     k_instr = K_ITER if args.family == "iterative" else K_CW
     peak_visits = sms * 128 * sm_max_mhz * 1e6 / k_instr
-    achieved_visits = visits / (kernel_ms / 1e3)
+    achieved_visits = N * nnz / (kernel_ms / 1e3)
     alg_bytes = 4 * nnz + 8 * (n_sets + 1) + 4 * n_sets * N
     traffic, traffic_src = _ncu_traffic(args.config, args.family)
     probe_v, probe_ms = C.c_double(0), C.c_float(0)
     probe_kind = 0 if args.family == "iterative" else (2 if fam.prime <= (1 << 23) else 1)
-    _lib.check(lib.mhb_probe_visit_rate(1 << 20, probe_kind, C.byref(probe_v), C.byref(probe_ms),
-                                        stream.cuda_stream))
+    _lib.check(ctx.lib.mhb_probe_visit_rate(1 << 20, probe_kind, C.byref(probe_v), C.byref(probe_ms),
+                                            stream.cuda_stream))
     probe_rate = probe_v.value / (probe_ms.value / 1e3)
-    roofline = {
+    return {
         "bound": "int", "unit": "Gvisit/s",
         "achieved": achieved_visits / 1e9, "peak": peak_visits / 1e9, "frac": achieved_visits / peak_visits,
         "traffic": traffic,
@@ -654,52 +663,103 @@ def main():
                 "traffic_source": traffic_src},
     }
 
-    # ---- e2e through the public API with pinned host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        ip_pin = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
-        ids_pin = torch.empty(ids.shape, dtype=torch.int32, pin_memory=True)
-        out_pin = torch.empty((n_sets, N), dtype=torch.int32, pin_memory=True)
-        ip_pin.copy_(indptr)
-        ids_pin.copy_(ids.view(torch.int32))
-        ip_np, ids_np = ip_pin.numpy(), ids_pin.numpy().view(np.uint32)
-        out_np = out_pin.numpy().view(np.uint32)
-        signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)  # warm buffers
-        if world > 1:
-            dist.barrier()
-        times = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)
-            times.append(time.perf_counter() - t0)
-        if not np.array_equal(out_np[:1000], out[:1000].cpu().numpy()):
-            raise SystemExit("e2e output differs from the device path")
-        e2e_max = max_over_ranks(statistics.mean(times))
-        e2e = {"value": world * n_sets * N / e2e_max, "unit": "entries/s",
-               "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
-               "ms_per_step": e2e_max * 1e3,
-               "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 4 streams)",
-               "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
 
-    aux = None
-    if args.aux:
-        aux = _aux_kernels(cfg, fam, indptr, ids, out, exact_j, dev)
+def _e2e(args, ctx, indptr, ids, fam, out):
+    """The same metric through the public API from pinned host buffers: every step copies
+    the inputs H2D and the signatures D2H inside the timed region."""
+    import numpy as np
+    import torch
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        ip_h = indptr.cpu().numpy()
-        ids_h = ids.cpu().numpy().view(np.uint32)
-        v, n_s, nnz_s, dt = cpu_baseline_run(ip_h, ids_h, fam, args.cpu_seconds, threads)
-        v1, n1, _, dt1 = cpu_baseline_run(ip_h, ids_h, fam, min(3.0, args.cpu_seconds / 4), 1)
-        cpu = {"value": v, "unit": "entries/s", "cores": threads, "kind": "port",
-               "sample": f"first {n_s} of {n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
-                         f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets",
-               "value_1core": v1, "sample_1core": f"first {n1} sets, {dt1:.1f} s, one thread"}
+    from paper_1401_6124_b200 import signatures_csr
 
-    if rank == 0:
+    n_sets, N = out.shape
+    ip_pin = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
+    ids_pin = torch.empty(ids.shape, dtype=torch.int32, pin_memory=True)
+    out_pin = torch.empty((n_sets, N), dtype=torch.int32, pin_memory=True)
+    ip_pin.copy_(indptr)
+    ids_pin.copy_(ids.view(torch.int32))
+    ip_np, ids_np = ip_pin.numpy(), ids_pin.numpy().view(np.uint32)
+    out_np = out_pin.numpy().view(np.uint32)
+    signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)  # warm buffers
+    ctx.barrier()
+    times = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)
+        times.append(time.perf_counter() - t0)
+    if not np.array_equal(out_np[:1000], out[:1000].cpu().numpy()):
+        raise SystemExit("e2e output differs from the device path")
+    e2e_max = ctx.max_over_ranks(statistics.mean(times))
+    return {"value": ctx.world * n_sets * N / e2e_max, "unit": "entries/s",
+            "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
+            "ms_per_step": e2e_max * 1e3,
+            "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 4 streams)",
+            "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
+
+
+def _cpu_baseline(args, indptr, ids, fam, n_sets):
+    """The oracle port on all host cores (and on one) over a bounded prefix of the batch."""
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    ip_h = indptr.cpu().numpy()
+    ids_h = ids.cpu().numpy().view(np.uint32)
+    v, n_s, nnz_s, dt = cpu_baseline_run(ip_h, ids_h, fam, args.cpu_seconds, threads)
+    v1, n1, _, dt1 = cpu_baseline_run(ip_h, ids_h, fam, min(3.0, args.cpu_seconds / 4), 1)
+    return {"value": v, "unit": "entries/s", "cores": threads, "kind": "port",
+            "sample": f"first {n_s} of {n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
+                      f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets",
+            "value_1core": v1, "sample_1core": f"first {n1} sets, {dt1:.1f} s, one thread"}
+
+
+def main():
+    args = _args()
+    if args.config == "corpus":
+        run_corpus(args)
+        return
+    if args.config == "c6":
+        run_c6(args)
+        return
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    from paper_1401_6124_b200 import make_family
+    from paper_1401_6124_b200.minhash import sign_csr_device
+
+    ctx = _Ctx()
+    cfg, indptr, ids, exact_j, gen_s = _workload(args, ctx)
+    n_sets, nnz = indptr.numel() - 1, int(ids.numel())
+    fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
+    N = fam.size
+    out = torch.empty((n_sets, N), dtype=torch.uint32, device=ctx.dev)
+    status = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
+    stream = torch.cuda.current_stream(ctx.dev)
+
+    def step():  # one pass of the hot path over the resident batch
+        sign_csr_device(indptr, ids, fam, out, status, stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    _guard(ctx, indptr, ids, fam, out, status)
+
+    max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream)
+    ms_per_step = max_ms / args.steps
+    value = ctx.world * n_sets * N * args.steps / (max_ms / 1e3)
+
+    gather_peer = _gather_peer(args, ctx, indptr, ids, fam, out, status, stream) if args.gather == "peer" else None
+    gather_ms = _gather_nccl(ctx, out) if ctx.world > 1 and args.gather == "nccl" else None
+    roofline = _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, stream)
+    e2e = None if args.no_e2e else _e2e(args, ctx, indptr, ids, fam, out)
+    aux = _aux_kernels(cfg, fam, indptr, ids, out, exact_j, ctx.dev) if args.aux else None
+    cpu = (_cpu_baseline(args, indptr, ids, fam, n_sets)
+           if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None)
+
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": ctx.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: " + _workload_name(cfg, args.family), "n_sets_per_rank": n_sets,
@@ -707,7 +767,7 @@ def main():
                        "out": "uint32 argmin ids, resident in HBM",
                        "l2": "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per step vs 126 MB L2)"
                              % (4 * nnz / 1e9, 4 * n_sets * N / 1e9),
-                       "parallelism": f"dp{world} (row shards, no collective in the step)",
+                       "parallelism": f"dp{ctx.world} (row shards, no collective in the step)",
                        "gen_seconds": round(gen_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 5 * args.steps, "clocks": clocks,  # plan_count, plan_scan, plan_scatter, sign, finalize
@@ -719,8 +779,8 @@ def main():
         if aux is not None:
             line["aux"] = aux
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if ctx.world > 1:
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":
