@@ -641,7 +641,8 @@ def _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, strea
     peak_visits = sms * 128 * sm_max_mhz * 1e6 / k_instr
     achieved_visits = N * nnz / (kernel_ms / 1e3)
     alg_bytes = 4 * nnz + 8 * (n_sets + 1) + 4 * n_sets * N
-    traffic, traffic_src = _ncu_traffic(args.config, args.family)
+    # the committed capture is of the full-size configuration: no traffic figure for resized runs
+    traffic, traffic_src = _ncu_traffic(args.config, args.family) if args.n_sets is None else (None, None)
     probe_v, probe_ms = C.c_double(0), C.c_float(0)
     probe_kind = 0 if args.family == "iterative" else (2 if fam.prime <= (1 << 23) else 1)
     _lib.check(ctx.lib.mhb_probe_visit_rate(1 << 20, probe_kind, C.byref(probe_v), C.byref(probe_ms),
