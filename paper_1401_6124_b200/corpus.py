@@ -2,11 +2,19 @@
 
 Mirrors ``minhashlab.corpus`` (reference src/corpus.py:18-80): ``tokenize``,
 ``Vocabulary``, ``CorpusData``, ``build_corpus`` keep their names, arguments and
-results.  The work runs in libmhb's native multi-threaded ingest
-(csrc/corpus.cpp, ``mhb_corpus_*``): pure-ASCII lines are tokenized and interned
-there; lines holding non-ASCII bytes are tokenized here with the reference's Unicode
-rule (``[^\\W_]+`` over ``str.lower()``) and handed back, so the vocabulary order and
-the documents are exactly the reference's.
+results.  The work runs in libmhb behind one ``mhb_corpus_*`` handle API with two
+backends:
+
+* device (csrc/corpus_gpu.cu, the default when a GPU is visible): tokens, vocabulary
+  and documents are computed on the GPU; non-ASCII lines too, with this Python's own
+  ``str.isalnum`` / ``str.lower`` (and Final_Sigma) tables (``unicode_tables``), so
+  only lines with invalid UTF-8 come back here -- to raise the reference's
+  ``UnicodeDecodeError``;
+* host (csrc/corpus.cpp, multi-threaded): pure-ASCII segments natively, segments with
+  non-ASCII bytes (whole lines holding U+03A3) tokenized here with the reference's
+  rule (``[^\\W_]+`` over ``str.lower()``) and handed back.
+
+Either way the vocabulary order and the documents are exactly the reference's.
 
 ``build_corpus_csr`` returns the batch layout the signing path consumes
 (int64 indptr + uint32 ids); ``sign_corpus`` is the reference CLI's ``sign``
