@@ -2,11 +2,13 @@
 //
 // Same result as corpus.cpp and as the reference's build_corpus (src/corpus.py:67-80):
 // universal-newline lines, lowercase alphanumeric runs deduplicated per line,
-// vocabulary ids in first-occurrence order, documents as sorted id sets.  Lines with
-// a byte >= 0x80 are deferred exactly as in the host backend: their pure-ASCII
-// segments are tokenized here, the caller's Unicode tokenizer supplies the terms of
-// the other segments (mhb_corpus_set_terms), and both are spliced in at their line, so
-// every later step sees the tokens in document order.
+// vocabulary ids in first-occurrence order, documents as sorted id sets.  With the
+// caller's Unicode tables (mhb_unicode_tables: this Python's str.isalnum / str.lower and
+// the Cased / Case_Ignorable sets of its Final_Sigma rule), lines holding non-ASCII
+// bytes are tokenized here as well (uni_lines); only lines with invalid UTF-8 are
+// deferred, and without tables the non-ASCII segments are deferred as in the host
+// backend.  Deferred terms come back through mhb_corpus_set_terms and are spliced in
+// at their line, so every later step sees the tokens in document order.
 //
 // Pipeline (one private stream, CUB device primitives + the kernels below):
 //   scan    break positions (universal newlines) -> line [start, end); one warp per
