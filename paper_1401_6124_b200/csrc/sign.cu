@@ -458,7 +458,7 @@ __host__ __device__ constexpr int kLog2() { return K <= 1 ? 0 : 1 + kLog2<K / 2>
 // SKEW: the shared-memory epilogue table holds lane i at i + i/K.  With large G (lane
 // blocks of the warp's threads K apart, N >= 16*K) the 8 threads of an LDS.128 phase
 // would otherwise all hit one bank group (an 8-way conflict at G = 32).
-template <int K, typename OutT, bool EPI_SMEM, bool BANDS, bool SKEW = false>
+template <int K, typename OutT, bool EPI_SMEM, bool BANDS, bool SKEW, bool UNROLL>
 __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
                                            bool merge, int64_t i0, const InvTab* epi_s) {
     constexpr int NQ = K / 4;
@@ -467,6 +467,25 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
     const int32_t N = A.n_hash;
     const bool vec_ok = (N & 3) == 0;
     OutT* row = reinterpret_cast<OutT*>(A.out) + set * (int64_t)N;
+    if constexpr (EPI_SMEM && !BANDS) {
+        // Common case: the thread's whole lane block lies inside the row.  i0 is a
+        // multiple of K, so the skew is one offset for the block and every index is a
+        // 32-bit constant offset: no per-quad bounds or 64-bit index arithmetic.
+        const int j0 = (int)i0;
+        if (!merge && vec_ok && j0 + K <= N) {
+            const InvTab* t = epi_s + (SKEW ? j0 + j0 / K : j0);
+            OutT* r = row + j0;
+            // UNROLL (skewed and float-quotient kernels): +0.8..3%; the cfg2/cfg3 iterative
+            // and Shoup random kernels lose 0.4..1% to the register assignment it brings
+#pragma unroll(UNROLL ? 4 : 1)
+            for (int q = 0; q < NQ; ++q) {
+                const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
+                store4(r + 4 * q, invert_entry(t[4 * q], m.x, p), invert_entry(t[4 * q + 1], m.y, p),
+                       invert_entry(t[4 * q + 2], m.z, p), invert_entry(t[4 * q + 3], m.w, p));
+            }
+            return;
+        }
+    }
     unsigned long long hk = 0;  // running band hash (BANDS)
 #pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
@@ -643,8 +662,8 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
             const bool merge = (ec.meta >> 11) & 1;
             const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
             dump_best<K>(best, dump_row, lane);
-            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW>(A, dump_row, lane, set, merge, i0, epi_s);
-            else emit_lanes<K, OutT, false, BANDS, SKEW>(A, dump_row, lane, set, merge, i0, epi_s);
+            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, SKEW || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
+            else emit_lanes<K, OutT, false, BANDS, SKEW, SKEW || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
         }
 
         it = itn;
