@@ -391,17 +391,56 @@ __device__ __forceinline__ void walk1_random_fpq(uint32_t (&best)[K], const uint
 template <int K, bool ITER>
 struct LaneState {
     uint32_t tA, tAp, tB;
-    uint32_t negp;  // 2^32 - p (kernel parameter; random family only)
+    uint32_t negp;  // 2^32 - p (kernel parameter)
+    uint32_t one;   // opaque 1 (kernel parameter), see Spelling
     uint32_t cA[ITER ? 1 : K], cAp[ITER ? 1 : K], cB[ITER ? 1 : K];
 };
 
-template <int K, bool ITER, bool NARROW, bool FIRST, bool FPQ = false>
+// Per-instantiation spelling of the main loop.  The options are semantically identical;
+// they steer ptxas's register assignment, whose register-bank conflicts move the visit
+// rate by several percent.  Chosen per kernel with
+// tools/variant_search.py (static bank-conflict score of the loop) and confirmed with
+// tools/ab.sh on the B200; every other instantiation keeps the plain spelling.
+template <int K, bool ITER, bool NARROW, bool FPQ, bool SKEW, bool BANDS>
+struct Spelling {
+    static constexpr bool kIter64 = ITER && NARROW && K == 64 && !BANDS;  // cfg1-4 iterative kernels
+    // start hash: min(r, r - p, r - 2p) with both subtractions as IMADs by an opaque 1
+    // (FMA pipe; plain subtractions fold into two VIADDMNMX on the ALU pipe)
+    static constexpr bool start_fma = kIter64;
+    // round loop: the id maximum after the round, the features passed as (b, a)
+    static constexpr bool maxid_after = kIter64;
+    static constexpr bool swap_features = kIter64;
+    // id address as one IMAD.WIDE by an opaque 4 instead of IADD3 + LEA + LEA.HI.X
+    static constexpr bool addr_fma = kIter64 && !SKEW;
+    static constexpr int maxnreg = (kIter64 && !SKEW) || FPQ ? 120 : 128;
+};
+
+// Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
+template <int K, bool ITER>
+__device__ __forceinline__ uint32_t start_hash_fma(const LaneState<K, ITER>& ls, uint32_t x) {
+    const uint32_t q = __umulhi(ls.tAp, x);
+    const uint32_t r = ls.tA * x + ls.tB + q * ls.negp;
+    return __vimin3_u32(r, r * ls.one + ls.negp, r * ls.one + 2u * ls.negp);
+}
+
+// ids[base + j] (see Spelling::addr_fma).
+__device__ __forceinline__ uint32_t ld_id_fma(const uint32_t* base, uint32_t j, uint32_t four) {
+    const uint32_t* a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(j), "r"(four), "l"(base));
+    return __ldg(a);
+}
+
+template <int K, bool ITER, bool NARROW, bool FIRST, bool FPQ = false, bool START_FMA = false>
 __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa, uint32_t xb,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
         // NARROW (3p < 2^32): the start hashes reduce with one VIMNMX3 each
-        const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
-        const uint32_t hb = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xb, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
+        const uint32_t ha = START_FMA ? start_hash_fma(ls, xa)
+                            : NARROW  ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p)
+                                      : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        const uint32_t hb = START_FMA ? start_hash_fma(ls, xb)
+                            : NARROW  ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xb, p)
+                                      : mul_add_mod(ls.tA, ls.tAp, ls.tB, xb, p);
         walk2_iter<K, FIRST>(best, ha, reduce_once(xa + bpar, p), hb, reduce_once(xb + bpar, p), p);
     } else if constexpr (FPQ) {
         walk2_random_fpq<K, FIRST>(best, ls.cA, ls.cAp, ls.cB, xa, xb, p, ls.negp);
@@ -410,11 +449,13 @@ __device__ __forceinline__ void round2(uint32_t (&best)[K], const LaneState<K, I
     }
 }
 
-template <int K, bool ITER, bool NARROW, bool FPQ = false>
+template <int K, bool ITER, bool NARROW, bool FPQ = false, bool START_FMA = false>
 __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, ITER>& ls, uint32_t xa,
                                        uint32_t p, uint32_t bpar) {
     if constexpr (ITER) {
-        const uint32_t ha = NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p) : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
+        const uint32_t ha = START_FMA ? start_hash_fma(ls, xa)
+                            : NARROW  ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, xa, p)
+                                      : mul_add_mod(ls.tA, ls.tAp, ls.tB, xa, p);
         walk1_iter<K>(best, ha, reduce_once(xa + bpar, p), p);
     } else if constexpr (FPQ) {
         walk1_random_fpq<K>(best, ls.cA, ls.cAp, ls.cB, xa, p, ls.negp);
@@ -530,7 +571,9 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
 template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false>
-__global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {
+__global__ void __maxnreg__((Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>::maxnreg))  // 128: 2 CTAs of 256 per SM
+sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) {
+    using S = Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>;
     extern __shared__ uint4 smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -567,6 +610,8 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
 
     LaneState<K, ITER> ls;
     ls.negp = negp;
+    ls.one = one;
+    const uint32_t four = one << 2;
     int cur_sb = -1;
     uint32_t maxid = 0;
 
@@ -616,7 +661,7 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
         if (rounds == 1) {
             const uint32_t pa = __ldg(nbase), pb = __ldg(nbase + min(1, nlast));
             maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
+            round2<K, ITER, NARROW, true, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
             xa = pa; xb = pb;
         } else {
             uint32_t pa = __ldg(base + min(2, last)), pb = __ldg(base + min(3, last));  // round 1
@@ -629,30 +674,42 @@ __global__ void __launch_bounds__(kBlock, 2) sign_kernel(SignArgs A, uint32_t p,
                 qb = __ldg(nbase + min(1, nlast));
             }
             maxid = __vimax3_u32(maxid, xa, xb);
-            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
+            round2<K, ITER, NARROW, true, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
             xa = pa; xb = pb; pa = qa; pb = qb;
             int o = 6;
 #pragma unroll 1
             for (int r = 1; r + 2 < rounds; ++r, o += 2) {
-                qa = __ldg(base + min(o, last));  // smaller sets of the group clamp to their last id
-                qb = __ldg(base + min(o + 1, last));
-                maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
+                // smaller sets of the group clamp to their last id
+                if constexpr (S::addr_fma) {
+                    qa = ld_id_fma(base, min(o, last), four);
+                    qb = ld_id_fma(base, min(o + 1, last), four);
+                } else {
+                    qa = __ldg(base + min(o, last));
+                    qb = __ldg(base + min(o + 1, last));
+                }
+                if constexpr (S::maxid_after) {
+                    if constexpr (S::swap_features) round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xb, xa, p, bpar);
+                    else round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
+                    maxid = __vimax3_u32(maxid, xa, xb);
+                } else {
+                    maxid = __vimax3_u32(maxid, xa, xb);
+                    round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
+                }
                 xa = pa; xb = pb; pa = qa; pb = qb;
             }
             if (rounds > 2) {
                 qa = __ldg(nbase);
                 qb = __ldg(nbase + min(1, nlast));
                 maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
+                round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
                 xa = pa; xb = pb; pa = qa; pb = qb;
             }
             if (odd) {
                 maxid = max(maxid, xa);
-                round1<K, ITER, NARROW, FPQ>(best, ls, xa, p, bpar);
+                round1<K, ITER, NARROW, FPQ, S::start_fma>(best, ls, xa, p, bpar);
             } else {
                 maxid = __vimax3_u32(maxid, xa, xb);
-                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
+                round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
             }
             xa = pa; xb = pb;
         }
@@ -711,7 +768,7 @@ int g_prof_cap = 0, g_prof_n = 0, g_prof_dev = -1;
 cudaEvent_t* g_prof_ev = nullptr;
 }  // namespace
 
-using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t);
+using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t, uint32_t);
 
 template <bool ITER, bool NARROW, typename OutT>
 static SignKernelFn pick_kernel(int K) {
@@ -931,7 +988,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
     }
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p);
+    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p, 1u);
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
     rc = cuda_check(cudaGetLastError(), "sign_kernel launch");
     if (rc) return rc;
