@@ -1,16 +1,19 @@
-"""Search semantically equivalent spellings of the iterative main loop for a
-register assignment with fewer register-bank conflicts (build container, no GPU).
+"""Search the per-kernel loop spellings of csrc/sign.cu (`Spelling`) for register
+assignments with fewer register-bank conflicts (build container, no GPU).
 
 usage: python tools/variant_search.py [out_dir] [-j jobs]
 
-Every combination of the source transformations below is written as a copy of
-csrc/sign.cu, compiled to a cubin, and its cfg2 (K=64, no skew) and cfg4 (skewed)
-kernels' main loops are scored: instruction count and the number of extra distinct
-registers per bank (index mod 2) among the non-reused sources of each instruction
-(`bank_conflicts`).  On the committed loop that score separates the variants A/B'd so
-far: 68 for the committed loop; 99 for the opaque-operand variant,
-which ran 3.4% slower.  The best candidates then go to `tools/build_variant.sh` +
-`tools/ab.sh` on the GPU.
+The spellings are semantically identical; they only steer ptxas:
+start-hash subtractions on the FMA pipe, id max after the round, features passed as
+(b, a), IMAD.WIDE id addresses, and `__maxnreg__`.  Each combination is applied to
+every kernel (the `Spelling` body is replaced), compiled to a cubin, and each kernel's
+main loop is scored: instructions, ALU-pipe instructions, and bank conflicts — the
+extra distinct registers with the same index mod 2 among an instruction's sources not
+served by the reuse cache.  Kernels are separate instantiations, so the best row per
+column can be combined per kernel class in `Spelling`.  The score is a filter: time
+the candidates with tools/build_variant.sh + tools/ab.sh before committing one.
+
+The first row is the committed source.
 """
 import itertools
 import os
@@ -23,90 +26,26 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "paper_1401_6124_b200", "csrc")
 FN_CFG2 = "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb0EEEvNS_8SignArgsEjjj"
 FN_CFG4 = "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb1EEEvNS_8SignArgsEjjj"
-KERNELS = (("cfg2", FN_CFG2),  # also cfg1 / cfg3 iterative
-           ("cfg4", FN_CFG4),
-           ("cfg5", "_ZN3mhb11sign_kernelILi64ELb1ELb0EjLb0ELb0ELb0EEEvNS_8SignArgsEjjj"),
-           ("rfpq", "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb1ELb0EEEvNS_8SignArgsEjjj"),
-           ("rshoup", "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb0ELb0EEEvNS_8SignArgsEjjj"))
-
-WALK_MIN3 = ("            best[k] = __vimin3_u32(best[k], ha, hb);\n"
-             "            best[k + 1] = __vimin3_u32(best[k + 1], ga, gb);\n")
-LOOP_BODY = ("                qa = __ldg(base + min(o, last));  // smaller sets of the group clamp to their last id\n"
-             "                qb = __ldg(base + min(o + 1, last));\n"
-             "                maxid = __vimax3_u32(maxid, xa, xb);\n"
-             "                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);\n")
-BOUNDS = "__global__ void __launch_bounds__(kBlock, 2) sign_kernel("
+KERNELS = (("iter64", FN_CFG2),  # cfg1/2/3/5 iterative
+           ("skew", FN_CFG4),  # cfg4
+           ("rfpq", "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb1ELb0EEEvNS_8SignArgsEjjj"),  # cfg1/3 random
+           ("rshoup", "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb0ELb0EEEvNS_8SignArgsEjjj"))  # cfg2 random
+ALU_OPS = ("VIADDMNMX", "VIMNMX3", "VIMNMX", "IADD3", "LEA", "ISETP", "LOP3", "SEL", "SHF", "IMNMX", "PLOP3")
 
 
-def opaque_one(s):
-    """Kernel parameter `one` (= 1): an operand ptxas cannot constant-fold."""
-    s = s.replace("sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp) {",
-                  "sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) {")
-    s = s.replace("using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t);",
-                  "using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t, uint32_t);")
-    s = s.replace("fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p);",
-                  "fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p, 1u);")
-    s = s.replace("    LaneState<K, ITER> ls;\n    ls.negp = negp;",
-                  "    LaneState<K, ITER> ls;\n    ls.negp = negp;\n    ls.one = one;")
-    s = s.replace("    uint32_t negp;  // 2^32 - p (kernel parameter; random family only)",
-                  "    uint32_t negp;  // 2^32 - p (kernel parameter; random family only)\n    uint32_t one;")
-    return s
+def spelling_body(start, maxid_after, swap, addr, maxnreg):
+    return (f"    static constexpr bool kIter64 = ITER && NARROW && K == 64 && !BANDS;\n"
+            f"    static constexpr bool start_fma = ITER && NARROW && {str(bool(start)).lower()};\n"
+            f"    static constexpr bool maxid_after = {str(bool(maxid_after)).lower()};\n"
+            f"    static constexpr bool swap_features = {str(bool(swap)).lower()};\n"
+            f"    static constexpr bool addr_fma = {str(bool(addr)).lower()};\n"
+            f"    static constexpr int maxnreg = {maxnreg};")
 
 
-ADDR_HELPER = """
-__device__ __forceinline__ uint32_t ld_id(const uint32_t* base, uint32_t j, uint32_t four) {
-    const uint32_t* a;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(j), "r"(four), "l"(base));
-    return __ldg(a);
-}
-
-// Per-thread hashing state"""
-
-START_HELPER = """
-template <int K, bool ITER>
-__device__ __forceinline__ uint32_t start_hash_min3(const LaneState<K, ITER>& ls, uint32_t x) {
-    const uint32_t q = __umulhi(ls.tAp, x);
-    const uint32_t r = ls.tA * x + ls.tB + q * ls.negp;
-    return __vimin3_u32(r, r * ls.one + ls.negp, r * ls.one + 2u * ls.negp);
-}
-
-template <int K, bool ITER, bool NARROW, bool FIRST, bool FPQ = false>
-__device__ __forceinline__ void round2("""
-
-
-def transform(src, min3_order, loads_swapped, maxid_after, features_swapped, maxnreg, addr=0, start=0):
-    s = src
-    assert WALK_MIN3 in s and LOOP_BODY in s and BOUNDS in s
-    if addr or start:
-        s = opaque_one(s)
-    if addr:
-        s = s.replace("\n// Per-thread hashing state", ADDR_HELPER, 1)
-        s = s.replace("    const int F = A.F;\n    const int g = lane >> A.log2F;",
-                      "    const uint32_t four = one << 2;\n    const int F = A.F;\n    const int g = lane >> A.log2F;")
-    if start:
-        s = s.replace("\ntemplate <int K, bool ITER, bool NARROW, bool FIRST, bool FPQ = false>\n"
-                      "__device__ __forceinline__ void round2(", START_HELPER, 1)
-        for x in ("xa", "xb"):
-            s = s.replace(f"NARROW ? mul_add_mod_min3(ls.tA, ls.tAp, ls.tB, {x}, p)",
-                          f"NARROW ? start_hash_min3(ls, {x})")
-    if min3_order:
-        s = s.replace(WALK_MIN3, "            best[k] = __vimin3_u32(ha, hb, best[k]);\n"
-                                 "            best[k + 1] = __vimin3_u32(ga, gb, best[k + 1]);\n")
-    if addr:
-        la = "                qa = ld_id(base, min(o, last), four);\n"
-        lb = "                qb = ld_id(base, min(o + 1, last), four);\n"
-    else:
-        la = "                qa = __ldg(base + min(o, last));  // smaller sets of the group clamp to their last id\n"
-        lb = "                qb = __ldg(base + min(o + 1, last));\n"
-    mx = "                maxid = __vimax3_u32(maxid, xa, xb);\n"
-    rd = ("                round2<K, ITER, NARROW, false, FPQ>(best, ls, xb, xa, p, bpar);\n" if features_swapped
-          else "                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);\n")
-    loads = lb + la if loads_swapped else la + lb
-    body = loads + (rd + mx if maxid_after else mx + rd)
-    s = s.replace(LOOP_BODY, body)
-    if maxnreg:
-        s = s.replace(BOUNDS, f"__global__ void __maxnreg__({maxnreg}) sign_kernel(")
-    return s
+def transform(src, *flags):
+    m = re.search(r"struct Spelling \{\n(.*?)\n\};", src, re.S)
+    assert m, "Spelling struct not found"
+    return src[:m.start(1)] + spelling_body(*flags) + src[m.end(1):]
 
 
 def loop_instructions(sass, fn):
@@ -142,13 +81,14 @@ def bank_conflicts(ins, n_banks=2):
     return total
 
 
-ALU_OPS = ("VIADDMNMX", "VIMNMX3", "VIMNMX", "IADD3", "LEA", "ISETP", "LOP3", "SEL", "SHF", "IMNMX", "PLOP3")
-
-
 def alu_count(ins):
     """Instructions that issue to the ALU pipe (B300_MICROARCH.md: IADD3/LOP3/SHF/... on alu)."""
-    return sum(1 for t in ins if t.split()[0].lstrip("@!P0123456789").split(".")[0] in ALU_OPS
-               or (t.startswith("@") and t.split()[1].split(".")[0] in ALU_OPS))
+    n = 0
+    for t in ins:
+        words = t.split()
+        op = words[1] if words[0].startswith("@") else words[0]
+        n += op.split(".")[0] in ALU_OPS
+    return n
 
 
 def build_one(out_dir, name, text):
@@ -161,7 +101,7 @@ def build_one(out_dir, name, text):
         with open(path, "w") as f:
             f.write(text)
         subprocess.run(["nvcc", "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a",
-                       "--expt-relaxed-constexpr", f"-I{ROOT}/include", f"-I{SRC}", "-cubin", "-o", cubin, path],
+                        "--expt-relaxed-constexpr", f"-I{ROOT}/include", f"-I{SRC}", "-cubin", "-o", cubin, path],
                        check=True, capture_output=True)
     sass = subprocess.run(["cuobjdump", "-sass", cubin], check=True, capture_output=True, text=True).stdout
     res = {}
@@ -175,17 +115,15 @@ def main():
     out_dir = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "/tmp/variant_search"
     jobs = int(sys.argv[sys.argv.index("-j") + 1]) if "-j" in sys.argv else os.cpu_count()
     src = open(os.path.join(SRC, "sign.cu")).read()
-    combos = list(itertools.product([0, 1], [0, 1], [0, 1], [0, 1], [0, 120], [0, 1], [0, 1]))
-    tasks = []
-    for c in combos:
-        name = "v_" + "".join(str(int(bool(x))) for x in c[:4]) + f"_{c[4]}_" + f"{c[5]}{c[6]}"
-        tasks.append((name, transform(src, *c)))
+    tasks = [("committed", src)]
+    for c in itertools.product([0, 1], [0, 1], [0, 1], [0, 1], [128, 120]):
+        tasks.append(("s" + "".join(map(str, c[:4])) + f"_{c[4]}", transform(src, *c)))
     with ThreadPoolExecutor(jobs) as ex:
         results = list(ex.map(lambda t: build_one(out_dir, *t), tasks))
-    results.sort(key=lambda r: (r[1]["cfg2"][2], r[1]["cfg2"][1]))
-    print("variant          " + "".join(f"{k:>18s}" for k, _ in KERNELS) + "   (inst, ALU, bank conflicts)")
+    print("spelling: start_fma maxid_after swap_features addr_fma _maxnreg; (instructions, ALU, bank conflicts)")
+    print(f"{'variant':12s}" + "".join(f"{k:>18s}" for k, _ in KERNELS))
     for name, r in results:
-        print(f"{name:16s} " + "".join(f"{str(r[k]):>18s}" for k, _ in KERNELS))
+        print(f"{name:12s}" + "".join(f"{str(r[k]):>18s}" for k, _ in KERNELS))
 
 
 if __name__ == "__main__":
