@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -77,6 +78,15 @@ class Signature:
 
     def __len__(self) -> int:
         return int(self.mins.size)
+
+    @classmethod
+    def _wrap(cls, arr: np.ndarray, key: tuple) -> "Signature":
+        """A Signature around a fresh contiguous int64 array (no copy, no checks)."""
+        arr.setflags(write=False)
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "mins", arr)
+        object.__setattr__(obj, "family_key", key)
+        return obj
 
 
 def exact_jaccard(s1: FeatureSet, s2: FeatureSet) -> float:
@@ -293,11 +303,13 @@ def _signatures_csr_host(indptr, ids, family, out_dtype, out, device):
 def signature(s: FeatureSet, family: Family) -> Signature:
     """MinHash signature of one non-empty set (reference minhash.py:91-110): mins[i] is
     the feature id minimising h_i over s.  Runs the CUDA kernel on the current device."""
-    if len(s) == 0:
+    ids = s.ids
+    if ids.size == 0:
         raise ValueError("cannot build a signature for an empty feature set")
-    if s.max_id >= family.prime:
-        raise ValueError(f"feature id {s.max_id} >= family prime {family.prime}")
-    if s.max_id > MAX_ID:  # int64 ids beyond 2^32: the 64-bit-id device entry
+    max_id = int(ids[-1])  # canonical: sorted ascending
+    if max_id >= family.prime:
+        raise ValueError(f"feature id {max_id} >= family prime {family.prime}")
+    if max_id > MAX_ID:  # int64 ids beyond 2^32: the 64-bit-id device entry
         torch = _torch()
         dev = torch.device("cuda", torch.cuda.current_device())
         ip = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
@@ -307,30 +319,65 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     if isinstance(family, RandomFamily) and family.prime > MAX_KERNEL_PRIME:  # 64-bit a, b: device entry
         torch = _torch()
         dev = torch.device("cuda", torch.cuda.current_device())
-        ids = torch.from_numpy(s.ids.astype(np.uint32)).to(dev, non_blocking=False)
+        dids = torch.from_numpy(ids.astype(np.uint32)).to(dev, non_blocking=False)
         indptr = torch.tensor([0, len(s)], dtype=torch.int64, device=dev)
-        out = signatures_csr(indptr, ids, family, out_dtype="int64", validate=False)
+        out = signatures_csr(indptr, dids, family, out_dtype="int64", validate=False)
         return Signature(out[0].cpu().numpy(), family.key)
-    # host buffers -> mhb_sign_csr_host, whose small-batch path is one launch (csrc/host.cu);
-    # the FeatureSet is already canonical and checked above, so the call goes straight through
-    lib = _lib.load()
-    ids = s.ids.astype(np.uint32)
-    indptr = np.array([0, ids.size], dtype=np.int64)
-    out = np.empty((1, family.size), dtype=np.int64)
-    status = C.c_int32(0)
-    dev = _torch().cuda.current_device()
-    if isinstance(family, IterativeFamily):
-        rc = lib.mhb_sign_csr_host(_lib.KIND_ITERATIVE, indptr.ctypes.data, ids.ctypes.data, 1, ids.size,
-                                   family.base.a, family.base.b, None, None, family.prime, family.size,
-                                   out.ctypes.data, _lib.OUT_I64, C.addressof(status), dev)
-    else:
-        a, b = family.host_params()
-        rc = lib.mhb_sign_csr_host(_lib.KIND_RANDOM, indptr.ctypes.data, ids.ctypes.data, 1, ids.size, 0, 0,
-                                   a.ctypes.data, b.ctypes.data, family.prime, family.size, out.ctypes.data,
-                                   _lib.OUT_I64, C.addressof(status), dev)
-    _lib.check(rc)
-    _raise_status(status.value, family)
-    return Signature(out[0], family.key)
+    # host buffers -> mhb_sign_csr_host, whose small-batch path is served by the resident
+    # doorbell block (csrc/host.cu); the FeatureSet is already canonical and checked above,
+    # so the call goes straight through, staged in this thread's reusable buffers
+    st = _PERSET
+    n = int(ids.size)
+    if n > st.ids.size or family.size > st.out.size:
+        st.grow(n, family.size)
+    np.copyto(st.ids[:n], ids, casting="unsafe")
+    st.indptr[1] = n
+    kind, a, b, a_ptr, b_ptr = _percall_params(family)
+    rc = _lib.load().mhb_sign_csr_host(kind, st.indptr_ptr, st.ids_ptr, 1, n, a, b, a_ptr, b_ptr, family.prime,
+                                       family.size, st.out_ptr, _lib.OUT_I64, st.status_ptr, -1)
+    if rc:
+        _lib.check(rc)
+    if st.status.value:
+        _raise_status(st.status.value, family)
+    return Signature._wrap(st.out[:family.size].copy(), family.key)
+
+
+class _PerSetStage(threading.local):
+    """Per-thread reusable host buffers of the per-set API, their addresses taken once
+    (numpy's .ctypes costs more than the GPU round trip of a small set)."""
+
+    def __init__(self):
+        self.indptr = np.zeros(2, dtype=np.int64)
+        self.indptr_ptr = self.indptr.ctypes.data
+        self.status = C.c_int32(0)
+        self.status_ptr = C.addressof(self.status)
+        self.ids = np.empty(0, dtype=np.uint32)
+        self.out = np.empty(0, dtype=np.int64)
+        self.ids_ptr = self.out_ptr = 0
+
+    def grow(self, n: int, n_hash: int) -> None:
+        if n > self.ids.size:
+            self.ids = np.empty(max(n, 4096), dtype=np.uint32)
+            self.ids_ptr = self.ids.ctypes.data
+        if n_hash > self.out.size:
+            self.out = np.empty(max(n_hash, 1024), dtype=np.int64)
+            self.out_ptr = self.out.ctypes.data
+
+
+_PERSET = _PerSetStage()
+
+
+def _percall_params(family: Family) -> tuple:
+    """(kind, a, b, a_host_ptr, b_host_ptr) of mhb_sign_csr_host for this family, built once."""
+    hit = family.__dict__.get("_percall")
+    if hit is None:
+        if isinstance(family, IterativeFamily):
+            hit = (_lib.KIND_ITERATIVE, family.base.a, family.base.b, None, None)
+        else:
+            a, b = family.host_params()  # cached on the family: the pointers stay valid
+            hit = (_lib.KIND_RANDOM, 0, 0, a.ctypes.data, b.ctypes.data)
+        family.__dict__["_percall"] = hit
+    return hit
 
 
 def signatures(sets, family: Family) -> list[Signature]:

@@ -1,0 +1,132 @@
+"""GPU: the doorbell server behind the per-set API (csrc/host.cu, doorbell_kernel).
+
+signature(FeatureSet, family) -- the reference's per-set call (minhash.py:91-110) --
+is served by one resident block that polls a request word in mapped host memory.
+These tests cover its protocol rather than the arithmetic (the small-batch parity
+tests in test_gpu_parity.py run through it too): relaunch after the idle exit,
+concurrent callers, interleaving with the chunked pipeline and device-wide syncs,
+release while running, and equality with the launched small kernel
+(MHB_DOORBELL=0) in a fresh process.  Bar: bit-exact against the oracle.
+"""
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1401_6124_b200 import FeatureSet, make_family, signature, signatures_csr
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _sets(seed, n, lo=1, hi=300, p=1_048_583):
+    rng = np.random.default_rng(seed)
+    return [FeatureSet(rng.integers(0, p, size=int(rng.integers(lo, hi)))) for _ in range(n)]
+
+
+def _want(sets, fam):
+    ip = np.zeros(len(sets) + 1, dtype=np.int64)
+    ip[1:] = np.cumsum([len(s) for s in sets])
+    ids = np.concatenate([s.ids for s in sets]).astype(np.uint32)
+    return oracle.sign_family_csr(ip, ids, fam)
+
+
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_per_set_calls_and_relaunch_after_idle(cuda_device, kind):
+    fam = make_family(kind, 11, 128, 1_048_583)
+    sets = _sets(1, 60)
+    want = _want(sets, fam)
+    for k, s in enumerate(sets):
+        if k % 15 == 14:
+            time.sleep(0.005)  # > the 1 ms idle exit: the next call relaunches the server
+        assert np.array_equal(signature(s, fam).mins, want[k]), k
+
+
+def test_concurrent_callers(cuda_device):
+    import torch
+
+    fam = make_family("iterative", 5, 200, 16_777_259)
+    sets = _sets(2, 200, p=16_777_259)
+    want = _want(sets, fam)
+    got = [None] * len(sets)
+    errors = []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(cuda_device)
+            for k in range(t, len(sets), 4):
+                got[k] = signature(sets[k], fam).mins
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for k in range(len(sets)):
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_interleaved_with_batches_and_device_syncs(cuda_device):
+    import torch
+
+    from paper_1401_6124_b200 import gen
+
+    fam = make_family("iterative", 9, 128, 1_048_583)
+    indptr, ids = gen.cfg1_numpy(n_sets=3000, seed=4)
+    want_batch = oracle.sign_family_csr(indptr, ids, fam)
+    sets = _sets(3, 20)
+    want = _want(sets, fam)
+    for k, s in enumerate(sets):
+        assert np.array_equal(signature(s, fam).mins, want[k])
+        if k % 5 == 0:
+            t0 = time.perf_counter()
+            torch.cuda.synchronize()  # waits for the server's idle exit (<= 1 ms + slack)
+            assert time.perf_counter() - t0 < 1.0
+        if k % 7 == 0:
+            got = signatures_csr(indptr, ids, fam, out_dtype="int64")  # chunked host pipeline
+            assert np.array_equal(got, want_batch)
+
+
+def test_release_while_running(cuda_device):
+    from paper_1401_6124_b200 import _lib
+
+    fam = make_family("random", 2, 64, 1_048_583)
+    sets = _sets(4, 6)
+    want = _want(sets, fam)
+    for k, s in enumerate(sets):
+        assert np.array_equal(signature(s, fam).mins, want[k])
+        _lib.load().mhb_host_release()  # stops the resident block; the next call starts over
+
+
+_CHILD = r"""
+import numpy as np
+from paper_1401_6124_b200 import FeatureSet, make_family, signature
+rng = np.random.default_rng(8)
+out = []
+for kind, p in (("iterative", 1_048_583), ("random", 16_777_259), ("iterative", 4_294_967_291)):
+    fam = make_family(kind, 3, 96, p)
+    for _ in range(40):
+        s = FeatureSet(rng.integers(0, p, size=int(rng.integers(1, 500))))
+        out.append(signature(s, fam).mins)
+np.save(__import__("sys").argv[1], np.concatenate(out))
+"""
+
+
+def test_doorbell_equals_launched_kernel(cuda_device, tmp_path):
+    res = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, MHB_DOORBELL=mode, MHB_DOORBELL_IDLE_US="50",
+                   PYTHONPATH=str(ROOT) + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        f = tmp_path / f"m{mode}.npy"
+        subprocess.run([sys.executable, "-c", _CHILD, str(f)], check=True, env=env, cwd=ROOT, timeout=300)
+        res[mode] = np.load(f)
+    assert np.array_equal(res["0"], res["1"])
