@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <chrono>
 #include <atomic>
 #include <condition_variable>
@@ -147,27 +150,83 @@ int grow_pinned(void** ptr, size_t* cap, size_t need) {
     return MHB_OK;
 }
 
+// Non-temporal (streaming) stores for the staging copies: the destination is written
+// once and not read back by this CPU (a DMA source, or the caller's result), so the
+// stores skip the read-for-ownership of every destination line.  SSE2 is baseline
+// x86-64.  MHB_HOST_NT=0 uses plain stores (A/B: tools/e2e_chunks.py).
+bool host_nt() {
+    static const bool on = [] {
+        const char* e = std::getenv("MHB_HOST_NT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// dst[i] = src[i] (widen: as int64) for i in [0, n), streaming stores once dst is 16-byte aligned.
+void copy_span(const uint32_t* src, void* dst_v, int64_t n, bool widen, bool nt) {
+    int64_t i = 0;
+#if defined(__SSE2__)
+    if (nt) {
+        if (widen) {
+            long long* d = static_cast<long long*>(dst_v);
+            for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = (long long)src[i];
+            const __m128i z = _mm_setzero_si128();
+            for (; i + 4 <= n; i += 4) {
+                const __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), _mm_unpacklo_epi32(v, z));
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 2), _mm_unpackhi_epi32(v, z));
+            }
+            for (; i < n; ++i) d[i] = (long long)src[i];
+        } else {
+            uint32_t* d = static_cast<uint32_t*>(dst_v);
+            for (; i < n && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) d[i] = src[i];
+            for (; i + 8 <= n; i += 8) {
+                const __m128i v0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+                const __m128i v1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 4));
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), v0);
+                _mm_stream_si128(reinterpret_cast<__m128i*>(d + i + 4), v1);
+            }
+            for (; i < n; ++i) d[i] = src[i];
+        }
+        _mm_sfence();  // order the streaming stores before the pool's completion signal
+        return;
+    }
+#endif
+    if (widen) {
+        long long* d = static_cast<long long*>(dst_v);
+        for (; i < n; ++i) d[i] = (long long)src[i];
+    } else {
+        std::memcpy(dst_v, src, (size_t)n * 4);
+    }
+}
+
+bool direct_i64() {
+    static const bool on = [] {
+        const char* e = std::getenv("MHB_DIRECT_I64");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // Parallel copy (u32 -> u32, or u32 -> int64 widening) of `n` elements.
 void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen) {
     HostPool& pool = host_pool();
     const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n >> 18));
+    const bool nt = host_nt();
     pool.run(parts, [&](int k) {
         const int64_t lo = n * k / parts, hi = n * (k + 1) / parts;
-        if (widen) {
-            long long* d = static_cast<long long*>(dst);
-            for (int64_t i = lo; i < hi; ++i) d[i] = (long long)src[i];
-        } else {
-            std::memcpy(static_cast<uint32_t*>(dst) + lo, src + lo, (size_t)(hi - lo) * 4);
-        }
+        char* d = static_cast<char*>(dst) + (size_t)lo * (widen ? 8 : 4);
+        copy_span(src + lo, d, hi - lo, widen, nt);
     });
 }
 
 void host_copy_in(const uint32_t* src, uint32_t* dst, int64_t n) {
     HostPool& pool = host_pool();
     const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n >> 18));
+    const bool nt = host_nt();
     pool.run(parts, [&](int k) {
         const int64_t lo = n * k / parts, hi = n * (k + 1) / parts;
-        std::memcpy(dst + lo, src + lo, (size_t)(hi - lo) * 4);
+        copy_span(src + lo, dst + lo, hi - lo, false, nt);
     });
 }
 
@@ -751,9 +810,10 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     // lands in a pinned lane buffer, and the pool copies (or widens to int64: half the
     // PCIe bytes) into the caller's array once the lane drains -- overlapped with the
     // transfers of the other lanes.  Pinned output keeps the direct D2H.
-    // (pinned int64 output keeps the direct int64 D2H: widening 2x the bytes on the host
-    // is no faster than the DMA writing them)
-    const bool stage_out = !is_pinned(out);
+    // Pinned int64 output is staged the same way: uint32 over PCIe plus a streaming-store
+    // widening on the host beats the DMA writing twice the bytes (37 vs 42 ms on cfg2;
+    // MHB_DIRECT_I64=1 keeps the direct int64 D2H).
+    const bool stage_out = !is_pinned(out) || (out_dtype == MHB_OUT_I64 && !direct_i64());
     const bool widen = stage_out && out_dtype == MHB_OUT_I64;
     const bool stage_in = nnz > 0 && !is_pinned(ids);
     auto drain = [&](Lane& ln) {

@@ -13,8 +13,9 @@ from paper_1401_6124_b200 import gen, make_family, signatures_csr  # noqa: E402
 cfg = gen.CONFIGS["cfg2"]
 ip, ids = gen.make_csr(cfg, device="cuda:0")
 fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
-ip_pin = torch.empty(ip.numel(), dtype=torch.int64, pin_memory=True)
-ids_pin = torch.empty(ids.numel(), dtype=torch.int32, pin_memory=True)
+pin_in = os.environ.get("E2E_PAGEABLE_IN") != "1"
+ip_pin = torch.empty(ip.numel(), dtype=torch.int64, pin_memory=pin_in)
+ids_pin = torch.empty(ids.numel(), dtype=torch.int32, pin_memory=pin_in)
 DT = os.environ.get("E2E_DTYPE", "uint32")
 out_pin = torch.empty((ip.numel() - 1, fam.size), dtype=torch.int32 if DT == "uint32" else torch.int64,
                       pin_memory=os.environ.get("E2E_PAGEABLE") != "1")
@@ -29,4 +30,5 @@ for _ in range(5):
     t0 = time.perf_counter()
     signatures_csr(a, b, fam, out_dtype=DT, out=o)
     t.append(time.perf_counter() - t0)
-print(DT, os.environ.get("MHB_HOST_CHUNKS", "16"), "chunks:", round(statistics.mean(t) * 1e3, 2), "ms", round(min(t) * 1e3, 2))
+print(DT, "in", "pinned" if pin_in else "pageable", "out", "pageable" if os.environ.get("E2E_PAGEABLE") == "1" else "pinned",
+      "nt", os.environ.get("MHB_HOST_NT", "1"), os.environ.get("MHB_HOST_CHUNKS", "16"), "chunks:", round(statistics.mean(t) * 1e3, 2), "ms", round(min(t) * 1e3, 2))
