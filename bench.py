@@ -290,25 +290,33 @@ def run_c6(args):
     res = {}
     dev_out = torch.empty((n_sets, n_hash), dtype=torch.int64, device=dev)
     host_out = torch.empty((n_sets, n_hash), dtype=torch.int64, pin_memory=True)  # reused, like a caller's buffer
+    out = host_out.numpy()
+    ids32 = ids.astype(np.uint32)
     for kind in ("random", "iterative"):
         for r in range(args.warmup):
             fam = make_family(kind, derive_seed(seed, 1000 + r), n_hash, prime)
-            host_out.copy_(signatures_csr(ip, di, fam, out_dtype="int64", out=dev_out))
+            signatures_csr(indptr, ids32, fam, out_dtype="int64", out=out)
+            signatures_csr(ip, di, fam, out_dtype="int64", out=dev_out)
         times, kernel = [], []
         for r in range(args.steps):
+            # the repetition as the reference's run_timing times it: numpy in, int64 numpy out
+            # (mhb_sign_csr_host: chunks signed, copied D2H as uint32 and widened on the host,
+            # overlapped)
+            t0 = time.perf_counter()
+            fam = make_family(kind, derive_seed(seed, r), n_hash, prime)
+            signatures_csr(indptr, ids32, fam, out_dtype="int64", out=out)
+            times.append(time.perf_counter() - t0)
+            # family + device signing alone (device-resident inputs and output)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             fam = make_family(kind, derive_seed(seed, r), n_hash, prime)
             signatures_csr(ip, di, fam, out_dtype="int64", out=dev_out)
-            t1 = time.perf_counter()
-            host_out.copy_(dev_out)
-            times.append(time.perf_counter() - t0)
-            kernel.append(t1 - t0)
-        out = host_out.numpy()
+            torch.cuda.synchronize()
+            kernel.append(time.perf_counter() - t0)
         res[kind] = {"rep_seconds_mean": statistics.mean(times), "rep_seconds_std": statistics.pstdev(times),
                      "entries_per_s": n_sets * n_hash / statistics.mean(times),
                      "family_plus_sign_seconds_mean": statistics.mean(kernel),
-                     "d2h_bytes": n_sets * n_hash * 8}
+                     "d2h_bytes": n_sets * n_hash * 4, "path": "signatures_csr(numpy) -> mhb_sign_csr_host"}
         if kind == "iterative":
             from oracle import oracle
 
