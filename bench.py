@@ -158,14 +158,16 @@ def run_reference(args):
     cfg = gen.CONFIGS[args.config]
     fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
     threads = os.cpu_count() or 1
-    # bounded sample of the same workload (same generator and distributions), sized to ~3 s per step
+    # bounded sample of the same workload (same generator and distributions)
     n_sample = 4000
     ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_sample)
     ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
     t0 = time.perf_counter()
     oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
     dt = time.perf_counter() - t0
-    n_step = int(max(1000, min(200_000, n_sample * 3.0 / max(dt, 1e-6))))
+    # per step about 3 s, less when K + W steps would exceed ~90 s in total
+    step_target = min(3.0, 90.0 / max(1, args.steps + args.warmup))
+    n_step = int(max(1000, min(200_000, n_sample * step_target / max(dt, 1e-6))))
     if n_step > n_sample:
         ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_step)
         ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
