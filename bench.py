@@ -53,6 +53,9 @@ def _args():
                          "torch.distributed.gather) or 'peer' (fused: kernels store into rank 0's matrix "
                          "over CUDA IPC / NVLink)")
     ap.add_argument("--corpus-lines", type=int, default=400_000, help="--config corpus: text lines")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as one CUDA graph (plan + sign + finalize launches captured once): "
+                         "value and ms_per_step from the replays; the eager pass still gives the kernel time")
     ap.add_argument("--aux", action="store_true",
                     help="also time the pairwise-Jaccard and bucket-histogram kernels (cfg3: planted pairs)")
     return ap.parse_args()
@@ -577,6 +580,41 @@ def _timed_steps(args, ctx, step, stream):
     return ctx.max_over_ranks(e0.elapsed_time(e1)), kms.value / max(kn.value, 1), clocks
 
 
+def _timed_graph(args, ctx, indptr, ids, fam, out, status):
+    """The step captured once as a CUDA graph and replayed K times (after W replays),
+    timed like _timed_steps.  For launch-bound batches (cfg1) the five launches of a
+    step cost more than their kernels."""
+    import torch
+
+    from paper_1401_6124_b200.minhash import sign_csr_device
+
+    def step():
+        sign_csr_device(indptr, ids, fam, out, status, torch.cuda.current_stream())
+
+    side = torch.cuda.Stream(ctx.dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()  # workspace allocations outside the capture
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        graph.replay()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        graph.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    return ctx.max_over_ranks(e0.elapsed_time(e1))
+
+
 def _gather_peer(args, ctx, indptr, ids, fam, out, status, stream):
     """Fused sign + gather: every step signs straight into rank 0's [world*S, N] matrix."""
     import torch
@@ -757,6 +795,12 @@ def main():
     _guard(ctx, indptr, ids, fam, out, status)
 
     max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream)
+    eager_ms = None
+    if args.graph:
+        eager_ms = max_ms / args.steps
+        out.view(torch.int32).zero_()
+        max_ms = _timed_graph(args, ctx, indptr, ids, fam, out, status)
+        _guard(ctx, indptr, ids, fam, out, status)  # the replays produced the signatures
     ms_per_step = max_ms / args.steps
     value = ctx.world * n_sets * N * args.steps / (max_ms / 1e3)
 
@@ -783,6 +827,9 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 5 * args.steps, "clocks": clocks,  # plan_count, plan_scan, plan_scatter, sign, finalize
         }
+        if eager_ms is not None:
+            line["graph"] = {"replayed": True, "eager_ms_per_step": eager_ms,
+                             "launches_per_replay": 5}
         if gather_ms is not None:
             line["gather_ms"] = gather_ms
         if gather_peer is not None:
