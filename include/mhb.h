@@ -143,8 +143,9 @@ int mhb_sign_csr_ids64(int32_t kind, const int64_t* indptr, const uint64_t* ids,
  * HOST pointers (page-locked for full copy bandwidth; pageable also works).  The
  * library stages chunks through its own device buffers on `device` with copy/
  * compute overlap, and returns when out is complete.  kind: 0 iterative, 1 random
- * (a_host/b_host used for random, a/b scalars for iterative).  device -1: the calling
- * thread's current CUDA device.
+ * (a_host/b_host used for random, a/b scalars for iterative; a_host/b_host may also be
+ * device arrays -- UVA tells them apart -- and are then used in place).  device -1: the
+ * calling thread's current CUDA device.
  * Small batches (<= 64 sets, the per-set reference call) take no launch: a resident
  * block polling mapped host memory serves them (the "doorbell"; it exits after
  * MHB_DOORBELL_IDLE_US, default 1000, of no requests; MHB_DOORBELL=0 launches a

@@ -138,6 +138,15 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
 int grow_pinned(void** ptr, size_t* cap, size_t need) {
     if (*cap >= need && *ptr) return MHB_OK;
     if (*ptr) cudaFreeHost(*ptr);
@@ -231,20 +240,29 @@ void host_copy_in(const uint32_t* src, uint32_t* dst, int64_t n) {
 }
 
 // Small batches (the per-set reference API: signature() on one FeatureSet) skip the
-// chunk pipeline: inputs are staged in mapped pinned memory, one kernel launch reads
-// them over PCIe (ids once into shared memory), computes every (set, hash) argmin
-// exactly in 64-bit arithmetic and writes the result back into mapped memory.
+// chunk pipeline.  Inputs are staged in mapped pinned memory and read over PCIe (ids
+// once into shared memory); every (set, hash) argmin is computed exactly and written
+// straight into mapped memory: the caller's own buffer when it is page-locked, else a
+// mapped stage copied out on the host.  Light requests go to the resident doorbell
+// block (no launch); heavier ones (the reference's C6 timing loop: one set, 100,000
+// hashes per call) to one launch of sign_small_kernel over (hash slice, set) blocks.
 constexpr int64_t kSmallSets = 64;
 constexpr int64_t kSmallNnz = 1 << 16;
-constexpr int64_t kSmallSetMax = 8192;  // ids of one set in shared memory
-constexpr int32_t kSmallHash = 16384;
+constexpr int64_t kSmallSetMax = 8192;     // ids of one set in shared memory
+constexpr int64_t kSmallEntries = 1 << 21;  // n_sets * n_hash (16 MB of int64 output)
+constexpr int32_t kSmallSliceHashes = 256;  // hashes per block of sign_small_kernel
+constexpr int64_t kSmallStatus = kSmallEntries / kSmallSliceHashes + kSmallSets;  // >= its blocks
 
 struct Doorbell;
 
 struct SmallStage {
-    char* in = nullptr;    // indptr | ids | a | b   (mapped pinned)
-    char* out = nullptr;   // [sets, hashes] u32 / i64 (mapped pinned)
-    int32_t* status = nullptr;
+    char* in = nullptr;    // indptr | ids | a | b   (mapped pinned, grown on demand)
+    size_t in_cap = 0;
+    char* out = nullptr;   // [sets, hashes] u32 / i64 (mapped pinned, grown on demand)
+    size_t out_cap = 0;
+    int32_t* status = nullptr;  // kSmallStatus words (mapped pinned): one per block of sign_small_kernel
+    void* dev = nullptr;        // device stage of wide launched batches: request | output | status
+    size_t dev_cap = 0;
     Doorbell* db = nullptr;          // mapped pinned control block of the doorbell server
     char* req = nullptr;             // mapped pinned packed request (kDoorbellBytes)
     cudaStream_t db_stream = nullptr;  // the server's own non-blocking stream
@@ -308,17 +326,18 @@ __device__ __forceinline__ uint64_t mul_add_mod64(uint64_t A, uint64_t B, uint32
 // (any address space).  Returns this thread's status flags.
 __device__ __forceinline__ int small_set_hashes(const uint32_t* xs, int n, int kind, uint64_t a, uint64_t b,
                                                 const uint32_t* ra, const uint32_t* rb, uint64_t p, int32_t n_hash,
-                                                void* out, int32_t out_dtype, int64_t set) {
+                                                int32_t i_begin, int32_t i_end, void* out, int32_t out_dtype,
+                                                int64_t set) {
     const int T = blockDim.x;  // a multiple of 32
     int S = 1;
-    while (S < 32 && 2 * S * n_hash <= T && 2 * S <= n) S *= 2;
+    while (S < 32 && 2 * S * (i_end - i_begin) <= T && 2 * S <= n) S *= 2;
     const int per_round = T / S, slice = threadIdx.x % S;
     const double inv_p = 1.0 / (double)p;
     int flags = 0;
-    for (int i0 = 0; i0 < n_hash; i0 += per_round) {  // uniform trip count: whole warps shuffle below
+    for (int i0 = i_begin; i0 < i_end; i0 += per_round) {  // uniform trip count: whole warps shuffle below
         const int i = i0 + threadIdx.x / S;
         unsigned long long key = ~0ull;
-        if (i < n_hash) {
+        if (i < i_end) {
             uint64_t A, B;
             if (kind == KIND_ITERATIVE) {  // h_i(x) = ((a + i) x + i b) mod p, families.py:170-176
                 A = a + (uint64_t)i;
@@ -363,7 +382,7 @@ __device__ __forceinline__ int small_set_hashes(const uint32_t* xs, int n, int k
             const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
             key = other < key ? other : key;
         }
-        if (i < n_hash && slice == 0) {
+        if (i < i_end && slice == 0) {
             const uint32_t arg = (uint32_t)key;
             if (out_dtype == MHB_OUT_I64) reinterpret_cast<long long*>(out)[set * n_hash + i] = (long long)arg;
             else reinterpret_cast<uint32_t*>(out)[set * n_hash + i] = arg;
@@ -379,6 +398,7 @@ __device__ __forceinline__ int check_ids(const uint32_t* xs, int n, uint64_t p) 
     return flags;
 }
 
+// grid (hash slices, sets): block (x, s) computes hashes [x*kSmallSliceHashes, ...) of set s.
 __global__ void __launch_bounds__(256) sign_small_kernel(int kind, const int64_t* indptr, const uint32_t* ids,
                                                         uint64_t a, uint64_t b, const uint32_t* ra,
                                                         const uint32_t* rb, uint64_t p, int32_t n_hash, void* out,
@@ -386,17 +406,19 @@ __global__ void __launch_bounds__(256) sign_small_kernel(int kind, const int64_t
     __shared__ uint32_t xs[kSmallSetMax];
     __shared__ int block_flags;
     if (threadIdx.x == 0) block_flags = 0;
-    const int64_t set = blockIdx.x;
+    const int64_t set = blockIdx.y;
     const int64_t f0 = indptr[set] - indptr[0];
     const int n = (int)(indptr[set + 1] - indptr[set]);
+    const int32_t i_begin = (int32_t)blockIdx.x * kSmallSliceHashes;
+    const int32_t i_end = min(n_hash, i_begin + kSmallSliceHashes);
     int flags = n <= 0 ? MHB_STATUS_EMPTY_SET : 0;
     for (int k = threadIdx.x; k < n; k += blockDim.x) xs[k] = ids[f0 + k];
     __syncthreads();
-    flags |= check_ids(xs, n, p);
-    flags |= small_set_hashes(xs, n, kind, a, b, ra, rb, p, n_hash, out, out_dtype, set);
+    if (blockIdx.x == 0) flags |= check_ids(xs, n, p);
+    flags |= small_set_hashes(xs, n, kind, a, b, ra, rb, p, n_hash, i_begin, i_end, out, out_dtype, set);
     if (flags) atomicOr(&block_flags, flags);  // (__syncthreads_or would only say "some flag")
     __syncthreads();
-    if (threadIdx.x == 0) status[set] = block_flags;
+    if (threadIdx.x == 0) status[blockIdx.y * gridDim.x + blockIdx.x] = block_flags;  // one word per block
 }
 
 // ---- doorbell server: the per-set API without a kernel launch per call ----
@@ -417,7 +439,7 @@ struct DoorbellReq {  // header of a packed request; then indptr[n_sets+1] | ids
     int32_t kind, n_hash, out_dtype, n_sets;
     uint64_t a, b, p;
     uint32_t ids_off, ra_off, rb_off, pad;  // byte offsets into the request
-    uint64_t pad2;
+    unsigned long long out;                 // device address of the [n_sets, n_hash] output
 };
 static_assert(sizeof(DoorbellReq) % 16 == 0, "request header must keep 16-byte alignment");
 constexpr uint32_t kDoorbellBytes = 40 * 1024;  // largest request the block stages in shared memory
@@ -452,7 +474,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 constexpr int kDoorbellThreads = 1024;
 
 __global__ void __launch_bounds__(kDoorbellThreads, 1)
-    doorbell_kernel(Doorbell* db, const uint4* req, void* out, int32_t* status, uint32_t served, uint64_t idle_ns) {
+    doorbell_kernel(Doorbell* db, const uint4* req, int32_t* status, uint32_t served, uint64_t idle_ns) {
     __shared__ uint4 buf[kDoorbellBytes / 16];
     __shared__ uint32_t s_seq, s_bytes;
     __shared__ int s_go, block_flags;
@@ -503,8 +525,8 @@ __global__ void __launch_bounds__(kDoorbellThreads, 1)
             const int n = (int)(indptr[set + 1] - indptr[set]);
             if (n <= 0) flags |= MHB_STATUS_EMPTY_SET;
             flags |= check_ids(ids + f0, n, rq.p);
-            flags |= small_set_hashes(ids + f0, n, rq.kind, rq.a, rq.b, ra, rb, rq.p, rq.n_hash, out, rq.out_dtype,
-                                      set);
+            flags |= small_set_hashes(ids + f0, n, rq.kind, rq.a, rq.b, ra, rb, rq.p, rq.n_hash, 0, rq.n_hash,
+                                      reinterpret_cast<void*>(rq.out), rq.out_dtype, set);
         }
         if (flags) atomicOr(&block_flags, flags);
         __syncthreads();
@@ -584,7 +606,7 @@ namespace mhb {
 namespace {
 
 bool small_batch(const int64_t* indptr, int64_t n_sets, int32_t n_hash, uint64_t prime) {
-    if (n_sets > kSmallSets || n_hash > kSmallHash || prime >= (1ull << 32)) return false;
+    if (n_sets > kSmallSets || n_sets * (int64_t)n_hash > kSmallEntries || prime >= (1ull << 32)) return false;
     if (indptr[n_sets] - indptr[0] > kSmallNnz) return false;
     for (int64_t s = 0; s < n_sets; ++s)
         if (indptr[s + 1] - indptr[s] > kSmallSetMax || indptr[s + 1] < indptr[s]) return false;
@@ -608,8 +630,11 @@ uint64_t doorbell_idle_ns() {
     return ns;
 }
 
-// Doorbell eligibility: the packed request fits the block's shared-memory stage.
-uint32_t doorbell_request_bytes(int32_t kind, int64_t n_sets, int64_t nnz, int32_t n_hash) {
+// Doorbell eligibility: the packed request fits the block's shared-memory stage, and the
+// work suits one SM (<= 2^18 visits, ~15 us; <= 128 KB of output over PCIe from one SM).
+// Returns the request bytes, or 0 for "launch sign_small_kernel instead".
+uint32_t doorbell_request_bytes(int32_t kind, int64_t n_sets, int64_t nnz, int32_t n_hash, size_t out_bytes) {
+    if ((uint64_t)nnz * (uint64_t)n_hash > (1ull << 18) || out_bytes > (128u << 10)) return 0u;
     auto up16 = [](uint64_t v) { return (v + 15) & ~15ull; };
     uint64_t bytes = sizeof(DoorbellReq) + up16((uint64_t)(n_sets + 1) * 8) + up16((uint64_t)nnz * 4);
     if (kind == KIND_RANDOM) bytes += 2 * up16((uint64_t)n_hash * 4);
@@ -620,7 +645,7 @@ uint32_t doorbell_request_bytes(int32_t kind, int64_t n_sets, int64_t nnz, int32
 // (launching one if none is running) and spin until it has been served.
 int doorbell_call(SmallStage& sm, int32_t kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets,
                   uint64_t a, uint64_t b, const uint32_t* a_host, const uint32_t* b_host, uint64_t prime,
-                  int32_t n_hash, int32_t out_dtype, uint32_t bytes) {
+                  int32_t n_hash, void* out_dev, int32_t out_dtype, uint32_t bytes) {
     int rc;
     if (!sm.db) {
         if ((rc = cuda_check(cudaHostAlloc((void**)&sm.db, sizeof(Doorbell), cudaHostAllocMapped),
@@ -635,7 +660,8 @@ int doorbell_call(SmallStage& sm, int32_t kind, const int64_t* indptr, const uin
     }
     auto up16 = [](uint64_t v) { return (uint32_t)((v + 15) & ~15ull); };
     const int64_t nnz = indptr[n_sets] - indptr[0];
-    DoorbellReq h{kind, n_hash, out_dtype, (int32_t)n_sets, a, b, prime, 0, 0, 0, 0, 0};
+    DoorbellReq h{kind, n_hash, out_dtype, (int32_t)n_sets, a, b, prime, 0, 0, 0, 0,
+                  (unsigned long long)reinterpret_cast<uintptr_t>(out_dev)};
     h.ids_off = (uint32_t)sizeof(DoorbellReq) + up16((uint64_t)(n_sets + 1) * 8);
     h.ra_off = h.ids_off + up16((uint64_t)nnz * 4);
     h.rb_off = h.ra_off + (kind == KIND_RANDOM ? up16((uint64_t)n_hash * 4) : 0);
@@ -659,8 +685,8 @@ int doorbell_call(SmallStage& sm, int32_t kind, const int64_t* indptr, const uin
             if (__atomic_load_n(&db->done_seq, __ATOMIC_ACQUIRE) == seq) break;
             __atomic_store_n(&db->stop, 0u, __ATOMIC_RELEASE);
             __atomic_store_n(&db->running, 1u, __ATOMIC_RELEASE);
-            doorbell_kernel<<<1, kDoorbellThreads, 0, sm.db_stream>>>(db, reinterpret_cast<const uint4*>(sm.req), sm.out,
-                                                         sm.status, sm.seq, doorbell_idle_ns());
+            doorbell_kernel<<<1, kDoorbellThreads, 0, sm.db_stream>>>(db, reinterpret_cast<const uint4*>(sm.req),
+                                                                      sm.status, sm.seq, doorbell_idle_ns());
             if ((rc = cuda_check(cudaGetLastError(), "doorbell_kernel launch"))) {
                 __atomic_store_n(&db->running, 0u, __ATOMIC_RELEASE);
                 return rc;
@@ -694,49 +720,112 @@ void doorbell_stop(SmallStage& sm) {
     __atomic_store_n(&sm.db->running, 0u, __ATOMIC_RELEASE);
 }
 
+bool small_dev_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MHB_SMALL_DEV");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+int grow_mapped(char** ptr, size_t* cap, size_t need, const char* what) {
+    if (*cap >= need && *ptr) return MHB_OK;
+    if (*ptr) cudaFreeHost(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    const size_t want = std::max<size_t>(need + need / 4, 1 << 20);
+    int rc = cuda_check(cudaHostAlloc((void**)ptr, want, cudaHostAllocMapped), what);
+    if (rc) return rc;
+    *cap = want;
+    return MHB_OK;
+}
+
 int sign_small(DeviceCache& dc, int32_t kind, const int64_t* indptr, const uint32_t* ids, int64_t n_sets,
-               uint64_t a, uint64_t b, const uint32_t* a_host, const uint32_t* b_host, uint64_t prime,
-               int32_t n_hash, void* out, int32_t out_dtype, int32_t* status_host) {
+               uint64_t a, uint64_t b, const uint32_t* a_host, const uint32_t* b_host, bool params_dev,
+               uint64_t prime, int32_t n_hash, void* out, int32_t out_dtype, int32_t* status_host) {
     SmallStage& sm = dc.small;
-    const size_t in_bytes = (kSmallSets + 1) * 8 + kSmallNnz * 4 + 2 * (size_t)kSmallHash * 4;
-    const size_t out_cap = kSmallSets * (size_t)kSmallHash * 8;
-    if (!sm.in) {
-        int rc = cuda_check(cudaHostAlloc((void**)&sm.in, in_bytes, cudaHostAllocMapped), "cudaHostAlloc (small in)");
-        if (rc) return rc;
-        rc = cuda_check(cudaHostAlloc((void**)&sm.out, out_cap, cudaHostAllocMapped), "cudaHostAlloc (small out)");
-        if (rc) return rc;
-        rc = cuda_check(cudaHostAlloc((void**)&sm.status, kSmallSets * 4, cudaHostAllocMapped),
-                        "cudaHostAlloc (small status)");
-        if (rc) return rc;
+    int rc;
+    if (!sm.status) {
+        if ((rc = cuda_check(cudaHostAlloc((void**)&sm.status, kSmallStatus * 4, cudaHostAllocMapped),
+                             "cudaHostAlloc (small status)")))
+            return rc;
     }
     const int64_t nnz = indptr[n_sets] - indptr[0];
-    const uint32_t db_bytes = doorbell_enabled() ? doorbell_request_bytes(kind, n_sets, nnz, n_hash) : 0u;
+    const size_t out_bytes = (size_t)n_sets * n_hash * (out_dtype == MHB_OUT_I64 ? 8 : 4);
+    // A page-locked caller buffer is written by the kernel directly (UVA: the device address
+    // of mapped host memory); the pointer query is paid only where a host copy would cost more.
+    void* out_dev = nullptr;
+    if (out_bytes >= (64u << 10) && is_pinned(out)) {
+        if (cudaHostGetDevicePointer(&out_dev, out, 0) != cudaSuccess) {
+            cudaGetLastError();
+            out_dev = nullptr;
+        }
+    }
+    if (!out_dev) {
+        if ((rc = grow_mapped(&sm.out, &sm.out_cap, out_bytes, "cudaHostAlloc (small out)"))) return rc;
+        out_dev = sm.out;
+    }
+    // (random-family parameters already on the device go to the launched kernel as they are)
+    const uint32_t db_bytes = doorbell_enabled() && !params_dev
+                                  ? doorbell_request_bytes(kind, n_sets, nnz, n_hash, out_bytes) : 0u;
+    int64_t n_status = 1;  // words of sm.status the call wrote
     if (db_bytes) {
-        int rc = doorbell_call(sm, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out_dtype,
-                               db_bytes);
-        if (rc) return rc;
+        if ((rc = doorbell_call(sm, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out_dev,
+                                out_dtype, db_bytes)))
+            return rc;
     } else {
-        int64_t* ip = reinterpret_cast<int64_t*>(sm.in);
-        uint32_t* x = reinterpret_cast<uint32_t*>(sm.in + (kSmallSets + 1) * 8);
-        uint32_t* ra = x + kSmallNnz;
-        uint32_t* rb = ra + kSmallHash;
-        std::memcpy(ip, indptr, (n_sets + 1) * 8);
-        if (nnz) std::memcpy(x, ids + indptr[0], nnz * 4);
-        if (kind == KIND_RANDOM) {
-            std::memcpy(ra, a_host, n_hash * 4);
-            std::memcpy(rb, b_host, n_hash * 4);
+        // Launched grid.  Wide outputs (>= 64 KB: the C6 shape, 100,000 hashes per set) go
+        // through device memory with the copy engines on both sides -- one DMA of the packed
+        // request in, one of the argmins out -- because thousands of blocks reading and writing
+        // mapped host memory directly cost 2-3x more (MHB_SMALL_DEV=0 keeps that path).
+        auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+        const bool stage_params = kind == KIND_RANDOM && !params_dev;
+        const size_t ids_off = up16((size_t)(n_sets + 1) * 8), ra_off = ids_off + up16((size_t)nnz * 4);
+        const size_t in_bytes = ra_off + (stage_params ? 2 * (size_t)n_hash * 4 : 0);
+        if ((rc = grow_mapped(&sm.in, &sm.in_cap, in_bytes, "cudaHostAlloc (small in)"))) return rc;
+        std::memcpy(sm.in, indptr, (n_sets + 1) * 8);
+        if (nnz) std::memcpy(sm.in + ids_off, ids + indptr[0], nnz * 4);
+        if (stage_params) {
+            std::memcpy(sm.in + ra_off, a_host, n_hash * 4);
+            std::memcpy(sm.in + ra_off + (size_t)n_hash * 4, b_host, n_hash * 4);
         }
         cudaStream_t st = dc.lanes[0].stream;
-        sign_small_kernel<<<(unsigned)n_sets, 256, 0, st>>>(kind, ip, x, a, b, ra, rb, prime, n_hash, sm.out, out_dtype,
-                                                      sm.status);
-        int rc = cuda_check(cudaGetLastError(), "sign_small_kernel launch");
-        if (rc) return rc;
-        rc = cuda_check(cudaStreamSynchronize(st), "sign_small_kernel");
-        if (rc) return rc;
+        const dim3 grid((unsigned)((n_hash + kSmallSliceHashes - 1) / kSmallSliceHashes), (unsigned)n_sets);
+        n_status = (int64_t)grid.x * grid.y;
+        const bool via_dev = out_bytes >= (64u << 10) && small_dev_enabled();
+        char* base = sm.in;  // where the kernel reads the request
+        void* kout = out_dev;
+        int32_t* kstatus = sm.status;
+        if (via_dev) {
+            const size_t out_off = up16(in_bytes), st_off = out_off + up16(out_bytes);
+            if ((rc = grow(&sm.dev, &sm.dev_cap, st_off + (size_t)n_status * 4))) return rc;
+            base = static_cast<char*>(sm.dev);
+            kout = base + out_off;
+            kstatus = reinterpret_cast<int32_t*>(base + st_off);
+            if ((rc = cuda_check(cudaMemcpyAsync(base, sm.in, in_bytes, cudaMemcpyHostToDevice, st), "H2D small")))
+                return rc;
+        }
+        const int64_t* ip = reinterpret_cast<const int64_t*>(base);
+        const uint32_t* x = reinterpret_cast<const uint32_t*>(base + ids_off);
+        const uint32_t* ra = stage_params ? reinterpret_cast<const uint32_t*>(base + ra_off) : a_host;
+        const uint32_t* rb = stage_params ? ra + n_hash : b_host;
+        sign_small_kernel<<<grid, 256, 0, st>>>(kind, ip, x, a, b, ra, rb, prime, n_hash, kout, out_dtype, kstatus);
+        if ((rc = cuda_check(cudaGetLastError(), "sign_small_kernel launch"))) return rc;
+        if (via_dev) {
+            if ((rc = cuda_check(cudaMemcpyAsync(out_dev, kout, out_bytes, cudaMemcpyDeviceToHost, st), "D2H small")))
+                return rc;
+            if ((rc = cuda_check(cudaMemcpyAsync(sm.status, kstatus, (size_t)n_status * 4, cudaMemcpyDeviceToHost,
+                                                 st), "D2H small status")))
+                return rc;
+        }
+        if ((rc = cuda_check(cudaStreamSynchronize(st), "sign_small_kernel"))) return rc;
     }
-    std::memcpy(out, sm.out, (size_t)n_sets * n_hash * (out_dtype == MHB_OUT_I64 ? 8 : 4));
+    if (out_dev == sm.out) {
+        if (out_bytes >= (1u << 20)) host_copy_out(reinterpret_cast<const uint32_t*>(sm.out), out, out_bytes / 4, false);
+        else std::memcpy(out, sm.out, out_bytes);
+    }
     int32_t st_or = 0;
-    for (int64_t s = 0; s < (db_bytes ? 1 : n_sets); ++s) st_or |= sm.status[s];
+    for (int64_t s = 0; s < n_status; ++s) st_or |= sm.status[s];
     if (status_host) *status_host = st_or;
     return MHB_OK;
 }
@@ -793,14 +882,20 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         if (rc) return rc;
         dc.init = true;
     }
+    if (kind == KIND_RANDOM && (!a_host || !b_host)) return set_error(MHB_ERR_INVALID, "random family needs a and b");
+    // random-family a/b may also be device arrays (UVA): used in place, no staging
+    const bool params_dev = kind == KIND_RANDOM && is_device_ptr(a_host) && is_device_ptr(b_host);
     if (small_batch(indptr, n_sets, n_hash, prime)) {
-        if (kind == KIND_RANDOM && (!a_host || !b_host)) return set_error(MHB_ERR_INVALID, "random family needs a and b");
         if ((rc = check_sign_params(kind, a, b, true, prime, n_hash))) return rc;
-        return sign_small(dc, kind, indptr, ids, n_sets, a, b, a_host, b_host, prime, n_hash, out, out_dtype,
-                          status_host);
+        return sign_small(dc, kind, indptr, ids, n_sets, a, b, a_host, b_host, params_dev, prime, n_hash, out,
+                          out_dtype, status_host);
     }
-    if (kind == KIND_RANDOM) {
-        if (!a_host || !b_host) return set_error(MHB_ERR_INVALID, "random family needs a and b");
+    const uint32_t* ra_dev = dc.ra;
+    const uint32_t* rb_dev = dc.rb;
+    if (params_dev) {
+        ra_dev = a_host;
+        rb_dev = b_host;
+    } else if (kind == KIND_RANDOM) {
         if ((rc = grow((void**)&dc.ra, &dc.ra_cap, (size_t)n_hash * 4))) return rc;
         if ((rc = grow((void**)&dc.rb, &dc.rb_cap, (size_t)n_hash * 4))) return rc;
         cudaStream_t s0 = dc.lanes[0].stream;
@@ -809,6 +904,8 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         if ((rc = cuda_check(cudaMemcpyAsync(dc.rb, b_host, (size_t)n_hash * 4, cudaMemcpyHostToDevice, s0), "H2D b")))
             return rc;
         if ((rc = cuda_check(cudaStreamSynchronize(s0), "sync params"))) return rc;
+        ra_dev = dc.ra;
+        rb_dev = dc.rb;
     }
 
     const std::vector<Chunk> chunks = plan_chunks(indptr, n_sets, n_hash, out_bytes);
@@ -871,7 +968,7 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
             rebase_indptr_kernel<<<(unsigned)nb, 256, 0, ln.stream>>>(ln.indptr, rows + 1, id0);
             if ((rc = cuda_check(cudaGetLastError(), "rebase_indptr launch"))) return rc;
         }
-        rc = launch_sign(kind, ln.indptr, ln.ids, rows, cnnz, a, b, dc.ra, dc.rb, prime, n_hash, ln.out,
+        rc = launch_sign(kind, ln.indptr, ln.ids, rows, cnnz, a, b, ra_dev, rb_dev, prime, n_hash, ln.out,
                          stage_out ? MHB_OUT_U32 : out_dtype, dc.status + c, ln.ws, ln.ws_cap, ln.stream);
         if (rc) return rc;
         if (stage_out) {
@@ -926,6 +1023,7 @@ extern "C" void mhb_host_release(void) {
         if (dc.small.db_stream) cudaStreamDestroy(dc.small.db_stream);
         if (dc.small.db) cudaFreeHost(dc.small.db);
         if (dc.small.req) cudaFreeHost(dc.small.req);
+        if (dc.small.dev) cudaFree(dc.small.dev);
         if (dc.small.in) cudaFreeHost(dc.small.in);
         if (dc.small.out) cudaFreeHost(dc.small.out);
         if (dc.small.status) cudaFreeHost(dc.small.status);

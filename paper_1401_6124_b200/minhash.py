@@ -328,18 +328,32 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     # so the call goes straight through, staged in this thread's reusable buffers
     st = _PERSET
     n = int(ids.size)
-    if n > st.ids.size or family.size > st.out.size:
-        st.grow(n, family.size)
+    n_hash = family.size
+    if n > st.ids.size or (n_hash < _PERSET_WIDE and n_hash > st.out.size):
+        st.grow(n, n_hash)
     np.copyto(st.ids[:n], ids, casting="unsafe")
     st.indptr[1] = n
+    if n_hash >= _PERSET_WIDE:
+        # wide signatures (the reference's C6 loop: 100,000 hashes per call): a fresh
+        # page-locked result the kernel writes directly, instead of a stage and two copies
+        buf = _torch().empty(n_hash, dtype=_torch().int64, pin_memory=True)
+        out, out_ptr = buf.numpy(), buf.data_ptr()
+    else:
+        out, out_ptr = None, st.out_ptr
     kind, a, b, a_ptr, b_ptr = _percall_params(family)
+    if out is not None and kind == _lib.KIND_RANDOM:  # wide random family: a, b already on the device
+        da, db = family.device_params(_torch().device("cuda", _torch().cuda.current_device()))
+        a_ptr, b_ptr = da.data_ptr(), db.data_ptr()
     rc = _lib.load().mhb_sign_csr_host(kind, st.indptr_ptr, st.ids_ptr, 1, n, a, b, a_ptr, b_ptr, family.prime,
-                                       family.size, st.out_ptr, _lib.OUT_I64, st.status_ptr, -1)
+                                       n_hash, out_ptr, _lib.OUT_I64, st.status_ptr, -1)
     if rc:
         _lib.check(rc)
     if st.status.value:
         _raise_status(st.status.value, family)
-    return Signature._wrap(st.out[:family.size].copy(), family.key)
+    return Signature._wrap(st.out[:n_hash].copy() if out is None else out, family.key)
+
+
+_PERSET_WIDE = 8192  # per-set results at least this wide go to a fresh pinned array
 
 
 class _PerSetStage(threading.local):

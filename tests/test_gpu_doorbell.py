@@ -1,4 +1,5 @@
-"""GPU: the doorbell server behind the per-set API (csrc/host.cu, doorbell_kernel).
+"""GPU: the per-set / small-batch paths of the host entry (csrc/host.cu): the doorbell
+server (doorbell_kernel) and the launched (hash slice, set) grid (sign_small_kernel).
 
 signature(FeatureSet, family) -- the reference's per-set call (minhash.py:91-110) --
 is served by one resident block that polls a request word in mapped host memory.
@@ -6,7 +7,9 @@ These tests cover its protocol rather than the arithmetic (the small-batch parit
 tests in test_gpu_parity.py run through it too): relaunch after the idle exit,
 concurrent callers, interleaving with the chunked pipeline and device-wide syncs,
 release while running, and equality with the launched small kernel
-(MHB_DOORBELL=0) in a fresh process.  Bar: bit-exact against the oracle.
+(MHB_DOORBELL=0) in a fresh process; then the wide per-set calls of the reference's C6
+loop (100,000 hashes) and the output targets (caller's pinned buffer written directly,
+or the mapped stage copied).  Bar: bit-exact against the oracle.
 """
 import os
 import subprocess
@@ -130,3 +133,40 @@ def test_doorbell_equals_launched_kernel(cuda_device, tmp_path):
         subprocess.run([sys.executable, "-c", _CHILD, str(f)], check=True, env=env, cwd=ROOT, timeout=300)
         res[mode] = np.load(f)
     assert np.array_equal(res["0"], res["1"])
+
+
+@pytest.mark.parametrize("kind", ["iterative", "random"])
+def test_wide_per_set_calls(cuda_device, kind):
+    """The reference's C6 call shape (one set, 100,000 hashes per signature() call): the
+    launched (hash slice, set) grid writing straight into a fresh pinned result."""
+    p = 200_003
+    fam = make_family(kind, 6, 100_000, p)
+    sets = _sets(7, 6, lo=1, hi=400, p=p)
+    want = _want(sets, fam)
+    for k, s in enumerate(sets):
+        got = signature(s, fam)
+        assert got.mins.dtype == np.int64 and not got.mins.flags.writeable
+        assert np.array_equal(got.mins, want[k]), k
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("n_hash", [300, 5000, 40_000])
+def test_small_batch_output_targets(cuda_device, pinned, n_hash):
+    """Small batches whose output is written into the caller's page-locked buffer directly,
+    or into the mapped stage and copied (in parallel above 1 MB), both dtypes."""
+    import torch
+
+    from paper_1401_6124_b200.minhash import _signatures_csr_host
+
+    fam = make_family("iterative", 8, n_hash, 1_048_583)
+    sets = _sets(9, 40, p=1_048_583)
+    want = _want(sets, fam)
+    ip = np.zeros(len(sets) + 1, dtype=np.int64)
+    ip[1:] = np.cumsum([len(s) for s in sets])
+    ids = np.concatenate([s.ids for s in sets]).astype(np.uint32)
+    for dt, tdt in (("int64", torch.int64), ("uint32", torch.int32)):
+        buf = torch.empty((len(sets), n_hash), dtype=tdt, pin_memory=pinned)
+        out = buf.numpy() if dt == "int64" else buf.numpy().view(np.uint32)
+        got = _signatures_csr_host(ip, ids, fam, dt, out, None)
+        assert got is out or np.shares_memory(got, out)
+        assert np.array_equal(out.astype(np.int64), want), (dt, pinned, n_hash)

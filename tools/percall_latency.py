@@ -50,5 +50,21 @@ for _ in range(5000):
 print(f"raw mhb_sign_csr_host (S=1): {(time.perf_counter() - t0) / 5000 * 1e6:.1f} us/call")
 import cProfile, pstats  # noqa: E402,E401
 
-cProfile.run("for s in sets[:500]: signature(s, fam)", "/tmp/sig.prof")
+cProfile.run("for s in sets[:500]: signature(s, fam)", "/tmp/sig.prof")  # noqa: E702
 pstats.Stats("/tmp/sig.prof").sort_stats("tottime").print_stats(10)
+
+# the reference's timing experiment calls signature() once per document with N = 100,000
+# (run_timing, bench.py:97-102; acceptance C6): per-document latency at that width
+from paper_1401_6124_b200 import derive_seed  # noqa: E402
+
+c6_ip, c6_ids, c6_p, c6_seed = gen.c6_workload()
+c6_sets = [FeatureSet(c6_ids[c6_ip[s]:c6_ip[s + 1]]) for s in range(c6_ip.size - 1)]
+for kind in ("iterative", "random"):
+    fam = make_family(kind, derive_seed(c6_seed, 0), 100_000, c6_p)
+    for s in c6_sets[:20]:
+        signature(s, fam)
+    t0 = time.perf_counter()
+    for s in c6_sets:
+        signature(s, fam)
+    dt = time.perf_counter() - t0
+    print(f"C6 per-document signature() {kind}: {dt / len(c6_sets) * 1e6:.1f} us/doc, {dt * 1e3:.1f} ms for {len(c6_sets)} docs")
