@@ -776,8 +776,8 @@ int sign_small(DeviceCache& dc, int32_t kind, const int64_t* indptr, const uint3
     } else {
         // Launched grid.  Wide outputs (>= 64 KB: the C6 shape, 100,000 hashes per set) go
         // through device memory with the copy engines on both sides -- one DMA of the packed
-        // request in, one of the argmins out -- because thousands of blocks reading and writing
-        // mapped host memory directly cost 2-3x more (MHB_SMALL_DEV=0 keeps that path).
+        // request in, one of the argmins out -- because hundreds of blocks reading and writing
+        // mapped host memory directly cost 1.4x more (MHB_SMALL_DEV=0 keeps that path).
         auto up16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
         const bool stage_params = kind == KIND_RANDOM && !params_dev;
         const size_t ids_off = up16((size_t)(n_sets + 1) * 8), ra_off = ids_off + up16((size_t)nnz * 4);
@@ -795,13 +795,12 @@ int sign_small(DeviceCache& dc, int32_t kind, const int64_t* indptr, const uint3
         const bool via_dev = out_bytes >= (64u << 10) && small_dev_enabled();
         char* base = sm.in;  // where the kernel reads the request
         void* kout = out_dev;
-        int32_t* kstatus = sm.status;
+        int32_t* kstatus = sm.status;  // one plain store per block into mapped memory, either way
         if (via_dev) {
-            const size_t out_off = up16(in_bytes), st_off = out_off + up16(out_bytes);
-            if ((rc = grow(&sm.dev, &sm.dev_cap, st_off + (size_t)n_status * 4))) return rc;
+            const size_t out_off = up16(in_bytes);
+            if ((rc = grow(&sm.dev, &sm.dev_cap, out_off + out_bytes))) return rc;
             base = static_cast<char*>(sm.dev);
             kout = base + out_off;
-            kstatus = reinterpret_cast<int32_t*>(base + st_off);
             if ((rc = cuda_check(cudaMemcpyAsync(base, sm.in, in_bytes, cudaMemcpyHostToDevice, st), "H2D small")))
                 return rc;
         }
@@ -813,9 +812,6 @@ int sign_small(DeviceCache& dc, int32_t kind, const int64_t* indptr, const uint3
         if ((rc = cuda_check(cudaGetLastError(), "sign_small_kernel launch"))) return rc;
         if (via_dev) {
             if ((rc = cuda_check(cudaMemcpyAsync(out_dev, kout, out_bytes, cudaMemcpyDeviceToHost, st), "D2H small")))
-                return rc;
-            if ((rc = cuda_check(cudaMemcpyAsync(sm.status, kstatus, (size_t)n_status * 4, cudaMemcpyDeviceToHost,
-                                                 st), "D2H small status")))
                 return rc;
         }
         if ((rc = cuda_check(cudaStreamSynchronize(st), "sign_small_kernel"))) return rc;
