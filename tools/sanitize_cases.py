@@ -23,5 +23,22 @@ for kind in ("iterative", "random"):
         estimate_pairs(d, pi, pi + 1)
         jaccard_block(d[:100], d[100:300])
         bucket_histogram(ids[:5000], fam, 4096)
+# per-set and small-batch paths: the doorbell block (light requests), the launched
+# (hash slice, set) grid with mapped or device staging, pinned and pageable outputs
+from paper_1401_6124_b200 import FeatureSet, signature  # noqa: E402
+from paper_1401_6124_b200.minhash import _signatures_csr_host  # noqa: E402
+
+rng = np.random.default_rng(3)
+for kind in ("iterative", "random"):
+    for n_hash in (1, 128, 3000, 20_000):
+        fam = make_family(kind, 9, n_hash, 1_048_583)
+        for n in (1, 40, 900):
+            s = FeatureSet(rng.integers(0, 1_048_583, size=n))
+            signature(s, fam)
+        for pinned in (False, True):
+            buf = torch.empty((3, n_hash), dtype=torch.int64, pin_memory=pinned)
+            _signatures_csr_host(np.array([0, 5, 5 + 700, 5 + 700 + 1], dtype=np.int64),
+                                 rng.integers(0, 1_048_583, size=706).astype(np.uint32), fam, "int64", buf.numpy(),
+                                 None)
 torch.cuda.synchronize()
 print("sanitize cases ok")
