@@ -4,8 +4,9 @@ usage: python tools/stress.py [seconds] [seed]
 
 Each case draws a family (random / iterative), N, a prime (tiny .. 2^31, and wide
 ones up to 2^32), set sizes (1 .. a few chunks, repeated ids), and an entry path:
-device CSR, host pipeline (pinned / pageable, uint32 / int64), small-batch host path,
-fused band keys (keys only), 64-bit ids.  Any mismatch is printed with its seed and the
+device CSR, host pipeline (pinned / pageable, uint32 / int64, pinned int64), small-batch
+host path (doorbell block / launched grid, wide N up to 100,000), the per-set
+signature() API, fused band keys (keys only), 64-bit ids.  Any mismatch is printed with its seed and the
 run exits non-zero.
 """
 import sys
@@ -16,7 +17,8 @@ import torch
 
 sys.path.insert(0, ".")
 from oracle import oracle  # noqa: E402
-from paper_1401_6124_b200 import band_keys, make_family, signatures_band_keys, signatures_csr  # noqa: E402
+from paper_1401_6124_b200 import (FeatureSet, band_keys, make_family, signature, signatures_band_keys,  # noqa: E402
+                                  signatures_csr)
 from paper_1401_6124_b200.minhash import _signatures_csr_host  # noqa: E402
 
 PRIMES = [11, 101, 7757, 65537, 1_048_583, 4_194_319, 8_388_593, 16_777_259, 67_108_879, 1_073_741_827,
@@ -33,6 +35,12 @@ def case(rng, dev):
         p = 2_147_483_647 if rng.random() < 0.5 else 1_073_741_827
     fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
     n_sets = int(rng.choice([1, 2, 7, 64, 65, 300, 2000]))
+    if rng.random() < 0.15:  # wide small batches: the launched (hash slice, set) grid, device staging
+        n_sets = int(rng.choice([1, 3, 20]))
+        n_hash = int(rng.choice([4000, 8192, 20_000, 100_000]))
+        if kind == "iterative" and 2 * n_hash + 3 >= p:
+            p = 1_073_741_827
+        fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
     sizes = rng.choice([1, 2, 3, 50, 200, 1023, 1024, 1025, 3000], size=n_sets,
                        p=[.1, .1, .1, .3, .2, .05, .05, .05, .05])
     rows = []
@@ -45,7 +53,8 @@ def case(rng, dev):
     ip = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int64)
     ids = np.concatenate(rows)
     want = oracle.sign_family_csr(ip, ids, fam)
-    path = rng.choice(["device", "host_pinned", "host_pageable", "host_int64", "bands", "ids64"])
+    path = rng.choice(["device", "host_pinned", "host_pageable", "host_int64", "bands", "ids64", "per_set",
+                       "host_pinned_int64"])
     if path == "device":
         got = signatures_csr(torch.as_tensor(ip, device=dev), torch.as_tensor(ids.astype(np.int64), device=dev),
                              fam, out_dtype=str(rng.choice(["uint32", "int64"]))).cpu().numpy().astype(np.int64)
@@ -57,6 +66,13 @@ def case(rng, dev):
         got = signatures_csr(ip, ids, fam, out_dtype="uint32").astype(np.int64)
     elif path == "host_int64":
         got = _signatures_csr_host(ip, ids, fam, "int64", None, None)
+    elif path == "per_set":  # the reference API, one signature() per set (doorbell / launched grid)
+        k = min(n_sets, 4)
+        got = np.stack([signature(FeatureSet(rows[i].astype(np.int64)), fam).mins for i in range(k)])
+        return kind, p, n_hash, n_sets, path, bool(np.array_equal(got, want[:k]))
+    elif path == "host_pinned_int64":  # written straight into the caller's page-locked buffer
+        out = torch.empty((n_sets, n_hash), dtype=torch.int64).pin_memory().numpy()
+        got = _signatures_csr_host(ip, ids, fam, "int64", out, None)
     elif path == "bands":
         rows_b = next((r for r in (16, 8, 4) if n_hash % r == 0), None)
         if rows_b is None:
