@@ -1,4 +1,4 @@
-"""GPU: the per-set / small-batch paths of the host entry (csrc/host.cu): the doorbell
+"""GPU: the per-set / small-batch paths of the host entry (csrc/small.cu): the doorbell
 server (doorbell_kernel) and the launched (hash slice, set) grid (sign_small_kernel).
 
 signature(FeatureSet, family) -- the reference's per-set call (minhash.py:91-110) --

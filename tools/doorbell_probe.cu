@@ -1,6 +1,6 @@
 // doorbell_probe.cu -- host <-> resident-block round trips over mapped host memory.
 //
-// Measures the building blocks of the per-set doorbell server (csrc/host.cu):
+// Measures the building blocks of the per-set doorbell server (csrc/small.cu):
 // the poll/acknowledge ping-pong alone, then with input reads over PCIe, output
 // writes + fence.sys, in several spellings.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o doorbell_probe doorbell_probe.cu
