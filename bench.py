@@ -761,6 +761,34 @@ def _e2e(args, ctx, indptr, ids, fam, out):
             "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
 
 
+def _per_set(ctx):
+    """The reference's per-set call, signature(FeatureSet, family), at the cfg1 shape
+    (N=128, ~50 ids): the latency a drop-in caller of the reference API sees (served by
+    the resident doorbell block, csrc/small.cu)."""
+    import numpy as np
+
+    from paper_1401_6124_b200 import FeatureSet, gen, make_family, signature
+
+    cfg = gen.CONFIGS["cfg1"]
+    ip, ids = gen.cfg1_numpy(n_sets=2000, seed=3)
+    sets = [FeatureSet(ids[ip[k]:ip[k + 1]]) for k in range(2000)]
+    res = {}
+    for kind in ("iterative", "random"):
+        fam = make_family(kind, cfg.family_seed(kind), cfg.n_hash, cfg.prime)
+        for s in sets[:100]:
+            signature(s, fam)
+        t0 = time.perf_counter()
+        for s in sets:
+            signature(s, fam)
+        res[kind + "_us_per_call"] = (time.perf_counter() - t0) / len(sets) * 1e6
+    res.update({"n_hash": cfg.n_hash, "mean_ids": float(np.diff(ip).mean()),
+                "path": "signature(FeatureSet, family) -> mhb_sign_csr_host -> doorbell block (no launch)",
+                "reference_numba_us_estimate": 18.5, "reference_numba_us_build_container": {"iterative": 20.0, "random": 28.6},
+                "reference_source": "estimate: 6,400 visits at the 3.8e8 visits/s of SURVEY §6 (numba, 1 core) + 7-13% API "
+                                    "overhead; measured: tools/reference_percall.py in the build container (slower CPU)"})
+    return res
+
+
 def _cpu_baseline(args, indptr, ids, fam, n_sets):
     """The oracle port on all host cores (and on one) over a bounded prefix of the batch."""
     import numpy as np
@@ -826,6 +854,7 @@ def main():
     aux = _aux_kernels(cfg, fam, indptr, ids, out, exact_j, ctx.dev) if args.aux else None
     cpu = (_cpu_baseline(args, indptr, ids, fam, n_sets)
            if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None)
+    per_set = _per_set(ctx) if ctx.rank == 0 and ctx.world == 1 and not args.no_e2e else None
 
     if ctx.rank == 0:
         line = {
@@ -842,6 +871,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 5 * args.steps, "clocks": clocks,  # plan_count, plan_scan, plan_scatter, sign, finalize
         }
+        if per_set is not None:
+            line["per_set"] = per_set
         if eager_ms is not None:
             line["graph"] = {"replayed": True, "eager_ms_per_step": eager_ms,
                              "launches_per_replay": 5}
