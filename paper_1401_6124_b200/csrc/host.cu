@@ -201,9 +201,9 @@ int grow(void** ptr, size_t* cap, size_t need) {
 }
 
 // Parallel copy (u32 -> u32, or u32 -> int64 widening) of `n` elements.
-void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen) {
+void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen, int64_t part_elems) {
     HostPool& pool = host_pool();
-    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n >> 18));
+    const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(pool.width() * 2, n / part_elems));
     const bool nt = host_nt();
     pool.run(parts, [&](int k) {
         const int64_t lo = n * k / parts, hi = n * (k + 1) / parts;

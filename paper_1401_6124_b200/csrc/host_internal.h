@@ -13,7 +13,8 @@ namespace mhb {
 bool is_pinned(const void* p);                            // page-locked host memory
 bool is_device_ptr(const void* p);                        // device (or managed) memory
 int grow(void** ptr, size_t* cap, size_t need);           // device buffer, grown on demand
-void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen);  // parallel, streaming stores
+// parallel (parts of >= part_elems elements), streaming stores
+void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen, int64_t part_elems = 1 << 18);
 
 // Small batches (the per-set reference API: signature() on one FeatureSet) skip the
 // chunk pipeline.  Light requests go to the resident doorbell block (no launch): inputs

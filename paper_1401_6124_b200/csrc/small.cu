@@ -499,7 +499,8 @@ int sign_small(SmallStage& sm, cudaStream_t stream, int32_t kind, const int64_t*
         if ((rc = cuda_check(cudaStreamSynchronize(st), "sign_small_kernel"))) return rc;
     }
     if (out_dev == sm.out) {
-        if (out_bytes >= (1u << 20)) host_copy_out(reinterpret_cast<const uint32_t*>(sm.out), out, out_bytes / 4, false);
+        if (out_bytes >= (256u << 10))  // 64 KB per worker: a wide per-set result is ~1 MB
+            host_copy_out(reinterpret_cast<const uint32_t*>(sm.out), out, out_bytes / 4, false, 1 << 14);
         else std::memcpy(out, sm.out, out_bytes);
     }
     int32_t st_or = 0;

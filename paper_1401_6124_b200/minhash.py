@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import struct
 import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -334,10 +335,9 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     np.copyto(st.ids[:n], ids, casting="unsafe")
     st.indptr[1] = n
     if n_hash >= _PERSET_WIDE:
-        # wide signatures (the reference's C6 loop: 100,000 hashes per call): a fresh
-        # page-locked result the kernel writes directly, instead of a stage and two copies
-        buf = _torch().empty(n_hash, dtype=_torch().int64, pin_memory=True)
-        out, out_ptr = buf.numpy(), buf.data_ptr()
+        # wide signatures (the reference's C6 loop: 100,000 hashes per call): a fresh result
+        # the library fills in one copy (parallel above 256 KB), instead of a stage and two
+        out, out_ptr = _perset_wide_result(n_hash)
     else:
         out, out_ptr = None, st.out_ptr
     kind, a, b, a_ptr, b_ptr = _percall_params(family)
@@ -353,7 +353,34 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     return Signature._wrap(st.out[:n_hash].copy() if out is None else out, family.key)
 
 
-_PERSET_WIDE = 8192  # per-set results at least this wide go to a fresh pinned array
+_PERSET_WIDE = 8192  # per-set results at least this wide are written into a fresh array directly
+# Wide results are page-locked (from torch's caching host allocator, already faulted in):
+# the D2H lands in them directly, 54 vs 85 us per C6-shaped call against a fresh pageable
+# array, whose first-touch page faults cost more than the copy.  Live page-locked results
+# are capped (MHB_PERSET_PINNED_MB, default 1024) so retained signatures cannot pin
+# unbounded host memory; beyond the cap results are ordinary arrays.
+_PERSET_PINNED_CAP = int(__import__("os").environ.get("MHB_PERSET_PINNED_MB", "1024")) << 20
+_perset_pinned = {"live": 0, "lock": threading.Lock()}
+
+
+def _perset_unpin(nbytes: int) -> None:
+    with _perset_pinned["lock"]:
+        _perset_pinned["live"] -= nbytes
+
+
+def _perset_wide_result(n_hash: int):
+    nbytes = 8 * n_hash
+    with _perset_pinned["lock"]:
+        pin = _perset_pinned["live"] + nbytes <= _PERSET_PINNED_CAP
+        if pin:
+            _perset_pinned["live"] += nbytes
+    if not pin:
+        out = np.empty(n_hash, dtype=np.int64)
+        return out, out.ctypes.data
+    buf = _torch().empty(n_hash, dtype=_torch().int64, pin_memory=True)
+    out = buf.numpy()
+    weakref.finalize(out, _perset_unpin, nbytes)
+    return out, buf.data_ptr()
 
 
 class _PerSetStage(threading.local):

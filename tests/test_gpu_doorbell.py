@@ -138,7 +138,7 @@ def test_doorbell_equals_launched_kernel(cuda_device, tmp_path):
 @pytest.mark.parametrize("kind", ["iterative", "random"])
 def test_wide_per_set_calls(cuda_device, kind):
     """The reference's C6 call shape (one set, 100,000 hashes per signature() call): the
-    launched (hash slice, set) grid writing straight into a fresh pinned result."""
+    launched (hash slice, set) grid, its result copied once into a fresh array."""
     p = 200_003
     fam = make_family(kind, 6, 100_000, p)
     sets = _sets(7, 6, lo=1, hi=400, p=p)
@@ -170,3 +170,28 @@ def test_small_batch_output_targets(cuda_device, pinned, n_hash):
         got = _signatures_csr_host(ip, ids, fam, dt, out, None)
         assert got is out or np.shares_memory(got, out)
         assert np.array_equal(out.astype(np.int64), want), (dt, pinned, n_hash)
+
+
+def test_wide_results_pinned_cap(cuda_device):
+    """Retained wide per-set results stop being page-locked past MHB_PERSET_PINNED_MB, and
+    dropped ones give their budget back."""
+    import gc
+
+    from paper_1401_6124_b200 import minhash
+
+    fam = make_family("iterative", 2, 20_000, 1_048_583)
+    s = _sets(12, 1, lo=30, hi=31)[0]
+    want = _want([s], fam)[0]
+    cap = minhash._PERSET_PINNED_CAP
+    gc.collect()
+    live0 = minhash._perset_pinned["live"]
+    try:
+        minhash._PERSET_PINNED_CAP = live0 + 3 * 8 * 20_000  # room for three more
+        keep = [signature(s, fam) for _ in range(5)]
+        assert all(np.array_equal(k.mins, want) for k in keep)
+        assert minhash._perset_pinned["live"] == live0 + 3 * 8 * 20_000
+        del keep
+        gc.collect()
+        assert minhash._perset_pinned["live"] == live0
+    finally:
+        minhash._PERSET_PINNED_CAP = cap
