@@ -325,7 +325,7 @@ def signature(s: FeatureSet, family: Family) -> Signature:
         out = signatures_csr(indptr, dids, family, out_dtype="int64", validate=False)
         return Signature(out[0].cpu().numpy(), family.key)
     # host buffers -> mhb_sign_csr_host, whose small-batch path is served by the resident
-    # doorbell block (csrc/host.cu); the FeatureSet is already canonical and checked above,
+    # doorbell block (csrc/small.cu); the FeatureSet is already canonical and checked above,
     # so the call goes straight through, staged in this thread's reusable buffers
     st = _PERSET
     n = int(ids.size)
