@@ -33,7 +33,22 @@ static uint64_t powmod64(uint64_t b, uint64_t e, uint64_t m) {
     return r;
 }
 
+static bool is_prime_u64_uncached(uint64_t n);
+
+// Deterministic Miller-Rabin (the 12 bases are exact below 3.3e24).  A per-thread memo of
+// the last few primes confirmed: every signing call checks its modulus (~1.6 us of
+// 128-bit modular arithmetic, a tenth of a per-set call), and callers reuse one family.
 bool is_prime_u64(uint64_t n) {
+    static thread_local uint64_t memo[4] = {0, 0, 0, 0};
+    static thread_local unsigned next = 0;
+    for (uint64_t m : memo)
+        if (m == n && n != 0) return true;
+    if (!is_prime_u64_uncached(n)) return false;
+    memo[next++ & 3] = n;
+    return true;
+}
+
+static bool is_prime_u64_uncached(uint64_t n) {
     static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
     if (n < 2) return false;
     for (uint64_t b : bases) {
