@@ -4,7 +4,7 @@
 // arrays back (minhash.py:91-110, bench.py:97-102).  mhb_sign_csr_host is the
 // native equivalent for a whole CSR batch living in host memory: the sets are
 // cut into nnz-balanced chunks; each chunk goes H2D -> sign kernels -> D2H on
-// one of kLanes streams, so the copy engines (both directions) and the SMs
+// one of 4 stream lanes, so the copy engines (both directions) and the SMs
 // work on different chunks at the same time.  Device buffers are cached per
 // device between calls (mhb_host_release frees them).  Small batches (the per-set
 // reference API) take the paths of small.cu instead.
@@ -215,7 +215,18 @@ void host_copy_out(const uint32_t* src, void* dst, int64_t n, bool widen, int64_
 // ---- the chunked pipeline ----
 namespace {
 
-constexpr int kLanes = 4;
+constexpr int kMaxLanes = 8;
+
+// Stream lanes in use (MHB_HOST_LANES, 2..8; default 4): chunk c runs on lane c % lanes,
+// whose previous chunk must have drained before its buffers are reused.
+int host_lanes() {
+    static const int n = [] {
+        const char* e = std::getenv("MHB_HOST_LANES");
+        const int v = e ? std::atoi(e) : 4;
+        return v < 2 ? 2 : (v > kMaxLanes ? kMaxLanes : v);
+    }();
+    return n;
+}
 constexpr int kMaxChunks = 4096;
 
 struct Lane {
@@ -262,7 +273,7 @@ void host_copy_in(const uint32_t* src, uint32_t* dst, int64_t n) {
 struct DeviceCache {
     bool init = false;
     SmallStage small;
-    Lane lanes[kLanes];
+    Lane lanes[kMaxLanes];
     int32_t* status = nullptr;  // one word per chunk, read once at the end
     uint32_t* ra = nullptr;
     uint32_t* rb = nullptr;
@@ -398,6 +409,7 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     }
 
     const std::vector<Chunk> chunks = plan_chunks(indptr, n_sets, n_hash, out_bytes);
+    const int n_lanes = host_lanes();
     if (chunks.size() > (size_t)kMaxChunks) return set_error(MHB_ERR_INVALID, "batch needs more than %d chunks", kMaxChunks);
     int32_t status_acc = 0;
     // Pageable caller buffers would make every cudaMemcpyAsync synchronous (staged by the
@@ -421,11 +433,11 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     };
 
     for (size_t c = 0; c < chunks.size(); ++c) {
-        Lane& ln = dc.lanes[c % kLanes];
+        Lane& ln = dc.lanes[c % (size_t)n_lanes];
         const int64_t s0 = chunks[c].s0, s1 = chunks[c].s1, rows = s1 - s0;
         const int64_t id0 = indptr[s0], id1 = indptr[s1];
         const int64_t cnnz = id1 - id0;
-        if (c >= (size_t)kLanes) {
+        if (c >= (size_t)n_lanes) {
             // the lane's previous chunk must have drained before its buffers are reused
             if ((rc = cuda_check(cudaEventSynchronize(ln.done), "lane sync"))) return rc;
             drain(ln);
@@ -474,7 +486,7 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         }
         if ((rc = cuda_check(cudaEventRecord(ln.done, ln.stream), "event record"))) return rc;
     }
-    for (int l = 0; l < kLanes && (size_t)l < chunks.size(); ++l) {
+    for (int l = 0; l < n_lanes && (size_t)l < chunks.size(); ++l) {
         if ((rc = cuda_check(cudaStreamSynchronize(dc.lanes[l].stream), "final sync"))) return rc;
         drain(dc.lanes[l]);
     }
