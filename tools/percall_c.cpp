@@ -1,6 +1,8 @@
 // percall_c.cpp -- per-call latency of mhb_sign_csr_host for one small set, from C
 // (no Python / ctypes in the loop): the per-set reference call shape (N=128, ~50 ids).
-// Build (from tools/): g++ -O2 -I../include percall_c.cpp -L../paper_1401_6124_b200/lib -lmhb \
+// usage: percall_c [ids] [hashes] [out_dtype 0=u32 1=i64] [pinned 0/1]
+// Build (from tools/): g++ -O2 -I../include -I/usr/local/cuda/include percall_c.cpp \
+//   -L../paper_1401_6124_b200/lib -lmhb -L/usr/local/cuda/lib64 -lcudart \
 //   -Wl,-rpath,'$ORIGIN/../paper_1401_6124_b200/lib' -o percall_c
 #include <chrono>
 #include <cstdint>
