@@ -332,7 +332,7 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     n_hash = family.size
     if n > st.ids.size or (n_hash < _PERSET_WIDE and n_hash > st.out.size):
         st.grow(n, n_hash)
-    np.copyto(st.ids[:n], ids, casting="unsafe")
+    st.ids[:n] = ids  # int64 -> uint32 (ids < p < 2^32 checked above)
     st.indptr[1] = n
     if n_hash >= _PERSET_WIDE:
         # wide signatures (the reference's C6 loop: 100,000 hashes per call): a fresh result
@@ -344,8 +344,8 @@ def signature(s: FeatureSet, family: Family) -> Signature:
     if out is not None and kind == _lib.KIND_RANDOM:  # wide random family: a, b already on the device
         da, db = family.device_params(_torch().device("cuda", _torch().cuda.current_device()))
         a_ptr, b_ptr = da.data_ptr(), db.data_ptr()
-    rc = _lib.load().mhb_sign_csr_host(kind, st.indptr_ptr, st.ids_ptr, 1, n, a, b, a_ptr, b_ptr, family.prime,
-                                       n_hash, out_ptr, _lib.OUT_I64, st.status_ptr, -1)
+    rc = _sign_host()(kind, st.indptr_ptr, st.ids_ptr, 1, n, a, b, a_ptr, b_ptr, family.prime, n_hash, out_ptr,
+                      _lib.OUT_I64, st.status_ptr, -1)
     if rc:
         _lib.check(rc)
     if st.status.value:
@@ -406,6 +406,14 @@ class _PerSetStage(threading.local):
 
 
 _PERSET = _PerSetStage()
+_SIGN_HOST = []
+
+
+def _sign_host():
+    """mhb_sign_csr_host, looked up once."""
+    if not _SIGN_HOST:
+        _SIGN_HOST.append(_lib.load().mhb_sign_csr_host)
+    return _SIGN_HOST[0]
 
 
 def _percall_params(family: Family) -> tuple:
