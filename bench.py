@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark: MinHash signature entries/s on B200 (BASELINE.json metric).
 
-One step = one pass of the signing hot path (mhb_sign_iterative_csr) over one
-full batch of the workload, inputs resident in HBM.  Default workload at N=1 is
-BASELINE configs[1] ("cfg2"): 1,000,000 sets, lognormal(median 120, sigma 1.0)
-sizes capped at 20,000, Zipf(1.1) ids over 2^24, N=256 hashes, iterative family.
+One step = one pass of the signing hot path over one full batch of the workload,
+inputs resident in HBM.  The default workload is BASELINE configs[3] ("cfg4", the
+configuration the 1/2/4/8-GPU metric is quoted on): 2,000,000 sets, max(1,
+Poisson(80)) uniform ids over 2^26, N=2048 iterative hashes arranged as 128 bands x
+16 rows, whose uint64 band keys every step also emits (mhb_band_keys).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgK]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
 
-Multi-GPU is weak scaling: every rank signs its own full-size cfg2 batch (distinct
-seeds; the batch shards by rows with no exchange), value = all ranks' entries /
-max-over-ranks device time.  --impl reference times the reference algorithm's CPU
-restatement (oracle/, C + OpenMP, all host cores) on a bounded sample of the same
-workload; rank 0 only.
+Multi-GPU is the north star's split, strong scaling: ONE global batch (the same for
+every N: gen's blocked generator), cut into contiguous nnz-balanced row shards
+(dist.nnz_balanced_cuts); every rank generates only its own shard on its GPU, signs it
+with no collective in the step, and value = the batch's entries / max-over-ranks
+device time.  The gather of the uint32 signature blocks to rank 0 is reported
+beside it: the variable-size NCCL gather after signing, and the fused path whose
+kernels store straight into rank 0's matrix over NVLink.  --config cfg5 is the box
+scale (100M sets).  --impl reference times the reference algorithm's CPU restatement
+(oracle/, C + OpenMP, all host cores) on a bounded prefix of the same batch; rank 0.
 """
 from __future__ import annotations
 
@@ -41,17 +46,24 @@ def _args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg4",
+                    help="BASELINE workload: cfg1..cfg5 (default cfg4, the config the 1/2/4/8-GPU metric is quoted "
+                         "on), c6 (the reference's timing experiment) or corpus")
     ap.add_argument("--family", choices=["iterative", "random"], default="iterative")
     ap.add_argument("--n-sets", type=int, default=None, help="override the config's set count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-max-gb", type=float, default=17.0,
+                    help="job-wide host budget (uint32 output bytes per step) of the pinned e2e leg")
+    ap.add_argument("--e2e-dropin-gb", type=float, default=4.0,
+                    help="job-wide host budget (int64 output bytes per step) of the reference-convention e2e leg")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the reference-convention e2e leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
-    ap.add_argument("--gather", nargs="?", const="nccl", choices=["nccl", "peer"], default=None,
-                    help="also time gathering every rank's signatures on rank 0: 'nccl' (sign, then "
-                         "torch.distributed.gather) or 'peer' (fused: kernels store into rank 0's matrix "
-                         "over CUDA IPC / NVLink)")
+    ap.add_argument("--gather", choices=["auto", "none", "nccl", "peer"], default="auto",
+                    help="N>1: also time gathering every rank's signatures on rank 0 -- 'nccl' (sign, then "
+                         "the variable-size NCCL gather), 'peer' (fused: the kernels store into rank 0's matrix "
+                         "over CUDA IPC / NVLink), 'auto' both, 'none'")
     ap.add_argument("--corpus-lines", type=int, default=400_000, help="--config corpus: text lines")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (plan + sign + finalize launches captured once): "
@@ -161,10 +173,18 @@ def run_reference(args):
     cfg = gen.CONFIGS[args.config]
     fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
     threads = os.cpu_count() or 1
-    # bounded sample of the same workload (same generator and distributions)
+    # bounded sample of the same workload: a prefix of the same blocked global batch
+    # (gen.make_shard), so the reference arm signs exactly the sets our arm signs first
+    unit, _, _, n_total = gen.block_layout(cfg, args.n_sets)
+    ip_g = gen.global_indptr(cfg, "cpu", n_total)
+
+    def prefix(n):
+        n = min(n_total, n + (n % unit))
+        ip, ids, _ = gen.make_shard(cfg, 0, n, "cpu", n_total, indptr=ip_g)
+        return ip.numpy(), ids.numpy().view(np.uint32)
+
     n_sample = 4000
-    ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_sample)
-    ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
+    ip_h, ids_h = prefix(n_sample)
     t0 = time.perf_counter()
     oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
     dt = time.perf_counter() - t0
@@ -172,10 +192,10 @@ def run_reference(args):
     step_target = min(3.0, 90.0 / max(1, args.steps + args.warmup))
     n_step = int(max(1000, min(200_000, n_sample * step_target / max(dt, 1e-6))))
     if n_step > n_sample:
-        ip, ids = gen.make_csr(cfg, device="cpu", n_sets=n_step)
-        ip_h, ids_h = ip.numpy(), ids.numpy().view(np.uint32)
+        ip_h, ids_h = prefix(n_step)
     else:
         ip_h = ip_h[:n_step + 1]
+    n_step = ip_h.size - 1
     for _ in range(args.warmup):
         oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
     times = []
@@ -189,24 +209,28 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} sample ({n_step} sets, nnz {nnz}) of " + _workload_name(cfg, args.family),
-                   "n_hash": cfg.n_hash, "prime": cfg.prime, "family": args.family},
+        "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} sample (the first {n_step} sets, nnz {nnz}) of "
+                               + _workload_name(cfg, args.family, n_total) + "; signatures only (the reference has "
+                               "no band keys)",
+                   "n_sets": n_total, "n_hash": cfg.n_hash, "prime": cfg.prime, "family": args.family},
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "port",
-                         "sample": f"first {n_step} sets of {cfg.name} (same generator), "
+                         "sample": f"first {n_step} sets of {cfg.name} (the same blocked batch), "
                                    f"C restatement of kernels.py:21-73, OpenMP over sets"},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def _workload_name(cfg, family):
+def _workload_name(cfg, family, n_sets=None):
+    n_sets = cfg.n_sets if n_sets is None else n_sets
     if cfg.size_kind == "lognormal":
         sizes = f"lognormal(median {cfg.size_a:g}, sigma {cfg.size_b:g}) capped {cfg.size_cap}"
     else:
         sizes = f"max(1, Poisson({cfg.size_a:g}))"
     ids = f"Zipf({cfg.zipf_s:g})" if cfg.id_kind == "zipf" else "uniform"
-    return f"{cfg.n_sets} sets, {sizes}, {ids} ids over 2^{cfg.vocab_log2}, N={cfg.n_hash}, {family}"
+    what = f"{n_sets // 2} planted pairs ({n_sets} sets), base" if cfg.name == "cfg3" else f"{n_sets} sets,"
+    return f"{what} {sizes}, {ids} ids over 2^{cfg.vocab_log2}, N={cfg.n_hash}, {family}"
 
 
 def _time_cuda(fn, reps=5):
@@ -498,7 +522,8 @@ class _Ctx:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         # MHB_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- exercises the N>1 code
-        # path (barriers, max over ranks, peer gather) on a one-GPU box; its timings mean nothing
+        # path (shard generation, barriers, max over ranks, both gathers) on a one-GPU box;
+        # its timings mean nothing
         self.shared = os.environ.get("MHB_BENCH_SHARED_GPU") == "1"
         if self.shared:
             self.local = 0
@@ -516,51 +541,65 @@ class _Ctx:
         if self.world > 1:
             self.dist.barrier()
 
-    def max_over_ranks(self, x: float) -> float:
+    def _reduce(self, x: float, op) -> float:
         import torch
 
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.shared else self.dev)
         if self.world > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+            self.dist.all_reduce(t, op=op)
         return float(t.item())
 
+    def max_over_ranks(self, x: float) -> float:
+        return self._reduce(x, self.dist.ReduceOp.MAX)
 
-def _workload(args, ctx):
-    """This rank's batch of the configuration, generated on its GPU (outside any timing)."""
-    import torch
+    def sum_over_ranks(self, x: float) -> float:
+        return self._reduce(x, self.dist.ReduceOp.SUM)
 
-    from paper_1401_6124_b200 import gen
 
-    cfg = gen.CONFIGS[args.config]
-    n_sets = cfg.n_sets if args.n_sets is None else args.n_sets
-    if cfg.name == "cfg5" and args.n_sets is None:
-        n_sets = cfg.n_sets // 8  # box scale: one rank's 1/8 shard of the 100M-set batch
-    t0 = time.perf_counter()
-    exact_j = None
-    if cfg.name == "cfg3":
-        # planted near-duplicate pairs: n_sets/2 base sets, each followed by its mutant
-        indptr, ids, exact_j = gen.planted_pairs(cfg, device=ctx.dev, n_base=n_sets // 2 if args.n_sets else None,
-                                                 seed=cfg.data_seed() + ctx.rank)
-    else:
-        indptr, ids = gen.make_csr(cfg, device=ctx.dev, n_sets=n_sets, seed=cfg.data_seed() + ctx.rank)
-    torch.cuda.synchronize()
-    return cfg, indptr, ids, exact_j, time.perf_counter() - t0
+class _Workload:
+    """One global batch of the configuration, cut into nnz-balanced row shards; this
+    rank generated only its own shard, on its own GPU (gen.make_shard)."""
+
+    def __init__(self, args, ctx):
+        import torch
+
+        from paper_1401_6124_b200 import gen
+        from paper_1401_6124_b200.dist import nnz_balanced_cuts
+
+        self.cfg = cfg = gen.CONFIGS[args.config]
+        unit, _, _, self.n_total = gen.block_layout(cfg, args.n_sets)
+        t0 = time.perf_counter()
+        ip_g = gen.global_indptr(cfg, ctx.dev, self.n_total)
+        self.nnz_total = int(ip_g[-1])
+        # planted pairs (cfg3) never straddle ranks: cuts on even set indices
+        self.cuts = nnz_balanced_cuts(ip_g, ctx.world, align=unit)
+        self.s0, self.s1 = self.cuts[ctx.rank], self.cuts[ctx.rank + 1]
+        self.indptr, self.ids, self.exact_j = gen.make_shard(cfg, self.s0, self.s1, ctx.dev, self.n_total,
+                                                             indptr=ip_g)
+        del ip_g
+        torch.cuda.synchronize()
+        self.gen_s = time.perf_counter() - t0
+        self.n_sets = self.s1 - self.s0
+        self.nnz = int(self.ids.numel())
+        self.bands = 16 if cfg.name == "cfg4" else 0  # cfg4: 128 bands x 16 rows, u64 keys
 
 
 def _guard(ctx, indptr, ids, fam, out, status):
-    """Status flags clean and a few hundred rows equal to the oracle (the parity suite is in tests/)."""
+    """Status flags clean and a few hundred rows of every rank's shard equal to the oracle
+    (the parity suite is in tests/)."""
     import numpy as np
 
     if int(status.item()) != 0:
         raise SystemExit(f"device status flags {int(status.item())}")
-    if ctx.rank == 0:
-        from oracle import oracle
+    from oracle import oracle
 
-        k = 300
-        ip_h = indptr[:k + 1].cpu().numpy()
-        want = oracle.sign_family_csr(ip_h, ids[:int(ip_h[-1])].cpu().numpy().view(np.uint32), fam)
-        if not np.array_equal(out[:k].cpu().numpy().astype(np.int64), want):
-            raise SystemExit("bench guard: GPU signatures differ from the oracle")
+    k = min(300, out.shape[0])
+    if k == 0:
+        return
+    ip_h = indptr[:k + 1].cpu().numpy()
+    want = oracle.sign_family_csr(ip_h, ids[:int(ip_h[-1])].cpu().numpy().view(np.uint32), fam)
+    if not np.array_equal(out[:k].cpu().numpy().astype(np.int64), want):
+        raise SystemExit(f"bench guard: rank {ctx.rank} GPU signatures differ from the oracle")
 
 
 def _timed_steps(args, ctx, step, stream):
@@ -595,25 +634,20 @@ def _timed_steps(args, ctx, step, stream):
     return ctx.max_over_ranks(e0.elapsed_time(e1)), kms.value / max(kn.value, 1), clocks
 
 
-def _timed_graph(args, ctx, indptr, ids, fam, out, status):
+def _timed_graph(args, ctx, step):
     """The step captured once as a CUDA graph and replayed K times (after W replays),
-    timed like _timed_steps.  For launch-bound batches (cfg1) the five launches of a
-    step cost more than their kernels."""
+    timed like _timed_steps.  For launch-bound batches (cfg1) the launches of a step
+    cost more than their kernels."""
     import torch
-
-    from paper_1401_6124_b200.minhash import sign_csr_device
-
-    def step():
-        sign_csr_device(indptr, ids, fam, out, status, torch.cuda.current_stream())
 
     side = torch.cuda.Stream(ctx.dev)
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
-        step()  # workspace allocations outside the capture
+        step(torch.cuda.current_stream())  # workspace allocations outside the capture
     torch.cuda.current_stream().wait_stream(side)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
-        step()
+        step(torch.cuda.current_stream())
     stream = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 3)):
         graph.replay()
@@ -630,65 +664,84 @@ def _timed_graph(args, ctx, indptr, ids, fam, out, status):
     return ctx.max_over_ranks(e0.elapsed_time(e1))
 
 
-def _gather_peer(args, ctx, indptr, ids, fam, out, status, stream):
-    """Fused sign + gather: every step signs straight into rank 0's [world*S, N] matrix."""
+def _gather_nccl(args, ctx, W, out):
+    """Gather-inclusive leg, baseline: every rank's uint32 block to rank 0 with the
+    variable-size, unpadded dist.gather_blocks (NCCL point-to-point into rank 0's matrix
+    rows).  Returns max-over-ranks ms per gather."""
+    import torch
+
+    from paper_1401_6124_b200.dist import gather_blocks
+
+    rows = [W.cuts[r + 1] - W.cuts[r] for r in range(ctx.world)]
+    shared = ctx.shared
+
+    def once():
+        blk = out.cpu() if shared else out  # gloo (shared-GPU test mode) moves host tensors
+        full = gather_blocks(blk, rows, dst=0)
+        return full
+
+    full = once()  # warm-up (NCCL p2p setup) and the check
+    if ctx.rank == 0:
+        mine = full[:rows[0]]
+        if not torch.equal(mine.view(torch.int32).to(out.device), out.view(torch.int32)):
+            raise SystemExit("nccl gather: rank 0's rows differ")
+    del full
+    reps = 3
+    torch.cuda.synchronize()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        full = once()
+        del full
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / reps
+    ctx.barrier()
+    torch.cuda.empty_cache()
+    return ctx.max_over_ranks(ms)
+
+
+def _gather_peer(args, ctx, W, fam, out, status, stream):
+    """Gather-inclusive leg, fused: every step signs straight into rank 0's [S, N] matrix
+    (CUDA IPC mapping, NVLink stores from the signing epilogue); no separate gather."""
     import torch
 
     from paper_1401_6124_b200.dist import PeerMatrix
     from paper_1401_6124_b200.minhash import sign_csr_to_ptr
 
-    n_sets, N = out.shape
-    owner = PeerMatrix.allocate(ctx.world * n_sets, N, 4, ctx.local) if ctx.rank == 0 else None
+    N = out.shape[1]
+    owner = PeerMatrix.allocate(W.n_total, N, 4, ctx.local) if ctx.rank == 0 else None
     box = [owner.handle if owner is not None else None]
     if ctx.world > 1:
         ctx.dist.broadcast_object_list(box, src=0)
-    view = owner if ctx.rank == 0 else PeerMatrix.open(box[0], ctx.world * n_sets, N, 4, ctx.local)
-    dst_ptr = view.ptr(ctx.rank * n_sets)
-    for _ in range(args.warmup):
-        sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
-    torch.cuda.synchronize()
-    ctx.barrier()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        sign_csr_to_ptr(indptr, ids, fam, dst_ptr, False, status, stream)
-    p1.record(stream)
-    torch.cuda.synchronize()
-    pms = ctx.max_over_ranks(p0.elapsed_time(p1)) / args.steps
-    ctx.barrier()  # every rank's rows have landed
-    # each rank checks its rows of rank 0's matrix through its own mapping
-    mine = view.tensor()[ctx.rank * n_sets:(ctx.rank + 1) * n_sets]
-    if not torch.equal(mine.view(torch.int32), out.view(torch.int32)):
-        raise SystemExit(f"peer gather: rank {ctx.rank} rows in rank 0's matrix differ from its local signatures")
-    ctx.barrier()
-    if ctx.rank != 0:
-        view.close()
-    ctx.barrier()
-    if owner is not None:
-        owner.close()
-    return {"ms_per_step": pms, "entries_per_s": ctx.world * n_sets * N / (pms / 1e3),
-            "bytes_to_rank0_per_step": ctx.world * n_sets * N * 4,
-            "path": "mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC (csrc/peer.cu)"}
+    view = owner if ctx.rank == 0 else PeerMatrix.open(box[0], W.n_total, N, 4, ctx.local)
+    try:
+        dst_ptr = view.ptr(W.s0)
+        reps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
+        torch.cuda.synchronize()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
+        torch.cuda.synchronize()
+        ctx.barrier()  # every rank's rows have landed in rank 0's matrix
+        ms = ctx.max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
+        mine = view.tensor()[W.s0:W.s1]
+        ok = torch.equal(mine.view(torch.int32), out.view(torch.int32))
+        if ctx.sum_over_ranks(0.0 if ok else 1.0) > 0:
+            raise SystemExit("peer gather: a rank's rows in rank 0's matrix differ from its local signatures")
+    finally:
+        ctx.barrier()
+        if ctx.rank != 0:
+            view.close()
+        ctx.barrier()
+        if owner is not None:
+            owner.close()
+    return ms
 
 
-def _gather_nccl(ctx, out):
-    import torch
-
-    from paper_1401_6124_b200.dist import gather_blocks
-
-    torch.cuda.synchronize()
-    ctx.barrier()
-    g0 = torch.cuda.Event(enable_timing=True)
-    g1 = torch.cuda.Event(enable_timing=True)
-    g0.record()
-    gather_blocks(out, [out.shape[0]] * ctx.world)
-    g1.record()
-    torch.cuda.synchronize()
-    return g0.elapsed_time(g1)
-
-
-def _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, stream):
+def _roofline(args, ctx, W, fam, kernel_ms, ms_per_step, clocks, stream):
     """Visits/s of the main kernel against the integer peak, the register-only
     probe of the same visit sequence, and the HBM side with the ncu traffic per launch."""
     import ctypes as C
@@ -698,51 +751,65 @@ def _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, strea
     from paper_1401_6124_b200 import _lib
 
     N = fam.size
+    n_sets, nnz = W.n_sets, W.nnz
     hbm_gbs, sm_max_mhz, peak_src = _peaks()
     sms = torch.cuda.get_device_properties(ctx.dev).multi_processor_count
     k_instr = K_ITER if args.family == "iterative" else K_CW
     peak_visits = sms * 128 * sm_max_mhz * 1e6 / k_instr
     achieved_visits = N * nnz / (kernel_ms / 1e3)
     alg_bytes = 4 * nnz + 8 * (n_sets + 1) + 4 * n_sets * N
-    # the committed capture is of the full-size configuration: no traffic figure for resized runs
-    traffic, traffic_src = _ncu_traffic(args.config, args.family) if args.n_sets is None else (None, None)
+    # the committed capture is of the full-size single-GPU configuration
+    traffic, traffic_src = (_ncu_traffic(args.config, args.family) if args.n_sets is None and ctx.world == 1
+                            else (None, None))
     probe_v, probe_ms = C.c_double(0), C.c_float(0)
     probe_kind = 0 if args.family == "iterative" else (2 if fam.prime <= (1 << 23) else 1)
     _lib.check(ctx.lib.mhb_probe_visit_rate(1 << 20, probe_kind, C.byref(probe_v), C.byref(probe_ms),
                                             stream.cuda_stream))
     probe_rate = probe_v.value / (probe_ms.value / 1e3)
+    alu_ceiling = sms * 64 * sm_max_mhz * 1e6 / 1.5 if args.family == "iterative" else None
     return {
         "bound": "int", "unit": "Gvisit/s",
         "achieved": achieved_visits / 1e9, "peak": peak_visits / 1e9, "frac": achieved_visits / peak_visits,
         "traffic": traffic,
         "peak_basis": f"{sms} SMs x 128 int lanes/clk x {sm_max_mhz:g} MHz ({peak_src} sm_max_mhz) / "
-                      f"{k_instr} instr per visit; visit = (set, hash, feature)",
+                      f"{k_instr} instr per visit; visit = (set, hash, feature); this rank's shard",
         "kernel_ms": kernel_ms, "kernel_share_of_step": kernel_ms / ms_per_step,
         "frac_at_measured_clock": (achieved_visits / (sms * 128 * clocks["sm_mhz"] * 1e6 / k_instr)
                                    if clocks.get("sm_mhz") else None),
         "probe_register_only_gvisit_s": probe_rate / 1e9,
+        "probe_kind": ("iterative lookahead walk (walk2_iter's sequence), K=64" if probe_kind == 0 else
+                       "random family Shoup lanes, K=64" if probe_kind == 1 else "random family float-quotient lanes, K=16"),
         "frac_of_probe": achieved_visits / probe_rate,
+        "frac_of_alu_pipe_ceiling": (achieved_visits / alu_ceiling) if alu_ceiling else None,
         "hbm": {"algorithmic_bytes": alg_bytes, "achieved_gbs": alg_bytes / (kernel_ms / 1e3) / 1e9,
                 "peak_gbs": hbm_gbs, "frac": alg_bytes / (kernel_ms / 1e3) / 1e9 / hbm_gbs,
                 "traffic_source": traffic_src},
     }
 
 
-def _e2e(args, ctx, indptr, ids, fam, out):
-    """The same metric through the public API from pinned host buffers: every step copies
-    the inputs H2D and the signatures D2H inside the timed region."""
+def _e2e_rows(W, n_hash, world, budget_bytes, itemsize):
+    """Rows of this rank's shard (a prefix) whose output fits the job-wide host budget."""
+    per_rank = budget_bytes // max(1, world)
+    return int(min(W.n_sets, max(1, per_rank // (n_hash * itemsize))))
+
+
+def _e2e(args, ctx, W, fam, out):
+    """The metric through the public API with host buffers, H2D and D2H inside the
+    timed region (pinned numpy in, uint32 numpy out: the contract's e2e)."""
     import numpy as np
     import torch
 
     from paper_1401_6124_b200 import signatures_csr
 
-    n_sets, N = out.shape
-    ip_pin = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
-    ids_pin = torch.empty(ids.shape, dtype=torch.int32, pin_memory=True)
-    out_pin = torch.empty((n_sets, N), dtype=torch.int32, pin_memory=True)
-    ip_pin.copy_(indptr)
-    ids_pin.copy_(ids.view(torch.int32))
-    ip_np, ids_np = ip_pin.numpy(), ids_pin.numpy().view(np.uint32)
+    N = fam.size
+    rows = _e2e_rows(W, N, ctx.world, int(args.e2e_max_gb * 1e9), 4)
+    nnz = int(W.indptr[rows])
+    ip_pin = torch.empty(rows + 1, dtype=torch.int64, pin_memory=True)
+    ids_pin = torch.empty(max(nnz, 1), dtype=torch.int32, pin_memory=True)
+    out_pin = torch.empty((rows, N), dtype=torch.int32, pin_memory=True)
+    ip_pin.copy_(W.indptr[:rows + 1])
+    ids_pin[:nnz].copy_(W.ids[:nnz].view(torch.int32))
+    ip_np, ids_np = ip_pin.numpy(), ids_pin.numpy()[:nnz].view(np.uint32)
     out_np = out_pin.numpy().view(np.uint32)
     signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)  # warm buffers
     ctx.barrier()
@@ -751,14 +818,62 @@ def _e2e(args, ctx, indptr, ids, fam, out):
         t0 = time.perf_counter()
         signatures_csr(ip_np, ids_np, fam, out_dtype="uint32", out=out_np)
         times.append(time.perf_counter() - t0)
-    if not np.array_equal(out_np[:1000], out[:1000].cpu().numpy()):
+    k = min(1000, rows)
+    if not np.array_equal(out_np[:k], out[:k].cpu().numpy()):
         raise SystemExit("e2e output differs from the device path")
     e2e_max = ctx.max_over_ranks(statistics.mean(times))
-    return {"value": ctx.world * n_sets * N / e2e_max, "unit": "entries/s",
-            "h2d_bytes_per_step": int(ip_np.nbytes + ids_np.nbytes), "d2h_bytes_per_step": int(out_np.nbytes),
-            "ms_per_step": e2e_max * 1e3,
-            "path": "signatures_csr(numpy pinned) -> mhb_sign_csr_host (chunked H2D/kernels/D2H on 4 streams)",
-            "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
+    total_rows = ctx.sum_over_ranks(rows)
+    res = {"value": total_rows * N / e2e_max, "unit": "entries/s",
+           "h2d_bytes_per_step": int(ctx.sum_over_ranks(ip_np.nbytes + ids_np.nbytes)),
+           "d2h_bytes_per_step": int(ctx.sum_over_ranks(out_np.nbytes)),
+           "ms_per_step": e2e_max * 1e3, "sets_per_step": int(total_rows),
+           "path": "signatures_csr(pinned numpy indptr/ids, out=pinned uint32) -> mhb_sign_csr_host "
+                   "(chunked H2D/kernels/D2H on 4 streams)",
+           "sample": ("whole batch" if total_rows == W.n_total else
+                      f"first {rows} sets of each rank's shard (host budget {args.e2e_max_gb:g} GB of uint32 "
+                      f"output per step)"),
+           "pcie_ceiling": "measured 54/55 GB/s one way, 47 GB/s each way concurrently (tools/pcie_probe.py)"}
+    del ip_pin, ids_pin, out_pin
+    return res
+
+
+def _e2e_reference_convention(args, ctx, W, fam, out):
+    """The reference's calling convention (kernels.py:29,51-52): ordinary pageable numpy
+    ids in, a FRESH int64 numpy array out, allocated by the call as the reference's
+    kernel allocates its output -- `signatures_csr(indptr, ids, family)`."""
+    import numpy as np
+
+    from paper_1401_6124_b200 import signatures_csr
+
+    N = fam.size
+    rows = _e2e_rows(W, N, ctx.world, int(args.e2e_dropin_gb * 1e9), 8)
+    nnz = int(W.indptr[rows])
+    ip_np = W.indptr[:rows + 1].cpu().numpy().copy()
+    ids_np = W.ids[:nnz].cpu().numpy().view(np.uint32).copy()
+    res = signatures_csr(ip_np, ids_np, fam)  # warm
+    del res
+    ctx.barrier()
+    times = []
+    for _ in range(max(2, args.e2e_steps)):
+        t0 = time.perf_counter()
+        res = signatures_csr(ip_np, ids_np, fam)
+        times.append(time.perf_counter() - t0)
+        if _ + 1 < max(2, args.e2e_steps):
+            del res
+    k = min(1000, rows)
+    if res.dtype != np.int64 or not np.array_equal(res[:k], out[:k].cpu().numpy().astype(np.int64)):
+        raise SystemExit("drop-in e2e output differs from the device path")
+    del res
+    t = ctx.max_over_ranks(statistics.mean(times))
+    total_rows = ctx.sum_over_ranks(rows)
+    return {"value": total_rows * N / t, "unit": "entries/s", "ms_per_step": t * 1e3, "sets_per_step": int(total_rows),
+            "h2d_bytes_per_step": int(ctx.sum_over_ranks(ip_np.nbytes + ids_np.nbytes)),
+            "d2h_bytes_per_step": int(ctx.sum_over_ranks(rows * N * 4)),
+            "result_bytes_per_step": int(ctx.sum_over_ranks(rows * N * 8)),
+            "path": "signatures_csr(pageable numpy indptr/ids) -> fresh int64 numpy [S, N] (mhb_sign_csr_host: "
+                    "pinned staging lanes, uint32 over PCIe, widened on the host)",
+            "sample": f"first {rows} sets of each rank's shard (host budget {args.e2e_dropin_gb:g} GB of int64 "
+                      f"output per step)"}
 
 
 def _per_set(ctx):
@@ -789,17 +904,39 @@ def _per_set(ctx):
     return res
 
 
-def _cpu_baseline(args, indptr, ids, fam, n_sets):
-    """The oracle port on all host cores (and on one) over a bounded prefix of the batch."""
+def _cpu_baseline(args, W, fam):
+    """The oracle port on all host cores (and on one) over a bounded sample of the batch.
+    cfg5: the north star's 1% subsample (the first 1% of the sets -- i.i.d. blocks of the
+    same generator), timed in full and extrapolated x100."""
     import numpy as np
 
     threads = os.cpu_count() or 1
-    ip_h = indptr.cpu().numpy()
-    ids_h = ids.cpu().numpy().view(np.uint32)
+    if W.cfg.name == "cfg5":
+        from oracle import oracle
+
+        n1 = max(1, W.n_total // 100)
+        if n1 <= W.n_sets:
+            ip_h = W.indptr[:n1 + 1].cpu().numpy()
+            ids_h = W.ids[:int(ip_h[-1])].cpu().numpy().view(np.uint32)
+        else:  # shard smaller than the subsample: generate it on this GPU
+            from paper_1401_6124_b200 import gen
+
+            ip_t, ids_t, _ = gen.make_shard(W.cfg, 0, n1, W.ids.device, W.n_total)
+            ip_h, ids_h = ip_t.cpu().numpy(), ids_t.cpu().numpy().view(np.uint32)
+        t0 = time.perf_counter()
+        oracle.sign_family_csr(ip_h, ids_h, fam, threads=threads)
+        dt = time.perf_counter() - t0
+        return {"value": n1 * fam.size / dt, "unit": "entries/s", "cores": threads, "kind": "port",
+                "sample": f"1% subsample: the first {n1} of {W.n_total} sets (nnz {int(ip_h[-1])}), {dt:.1f} s; "
+                          f"extrapolated x100 = {dt * 100:.0f} s for the whole batch; C restatement of "
+                          f"kernels.py:44-73, OpenMP over sets",
+                "extrapolated_batch_seconds": dt * W.n_total / n1}
+    ip_h = W.indptr.cpu().numpy()
+    ids_h = W.ids.cpu().numpy().view(np.uint32)
     v, n_s, nnz_s, dt = cpu_baseline_run(ip_h, ids_h, fam, args.cpu_seconds, threads)
     v1, n1, _, dt1 = cpu_baseline_run(ip_h, ids_h, fam, min(3.0, args.cpu_seconds / 4), 1)
     return {"value": v, "unit": "entries/s", "cores": threads, "kind": "port",
-            "sample": f"first {n_s} of {n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
+            "sample": f"first {n_s} of {W.n_sets} sets (nnz {nnz_s}) of the same batch, {dt:.1f} s, "
                       f"C restatement of kernels.py:44-73 / 21-41, OpenMP over sets",
             "value_1core": v1, "sample_1core": f"first {n1} sets, {dt1:.1f} s, one thread"}
 
@@ -815,71 +952,105 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    import numpy as np
     import torch
 
-    from paper_1401_6124_b200 import make_family
+    from paper_1401_6124_b200 import band_keys, make_family
     from paper_1401_6124_b200.minhash import sign_csr_device
 
     ctx = _Ctx()
-    cfg, indptr, ids, exact_j, gen_s = _workload(args, ctx)
-    n_sets, nnz = indptr.numel() - 1, int(ids.numel())
+    W = _Workload(args, ctx)
+    cfg = W.cfg
     fam = make_family(args.family, cfg.family_seed(args.family), cfg.n_hash, cfg.prime)
     N = fam.size
-    out = torch.empty((n_sets, N), dtype=torch.uint32, device=ctx.dev)
+    out = torch.empty((W.n_sets, N), dtype=torch.uint32, device=ctx.dev)
+    keys = torch.empty((W.n_sets, N // W.bands), dtype=torch.uint64, device=ctx.dev) if W.bands else None
     status = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
     stream = torch.cuda.current_stream(ctx.dev)
 
-    def step():  # one pass of the hot path over the resident batch
-        sign_csr_device(indptr, ids, fam, out, status, stream)
+    def step(st=stream):  # one pass of the hot path over this rank's resident shard
+        if W.n_sets:
+            sign_csr_device(W.indptr, W.ids, fam, out, status, st)
+            if keys is not None:  # cfg4: LSH band keys (uint64) emitted from the signatures
+                band_keys(out, W.bands, keys=keys, stream=st)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    _guard(ctx, indptr, ids, fam, out, status)
+    _guard(ctx, W.indptr, W.ids, fam, out, status)
+    if keys is not None and W.n_sets:
+        from oracle import oracle
+
+        k = min(200, W.n_sets)
+        want = oracle.band_keys(out[:k].cpu().numpy(), W.bands)
+        if not np.array_equal(keys[:k].cpu().numpy().view(np.uint64), want):
+            raise SystemExit("bench guard: band keys differ from the oracle")
 
     max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream)
     eager_ms = None
     if args.graph:
         eager_ms = max_ms / args.steps
         out.view(torch.int32).zero_()
-        max_ms = _timed_graph(args, ctx, indptr, ids, fam, out, status)
-        _guard(ctx, indptr, ids, fam, out, status)  # the replays produced the signatures
+        max_ms = _timed_graph(args, ctx, step)
+        _guard(ctx, W.indptr, W.ids, fam, out, status)  # the replays produced the signatures
     ms_per_step = max_ms / args.steps
-    value = ctx.world * n_sets * N * args.steps / (max_ms / 1e3)
+    value = W.n_total * N * args.steps / (max_ms / 1e3)
 
-    gather_peer = _gather_peer(args, ctx, indptr, ids, fam, out, status, stream) if args.gather == "peer" else None
-    gather_ms = _gather_nccl(ctx, out) if ctx.world > 1 and args.gather == "nccl" else None
-    roofline = _roofline(args, ctx, fam, n_sets, nnz, kernel_ms, ms_per_step, clocks, stream)
-    e2e = None if args.no_e2e else _e2e(args, ctx, indptr, ids, fam, out)
-    aux = _aux_kernels(cfg, fam, indptr, ids, out, exact_j, ctx.dev) if args.aux else None
-    cpu = (_cpu_baseline(args, indptr, ids, fam, n_sets)
-           if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None)
+    gather = None
+    if ctx.world > 1 and args.gather != "none":
+        gather = {"bytes_to_rank0_per_step": W.n_total * N * 4}
+        try:
+            if args.gather in ("auto", "nccl"):
+                g_ms = _gather_nccl(args, ctx, W, out)
+                gather["nccl"] = {"ms": g_ms, "gbs_into_rank0": W.n_total * N * 4 / (g_ms / 1e3) / 1e9,
+                                  "compute_plus_gather_entries_per_s": W.n_total * N / ((ms_per_step + g_ms) / 1e3),
+                                  "path": "sign on every rank, then dist.gather_blocks: variable-size unpadded "
+                                          "NCCL send/recv straight into rank 0's [S, N] rows"}
+            if args.gather in ("auto", "peer"):
+                p_ms = _gather_peer(args, ctx, W, fam, out, status, stream)
+                gather["peer"] = {"ms_per_step": p_ms, "entries_per_s": W.n_total * N / (p_ms / 1e3),
+                                  "path": "fused: mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC "
+                                          "(epilogue stores cross NVLink tile by tile; csrc/peer.cu)"}
+        except SystemExit:
+            raise
+        except Exception as e:  # noqa: BLE001 -- the compute-phase line still stands
+            gather["error"] = f"{type(e).__name__}: {e}"
+    roofline = _roofline(args, ctx, W, fam, kernel_ms, ms_per_step, clocks, stream)
+    e2e = None if args.no_e2e or not W.n_sets else _e2e(args, ctx, W, fam, out)
+    e2e_ref = (None if args.no_e2e or args.no_dropin or not W.n_sets
+               else _e2e_reference_convention(args, ctx, W, fam, out))
+    aux = (_aux_kernels(cfg, fam, W.indptr, W.ids, out, W.exact_j, ctx.dev)
+           if args.aux and ctx.rank == 0 else None)
+    cpu = _cpu_baseline(args, W, fam) if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None
     per_set = _per_set(ctx) if ctx.rank == 0 and ctx.world == 1 and not args.no_e2e else None
+    launches = (5 + (1 if keys is not None else 0)) * args.steps  # plan x3, sign, finalize (+ band keys)
 
     if ctx.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": ctx.world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if ctx.world > 1 else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: " + _workload_name(cfg, args.family), "n_sets_per_rank": n_sets,
-                       "nnz_per_rank": nnz, "n_hash": N, "prime": cfg.prime, "family": args.family,
-                       "out": "uint32 argmin ids, resident in HBM",
-                       "l2": "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per step vs 126 MB L2)"
-                             % (4 * nnz / 1e9, 4 * n_sets * N / 1e9),
+            "config": {"workload": f"{cfg.name}: " + _workload_name(cfg, args.family, W.n_total)
+                                   + (f"; {W.bands}-row band keys (uint64) per step" if W.bands else ""),
+                       "n_sets": W.n_total, "nnz": W.nnz_total, "n_hash": N, "prime": cfg.prime,
+                       "family": args.family, "out": "uint32 argmin ids, resident in HBM",
+                       "split": (f"one global batch, nnz-balanced row shards {W.cuts} (dist.nnz_balanced_cuts); "
+                                 f"every rank generated only its own shard (gen.make_shard)"),
+                       "shard_sets_rank0": W.n_sets, "shard_nnz_rank0": W.nnz,
+                       "l2": "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per rank per step vs 126 MB L2)"
+                             % (4 * W.nnz / 1e9, 4 * W.n_sets * N / 1e9),
                        "parallelism": f"dp{ctx.world} (row shards, no collective in the step)",
-                       "gen_seconds": round(gen_s, 2)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": 5 * args.steps, "clocks": clocks,  # plan_count, plan_scan, plan_scatter, sign, finalize
+                       "gen_seconds": round(W.gen_s, 2)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_reference_convention": e2e_ref,
+            "gpu_launches": launches, "clocks": clocks,
         }
         if per_set is not None:
             line["per_set"] = per_set
         if eager_ms is not None:
-            line["graph"] = {"replayed": True, "eager_ms_per_step": eager_ms,
-                             "launches_per_replay": 5}
-        if gather_ms is not None:
-            line["gather_ms"] = gather_ms
-        if gather_peer is not None:
-            line["gather_peer"] = gather_peer
+            line["graph"] = {"replayed": True, "eager_ms_per_step": eager_ms, "launches_per_replay": launches // args.steps}
+        if gather is not None:
+            line["gather"] = gather
         if aux is not None:
             line["aux"] = aux
         print(json.dumps(line), flush=True)

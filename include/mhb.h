@@ -198,6 +198,15 @@ int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x,
 int mhb_bucket_hist_random(const uint32_t* xs, int64_t n_x,
                            const uint32_t* a, const uint32_t* b, uint64_t prime, int32_t n_hash,
                            uint32_t buckets, unsigned long long* counts, void* stream);
+/*
+ * The same counts for any prime up to 2^63 (families.py:105-112 counts for every
+ * prime): kind 0 = iterative (a, b), kind 1 = random (device uint64 arrays ra, rb);
+ * xs are uint64 (< prime).  64-bit residues; the u32 entries above route iterative
+ * families with 2^31 <= prime here themselves.
+ */
+int mhb_bucket_hist_u64(int32_t kind, const uint64_t* xs, int64_t n_x, uint64_t a, uint64_t b,
+                        const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash,
+                        uint64_t buckets, unsigned long long* counts, void* stream);
 
 /*
  * Signature-file records from a device signature block (the reference's formats,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "mhb_format_text_records": (C.c_int, [_P, _I32, _I64, _I32, _P, _I64, _P, _P, _P]),
     "mhb_bucket_hist_iterative": (C.c_int, [_P, _I64, _U64, _U64, _U64, _I32, _U32, _P, _P]),
     "mhb_bucket_hist_random": (C.c_int, [_P, _I64, _P, _P, _U64, _I32, _U32, _P, _P]),
+    "mhb_bucket_hist_u64": (C.c_int, [_I32, _P, _I64, _U64, _U64, _P, _P, _U64, _I32, _U64, _P, _P]),
     "mhb_corpus_scan": (C.c_int, [_P, _I64, _I32, _P]),
     "mhb_corpus_scan_device": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "mhb_corpus_info": (C.c_int, [_P, _P, _P]),

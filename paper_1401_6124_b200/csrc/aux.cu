@@ -101,10 +101,23 @@ __global__ void jaccard_block_kernel(const T* __restrict__ A, int64_t n_rows, co
 }
 
 // ---------------------------------------------------------------------------
-// Bucket histogram.  Work unit = (x, run of up to kRun consecutive members).
-// Bins live in shared memory when they fit (privatised per CTA), else in global.
+// Bucket histogram (stats.py:221-224 generalised to a batch of x): counts[b] =
+// #{(x, i) : h_i(x) mod m = b}.
+//
+// One count per (x, i) evaluation.  Shared-memory atomics on one CTA-wide table
+// serialise on bank conflicts (uniform bins over 4096 entries: ~3.5 lanes per bank per
+// warp access, 4.7 counts/clk/SM measured in round 1).  hist_rep_kernel gives every
+// lane of the warp its OWN replica of the table in its OWN bank: lane L's byte counter
+// for bin b lives in word (b >> 2) * 32 + L, byte b & 3, so a warp's 32 ATOMS land in
+// 32 distinct banks -- one wavefront per instruction.  32 replicas x m bytes fit 128 KB
+// for m <= 4096.  Byte counters carry 127 at most: the increment that moves a byte from
+// 127 to 128 (bit 7 flips; exactly one thread observes it, atomics being serialised)
+// moves 128 into the global count and subtracts it back out.  The byte never wraps
+// in between (the replica is shared by one lane of each warp: a few in-flight
+// increments, far below 128), so no carry ever reaches a neighbouring bin.
 // ---------------------------------------------------------------------------
 constexpr int kRun = 256;
+constexpr int kRepMaxBins = 4096;  // 32 replicas x 4096 one-byte counters = 128 KB
 
 struct HistArgs {
     const uint32_t* xs;
@@ -118,6 +131,7 @@ struct HistArgs {
     unsigned long long* counts;
     int kind;
     int use_smem;
+    int nblk, run;   // hist_rep_kernel: lane blocks per x (power of two) and lanes per block
 };
 
 __device__ __forceinline__ uint32_t mod_bucket(uint32_t h, uint32_t m, uint32_t mp) {
@@ -126,6 +140,163 @@ __device__ __forceinline__ uint32_t mod_bucket(uint32_t h, uint32_t m, uint32_t 
     return __viaddmin_u32(r, 0u - m, r);
 }
 
+// 1 << (8 * (s & 3)) in one PRMT: backward-4-extract of the byte string {1,0,0,0,0,0,0,0}.
+__device__ __forceinline__ uint32_t byte_one(uint32_t s) {
+    uint32_t d;
+    asm("prmt.b32.b4e %0, %1, %2, %3;" : "=r"(d) : "r"(1u), "r"(0u), "r"(s));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void reds_add(uint32_t saddr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
+// One evaluation's count: the lane's byte for bin = h mod m lives in word
+// (bin >> 2) * 32 + lane, byte bin & 3 (`rep_lane` = shared address of word `lane`;
+// POW2: m >= 4 is a power of two, so bin & 3 = h & 3 and the byte select reads h).
+// Returns (new ^ old) of the counter word: bit 7 of a byte flips only when this
+// increment took that byte from 127 to 128 (no other byte changes: no carries).
+template <bool POW2>
+__device__ __forceinline__ uint32_t count_bin(uint32_t rep_lane, uint32_t h, uint32_t m, uint32_t mp,
+                                              uint32_t wmask) {
+    uint32_t addr, inc;
+    if (POW2) {
+        addr = (h & wmask) * 32u + rep_lane;  // wmask = (m - 1) & ~3
+        inc = byte_one(h);
+    } else {
+        const uint32_t bin = mod_bucket(h, m, mp);
+        addr = (bin & ~3u) * 32u + rep_lane;
+        inc = byte_one(bin);
+    }
+    const uint32_t old = atoms_add(addr, inc);
+    return (old + inc) ^ old;
+}
+
+// The evaluation of `h` moved its byte to 128: take the 128 out again and add it to
+// the global count.  Deferring this by a few evaluations is safe: until the
+// subtraction lands the byte only grows by the few increments in flight from the
+// threads sharing the replica (<< 127).
+template <bool POW2>
+__device__ __forceinline__ void spill_bin(uint32_t rep_lane, uint32_t h, uint32_t m, uint32_t mp,
+                                          unsigned long long* counts) {
+    const uint32_t bin = POW2 ? (h & (m - 1)) : mod_bucket(h, m, mp);
+    reds_add((bin & ~3u) * 32u + rep_lane, 0u - (byte_one(bin) << 7));
+    atomicAdd(counts + bin, 128ull);
+}
+
+constexpr uint32_t kBit7 = 0x80808080u;
+
+template <bool ITER, bool POW2, int RL>
+__global__ void __launch_bounds__(512) hist_rep_kernel(HistArgs H) {
+    extern __shared__ uint32_t rep[];  // [ceil(m/4)][32] words
+    const int words = (int)((H.m + 3) >> 2) * 32;
+    for (int i = threadIdx.x; i < words; i += blockDim.x) rep[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t rep_lane = (uint32_t)__cvta_generic_to_shared(rep + lane);
+    const uint32_t p = H.p, m = H.m, mp = H.mp;
+    const uint32_t wmask = (m - 1) & ~3u;
+    unsigned long long* counts = H.counts;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;  // a multiple of nblk
+    // this thread's lane block is fixed: units u = gtid + k * nthreads, blk = u % nblk
+    const int blk = (int)(gtid & (H.nblk - 1));
+    const int32_t i0 = blk * H.run;
+    const int32_t i1 = min(i0 + H.run, H.n_hash);
+    const int n = i1 - i0;
+    const int64_t xstride = nthreads / H.nblk;
+    if (ITER) {
+        // h_{i0}(x) = (a + i0) x + i0 b mod p (families.py:170-176), then the additive walk
+        const uint32_t A = (uint32_t)((H.a + (uint64_t)i0) % p);
+        const uint32_t Ap = shoup_companion(A, p);
+        const uint32_t B = (uint32_t)((uint64_t)i0 * H.b % p);
+        for (int64_t xi = gtid / H.nblk; xi < H.n_x && n > 0; xi += xstride) {
+            const uint32_t x = __ldg(H.xs + xi);
+            uint32_t h = mul_add_mod(A, Ap, B, x, p);
+            const uint32_t dh = reduce_once(x + H.b, p);
+            int k = 0;
+            // four evaluations per check of the 127 -> 128 flags
+            for (; k + 4 <= n; k += 4) {
+                const uint32_t h0 = h;
+                const uint32_t f0 = count_bin<POW2>(rep_lane, h0, m, mp, wmask);
+                const uint32_t h1 = reduce_once(h0 + dh, p);
+                const uint32_t f1 = count_bin<POW2>(rep_lane, h1, m, mp, wmask);
+                const uint32_t h2 = reduce_once(h1 + dh, p);
+                const uint32_t f2 = count_bin<POW2>(rep_lane, h2, m, mp, wmask);
+                const uint32_t h3 = reduce_once(h2 + dh, p);
+                const uint32_t f3 = count_bin<POW2>(rep_lane, h3, m, mp, wmask);
+                h = reduce_once(h3 + dh, p);
+                if ((f0 | f1 | f2 | f3) & kBit7) {
+                    if (f0 & kBit7) spill_bin<POW2>(rep_lane, h0, m, mp, counts);
+                    if (f1 & kBit7) spill_bin<POW2>(rep_lane, h1, m, mp, counts);
+                    if (f2 & kBit7) spill_bin<POW2>(rep_lane, h2, m, mp, counts);
+                    if (f3 & kBit7) spill_bin<POW2>(rep_lane, h3, m, mp, counts);
+                }
+            }
+            for (; k < n; ++k) {
+                if (count_bin<POW2>(rep_lane, h, m, mp, wmask) & kBit7) spill_bin<POW2>(rep_lane, h, m, mp, counts);
+                h = reduce_once(h + dh, p);
+            }
+        }
+    } else {
+        // random family: RL lanes' constants in registers (Shoup companions), one
+        // multiply-add per evaluation
+        uint32_t cA[RL], cAp[RL], cB[RL];
+#pragma unroll
+        for (int k = 0; k < RL; ++k) {
+            const int32_t i = min(i0 + k, H.n_hash - 1);
+            cA[k] = H.ra[i];
+            cAp[k] = shoup_companion(cA[k], p);
+            cB[k] = H.rb[i];
+        }
+        const bool narrow = 3ull * p < (1ull << 32);
+        for (int64_t xi = gtid / H.nblk; xi < H.n_x && n > 0; xi += xstride) {
+            const uint32_t x = __ldg(H.xs + xi);
+            if (n == RL && narrow) {
+#pragma unroll
+                for (int k = 0; k < RL; k += 4) {
+                    uint32_t hh[4], f[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        hh[e] = mul_add_mod_narrow(cA[k + e], cAp[k + e], cB[k + e], x, p);
+                        f[e] = count_bin<POW2>(rep_lane, hh[e], m, mp, wmask);
+                    }
+                    if ((f[0] | f[1] | f[2] | f[3]) & kBit7) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (f[e] & kBit7) spill_bin<POW2>(rep_lane, hh[e], m, mp, counts);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < RL; ++k) {
+                    if (k < n) {
+                        const uint32_t hk = mul_add_mod(cA[k], cAp[k], cB[k], x, p);
+                        if (count_bin<POW2>(rep_lane, hk, m, mp, wmask) & kBit7) spill_bin<POW2>(rep_lane, hk, m, mp, counts);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // fold the 32 byte replicas of every bin into the global counts
+    for (uint32_t bin = threadIdx.x; bin < m; bin += blockDim.x) {
+        const uint32_t* wrow = rep + ((bin >> 2) << 5);
+        const int sh = (int)(bin & 3) * 8;
+        uint32_t c = 0;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) c += (wrow[r] >> sh) & 0xFFu;
+        if (c) atomicAdd(counts + bin, (unsigned long long)c);
+    }
+}
+
+// Fallback for m > 4096 (or p >= 2^31 is handled below): one u32 table per CTA in
+// shared memory when it fits, else global atomics.
 __global__ void hist_kernel(HistArgs H) {
     extern __shared__ uint32_t bins[];
     if (H.use_smem) {
@@ -142,11 +313,10 @@ __global__ void hist_kernel(HistArgs H) {
         const int32_t i1 = min(i0 + kRun, H.n_hash);
         const uint32_t x = H.xs[xi];
         if (H.kind == 0) {
-            // h_{i0}(x) = (a + i0) x + i0 b mod p, then the additive walk (families.py:153-176)
-            const uint64_t A = (H.a + (uint64_t)i0) % p;
-            const uint64_t Bv = (uint64_t)i0 * H.b % p;
-            uint32_t h = (uint32_t)((A * (x % p) + Bv) % p);
-            const uint32_t dh = (uint32_t)(((uint64_t)x + H.b) % p);
+            const uint32_t A = (uint32_t)((H.a + (uint64_t)i0) % p);
+            const uint32_t B = (uint32_t)((uint64_t)i0 * H.b % p);
+            uint32_t h = mul_add_mod(A, shoup_companion(A, p), B, x, p);
+            const uint32_t dh = reduce_once(x + H.b, p);
             for (int32_t i = i0; i < i1; ++i) {
                 const uint32_t bin = mod_bucket(h, H.m, H.mp);
                 if (H.use_smem) atomicAdd(&bins[bin], 1u);
@@ -155,7 +325,8 @@ __global__ void hist_kernel(HistArgs H) {
             }
         } else {
             for (int32_t i = i0; i < i1; ++i) {
-                const uint32_t h = (uint32_t)(((uint64_t)H.ra[i] * (x % p) + H.rb[i]) % p);
+                const uint32_t a = H.ra[i];
+                const uint32_t h = mul_add_mod(a, shoup_companion(a, p), H.rb[i], x, p);
                 const uint32_t bin = mod_bucket(h, H.m, H.mp);
                 if (H.use_smem) atomicAdd(&bins[bin], 1u);
                 else atomicAdd(&H.counts[bin], 1ull);
@@ -169,6 +340,75 @@ __global__ void hist_kernel(HistArgs H) {
     }
 }
 
+// Primes 2^31 <= p < 2^63 (the reference counts for any prime, families.py:105-112):
+// 64-bit residues with 128-bit products, global atomics.  Correctness path.
+__device__ __forceinline__ uint64_t hist_mulmod64(uint64_t a, uint64_t b, uint64_t p) {
+    return (uint64_t)(((unsigned __int128)a * b) % p);
+}
+
+template <typename IdT>
+__global__ void hist_wide_kernel(const IdT* __restrict__ xs, int64_t n_x, int kind, uint64_t a, uint64_t b,
+                                 const uint64_t* __restrict__ ra, const uint64_t* __restrict__ rb, uint64_t p,
+                                 int32_t n_hash, uint64_t m, unsigned long long* __restrict__ counts) {
+    const int64_t runs_per_x = (n_hash + kRun - 1) / kRun;
+    const int64_t units = n_x * runs_per_x;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xi = u / runs_per_x;
+        const int32_t i0 = (int32_t)(u - xi * runs_per_x) * kRun;
+        const int32_t i1 = min(i0 + kRun, n_hash);
+        const uint64_t x = (uint64_t)xs[xi];
+        if (kind == 0) {
+            uint64_t h = (hist_mulmod64((a + (uint64_t)i0) % p, x, p) + hist_mulmod64((uint64_t)i0, b, p)) % p;
+            uint64_t dh = x + b;  // x, b < p < 2^63
+            if (dh >= p) dh -= p;
+            for (int32_t i = i0; i < i1; ++i) {
+                atomicAdd(&counts[h % m], 1ull);
+                h += dh;
+                if (h >= p) h -= p;
+            }
+        } else {
+            for (int32_t i = i0; i < i1; ++i) {
+                uint64_t h = hist_mulmod64(ra[i], x, p) + rb[i];
+                if (h >= p) h -= p;
+                atomicAdd(&counts[h % m], 1ull);
+            }
+        }
+    }
+}
+
+template <bool ITER, bool POW2>
+static int launch_rep(HistArgs H, const DeviceInfo& dev, cudaStream_t st) {
+    constexpr int RL = ITER ? 1 : 16;
+    auto fn = hist_rep_kernel<ITER, POW2, RL>;
+    const size_t smem = (size_t)((H.m + 3) / 4) * 32 * sizeof(uint32_t);
+    static int attr_done[64] = {0};
+    if (dev.device >= 0 && dev.device < 64 && !attr_done[dev.device]) {
+        int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kRepMaxBins / 4 * 32 * (int)sizeof(uint32_t)),
+                            "hist_rep smem attr");
+        if (rc) return rc;
+        attr_done[dev.device] = 1;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512, smem) != cudaSuccess || occ < 1) occ = 1;
+    // lane blocks per x: a power of two (so the grid's thread count is a multiple of it)
+    // with about 64 lanes each for the iterative walk, RL for the random family
+    const int want = ITER ? (H.n_hash + 63) / 64 : (H.n_hash + RL - 1) / RL;
+    int nblk = 1;
+    while (nblk < want && nblk < 512) nblk *= 2;
+    H.nblk = nblk;
+    H.run = (H.n_hash + nblk - 1) / nblk;
+    if (!ITER && H.run > RL) {  // more lanes than 512 blocks of RL: not representable
+        return set_error(MHB_ERR_UNSUPPORTED, "random-family histogram over %d members", H.n_hash);
+    }
+    int64_t blocks = (int64_t)occ * dev.sms;
+    const int64_t need = (H.n_x * nblk + 511) / 512;  // one unit per thread is enough
+    if (blocks > need) blocks = need < 1 ? 1 : need;
+    fn<<<(unsigned)blocks, 512, smem, st>>>(H);
+    return cuda_check(cudaGetLastError(), "hist_rep_kernel launch");
+}
+
 static int launch_hist(HistArgs H, cudaStream_t st) {
     clear_error();
     if (H.m < 1) return set_error(MHB_ERR_INVALID, "need at least one bucket, got %u", H.m);
@@ -179,6 +419,12 @@ static int launch_hist(HistArgs H, cudaStream_t st) {
     DeviceInfo dev;
     int rc = current_device_info(&dev);
     if (rc) return rc;
+    const bool pow2 = H.m >= 4 && (H.m & (H.m - 1)) == 0;
+    const bool rep_ok = H.m <= (uint32_t)kRepMaxBins && (H.kind == 0 || H.n_hash <= 512 * 16);
+    if (rep_ok) {
+        if (H.kind == 0) return pow2 ? launch_rep<true, true>(H, dev, st) : launch_rep<true, false>(H, dev, st);
+        return pow2 ? launch_rep<false, true>(H, dev, st) : launch_rep<false, false>(H, dev, st);
+    }
     size_t smem = (size_t)H.m * sizeof(uint32_t);
     H.use_smem = smem <= 96 * 1024;
     if (!H.use_smem) smem = 0;
@@ -193,6 +439,22 @@ static int launch_hist(HistArgs H, cudaStream_t st) {
     if (blocks < 1) blocks = 1;
     hist_kernel<<<(unsigned)blocks, 256, smem, st>>>(H);
     return cuda_check(cudaGetLastError(), "hist_kernel launch");
+}
+
+template <typename IdT>
+static int launch_hist_wide(const IdT* xs, int64_t n_x, int kind, uint64_t a, uint64_t b, const uint64_t* ra,
+                            const uint64_t* rb, uint64_t p, int32_t n_hash, uint64_t m,
+                            unsigned long long* counts, cudaStream_t st) {
+    if (n_x <= 0) return MHB_OK;
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    const int64_t units = n_x * ((n_hash + kRun - 1) / kRun);
+    int64_t blocks = (units + 255) / 256;
+    if (blocks > (int64_t)dev.sms * 8) blocks = (int64_t)dev.sms * 8;
+    if (blocks < 1) blocks = 1;
+    hist_wide_kernel<IdT><<<(unsigned)blocks, 256, 0, st>>>(xs, n_x, kind, a, b, ra, rb, p, n_hash, m, counts);
+    return cuda_check(cudaGetLastError(), "hist_wide_kernel launch");
 }
 
 // ---------------------------------------------------------------------------
@@ -253,21 +515,29 @@ __global__ void band_keys_vec4_kernel(const uint32_t* __restrict__ sig, int64_t 
 // ---------------------------------------------------------------------------
 __device__ uint32_t g_probe_sink;
 
+// The same two-feature lookahead walk as sign.cu walk2_iter (h_{k+1} and h_{k+2} both
+// from h_k), so the probe is the register-only ceiling of the kernel's own visit
+// sequence (tools/visit_probe.cu "lookahead": 41.9 visits/clk/SM).
 template <int K>
 __global__ void __launch_bounds__(256) probe_iter_kernel(int64_t rounds, uint32_t p, uint32_t seed) {
     uint32_t best[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) best[k] = 0xffffffffu;
-    uint32_t ha = (threadIdx.x * 2654435761u + seed) % p, hb = (ha * 7u + 13u) % p;
-    uint32_t da = (blockIdx.x * 40503u + 17u) % p, db = (da * 3u + 5u) % p;
+    uint32_t h0a = (threadIdx.x * 2654435761u + seed) % p, h0b = (threadIdx.x * 40503u + 7u * seed) % p;
+    const uint32_t da = (blockIdx.x * 40503u + 17u + seed) % p, db = (blockIdx.x * 977u + 5u) % p;
+    const uint32_t da2 = (2 * da) % p, db2 = (2 * db) % p;
     for (int64_t r = 0; r < rounds; ++r) {
+        uint32_t ha = h0a, hb = h0b;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < K; k += 2) {
+            const uint32_t ga = reduce_once(ha + da, p), gb = reduce_once(hb + db, p);
             best[k] = __vimin3_u32(best[k], ha, hb);
-            ha = reduce_once(ha + da, p);
-            hb = reduce_once(hb + db, p);
+            best[k + 1] = __vimin3_u32(best[k + 1], ga, gb);
+            ha = reduce_once(ha + da2, p);
+            hb = reduce_once(hb + db2, p);
         }
-        da ^= (uint32_t)r & 1u;  // keep the loop from being folded
+        h0a = reduce_once(h0a + (uint32_t)r, p);  // new start hashes per round (not foldable)
+        h0b = reduce_once(h0b + 3u, p);
     }
     uint32_t acc = 0;
 #pragma unroll
@@ -417,9 +687,16 @@ extern "C" int mhb_band_keys(const void* sig, int32_t sig_dtype, int64_t n_sets,
 extern "C" int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x, uint64_t a, uint64_t b,
                                          uint64_t prime, int32_t n_hash, uint32_t buckets,
                                          unsigned long long* counts, void* stream) {
-    if (prime >= (1ull << 31)) return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^31 not supported");
+    clear_error();
     if (a < 1 || a >= prime || b >= prime || a + (uint64_t)n_hash >= prime)
         return set_error(MHB_ERR_INVALID, "iterative parameters out of range");
+    if (prime >= (1ull << 31)) {
+        if (buckets < 1 || n_hash < 1) return set_error(MHB_ERR_INVALID, "need buckets >= 1 and n_hash >= 1");
+        if (prime >= (1ull << 63) || !is_prime_u64(prime))
+            return set_error(MHB_ERR_INVALID, "modulus %llu is not a prime below 2^63", (unsigned long long)prime);
+        return launch_hist_wide<uint32_t>(xs, n_x, 0, a, b, nullptr, nullptr, prime, n_hash, buckets, counts,
+                                          static_cast<cudaStream_t>(stream));
+    }
     HistArgs H{};
     H.xs = xs; H.n_x = n_x; H.p = (uint32_t)prime; H.b = (uint32_t)b; H.a = a;
     H.n_hash = n_hash; H.m = buckets; H.counts = counts; H.kind = 0;
@@ -429,11 +706,29 @@ extern "C" int mhb_bucket_hist_iterative(const uint32_t* xs, int64_t n_x, uint64
 extern "C" int mhb_bucket_hist_random(const uint32_t* xs, int64_t n_x, const uint32_t* a, const uint32_t* b,
                                       uint64_t prime, int32_t n_hash, uint32_t buckets,
                                       unsigned long long* counts, void* stream) {
-    if (prime >= (1ull << 31)) return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^31 not supported");
+    clear_error();
+    if (prime >= (1ull << 31))
+        return set_error(MHB_ERR_UNSUPPORTED, "prime >= 2^31: random-family parameters need 64 bits, use "
+                                              "mhb_bucket_hist_u64");
     HistArgs H{};
     H.xs = xs; H.n_x = n_x; H.p = (uint32_t)prime; H.n_hash = n_hash; H.m = buckets;
     H.ra = a; H.rb = b; H.counts = counts; H.kind = 1;
     return launch_hist(H, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int mhb_bucket_hist_u64(int32_t kind, const uint64_t* xs, int64_t n_x, uint64_t a, uint64_t b,
+                                   const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash,
+                                   uint64_t buckets, unsigned long long* counts, void* stream) {
+    clear_error();
+    if (kind != 0 && kind != 1) return set_error(MHB_ERR_INVALID, "unknown kind %d", kind);
+    if (buckets < 1 || n_hash < 1) return set_error(MHB_ERR_INVALID, "need buckets >= 1 and n_hash >= 1");
+    if (prime < 3 || prime >= (1ull << 63) || !is_prime_u64(prime))
+        return set_error(MHB_ERR_INVALID, "modulus %llu is not a prime below 2^63", (unsigned long long)prime);
+    if (kind == 0 && (a < 1 || a >= prime || b >= prime || a + (uint64_t)n_hash >= prime))
+        return set_error(MHB_ERR_INVALID, "iterative parameters out of range");
+    if (kind == 1 && (!ra || !rb)) return set_error(MHB_ERR_INVALID, "random family needs device arrays a and b");
+    return launch_hist_wide<uint64_t>(xs, n_x, kind, a, b, ra, rb, prime, n_hash, buckets, counts,
+                                      static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int mhb_probe_visit_rate(int64_t visits_per_thread, int32_t kind, double* visits_out,

@@ -53,22 +53,27 @@ class HostPool {
         cv_.notify_all();
         for (auto& t : th_) t.join();
     }
-    // fn(part) for part in [0, parts), spread over the pool and the caller
+    // fn(part) for part in [0, parts), spread over the pool and the caller.  Callers are
+    // serialised (one job at a time).
     void run(int parts, const std::function<void(int)>& fn) {
         if (parts <= 1 || th_.empty()) {
             for (int k = 0; k < parts; ++k) fn(k);
             return;
         }
+        std::lock_guard<std::mutex> serial(run_mu_);
+        uint64_t gen;
         {
             std::lock_guard<std::mutex> l(m_);
+            gen = ++gen_;
             fn_ = &fn;
             parts_ = parts;
-            next_.store(0);
             left_ = parts;
-            ++gen_;
+            // claims carry the job generation in the high word: a worker still holding the
+            // previous job can never take (and so never run or double-count) a part of this one
+            claim_.store(gen << 32);
         }
         cv_.notify_all();
-        work();
+        work(gen, &fn, parts);
         std::unique_lock<std::mutex> l(m_);
         done_.wait(l, [this] { return left_ == 0; });
         fn_ = nullptr;
@@ -76,9 +81,19 @@ class HostPool {
     int width() const { return (int)th_.size() + 1; }
 
   private:
-    void work() {
-        for (int k; (k = next_.fetch_add(1)) < parts_;) {
-            (*fn_)(k);
+    // Claim parts of job `gen` until none is left or a newer job replaced it.  The claim is
+    // a CAS on (gen << 32 | next part), so it fails instead of consuming a part of another job.
+    void work(uint64_t gen, const std::function<void(int)>* fn, int parts) {
+        for (;;) {
+            uint64_t v = claim_.load();
+            int k;
+            for (;;) {
+                if ((v >> 32) != (gen & 0xffffffffull)) return;
+                k = (int)(v & 0xffffffffull);
+                if (k >= parts) return;
+                if (claim_.compare_exchange_weak(v, v + 1)) break;
+            }
+            (*fn)(k);
             std::lock_guard<std::mutex> l(m_);
             if (--left_ == 0) done_.notify_all();
         }
@@ -86,21 +101,26 @@ class HostPool {
     void loop() {
         uint64_t seen = 0;
         for (;;) {
+            uint64_t gen;
+            const std::function<void(int)>* fn;
+            int parts;
             {
                 std::unique_lock<std::mutex> l(m_);
                 cv_.wait(l, [&] { return stop_ || gen_ != seen; });
                 if (stop_) return;
-                seen = gen_;
+                seen = gen = gen_;
+                fn = fn_;  // the job of generation `gen` (valid until its parts are all done)
+                parts = parts_;
             }
-            work();
+            if (fn) work(gen, fn, parts);
         }
     }
     std::vector<std::thread> th_;
-    std::mutex m_;
+    std::mutex m_, run_mu_;
     std::condition_variable cv_, done_;
     const std::function<void(int)>* fn_ = nullptr;
     int parts_ = 0, left_ = 0;
-    std::atomic<int> next_{0};
+    std::atomic<uint64_t> claim_{0};
     uint64_t gen_ = 0;
     bool stop_ = false;
 };
@@ -346,7 +366,11 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     if (n_sets == 0) return MHB_OK;
     if (!indptr || !out || (nnz > 0 && !ids)) return set_error(MHB_ERR_INVALID, "null host pointer");
     if (n_hash < 1) return set_error(MHB_ERR_INVALID, "need at least one hash function, got %d", n_hash);
-    if (indptr[n_sets] - indptr[0] > nnz) return set_error(MHB_ERR_INVALID, "indptr exceeds nnz");
+    // ids are read at the absolute offsets indptr[s]: they must lie in [0, nnz] and never decrease
+    if (indptr[0] < 0 || indptr[n_sets] > nnz)
+        return set_error(MHB_ERR_INVALID, "indptr must satisfy 0 <= indptr[0] and indptr[n_sets] <= nnz");
+    for (int64_t s = 0; s < n_sets; ++s)
+        if (indptr[s + 1] < indptr[s]) return set_error(MHB_ERR_INVALID, "indptr decreases at set %lld", (long long)s);
     if (out_dtype != MHB_OUT_U32 && out_dtype != MHB_OUT_I64)
         return set_error(MHB_ERR_INVALID, "unknown out_dtype %d", out_dtype);
     if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {  // -1: the calling thread's current device
@@ -431,6 +455,23 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
             ln.pend_s0 = -1;
         }
     };
+    // Any early return below leaves no work behind: every lane is synchronised (its D2H
+    // into the caller's buffers has finished) and its staged chunk is forgotten, so a later
+    // call never drains this call's rows into its own output.
+    struct LaneReset {
+        DeviceCache& dc;
+        int n;
+        bool ok = false;
+        ~LaneReset() {
+            if (ok) return;
+            for (int l = 0; l < n; ++l) {
+                cudaStreamSynchronize(dc.lanes[l].stream);
+                dc.lanes[l].pend_s0 = -1;
+            }
+            cudaGetLastError();
+        }
+    } reset{dc, n_lanes};
+    for (int l = 0; l < kMaxLanes; ++l) dc.lanes[l].pend_s0 = -1;
 
     for (size_t c = 0; c < chunks.size(); ++c) {
         Lane& ln = dc.lanes[c % (size_t)n_lanes];
@@ -496,6 +537,7 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
         return rc;
     for (int32_t v : st) status_acc |= v;
     if (status_host) *status_host = status_acc;
+    reset.ok = true;
     return MHB_OK;
 }
 

@@ -25,17 +25,27 @@ def nnz_balanced_cuts(indptr, world: int, align: int = 1) -> list[int]:
     """Set boundaries [0, c_1, ..., c_{world-1}, S] with ~equal nnz per range.
 
     c_r = searchsorted(indptr, r * nnz / world) rounded down to a multiple of
-    `align` (align=2 keeps planted pairs (2k, 2k+1) on one rank)."""
+    `align` (align=2 keeps planted pairs (2k, 2k+1) on one rank).  A device indptr
+    is searched on the device: only the world-1 cut points come back to the host."""
     if world < 1:
         raise ValueError("world size must be >= 1")
-    ip = np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64)
-    n_sets = ip.size - 1
-    base, total = int(ip[0]), int(ip[-1] - ip[0])
+    if hasattr(indptr, "is_cuda") and indptr.is_cuda:
+        import torch
+
+        n_sets = indptr.numel() - 1
+        ends = indptr[[0, -1]].cpu().tolist()
+        base, total = int(ends[0]), int(ends[1] - ends[0])
+        goals = torch.tensor([base + (total * r) // world for r in range(1, world)], dtype=torch.int64,
+                             device=indptr.device)
+        raw = torch.searchsorted(indptr.contiguous(), goals, side="left").cpu().tolist() if world > 1 else []
+    else:
+        ip = np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64)
+        n_sets = ip.size - 1
+        base, total = int(ip[0]), int(ip[-1] - ip[0])
+        raw = [int(np.searchsorted(ip, base + (total * r) // world, side="left")) for r in range(1, world)]
     cuts = [0]
-    for r in range(1, world):
-        goal = base + (total * r) // world
-        c = int(np.searchsorted(ip, goal, side="left"))
-        c = min(max(c, cuts[-1]), n_sets)
+    for c in raw:
+        c = min(max(int(c), cuts[-1]), n_sets)
         c -= c % align
         cuts.append(max(c, cuts[-1]))
     cuts.append(n_sets)
@@ -47,64 +57,133 @@ def shard_of(indptr, rank: int, world: int, align: int = 1) -> tuple[int, int]:
     return cuts[rank], cuts[rank + 1]
 
 
+def _flag_device(group=None):
+    """Where this process group's collectives take their tensors (NCCL: the current GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def agree_or_raise(err: BaseException | None, group=None, what: str = "signing") -> None:
+    """Collective error check: every rank reaches it, learns whether ANY rank failed,
+    and all raise together -- so no rank is left waiting in a later barrier or gather."""
+    import torch
+    import torch.distributed as dist
+
+    flag = torch.tensor([1 if err is not None else 0], dtype=torch.int32, device=_flag_device(group))
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if err is not None:
+        raise err
+    if int(flag.item()):
+        raise RuntimeError(f"{what} failed on another rank")
+
+
 def _default_sign(indptr, ids, family):
+    """This rank's rows with the library's checks: the reference's ValueErrors for empty
+    sets and ids >= p (status word), ids outside uint32 rejected before the cast."""
     import torch
 
-    from .minhash import sign_csr_device
+    from .minhash import signatures_csr
 
-    out = torch.empty((indptr.numel() - 1, family.size), dtype=torch.uint32, device=ids.device)
-    if out.shape[0]:
-        sign_csr_device(indptr, ids, family, out)
-    return out
+    if indptr.numel() - 1 == 0:
+        return torch.empty((0, family.size), dtype=torch.uint32, device=ids.device)
+    return signatures_csr(indptr, ids, family, out_dtype="uint32", validate=True)
+
+
+def _slice_shard(indptr, ids, s0: int, s1: int, device):
+    """Rows [s0, s1) of a global CSR batch as (indptr from 0, ids) on `device`.  Device
+    tensors are sliced in place (views; no host round trip); host arrays copy only the
+    slice."""
+    import torch
+
+    if torch.is_tensor(indptr) and indptr.is_cuda:
+        lo, hi = (int(v) for v in indptr[[s0, s1]].cpu().tolist())
+        ip = indptr[s0:s1 + 1] - lo
+    else:
+        ip_h = np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64)
+        lo, hi = int(ip_h[s0]), int(ip_h[s1])
+        ip = torch.as_tensor(ip_h[s0:s1 + 1] - lo)
+    if torch.is_tensor(ids):
+        x = ids[lo:hi]
+    else:
+        x = torch.as_tensor(np.ascontiguousarray(np.asarray(ids)[lo:hi]))
+    if device is not None:
+        ip, x = ip.to(device), x.to(device)
+    return ip.contiguous(), x.contiguous()
 
 
 def gather_blocks(block, rows_per_rank: list[int], dst: int = 0, group=None):
-    """Gather variable-height [rows, N] blocks to `dst` (padded to the max height on
-    the wire, trimmed on arrival).  Returns the stacked matrix on dst, None elsewhere."""
+    """Gather variable-height [rows, N] blocks to `dst` with no padding: `dst` allocates
+    the [sum(rows), N] matrix and receives every other rank's block straight into its
+    row range (point-to-point; one NCCL group on the GPU backend).  Returns the matrix
+    on dst, None elsewhere."""
     import torch
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    if len(rows_per_rank) != world:
+        raise ValueError("rows_per_rank needs one entry per rank")
+    if block.shape[0] != rows_per_rank[rank]:
+        raise ValueError(f"rank {rank} holds {block.shape[0]} rows, rows_per_rank says {rows_per_rank[rank]}")
     n = block.shape[1]
-    hmax = max(rows_per_rank) if rows_per_rank else 0
-    wire_dtype = torch.int32 if block.dtype == torch.uint32 else block.dtype
-    send = torch.zeros((hmax, n), dtype=wire_dtype, device=block.device)
-    if block.shape[0]:
-        send[:block.shape[0]].copy_(block.view(wire_dtype) if block.dtype == torch.uint32 else block)
-    bufs = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
-    dist.gather(send, gather_list=bufs, dst=dst, group=group)
-    if rank != dst:
-        return None
-    parts = [b[:h] for b, h in zip(bufs, rows_per_rank)]
-    full = torch.cat(parts, 0)
-    return full.view(torch.uint32) if block.dtype == torch.uint32 else full
+    is_u32 = block.dtype == torch.uint32
+    wire = block.view(torch.int32) if is_u32 else block
+    nccl = dist.get_backend(group) == "nccl"
+    g = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    if rank == dst:
+        full = torch.empty((sum(rows_per_rank), n), dtype=wire.dtype, device=block.device)
+        off = 0
+        ops, works = [], []
+        for r, h in enumerate(rows_per_rank):
+            part = full[off:off + h]
+            off += h
+            if r == rank:
+                part.copy_(wire)
+            elif h > 0:
+                if nccl:
+                    ops.append(dist.P2POp(dist.irecv, part, g(r), group))
+                else:
+                    works.append(dist.irecv(part, src=g(r), group=group))
+        if ops:
+            works += dist.batch_isend_irecv(ops)
+        for w in works:
+            w.wait()
+        return full.view(torch.uint32) if is_u32 else full
+    if rows_per_rank[rank] > 0:
+        if nccl:
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, wire.contiguous(), g(dst), group)]):
+                w.wait()
+        else:
+            dist.send(wire.contiguous(), dst=g(dst), group=group)
+    return None
 
 
 def sign_sharded(indptr, ids, family, *, sign_fn=None, gather: bool = True, dst: int = 0,
                  align: int = 1, device=None, group=None):
     """Sign this rank's nnz-balanced slice of a global CSR batch.
 
-    indptr/ids: the global batch (host numpy or torch; every rank sees the same
-    arrays).  Returns (local_block, (s0, s1), full) where full is the gathered
-    [S, N] matrix on `dst` when gather=True, else None."""
-    import torch
+    indptr/ids: the global batch -- device tensors (sliced in place, nothing copied to
+    the host) or host arrays (only this rank's slice is copied).  Every rank sees the
+    same batch and derives the same cuts.  Errors on any rank (an empty set, an id >= p)
+    raise on every rank before the gather.  Returns (local_block, (s0, s1), full) where
+    full is the gathered [S, N] matrix on `dst` when gather=True, else None."""
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     cuts = nnz_balanced_cuts(indptr, world, align)
     s0, s1 = cuts[rank], cuts[rank + 1]
-    ip = torch.as_tensor(np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64))
-    lo, hi = int(ip[s0]), int(ip[s1])
-    ids_t = torch.as_tensor(ids.cpu().numpy() if hasattr(ids, "cpu") else np.asarray(ids))
-    local_ip = (ip[s0:s1 + 1] - lo).clone()
-    local_ids = ids_t[lo:hi].clone()
-    if device is not None:
-        local_ip = local_ip.to(device)
-        local_ids = local_ids.to(device)
-    fn = sign_fn or _default_sign
-    block = fn(local_ip, local_ids, family)
+    block, err = None, None
+    try:
+        local_ip, local_ids = _slice_shard(indptr, ids, s0, s1, device)
+        block = (sign_fn or _default_sign)(local_ip, local_ids, family)
+    except Exception as e:  # noqa: BLE001 -- re-raised below, on every rank together
+        err = e
+    agree_or_raise(err, group)
     full = None
     if gather:
         rows = [cuts[r + 1] - cuts[r] for r in range(world)]
@@ -179,11 +258,13 @@ def sign_gather_peer(indptr, ids, family, *, dst: int = 0, align: int = 1, devic
 
     Returns (matrix, (s0, s1)): on `dst` the PeerMatrix holding every signature
     (``.tensor()`` views it; the caller closes it), elsewhere None.  Each rank's
-    kernels complete (stream sync) before the barrier that publishes the matrix."""
+    kernels complete (stream sync) before the barrier that publishes the matrix.  The
+    reference's input errors (empty set, id >= p) raise on every rank together, and
+    every rank passes the same barriers whatever happens."""
     import torch
     import torch.distributed as dist
 
-    from .minhash import sign_csr_to_ptr
+    from .minhash import _check_indptr_device, _raise_status, sign_csr_to_ptr
 
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
@@ -191,24 +272,41 @@ def sign_gather_peer(indptr, ids, family, *, dst: int = 0, align: int = 1, devic
     cuts = nnz_balanced_cuts(indptr, world, align)
     s0, s1 = cuts[rank], cuts[rank + 1]
     n_total = cuts[-1]
-    ip = np.asarray(indptr.cpu() if hasattr(indptr, "cpu") else indptr, dtype=np.int64)
-    lo, hi = int(ip[s0]), int(ip[s1])
-    local_ip = torch.as_tensor(ip[s0:s1 + 1] - lo).to(dev)
-    x = ids if torch.is_tensor(ids) else torch.from_numpy(np.asarray(ids))
-    local_ids = x[lo:hi].to(dev)
-    if local_ids.dtype != torch.uint32:
-        local_ids = local_ids.to(torch.int64).to(torch.uint32)
+    err, local_ip, local_ids = None, None, None
+    try:
+        local_ip, local_ids = _slice_shard(indptr, ids, s0, s1, dev)
+        if local_ids.dtype != torch.uint32:
+            if local_ids.numel() and (int(local_ids.min()) < 0 or int(local_ids.max()) >= family.prime):
+                raise ValueError(f"feature ids must be in [0, family.prime = {family.prime})")
+            local_ids = local_ids.to(torch.int64).to(torch.uint32)
+        if s1 > s0:
+            _check_indptr_device(local_ip, local_ids.numel())
+    except Exception as e:  # noqa: BLE001
+        err = e
+    agree_or_raise(err, group, "input checks")
     mat = PeerMatrix.allocate(n_total, family.size, 4, dev.index) if rank == dst else None
     box = [mat.handle if mat is not None else None]
     dist.broadcast_object_list(box, src=dst, group=group)
     view = mat if rank == dst else PeerMatrix.open(box[0], n_total, family.size, 4, dev.index)
+    err = None
     try:
         if s1 > s0:
-            sign_csr_to_ptr(local_ip, local_ids, family, view.ptr(s0))
+            status = torch.zeros(1, dtype=torch.int32, device=dev)
+            sign_csr_to_ptr(local_ip, local_ids, family, view.ptr(s0), False, status)
+            _raise_status(int(status.item()), family)
         torch.cuda.synchronize(dev)
-        dist.barrier(group=group)  # every row has landed in dst's matrix
-    finally:
+    except Exception as e:  # noqa: BLE001
+        err = e
+    try:
+        agree_or_raise(err, group)  # doubles as the barrier: every row has landed in dst's matrix
+    except BaseException:
         if rank != dst:
             view.close()
+        dist.barrier(group=group)
+        if mat is not None:
+            mat.close()
+        raise
+    if rank != dst:
+        view.close()
     dist.barrier(group=group)  # every mapping is closed before dst may free the matrix
     return (mat if rank == dst else None), (s0, s1)

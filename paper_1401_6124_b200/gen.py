@@ -353,3 +353,112 @@ def planted_pairs(cfg: Config | str = "cfg3", device="cuda", n_base: int | None 
     ids = (all_keys & 0xFFFFFFFF).to(torch.uint32)
     exact = keep.double() / (2.0 * sizes.double() - keep.double())
     return indptr, ids, exact
+
+
+# ---------------------------------------------------------------------------
+# Blocked batches: one global batch, any slice of it generated on its own
+# ---------------------------------------------------------------------------
+#
+# The multi-GPU driver cuts ONE global batch into nnz-balanced row shards and every
+# rank generates only its own shard on its own device.  So the batch is a sequence of
+# fixed blocks of BLOCK_SETS sets (pairs for cfg3), block b drawn by make_csr /
+# planted_pairs from its own seed derive_seed(data_seed, 7, b).  make_csr draws a
+# block's sizes first from that seed, so every rank can rebuild the global indptr from
+# the sizes alone (a few kernels per block), cut it, and generate just the blocks its
+# rows touch.  The batch is identical for any world size.
+
+BLOCK_SETS = 1 << 18
+
+
+def _block_seed(seed: int, b: int) -> int:
+    return derive_seed(seed, 7, b)
+
+
+def _planted(cfg: Config) -> bool:
+    return cfg.name == "cfg3"
+
+
+def block_layout(cfg: Config | str, n_sets: int | None = None, block: int = BLOCK_SETS):
+    """(unit, sets_per_block, n_blocks, n_sets): cfg3 blocks hold `block` planted pairs."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    unit = 2 if _planted(cfg) else 1
+    n = (cfg.n_sets * unit if n_sets is None else int(n_sets))
+    if n % unit:
+        raise ValueError("planted-pair batches hold an even number of sets")
+    bs = block * unit
+    return unit, bs, (n + bs - 1) // bs, n
+
+
+def global_sizes(cfg: Config | str, device="cuda", n_sets: int | None = None, seed: int | None = None,
+                 block: int = BLOCK_SETS):
+    """int64[S] set sizes of the blocked batch (no ids drawn)."""
+    import torch
+
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    device = torch.device(device)
+    seed = cfg.data_seed() if seed is None else int(seed)
+    unit, bs, nb, n = block_layout(cfg, n_sets, block)
+    parts = []
+    for b in range(nb):
+        nb_sets = min(bs, n - b * bs) // unit
+        g = torch.Generator(device=device)
+        g.manual_seed(_block_seed(seed, b) & ((1 << 63) - 1))
+        s = _draw_sizes(cfg, nb_sets, g, device)
+        parts.append(torch.repeat_interleave(s, unit) if unit > 1 else s)
+    return torch.cat(parts) if parts else torch.zeros(0, dtype=torch.int64, device=device)
+
+
+def global_indptr(cfg: Config | str, device="cuda", n_sets: int | None = None, seed: int | None = None,
+                  block: int = BLOCK_SETS):
+    import torch
+
+    sizes = global_sizes(cfg, device, n_sets, seed, block)
+    ip = torch.zeros(sizes.numel() + 1, dtype=torch.int64, device=sizes.device)
+    torch.cumsum(sizes, 0, out=ip[1:])
+    return ip
+
+
+def make_shard(cfg: Config | str, s0: int, s1: int, device="cuda", n_sets: int | None = None,
+               seed: int | None = None, block: int = BLOCK_SETS, indptr=None):
+    """Sets [s0, s1) of the blocked global batch on `device`.
+
+    Returns (indptr int64[s1-s0+1] starting at 0, ids uint32, exact_jaccard or None);
+    exact_jaccard (cfg3) holds the planted pairs of the slice, which must then start and
+    end on a pair boundary.  `indptr`: the global indptr if the caller has it."""
+    import torch
+
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    device = torch.device(device)
+    seed = cfg.data_seed() if seed is None else int(seed)
+    unit, bs, nb, n = block_layout(cfg, n_sets, block)
+    if not (0 <= s0 <= s1 <= n):
+        raise ValueError(f"slice [{s0}, {s1}) outside the batch of {n} sets")
+    if unit > 1 and (s0 % unit or s1 % unit):
+        raise ValueError("planted-pair slices must start and end on a pair boundary")
+    if indptr is None:
+        indptr = global_indptr(cfg, device, n, seed, block)
+    ip_g = indptr.to(device)
+    lo = int(ip_g[s0])
+    local_ip = (ip_g[s0:s1 + 1] - lo).contiguous()
+    nnz = int(local_ip[-1])
+    ids = torch.empty(nnz, dtype=torch.uint32, device=device)
+    exact = [] if unit > 1 else None
+    for b in range(s0 // bs, (s1 + bs - 1) // bs):
+        b_lo, b_hi = b * bs, min(n, (b + 1) * bs)
+        r0, r1 = max(s0, b_lo) - b_lo, min(s1, b_hi) - b_lo
+        if r1 <= r0:
+            continue
+        bseed = _block_seed(seed, b)
+        if unit > 1:
+            bip, bids, bj = planted_pairs(cfg, device=device, n_base=(b_hi - b_lo) // 2, seed=bseed)
+            exact.append(bj[r0 // 2:r1 // 2])
+        else:
+            bip, bids = make_csr(cfg, device=device, n_sets=b_hi - b_lo, seed=bseed)
+        a, z = int(bip[r0]), int(bip[r1])
+        dst = int(ip_g[b_lo + r0]) - lo
+        ids[dst:dst + (z - a)].copy_(bids[a:z])
+        del bip, bids
+    return local_ip, ids, (torch.cat(exact) if exact is not None and exact else exact)

@@ -149,8 +149,11 @@ def sign_csr_to_ptr(indptr, ids, family: Family, out_ptr: int, out_int64: bool =
     out_dtype = _lib.OUT_I64 if out_int64 else _lib.OUT_U32
     ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, nnz, n_hash)
     with torch.cuda.device(dev):
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
+        # the workspace belongs to the launch stream: allocated on it, the caching allocator
+        # cannot hand the block to another stream while the kernels still use it
+        with torch.cuda.stream(st):
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         sptr = st.cuda_stream
         status_ptr = status.data_ptr() if status is not None else None
         if isinstance(family, IterativeFamily):
@@ -205,6 +208,8 @@ def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
     ids = ids.contiguous()
     indptr = indptr.to(torch.int64).contiguous()
     n_sets = indptr.numel() - 1
+    if validate and n_sets > 0:
+        _check_indptr_device(indptr, ids.numel())
     tdt = torch.int64 if out_dtype == "int64" else torch.uint32
     if out is None:
         out = torch.empty((n_sets, family.size), dtype=tdt, device=ids.device)
@@ -215,6 +220,18 @@ def signatures_csr(indptr, ids, family: Family, *, out_dtype="int64", out=None,
     if validate:
         _raise_status(int(status.item()), family)
     return out
+
+
+def _check_indptr_device(indptr, nnz: int) -> None:
+    """ids are read at the absolute offsets indptr[s]: 0 <= indptr[0], indptr[-1] <= nnz and
+    no decrease (one small device reduction and one read, before any launch)."""
+    torch = _torch()
+    bad = torch.stack([(indptr[0] < 0), (indptr[-1] > nnz), (indptr[1:] < indptr[:-1]).any()])
+    flags = bad.cpu().tolist()
+    if flags[0] or flags[1]:
+        raise ValueError("indptr must satisfy 0 <= indptr[0] and indptr[-1] <= len(ids)")
+    if flags[2]:
+        raise ValueError("indptr must be non-decreasing")
 
 
 def _signatures_ids64(indptr, ids, family: Family, out_dtype, out, validate):
@@ -441,7 +458,9 @@ def signatures(sets, family: Family) -> list[Signature]:
     ids = np.concatenate([s.ids for s in sets])
     if ids.max() >= family.prime:
         raise ValueError(f"feature id {int(ids.max())} >= family prime {family.prime}")
-    mat = signatures_csr(indptr, ids.astype(np.uint32), family, out_dtype="int64")
+    # int64 ids as the FeatureSets hold them: signatures_csr narrows them to uint32 only
+    # when they fit, and routes ids beyond 2^32 (primes >= 2^32) to the 64-bit-id entry
+    mat = signatures_csr(indptr, ids, family, out_dtype="int64")
     return [Signature(row, family.key) for row in mat]
 
 
@@ -494,22 +513,29 @@ def jaccard_block(sig_a, sig_b):
     return counts
 
 
-def band_keys(sig, rows_per_band: int):
+def band_keys(sig, rows_per_band: int, *, keys=None, stream=None):
     """LSH band keys: uint64 [S, N/rows] from a device signature matrix [S, N].
 
     Bands are runs of `rows_per_band` consecutive hash positions; each key is
     splitmix64 of FNV-1a-64 over the band's argmin ids (include/mhb.h).  Equal keys
-    mean the two sets agree on every row of the band (the LSH candidate test)."""
+    mean the two sets agree on every row of the band (the LSH candidate test).
+    ``keys``: an optional preallocated uint64 [S, N/rows] output; ``stream``: the
+    launch stream (default: the current one)."""
     torch = _torch()
     lib = _lib.load()
     n_sets, n_hash = sig.shape
     if n_hash % rows_per_band:
         raise ValueError(f"rows_per_band {rows_per_band} must divide the signature length {n_hash}")
-    keys = torch.empty((n_sets, n_hash // rows_per_band), dtype=torch.uint64, device=sig.device)
+    shape = (n_sets, n_hash // rows_per_band)
+    if keys is None:
+        keys = torch.empty(shape, dtype=torch.uint64, device=sig.device)
+    elif keys.dtype != torch.uint64 or tuple(keys.shape) != shape or not keys.is_contiguous():
+        raise ValueError("keys must be a contiguous uint64 tensor of shape (n_sets, n_hash // rows_per_band)")
     dt = _lib.OUT_I64 if sig.dtype == torch.int64 else _lib.OUT_U32
     with torch.cuda.device(sig.device):
+        st = stream if stream is not None else torch.cuda.current_stream()
         rc = lib.mhb_band_keys(sig.contiguous().data_ptr(), dt, n_sets, n_hash, rows_per_band, keys.data_ptr(),
-                               torch.cuda.current_stream().cuda_stream)
+                               st.cuda_stream)
     _lib.check(rc)
     return keys
 
@@ -547,6 +573,8 @@ def signatures_band_keys(indptr, ids, family: Family, rows_per_band: int, *, wri
     ids = ids.contiguous()
     indptr = indptr.to(torch.int64).contiguous()
     n_sets = indptr.numel() - 1
+    if validate and n_sets > 0:
+        _check_indptr_device(indptr, ids.numel())
     tdt = torch.int64 if out_dtype == "int64" else torch.uint32
     lib = _lib.load()
     dev = ids.device

@@ -80,3 +80,107 @@ def test_gloo_sharded_sign_and_gather(world):
     for p in procs:
         p.join(timeout=60)
     assert all(results) and all(p.exitcode == 0 for p in procs)
+
+
+def _split_worker(rank, world, port, q):
+    """The north-star split on CPU: every rank rebuilds the global indptr of one blocked
+    batch, cuts it, generates only its own shard, signs it (oracle as the signer) and
+    gathers unpadded blocks; rank 0 compares with the whole batch generated in one piece."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_1401_6124_b200.dist import gather_blocks, nnz_balanced_cuts
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = gen.CONFIGS["cfg2"]
+        n = 3000
+        ip_g = gen.global_indptr(cfg, "cpu", n, block=700)
+        cuts = nnz_balanced_cuts(ip_g, world)
+        s0, s1 = cuts[rank], cuts[rank + 1]
+        ip, ids, _ = gen.make_shard(cfg, s0, s1, "cpu", n, block=700, indptr=ip_g)
+        fam = make_family("iterative", 3, 64, cfg.prime)
+        blk = oracle.sign_family_csr(ip.numpy(), ids.numpy().view(np.uint32), fam).astype(np.uint32)
+        full = gather_blocks(torch.from_numpy(blk.view(np.int32)).view(torch.uint32),
+                             [cuts[r + 1] - cuts[r] for r in range(world)])
+        if rank == 0:
+            ip1, ids1, _ = gen.make_shard(cfg, 0, n, "cpu", n, block=700)
+            want = oracle.sign_family_csr(ip1.numpy(), ids1.numpy().view(np.uint32), fam)
+            q.put(bool(np.array_equal(full.view(torch.int32).numpy().astype(np.int64), want)))
+        else:
+            q.put(full is None)
+    finally:
+        dist.destroy_process_group()
+
+
+def _error_worker(rank, world, port, q):
+    """A data error on ONE rank (an id >= p) raises on every rank before the gather --
+    nobody is left waiting in a collective."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6124_b200.dist import sign_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        indptr, ids = gen.cfg1_numpy(n_sets=200, seed=2)
+        fam = make_family("iterative", 7, 32, 1_048_583)
+
+        def sign_fn(ip, x, family):
+            if int(x.to(torch.int64).max()) >= family.prime or dist.get_rank() == 1:
+                raise ValueError("feature id >= family prime")
+            return torch.zeros((ip.numel() - 1, family.size), dtype=torch.int32).view(torch.uint32)
+
+        try:
+            sign_sharded(indptr, ids, fam, sign_fn=sign_fn)
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, "ValueError"))
+        except RuntimeError as e:
+            q.put((rank, "RuntimeError"))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(fn, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    return results, procs
+
+
+def test_gloo_split_of_one_global_batch():
+    results, procs = _spawn(_split_worker, 2)
+    assert all(results) and all(p.exitcode == 0 for p in procs)
+
+
+def test_gloo_error_on_one_rank_raises_everywhere():
+    results, procs = _spawn(_error_worker, 2)
+    got = dict(results)
+    assert got == {0: "RuntimeError", 1: "ValueError"}, got
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_gen_shards_concatenate_to_the_batch():
+    import torch
+
+    for name, n, block in (("cfg2", 2500, 600), ("cfg3", 2400, 300), ("cfg5", 1800, 500)):
+        cfg = gen.CONFIGS[name]
+        ip_g = gen.global_indptr(cfg, "cpu", n, block=block)
+        whole = gen.make_shard(cfg, 0, n, "cpu", n, block=block, indptr=ip_g)
+        for world in (2, 3):
+            cuts = nnz_balanced_cuts(ip_g, world, align=2 if name == "cfg3" else 1)
+            parts = [gen.make_shard(cfg, cuts[r], cuts[r + 1], "cpu", n, block=block, indptr=ip_g)
+                     for r in range(world)]
+            assert torch.equal(torch.cat([p[1] for p in parts]), whole[1])
+            if name == "cfg3":
+                assert torch.equal(torch.cat([p[2] for p in parts]), whole[2])

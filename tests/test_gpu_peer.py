@@ -99,9 +99,11 @@ def test_peer_matrix_single_rank(cuda_device):
 
 
 def test_bench_two_ranks_on_one_gpu():
-    """bench.py's N>1 path (torchrun, barriers, max over ranks, fused peer gather with
-    every rank checking its rows) with both ranks on the box's one GPU over gloo
-    (MHB_BENCH_SHARED_GPU=1).  Checks the plumbing, not the timings."""
+    """bench.py's N>1 path -- one global batch cut into nnz-balanced shards, each rank
+    generating only its own shard, barriers, max over ranks, the variable-size gather
+    and the fused peer gather with every rank checking its rows -- with both ranks on
+    the box's one GPU over gloo (MHB_BENCH_SHARED_GPU=1).  Checks the plumbing, not the
+    timings."""
     import json
     import subprocess
     import sys
@@ -109,10 +111,60 @@ def test_bench_two_ranks_on_one_gpu():
     env = dict(os.environ, MHB_BENCH_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
-           "--n-sets", "50000", "--gather", "peer", "--no-e2e", "--no-cpu-baseline"]
+           "--config", "cfg2", "--n-sets", "50000", "--gather", "auto", "--no-cpu-baseline", "--e2e-steps", "1"]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "weak"
-    assert line["gather_peer"]["bytes_to_rank0_per_step"] == 2 * 50000 * 256 * 4
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
+    assert line["config"]["n_sets"] == 50000
+    g = line["gather"]
+    assert "error" not in g, g
+    assert g["bytes_to_rank0_per_step"] == 50000 * 256 * 4
+    assert g["nccl"]["ms"] > 0 and g["peer"]["ms_per_step"] > 0
+    assert line["e2e"]["sets_per_step"] > 0 and line["e2e_reference_convention"]["value"] > 0
+
+
+def _shard_worker(rank, world, port, cfg_name, n_sets, q):
+    """One rank of the north-star split: global indptr -> cuts -> own shard -> sign ->
+    unpadded gather to rank 0, which compares with the single-process signatures of
+    the same global batch."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6124_b200 import gen, make_family, signatures_csr
+    from paper_1401_6124_b200.dist import gather_blocks, nnz_balanced_cuts
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = gen.CONFIGS[cfg_name]
+        dev = torch.device("cuda", 0)
+        ip_g = gen.global_indptr(cfg, dev, n_sets)
+        cuts = nnz_balanced_cuts(ip_g, world, align=2 if cfg_name == "cfg3" else 1)
+        s0, s1 = cuts[rank], cuts[rank + 1]
+        ip, ids, _ = gen.make_shard(cfg, s0, s1, dev, n_sets, indptr=ip_g)
+        fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+        block = signatures_csr(ip, ids, fam, out_dtype="uint32")
+        full = gather_blocks(block.cpu(), [cuts[r + 1] - cuts[r] for r in range(world)], dst=0)
+        if rank == 0:
+            ip1, ids1, _ = gen.make_shard(cfg, 0, n_sets, dev, n_sets)
+            want = signatures_csr(ip1, ids1, fam, out_dtype="uint32").cpu()
+            q.put(("ok", bool(torch.equal(full.view(torch.int32), want.view(torch.int32))), cuts))
+    except Exception as exc:
+        q.put(("error", repr(exc), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg_name,n_sets", [(2, "cfg2", 30_000), (3, "cfg3", 20_000), (2, "cfg5", 40_000)])
+def test_split_gather_equals_single_process(cuda_device, world, cfg_name, n_sets):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_shard_worker, args=(world, _free_port(), cfg_name, n_sets, q), nprocs=world, join=True,
+                       start_method="spawn")
+    status, equal, cuts = q.get(timeout=60)
+    assert status == "ok", equal
+    assert equal, f"gathered shards differ from the single-process batch (cuts {cuts})"
