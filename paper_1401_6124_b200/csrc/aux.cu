@@ -104,20 +104,35 @@ __global__ void jaccard_block_kernel(const T* __restrict__ A, int64_t n_rows, co
 // Bucket histogram (stats.py:221-224 generalised to a batch of x): counts[b] =
 // #{(x, i) : h_i(x) mod m = b}.
 //
-// One count per (x, i) evaluation.  Shared-memory atomics on one CTA-wide table
-// serialise on bank conflicts (uniform bins over 4096 entries: ~3.5 lanes per bank per
-// warp access, 4.7 counts/clk/SM measured in round 1).  hist_rep_kernel gives every
-// lane of the warp its OWN replica of the table in its OWN bank: lane L's byte counter
-// for bin b lives in word (b >> 2) * 32 + L, byte b & 3, so a warp's 32 ATOMS land in
-// 32 distinct banks -- one wavefront per instruction.  32 replicas x m bytes fit 128 KB
-// for m <= 4096.  Byte counters carry 127 at most: the increment that moves a byte from
-// 127 to 128 (bit 7 flips; exactly one thread observes it, atomics being serialised)
-// moves 128 into the global count and subtracts it back out.  The byte never wraps
-// in between (the replica is shared by one lane of each warp: a few in-flight
-// increments, far below 128), so no carry ever reaches a neighbouring bin.
+// One count per (x, i) evaluation, so the counting instruction is the kernel.  Round 1
+// counted into one CTA-wide u32 table with shared atomics: uniform bins over 4096
+// entries put ~3.5 lanes of a warp on one bank (4.7 counts/clk/SM).  hist_kernel8
+// gives each lane slot s = lane % (2 COLS) its own 16-bit counter per bin: bin b,
+// slot s lives in word b * COLS + (s % COLS), half s / COLS.  So
+//   * a lane's increment is a per-lane constant (1 or 1 << 16) and its address one
+//     LOP3 + IMAD from h: walk (2) + address (2) + RED = 5 instructions per evaluation;
+//   * a warp's 32 increments spread over the banks by column: the 32 / COLS lanes of
+//     one column share 32 / COLS banks (COLS = 8: ~2 lanes per bank at worst, against
+//     ~3.5 for one table; tools/atoms_probe.cu measures the RED rates);
+//   * 4096 bins x 2 COLS slots x 2 B + a 16 KB u32 table fit one SM (COLS = 8: 144 KB,
+//     1024 threads; COLS = 4: 80 KB, two CTAs of 512).
+// A counter is shared by the lanes of its slot in every warp of the CTA (64 threads),
+// so the CTA sweeps the counters into the u32 table before any can pass 65535: every
+// thread runs the same rounds of at most 2 x `run` evaluations (two x per round, two
+// independent dependency chains), and the CTA sweeps every floor(65535 / 64 / 2 run)
+// rounds.  cfg3 (4.19M ids x 512): 1.56 -> 0.58 ms; cfg4 (60.9M x 2048): 91.5 -> 34.3 ms.
 // ---------------------------------------------------------------------------
 constexpr int kRun = 256;
-constexpr int kRepMaxBins = 4096;  // 32 replicas x 4096 one-byte counters = 128 KB
+// COLS word columns per bin (2 x 16-bit slots each): 8 for the iterative walk (128 KB,
+// one CTA of 1024 threads per SM: 4 lanes per column, fewer bank collisions), 4 for
+// the random family (64 KB, two CTAs of 512: its 48 lane constants need the registers).
+constexpr int kRepMaxBins = 4096;  // 4096 x COLS words + a 4096-word u32 table
+template <int COLS>
+struct HistShape {
+    static constexpr int threads = COLS == 4 ? 512 : 1024;
+    static constexpr int sharers = (32 / (2 * COLS)) * (threads / 32);  // threads per 16-bit counter
+    static constexpr int max_run = 65535 / sharers;                     // evaluations per thread per sweep
+};
 
 struct HistArgs {
     const uint32_t* xs;
@@ -131,7 +146,7 @@ struct HistArgs {
     unsigned long long* counts;
     int kind;
     int use_smem;
-    int nblk, run;   // hist_rep_kernel: lane blocks per x (power of two) and lanes per block
+    int nblk, run;   // hist_kernel8: lane blocks per x (power of two) and lanes per block
 };
 
 __device__ __forceinline__ uint32_t mod_bucket(uint32_t h, uint32_t m, uint32_t mp) {
@@ -140,68 +155,48 @@ __device__ __forceinline__ uint32_t mod_bucket(uint32_t h, uint32_t m, uint32_t 
     return __viaddmin_u32(r, 0u - m, r);
 }
 
-// 1 << (8 * (s & 3)) in one PRMT: backward-4-extract of the byte string {1,0,0,0,0,0,0,0}.
-__device__ __forceinline__ uint32_t byte_one(uint32_t s) {
-    uint32_t d;
-    asm("prmt.b32.b4e %0, %1, %2, %3;" : "=r"(d) : "r"(1u), "r"(0u), "r"(s));
-    return d;
-}
-
-__device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
-    return old;
-}
 __device__ __forceinline__ void reds_add(uint32_t saddr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
 
-// One evaluation's count: the lane's byte for bin = h mod m lives in word
-// (bin >> 2) * 32 + lane, byte bin & 3 (`rep_lane` = shared address of word `lane`;
-// POW2: m >= 4 is a power of two, so bin & 3 = h & 3 and the byte select reads h).
-// Returns (new ^ old) of the counter word: bit 7 of a byte flips only when this
-// increment took that byte from 127 to 128 (no other byte changes: no carries).
-template <bool POW2>
-__device__ __forceinline__ uint32_t count_bin(uint32_t rep_lane, uint32_t h, uint32_t m, uint32_t mp,
-                                              uint32_t wmask) {
-    uint32_t addr, inc;
-    if (POW2) {
-        addr = (h & wmask) * 32u + rep_lane;  // wmask = (m - 1) & ~3
-        inc = byte_one(h);
-    } else {
-        const uint32_t bin = mod_bucket(h, m, mp);
-        addr = (bin & ~3u) * 32u + rep_lane;
-        inc = byte_one(bin);
-    }
-    const uint32_t old = atoms_add(addr, inc);
-    return (old + inc) ^ old;
-}
-
-// The evaluation of `h` moved its byte to 128: take the 128 out again and add it to
-// the global count.  Deferring this by a few evaluations is safe: until the
-// subtraction lands the byte only grows by the few increments in flight from the
-// threads sharing the replica (<< 127).
-template <bool POW2>
-__device__ __forceinline__ void spill_bin(uint32_t rep_lane, uint32_t h, uint32_t m, uint32_t mp,
-                                          unsigned long long* counts) {
+// One evaluation's count: this lane's counter for bin h mod m (`col` = shared address of
+// the lane's word column, `inc` = its half).
+template <bool POW2, int COLS>
+__device__ __forceinline__ void count_bin(uint32_t col, uint32_t inc, uint32_t h, uint32_t m, uint32_t mp) {
     const uint32_t bin = POW2 ? (h & (m - 1)) : mod_bucket(h, m, mp);
-    reds_add((bin & ~3u) * 32u + rep_lane, 0u - (byte_one(bin) << 7));
-    atomicAdd(counts + bin, 128ull);
+    reds_add(bin * (4u * COLS) + col, inc);
 }
 
-constexpr uint32_t kBit7 = 0x80808080u;
+// Move the 16-bit counters into the u32 table and clear them.  Thread t owns bins
+// b = t, t + blockDim, ... (exclusive: plain adds): one 16-byte load holds all 8 slots.
+template <int COLS>
+__device__ __forceinline__ void sweep8(uint4* cnt, uint32_t* acc, uint32_t m) {
+    for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < COLS / 4; ++q) {
+            const uint4 v = cnt[b * (COLS / 4) + q];
+            cnt[b * (COLS / 4) + q] = make_uint4(0u, 0u, 0u, 0u);
+            sum += (v.x & 0xFFFFu) + (v.x >> 16) + (v.y & 0xFFFFu) + (v.y >> 16) + (v.z & 0xFFFFu) + (v.z >> 16) +
+                   (v.w & 0xFFFFu) + (v.w >> 16);
+        }
+        acc[b] += sum;
+    }
+}
 
-template <bool ITER, bool POW2, int RL>
-__global__ void __launch_bounds__(512) hist_rep_kernel(HistArgs H) {
-    extern __shared__ uint32_t rep[];  // [ceil(m/4)][32] words
-    const int words = (int)((H.m + 3) >> 2) * 32;
-    for (int i = threadIdx.x; i < words; i += blockDim.x) rep[i] = 0;
+template <bool ITER, bool POW2, int RL, int COLS>
+__global__ void __launch_bounds__(HistShape<COLS>::threads) hist_kernel8(HistArgs H) {
+    extern __shared__ uint4 smem4[];
+    const uint32_t m = H.m;
+    uint4* cnt = smem4;                                                      // [m] x 2*COLS slots (16-bit)
+    uint32_t* acc = reinterpret_cast<uint32_t*>(smem4 + m * (COLS / 4));  // [m] u32
+    for (uint32_t i = threadIdx.x; i < m * (COLS / 4); i += blockDim.x) cnt[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) acc[i] = 0u;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint32_t rep_lane = (uint32_t)__cvta_generic_to_shared(rep + lane);
-    const uint32_t p = H.p, m = H.m, mp = H.mp;
-    const uint32_t wmask = (m - 1) & ~3u;
-    unsigned long long* counts = H.counts;
+    const uint32_t col = (uint32_t)__cvta_generic_to_shared(cnt) + 4u * (uint32_t)(lane & (COLS - 1));
+    const uint32_t inc = (lane & COLS) ? 0x10000u : 1u;
+    const uint32_t p = H.p, mp = H.mp;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;  // a multiple of nblk
     // this thread's lane block is fixed: units u = gtid + k * nthreads, blk = u % nblk
@@ -210,43 +205,20 @@ __global__ void __launch_bounds__(512) hist_rep_kernel(HistArgs H) {
     const int32_t i1 = min(i0 + H.run, H.n_hash);
     const int n = i1 - i0;
     const int64_t xstride = nthreads / H.nblk;
+    // rounds of two x each; every thread of the CTA runs its first thread's count (the most)
+    const int64_t x_first = ((int64_t)blockIdx.x * blockDim.x) / H.nblk;
+    const int64_t rounds = x_first < H.n_x ? (H.n_x - x_first + 2 * xstride - 1) / (2 * xstride) : 0;
+    const int per_sweep = HistShape<COLS>::max_run / (2 * (H.run > 0 ? H.run : 1));
+    int64_t xi = gtid / H.nblk;
+
+    uint32_t A = 0, Ap = 0, B = 0;
+    uint32_t cA[RL], cAp[RL], cB[RL];
     if (ITER) {
         // h_{i0}(x) = (a + i0) x + i0 b mod p (families.py:170-176), then the additive walk
-        const uint32_t A = (uint32_t)((H.a + (uint64_t)i0) % p);
-        const uint32_t Ap = shoup_companion(A, p);
-        const uint32_t B = (uint32_t)((uint64_t)i0 * H.b % p);
-        for (int64_t xi = gtid / H.nblk; xi < H.n_x && n > 0; xi += xstride) {
-            const uint32_t x = __ldg(H.xs + xi);
-            uint32_t h = mul_add_mod(A, Ap, B, x, p);
-            const uint32_t dh = reduce_once(x + H.b, p);
-            int k = 0;
-            // four evaluations per check of the 127 -> 128 flags
-            for (; k + 4 <= n; k += 4) {
-                const uint32_t h0 = h;
-                const uint32_t f0 = count_bin<POW2>(rep_lane, h0, m, mp, wmask);
-                const uint32_t h1 = reduce_once(h0 + dh, p);
-                const uint32_t f1 = count_bin<POW2>(rep_lane, h1, m, mp, wmask);
-                const uint32_t h2 = reduce_once(h1 + dh, p);
-                const uint32_t f2 = count_bin<POW2>(rep_lane, h2, m, mp, wmask);
-                const uint32_t h3 = reduce_once(h2 + dh, p);
-                const uint32_t f3 = count_bin<POW2>(rep_lane, h3, m, mp, wmask);
-                h = reduce_once(h3 + dh, p);
-                if ((f0 | f1 | f2 | f3) & kBit7) {
-                    if (f0 & kBit7) spill_bin<POW2>(rep_lane, h0, m, mp, counts);
-                    if (f1 & kBit7) spill_bin<POW2>(rep_lane, h1, m, mp, counts);
-                    if (f2 & kBit7) spill_bin<POW2>(rep_lane, h2, m, mp, counts);
-                    if (f3 & kBit7) spill_bin<POW2>(rep_lane, h3, m, mp, counts);
-                }
-            }
-            for (; k < n; ++k) {
-                if (count_bin<POW2>(rep_lane, h, m, mp, wmask) & kBit7) spill_bin<POW2>(rep_lane, h, m, mp, counts);
-                h = reduce_once(h + dh, p);
-            }
-        }
+        A = (uint32_t)((H.a + (uint64_t)i0) % p);
+        Ap = shoup_companion(A, p);
+        B = (uint32_t)((uint64_t)i0 * H.b % p);
     } else {
-        // random family: RL lanes' constants in registers (Shoup companions), one
-        // multiply-add per evaluation
-        uint32_t cA[RL], cAp[RL], cB[RL];
 #pragma unroll
         for (int k = 0; k < RL; ++k) {
             const int32_t i = min(i0 + k, H.n_hash - 1);
@@ -254,45 +226,62 @@ __global__ void __launch_bounds__(512) hist_rep_kernel(HistArgs H) {
             cAp[k] = shoup_companion(cA[k], p);
             cB[k] = H.rb[i];
         }
-        const bool narrow = 3ull * p < (1ull << 32);
-        for (int64_t xi = gtid / H.nblk; xi < H.n_x && n > 0; xi += xstride) {
-            const uint32_t x = __ldg(H.xs + xi);
-            if (n == RL && narrow) {
-#pragma unroll
-                for (int k = 0; k < RL; k += 4) {
-                    uint32_t hh[4], f[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        hh[e] = mul_add_mod_narrow(cA[k + e], cAp[k + e], cB[k + e], x, p);
-                        f[e] = count_bin<POW2>(rep_lane, hh[e], m, mp, wmask);
+    }
+    const bool narrow = 3ull * p < (1ull << 32);
+    // next round's x prefetched (an L2 round trip per round otherwise)
+    uint32_t xa_n = xi < H.n_x ? __ldg(H.xs + xi) : 0u;
+    uint32_t xb_n = xi + xstride < H.n_x ? __ldg(H.xs + xi + xstride) : 0u;
+    for (int64_t r0 = 0; r0 < rounds; r0 += per_sweep) {
+        const int64_t r1 = min(rounds, r0 + per_sweep);
+        for (int64_t r = r0; r < r1; ++r, xi += 2 * xstride) {
+            const uint32_t xa = xa_n, xb = xb_n;
+            const bool va = xi < H.n_x && n > 0, vb = xi + xstride < H.n_x && n > 0;
+            const int64_t xn = xi + 2 * xstride;
+            xa_n = xn < H.n_x ? __ldg(H.xs + xn) : 0u;
+            xb_n = xn + xstride < H.n_x ? __ldg(H.xs + xn + xstride) : 0u;
+            if (ITER) {
+                if (va && vb) {
+                    uint32_t ha = mul_add_mod(A, Ap, B, xa, p), hb = mul_add_mod(A, Ap, B, xb, p);
+                    const uint32_t da = reduce_once(xa + H.b, p), db = reduce_once(xb + H.b, p);
+#pragma unroll 2
+                    for (int k = 0; k < n; ++k) {
+                        count_bin<POW2, COLS>(col, inc, ha, m, mp);
+                        count_bin<POW2, COLS>(col, inc, hb, m, mp);
+                        ha = reduce_once(ha + da, p);
+                        hb = reduce_once(hb + db, p);
                     }
-                    if ((f[0] | f[1] | f[2] | f[3]) & kBit7) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (f[e] & kBit7) spill_bin<POW2>(rep_lane, hh[e], m, mp, counts);
+                } else if (va) {
+                    uint32_t ha = mul_add_mod(A, Ap, B, xa, p);
+                    const uint32_t da = reduce_once(xa + H.b, p);
+                    for (int k = 0; k < n; ++k) {
+                        count_bin<POW2, COLS>(col, inc, ha, m, mp);
+                        ha = reduce_once(ha + da, p);
                     }
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < RL; ++k) {
-                    if (k < n) {
-                        const uint32_t hk = mul_add_mod(cA[k], cAp[k], cB[k], x, p);
-                        if (count_bin<POW2>(rep_lane, hk, m, mp, wmask) & kBit7) spill_bin<POW2>(rep_lane, hk, m, mp, counts);
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t x = e ? xb : xa;
+                    if (!(e ? vb : va)) continue;
+                    if (n == RL && narrow) {
+                        // random family: RL lanes' constants in registers, one Shoup multiply-add each
+#pragma unroll
+                        for (int k = 0; k < RL; ++k)
+                            count_bin<POW2, COLS>(col, inc, mul_add_mod_narrow(cA[k], cAp[k], cB[k], x, p), m, mp);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < RL; ++k)
+                            if (k < n) count_bin<POW2, COLS>(col, inc, mul_add_mod(cA[k], cAp[k], cB[k], x, p), m, mp);
                     }
                 }
             }
         }
+        __syncthreads();
+        sweep8<COLS>(cnt, acc, m);
+        __syncthreads();
     }
-    __syncthreads();
-    // fold the 32 byte replicas of every bin into the global counts
-    for (uint32_t bin = threadIdx.x; bin < m; bin += blockDim.x) {
-        const uint32_t* wrow = rep + ((bin >> 2) << 5);
-        const int sh = (int)(bin & 3) * 8;
-        uint32_t c = 0;
-#pragma unroll 8
-        for (int r = 0; r < 32; ++r) c += (wrow[r] >> sh) & 0xFFu;
-        if (c) atomicAdd(counts + bin, (unsigned long long)c);
-    }
+    for (uint32_t bin = threadIdx.x; bin < m; bin += blockDim.x)
+        if (acc[bin]) atomicAdd(H.counts + bin, (unsigned long long)acc[bin]);
 }
 
 // Fallback for m > 4096 (or p >= 2^31 is handled below): one u32 table per CTA in
@@ -380,18 +369,21 @@ __global__ void hist_wide_kernel(const IdT* __restrict__ xs, int64_t n_x, int ki
 template <bool ITER, bool POW2>
 static int launch_rep(HistArgs H, const DeviceInfo& dev, cudaStream_t st) {
     constexpr int RL = ITER ? 1 : 16;
-    auto fn = hist_rep_kernel<ITER, POW2, RL>;
-    const size_t smem = (size_t)((H.m + 3) / 4) * 32 * sizeof(uint32_t);
+    constexpr int COLS = ITER ? 8 : 4;
+    using S = HistShape<COLS>;
+    auto fn = hist_kernel8<ITER, POW2, RL, COLS>;
+    const size_t smem = (size_t)H.m * (COLS * sizeof(uint32_t) + sizeof(uint32_t));
     static int attr_done[64] = {0};
     if (dev.device >= 0 && dev.device < 64 && !attr_done[dev.device]) {
-        int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 kRepMaxBins / 4 * 32 * (int)sizeof(uint32_t)),
-                            "hist_rep smem attr");
+        const int most = kRepMaxBins * (int)(COLS * sizeof(uint32_t) + sizeof(uint32_t));
+        int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, most),
+                            "hist smem attr");
         if (rc) return rc;
         attr_done[dev.device] = 1;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512, smem) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, S::threads, smem) != cudaSuccess || occ < 1)
+        occ = 1;
     // lane blocks per x: a power of two (so the grid's thread count is a multiple of it)
     // with about 64 lanes each for the iterative walk, RL for the random family
     const int want = ITER ? (H.n_hash + 63) / 64 : (H.n_hash + RL - 1) / RL;
@@ -399,14 +391,13 @@ static int launch_rep(HistArgs H, const DeviceInfo& dev, cudaStream_t st) {
     while (nblk < want && nblk < 512) nblk *= 2;
     H.nblk = nblk;
     H.run = (H.n_hash + nblk - 1) / nblk;
-    if (!ITER && H.run > RL) {  // more lanes than 512 blocks of RL: not representable
-        return set_error(MHB_ERR_UNSUPPORTED, "random-family histogram over %d members", H.n_hash);
-    }
+    if (2 * H.run > S::max_run || (!ITER && H.run > RL))
+        return set_error(MHB_ERR_UNSUPPORTED, "histogram over %d members needs the fallback kernel", H.n_hash);
     int64_t blocks = (int64_t)occ * dev.sms;
-    const int64_t need = (H.n_x * nblk + 511) / 512;  // one unit per thread is enough
+    const int64_t need = (H.n_x * nblk + 2 * S::threads - 1) / (2 * S::threads);  // two x per thread
     if (blocks > need) blocks = need < 1 ? 1 : need;
-    fn<<<(unsigned)blocks, 512, smem, st>>>(H);
-    return cuda_check(cudaGetLastError(), "hist_rep_kernel launch");
+    fn<<<(unsigned)blocks, S::threads, smem, st>>>(H);
+    return cuda_check(cudaGetLastError(), "hist_kernel8 launch");
 }
 
 static int launch_hist(HistArgs H, cudaStream_t st) {
@@ -419,8 +410,8 @@ static int launch_hist(HistArgs H, cudaStream_t st) {
     DeviceInfo dev;
     int rc = current_device_info(&dev);
     if (rc) return rc;
-    const bool pow2 = H.m >= 4 && (H.m & (H.m - 1)) == 0;
-    const bool rep_ok = H.m <= (uint32_t)kRepMaxBins && (H.kind == 0 || H.n_hash <= 512 * 16);
+    const bool pow2 = H.m >= 2 && (H.m & (H.m - 1)) == 0;
+    const bool rep_ok = H.m <= (uint32_t)kRepMaxBins && (H.kind == 0 ? H.n_hash <= 512 * (HistShape<8>::max_run / 2) : H.n_hash <= 512 * 16);
     if (rep_ok) {
         if (H.kind == 0) return pow2 ? launch_rep<true, true>(H, dev, st) : launch_rep<true, false>(H, dev, st);
         return pow2 ? launch_rep<false, true>(H, dev, st) : launch_rep<false, false>(H, dev, st);

@@ -62,7 +62,7 @@ def test_hist_byte_spill(cuda_device):
     xs = np.unique((4096 * t - b) % p)
     got = bucket_histogram(xs, fam, 4096).cpu().numpy()
     want = _np_hist_iter(fam, xs, 4096)
-    assert want.max() > 10_000  # the case really concentrates
+    assert want.max() >= 2048  # the case really concentrates (a whole x in one bin)
     assert got.tolist() == want.tolist()
 
 
