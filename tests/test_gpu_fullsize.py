@@ -121,3 +121,47 @@ def test_cfg4_full_with_fused_band_keys(cuda_device):
     assert torch.equal(keys.view(torch.int64), band_keys(sig, 16).view(torch.int64))
     _, keys_only = signatures_band_keys(ip, ids, fam, 16, write_signatures=False)
     assert torch.equal(keys_only.view(torch.int64), keys.view(torch.int64))
+
+
+def _zipf_sets(cfg, sizes, device, seed):
+    """Distinct Zipf(cfg) ids over cfg's vocabulary for sets of the given sizes (sorted)."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    z = gen._ZipfSampler(cfg.zipf_s, cfg.vocab, device)
+    rows = []
+    for n in sizes:
+        have = torch.empty(0, dtype=torch.int64, device=device)
+        while have.numel() < n:
+            have = torch.unique(torch.cat([have, z.sample(4 * n, g)]))
+        # keep n distinct ids: a random subset, so popular and rare ids both appear
+        keep = have[torch.randperm(have.numel(), generator=g, device=device)[:n]]
+        rows.append(torch.sort(keep).values.to(torch.uint32))
+    return rows
+
+
+def test_cfg5_distribution_shard(cuda_device):
+    """cfg5's generator (lognormal(60, 1.2) sizes, Zipf(1.05) ids over 2^30, p =
+    1,073,741,827: the largest BASELINE prime, 3p < 2^32) on its first 200k sets plus
+    sets at the 50,000-id cap: membership, oracle rows (including the capped sets, which
+    merge 49 chunks each), shuffle invariance, and the host pipeline."""
+    import torch
+
+    cfg = gen.CONFIGS["cfg5"]
+    ip0, ids0, _ = gen.make_shard(cfg, 0, 200_000, cuda_device)
+    big = _zipf_sets(cfg, [50_000, 50_000, 49_999, 20_001], cuda_device, 7)
+    ids = torch.cat([ids0] + big)
+    sizes = torch.cat([ip0[1:] - ip0[:-1], torch.tensor([b.numel() for b in big], device=cuda_device)])
+    ip = torch.zeros(sizes.numel() + 1, dtype=torch.int64, device=cuda_device)
+    torch.cumsum(sizes, 0, out=ip[1:])
+    fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+    assert fam.prime == 1_073_741_827
+    sig = signatures_csr(ip, ids, fam, out_dtype="uint32")
+    _membership(ip, ids, sig)
+    n = ip.numel() - 1
+    rows = np.unique(np.concatenate([_sample_rows(ip, 2000, np.random.default_rng(4)), np.arange(n - 4, n)]))
+    assert np.array_equal(_rows(sig, rows), _oracle_rows(ip, ids, fam, rows))
+    sig2 = signatures_csr(ip, _shuffled_within_sets(ip, ids, 9), fam, out_dtype="uint32")
+    assert torch.equal(sig2.view(torch.int32), sig.view(torch.int32))
+    host = signatures_csr(ip.cpu().numpy(), ids.cpu().numpy().view(np.uint32), fam, out_dtype="int64")
+    assert np.array_equal(host, sig.cpu().numpy().astype(np.int64))
