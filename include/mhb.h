@@ -161,6 +161,14 @@ int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint32_t* ids,
 void mhb_host_release(void);
 
 /*
+ * Diagnostic (no GPU needed): runs `jobs` back-to-back jobs of 2..64 parts on the host
+ * copy pool mhb_sign_csr_host stages pageable buffers with, from `threads` concurrent
+ * callers, each part recording how often it ran.  *bad = parts that ran other than
+ * exactly once (0 for a correct pool).  Returns MHB_OK.
+ */
+int mhb_host_pool_selftest(int64_t jobs, uint64_t seed, int32_t threads, int64_t* bad);
+
+/*
  * Pairwise Jaccard estimates for listed pairs (replaces estimate_jaccard,
  * minhash.py:130-137): counts[k] = #{i : sig[pi[k]][i] == sig[pj[k]][i]};
  * est[k] = (double)counts[k] / n_hash (IEEE division, bit-identical to numpy's

@@ -49,6 +49,7 @@ SIGNATURES = {
     "mhb_sign_csr_ids64": (C.c_int, [_I32, _P, _P, _I64, _I64, _U64, _U64, _P, _P, _U64, _I32, _P, _P, _P]),
     "mhb_sign_csr_host": (C.c_int, [_I32, _P, _P, _I64, _I64, _U64, _U64, _P, _P, _U64, _I32, _P, _I32, _P, _I32]),
     "mhb_host_release": (None, []),
+    "mhb_host_pool_selftest": (C.c_int, [_I64, _U64, _I32, _P]),
     "mhb_jaccard_pairs": (C.c_int, [_P, _I32, _I32, _P, _P, _I64, _P, _P, _P]),
     "mhb_jaccard_block": (C.c_int, [_P, _I64, _P, _I64, _I32, _I32, _P, _P]),
     "mhb_band_keys": (C.c_int, [_P, _I32, _I64, _I32, _I32, _P, _P]),

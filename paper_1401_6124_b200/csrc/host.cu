@@ -541,6 +541,35 @@ extern "C" int mhb_sign_csr_host(int32_t kind, const int64_t* indptr, const uint
     return MHB_OK;
 }
 
+extern "C" int mhb_host_pool_selftest(int64_t jobs, uint64_t seed, int32_t threads, int64_t* bad) {
+    clear_error();
+    if (!bad || jobs < 0 || threads < 1 || threads > 64) return set_error(MHB_ERR_INVALID, "bad arguments");
+    std::atomic<int64_t> wrong{0};
+    auto caller = [&](int t) {
+        uint64_t s = seed * 6364136223846793005ull + (uint64_t)t * 1442695040888963407ull + 1;
+        std::vector<std::atomic<int>> hits(64);
+        for (int64_t j = t; j < jobs; j += threads) {
+            s = s * 6364136223846793005ull + 1442695040888963407ull;
+            const int parts = 2 + (int)((s >> 33) % 63);
+            for (int k = 0; k < parts; ++k) hits[k].store(0);
+            const int spin = (int)((s >> 20) & 255);
+            host_pool().run(parts, [&](int k) {
+                volatile int x = 0;  // uneven part lengths: workers finish at different times
+                for (int i = 0; i < spin * (k & 3); ++i) x = x + i;
+                hits[k].fetch_add(1);
+            });
+            for (int k = 0; k < parts; ++k)
+                if (hits[k].load() != 1) wrong.fetch_add(1);
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < threads; ++t) th.emplace_back(caller, t);
+    caller(0);
+    for (auto& x : th) x.join();
+    *bad = wrong.load();
+    return MHB_OK;
+}
+
 extern "C" void mhb_host_release(void) {
     std::lock_guard<std::mutex> lock(g_mu);
     for (int d = 0; d < 64; ++d) {
