@@ -75,13 +75,21 @@ __host__ __device__ __forceinline__ uint32_t shoup_companion(uint32_t w, uint32_
     return (uint32_t)(((uint64_t)w << 32) / p);
 }
 
-// Modular inverse of w in Z_p (w != 0 mod p, p prime) by the extended Euclid.
+// Modular inverse of w in Z_p (w != 0 mod p, p prime) by the extended Euclid.  The
+// remainders stay below 2^32, so the quotients are 32-bit divisions (the 64-bit
+// division the naive spelling emits is a long emulated sequence on the GPU); the
+// Bezout coefficients are bounded by p in magnitude.
 __host__ __device__ inline uint32_t inv_mod(uint32_t w, uint32_t p) {
-    int64_t t = 0, nt = 1, r = p, nr = w % p;
+    int64_t t = 0, nt = 1;
+    uint32_t r = p, nr = w % p;
     while (nr != 0) {
-        int64_t q = r / nr;
-        int64_t tmp = t - q * nt; t = nt; nt = tmp;
-        tmp = r - q * nr; r = nr; nr = tmp;
+        const uint32_t q = r / nr;
+        const int64_t tmp = t - (int64_t)q * nt;
+        t = nt;
+        nt = tmp;
+        const uint32_t rr = r - q * nr;
+        r = nr;
+        nr = rr;
     }
     if (t < 0) t += p;
     return (uint32_t)t;

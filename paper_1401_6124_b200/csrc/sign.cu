@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -45,14 +46,14 @@ static int next_pow2(int v) {
     return r;
 }
 
-Geometry choose_geometry(int kind, int32_t n_hash) {
+static int default_lanes(int kind, int32_t n_hash) {
+    if (kind == KIND_ITERATIVE) return n_hash >= 128 ? 64 : n_hash >= 32 ? 32 : n_hash >= 16 ? 16 : 8;
+    return n_hash >= 16 ? 16 : 8;  // 3 constants + 1 minimum per lane in registers
+}
+
+Geometry choose_geometry(int kind, int32_t n_hash, int K) {
     Geometry g{};
-    int K;
-    if (kind == KIND_ITERATIVE) {
-        K = n_hash >= 128 ? 64 : n_hash >= 32 ? 32 : n_hash >= 16 ? 16 : 8;
-    } else {
-        K = n_hash >= 16 ? 16 : 8;  // 3 constants + 1 minimum per lane in registers
-    }
+    if (K <= 0) K = default_lanes(kind, n_hash);
     int lg = (n_hash + K - 1) / K;
     if (lg <= 32) {
         g.G = next_pow2(lg);
@@ -72,11 +73,39 @@ Geometry choose_geometry(int kind, int32_t n_hash) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Lanes per thread for this batch.  The default K amortises each feature's start hash
+// over many lanes, but a small batch then has too few work items (warps) to fill the
+// SMs: cfg1 (10,000 sets, N = 128) gives 625 warps at K = 64 for 148 SMs x 16 warps.
+// Halve K (iterative family; more lane groups per set, so more warps) until the
+// items cover one wave of warp slots.  MHB_SIGN_K forces K (tuning).
+static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fixed) {
+    static const int forced = [] {
+        const char* e = std::getenv("MHB_SIGN_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int K0 = default_lanes(kind, n_hash);
+    if (forced == 8 || forced == 16 || (kind == KIND_ITERATIVE && (forced == 32 || forced == 64)))
+        return fixed ? K0 : forced;
+    if (fixed || kind != KIND_ITERATIVE) return K0;
+    const int64_t slots = (int64_t)sms * 2 * (kBlock / 32);  // one wave of warp slots (2 CTAs/SM)
+    int K = K0;
+    while (K > 8) {
+        const Geometry g = choose_geometry(kind, n_hash, K);
+        const int64_t items = (n_sets + g.F - 1) / g.F * g.n_super;
+        if (items >= slots) break;
+        K /= 2;
+    }
+    return K;
+}
+
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
-    // Both families share one layout; size for the larger lane table.
-    Geometry gi = choose_geometry(KIND_ITERATIVE, n_hash);
-    Geometry gr = choose_geometry(KIND_RANDOM, n_hash);
-    int64_t n_tot = gi.n_tot > gr.n_tot ? gi.n_tot : gr.n_tot;
+    // Both families and every lane count share one layout; size for the largest lane table.
+    int64_t n_tot = 0;
+    for (int K = 8; K <= 64; K *= 2)
+        for (int kind = 0; kind < 2; ++kind) {
+            const Geometry g = choose_geometry(kind, n_hash, K);
+            if (g.n_tot > n_tot) n_tot = g.n_tot;
+        }
     int64_t nnz_pos = nnz > 0 ? nnz : 0;
     int64_t sets = n_sets > 0 ? n_sets : 0;
     int64_t max_big = nnz_pos / (kChunk + 1);
@@ -99,6 +128,56 @@ WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
 // Plan: lane tables, size histogram of virtual sets, long-set bookkeeping
 // ----------------------------------------------------------------------------
 
+// floor(w * 2^32 / p) for w < p < 2^31 without the 64-bit division (a long emulated
+// sequence): a double-precision estimate, corrected against the exact 64-bit remainder.
+__device__ __forceinline__ uint32_t companion_fast(uint32_t w, uint32_t p) {
+    uint32_t q = (uint32_t)(((double)w * 4294967296.0) / (double)p);
+    int64_t r = (int64_t)((uint64_t)w << 32) - (int64_t)q * (int64_t)p;
+    while (r < 0) { --q; r += p; }
+    while (r >= (int64_t)p) { ++q; r -= p; }
+    return q;
+}
+
+// Lane i's tables: the start-hash constants (A, Shoup(A), B) and the argmin recovery
+// (B, A^{-1}, Shoup(A^{-1})).  All 32-bit arithmetic (p < 2^31).
+__device__ __forceinline__ void fill_lane_tables(const SignArgs& A, int64_t i) {
+    const uint32_t p = A.p;
+    uint32_t w, c;
+    if (A.kind == KIND_ITERATIVE) {
+        // member i: multiplier a+i, offset i*b (families.py:124-131)
+        w = (uint32_t)(((uint32_t)A.ia + (uint32_t)(i % p)) % p);  // a < p < 2^31: no overflow
+        if (w == 0) w = 1;  // only reachable on padded lanes i >= n_hash
+        c = reduce_once(shoup_lazy(A.b, companion_fast(A.b, p), (uint32_t)(i % p), p), p);
+    } else if (i < A.n_hash) {
+        w = A.ra[i];
+        c = A.rb[i];
+        if (w == 0 || w >= p || c >= p) {
+            if (A.status) atomicOr(A.status, MHB_STATUS_BAD_PARAM);
+            w = 1;
+            c = 0;
+        }
+    } else {
+        w = 1;
+        c = 0;
+    }
+    LaneTab t;
+    t.A = w;
+    t.Ap = companion_fast(w, p);
+    t.B = c;
+    if (A.fpq) {  // float-quotient lanes (walk2_random_fpq): rd(w/p) and c + 2^23-magic * p
+        t.Ap = __float_as_uint(__double2float_rd((double)w / (double)p));
+        t.B = c + 0x4B000000u * p;
+    }
+    t.pad = 0;
+    A.tab[i] = t;
+    InvTab v;
+    v.B = c;
+    v.inv = inv_mod(w, p);
+    v.invp = companion_fast(v.inv, p);
+    v.pad = 0;
+    A.inv[i] = v;
+}
+
 template <typename OutT>
 __global__ void plan_count_kernel(SignArgs A) {
     __shared__ unsigned sh[kChunk];
@@ -108,42 +187,7 @@ __global__ void plan_count_kernel(SignArgs A) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const uint32_t p = A.p;
 
-    for (int64_t i = tid; i < A.n_tot; i += stride) {
-        uint32_t w, c;
-        if (A.kind == KIND_ITERATIVE) {
-            // member i: multiplier a+i, offset i*b (families.py:124-131)
-            w = (uint32_t)((A.ia + (uint64_t)i) % p);
-            if (w == 0) w = 1;  // only reachable on padded lanes i >= n_hash
-            c = (uint32_t)(((uint64_t)i % p) * (uint64_t)A.b % p);
-        } else if (i < A.n_hash) {
-            w = A.ra[i];
-            c = A.rb[i];
-            if (w == 0 || w >= p || c >= p) {
-                if (A.status) atomicOr(A.status, MHB_STATUS_BAD_PARAM);
-                w = 1;
-                c = 0;
-            }
-        } else {
-            w = 1;
-            c = 0;
-        }
-        LaneTab t;
-        t.A = w;
-        t.Ap = shoup_companion(w, p);
-        t.B = c;
-        if (A.fpq) {  // float-quotient lanes (walk2_random_fpq): rd(w/p) and c + 2^23-magic * p
-            t.Ap = __float_as_uint(__double2float_rd((double)w / (double)p));
-            t.B = c + 0x4B000000u * p;
-        }
-        t.pad = 0;
-        A.tab[i] = t;
-        InvTab v;
-        v.B = c;
-        v.inv = inv_mod(w, p);
-        v.invp = shoup_companion(v.inv, p);
-        v.pad = 0;
-        A.inv[i] = v;
-    }
+    for (int64_t i = tid; i < A.n_tot; i += stride) fill_lane_tables(A, i);
 
     for (int64_t s = tid; s < A.n_sets; s += stride) {
         const int64_t n = A.indptr[s + 1] - A.indptr[s];
@@ -246,6 +290,135 @@ __global__ void plan_scatter_kernel(SignArgs A) {
         OutT* row = out + A.big[e] * (int64_t)A.n_hash;
         for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x) row[i] = (OutT)(~0u);
     }
+}
+
+// Small batches (n_sets <= kSmallPlan = 16384): the whole plan in ONE launch.  No size
+// sort: virtual sets stay in set order (each set's chunks consecutive), placed by a
+// single-pass prefix sum of the chunk counts over tiles of kSmallTile sets, one tile
+// per CTA: every CTA publishes its tile's aggregate, then sums the aggregates of the
+// tiles before it in parallel (a CTA takes its tile from a ticket counter and waits
+// only for tiles whose tickets were taken before its own -- CTAs already running).  The three sorted-plan kernels
+// cost ~16 us at 10,000 sets; a one-CTA plan ~24 us (one SM, latency-bound).  A warp
+// group then holds sets of unequal sizes, so the STATIC kernel instances run the
+// group's largest set (a warp max).  Lane tables: every CTA fills a slice.
+constexpr int64_t kSmallPlan = 1 << 14;
+constexpr int kSmallTile = 256;  // sets per tile = threads per CTA
+
+// hist[] doubles as the look-back state: [0] ticket counter, [2 + 2k] / [3 + 2k] tile
+// k's (chunks, long sets) aggregate + 1 (0 = not yet published).
+template <typename OutT>
+__global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
+    __shared__ unsigned warp_c[kSmallTile / 32], warp_b[kSmallTile / 32];
+    __shared__ unsigned tile_s, excl_c, excl_b, warp_tot2[2], warp_totb2[2];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    volatile unsigned* flags = A.hist;
+    if (t == 0) tile_s = atomicAdd(&A.hist[0], 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const int64_t s = (int64_t)tile * kSmallTile + t;
+    int64_t lo = 0, n = 0;
+    if (s < A.n_sets) {
+        lo = A.indptr[s];
+        n = A.indptr[s + 1] - lo;
+    }
+    unsigned chunks = 0, bigs = 0;
+    if (s < A.n_sets) {
+        if (n <= 0) {
+            if (A.status) atomicOr(A.status, MHB_STATUS_EMPTY_SET);
+        } else {
+            const int64_t nch = (n + kChunk - 1) / kChunk;
+            chunks = (unsigned)nch;
+            bigs = nch > 1 ? 1u : 0u;
+        }
+    }
+    unsigned ci = chunks, bi = bigs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, ci, o), z = __shfl_up_sync(0xffffffffu, bi, o);
+        if (lane >= o) {
+            ci += y;
+            bi += z;
+        }
+    }
+    if (lane == 31) {
+        warp_c[w] = ci;
+        warp_b[w] = bi;
+    }
+    __syncthreads();
+    if (t == 0) {
+        unsigned tc = 0, tb = 0;
+        for (int k = 0; k < kSmallTile / 32; ++k) {
+            const unsigned c = warp_c[k], b = warp_b[k];
+            warp_c[k] = tc;
+            warp_b[k] = tb;
+            tc += c;
+            tb += b;
+        }
+        // publish this tile's aggregate at once (no waiting): every tile's prefix is
+        // the sum of the aggregates before it, read in parallel below
+        flags[3 + 2 * tile] = tb + 1u;
+        __threadfence();
+        flags[2 + 2 * tile] = tc + 1u;
+        excl_c = tc;  // own aggregate, for the last tile's totals
+        excl_b = tb;
+    }
+    __syncthreads();
+    const unsigned own_c = excl_c, own_b = excl_b;
+    // exclusive prefix = sum over tiles < tile of their aggregates (<= 64 tiles: two warps)
+    if (w < 2) {
+        unsigned pc = 0, pb = 0;
+        const unsigned k = (unsigned)t;
+        if (k < tile) {
+            unsigned fc, fb;
+            do {
+                fc = flags[2 + 2 * k];
+                fb = flags[3 + 2 * k];
+            } while (fc == 0u || fb == 0u);
+            pc = fc - 1u;
+            pb = fb - 1u;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pc += __shfl_xor_sync(0xffffffffu, pc, o);
+            pb += __shfl_xor_sync(0xffffffffu, pb, o);
+        }
+        if (lane == 0) {
+            warp_tot2[w] = pc;
+            warp_totb2[w] = pb;
+        }
+    }
+    __syncthreads();
+    if (t == 0) {
+        const unsigned pc = warp_tot2[0] + warp_tot2[1], pb = warp_totb2[0] + warp_totb2[1];
+        excl_c = pc;
+        excl_b = pb;
+        const unsigned n_tiles = (unsigned)((A.n_sets + kSmallTile - 1) / kSmallTile);
+        if (tile + 1 == n_tiles) {
+            A.sched->next = 0;
+            A.sched->n_vsets = pc + own_c;
+            A.sched->n_big = pb + own_b;
+        }
+    }
+    __syncthreads();
+    if (chunks) {
+        unsigned pos = excl_c + warp_c[w] + ci - chunks;
+        const long long merge = chunks > 1 ? 1 : 0;
+        for (unsigned c = 0; c < chunks; ++c) {
+            const int size = (int)((c + 1 < chunks) ? kChunk : n - (int64_t)c * kChunk);
+            VSet vs;
+            vs.f0 = lo + (int64_t)c * kChunk;
+            vs.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
+            A.vsets[pos++] = vs;
+        }
+        if (merge) {
+            A.big[excl_b + warp_b[w] + bi - bigs] = s;
+            // rows of long sets start at UINT_MAX (their chunks merge with red.global.min)
+            OutT* row = reinterpret_cast<OutT*>(A.out) + s * (int64_t)A.n_hash;
+            for (int i = 0; i < A.n_hash; ++i) row[i] = (OutT)(~0u);
+        }
+    }
+    for (int64_t i = (int64_t)tile * kSmallTile + t; i < A.n_tot; i += (int64_t)gridDim.x * kSmallTile)
+        fill_lane_tables(A, i);
 }
 
 // ----------------------------------------------------------------------------
@@ -570,7 +743,8 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
-template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false>
+template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false,
+          bool STATIC = false>
 __global__ void __maxnreg__((Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>::maxnreg))  // 128: 2 CTAs of 256 per SM
 sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) {
     using S = Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>;
@@ -598,13 +772,22 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     // Work items flow through a 3-deep pipeline: the id of the item after next is
     // claimed while the current one runs, the next item's set entry is loaded, and
     // the last round of the current item prefetches the next item's first features.
+    // STATIC (small batches): warp w takes items w, w + W, w + 2W, ... -- one work
+    // counter's serialised atomics would be a large share of a short kernel.  Otherwise
+    // items come from the counter (dynamic balance of the size-sorted work).
+    const unsigned long long W = (unsigned long long)gridDim.x * (kBlock / 32);
     unsigned long long it = 0, itn = 0, itnn = 0;
-    if (lane == 0) {
-        it = atomicAdd(&A.sched->next, 1ull);
-        itn = atomicAdd(&A.sched->next, 1ull);
+    if constexpr (STATIC) {
+        it = (unsigned long long)blockIdx.x * (kBlock / 32) + warp;
+        itn = it + W;
+    } else {
+        if (lane == 0) {
+            it = atomicAdd(&A.sched->next, 1ull);
+            itn = atomicAdd(&A.sched->next, 1ull);
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+        itn = __shfl_sync(0xffffffffu, itn, 0);
     }
-    it = __shfl_sync(0xffffffffu, it, 0);
-    itn = __shfl_sync(0xffffffffu, itn, 0);
     VSet ec = load_vset(A, it, n_vsets, f);
     VSet en = load_vset(A, itn, n_vsets, f);
 
@@ -624,7 +807,11 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     }
 
     while (it < n_items) {
-        if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
+        if constexpr (STATIC) {
+            itnn = itn + W;
+        } else {
+            if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
+        }
         int sb = 0;
         if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
         if (sb != cur_sb) {  // lane constants change only with the lane pass
@@ -646,8 +833,9 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
         const int n = valid ? (int)(ec.meta & 2047) + 1 : 1;
         const int last = n - 1;
         const uint32_t* base = A.ids + (valid ? ec.f0 : 0);
-        // the group's first set is its largest (descending sort)
-        const int n_max = __shfl_sync(0xffffffffu, n, 0);
+        // the group's first set is its largest (descending sort); STATIC instances serve
+        // the unsorted small-batch plan: the group's largest set by a warp max
+        const int n_max = STATIC ? (int)__reduce_max_sync(0xffffffffu, (unsigned)n) : __shfl_sync(0xffffffffu, n, 0);
         const int rounds = (n_max + 1) >> 1;
         const bool odd = n_max & 1;
         // next item's first features (cross-item prefetch)
@@ -725,7 +913,7 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
 
         it = itn;
         ec = en;
-        itn = __shfl_sync(0xffffffffu, itnn, 0);
+        itn = STATIC ? itnn : __shfl_sync(0xffffffffu, itnn, 0);
         en = load_vset(A, itn, n_vsets, f);
     }
     if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
@@ -770,15 +958,15 @@ cudaEvent_t* g_prof_ev = nullptr;
 
 using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t, uint32_t);
 
-template <bool ITER, bool NARROW, typename OutT>
+template <bool ITER, bool NARROW, typename OutT, bool STATIC = false>
 static SignKernelFn pick_kernel(int K) {
     switch (K) {
-        case 8: return sign_kernel<8, ITER, NARROW, OutT>;
-        case 16: return sign_kernel<16, ITER, NARROW, OutT>;
-        case 32: return sign_kernel<32, ITER, NARROW, OutT>;
+        case 8: return sign_kernel<8, ITER, NARROW, OutT, false, false, false, STATIC>;
+        case 16: return sign_kernel<16, ITER, NARROW, OutT, false, false, false, STATIC>;
+        case 32: return sign_kernel<32, ITER, NARROW, OutT, false, false, false, STATIC>;
         default: break;
     }
-    if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT>;
+    if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT, false, false, false, STATIC>;
     return nullptr;
 }
 
@@ -791,8 +979,15 @@ static SignKernelFn select_skew_kernel(bool narrow, int out_dtype) {
                : sign_kernel<64, true, false, uint32_t, false, false, true>;
 }
 
-static SignKernelFn select_fpq_kernel(int out_dtype, int K) {
+static SignKernelFn select_fpq_kernel(int out_dtype, int K, bool stat) {
     const bool i64 = out_dtype == MHB_OUT_I64;
+    if (stat) {
+        if (K == 16) return i64 ? sign_kernel<16, false, true, long long, false, true, false, true>
+                                : sign_kernel<16, false, true, uint32_t, false, true, false, true>;
+        if (K == 8) return i64 ? sign_kernel<8, false, true, long long, false, true, false, true>
+                               : sign_kernel<8, false, true, uint32_t, false, true, false, true>;
+        return nullptr;
+    }
     if (K == 16) return i64 ? sign_kernel<16, false, true, long long, false, true>
                             : sign_kernel<16, false, true, uint32_t, false, true>;
     if (K == 8) return i64 ? sign_kernel<8, false, true, long long, false, true>
@@ -813,8 +1008,16 @@ static SignKernelFn select_bands_kernel(bool narrow, int out_dtype, int K) {
     return nullptr;
 }
 
-static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K) {
+static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K, bool stat) {
     const bool i64 = out_dtype == MHB_OUT_I64;
+    if (stat) {
+        if (kind == KIND_ITERATIVE) {
+            if (narrow) return i64 ? pick_kernel<true, true, long long, true>(K) : pick_kernel<true, true, uint32_t, true>(K);
+            return i64 ? pick_kernel<true, false, long long, true>(K) : pick_kernel<true, false, uint32_t, true>(K);
+        }
+        if (narrow) return i64 ? pick_kernel<false, true, long long, true>(K) : pick_kernel<false, true, uint32_t, true>(K);
+        return i64 ? pick_kernel<false, false, long long, true>(K) : pick_kernel<false, false, uint32_t, true>(K);
+    }
     if (kind == KIND_ITERATIVE) {
         if (narrow) return i64 ? pick_kernel<true, true, long long>(K) : pick_kernel<true, true, uint32_t>(K);
         return i64 ? pick_kernel<true, false, long long>(K) : pick_kernel<true, false, uint32_t>(K);
@@ -896,7 +1099,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         return set_error(MHB_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", wl.total,
                          workspace_bytes);
 
-    const Geometry geo = choose_geometry(kind, n_hash);
+    DeviceInfo dev;
+    int rc = current_device_info(&dev);
+    if (rc) return rc;
+    const Geometry geo = choose_geometry(kind, n_hash, pick_lanes(kind, n_hash, n_sets, dev.sms, keys != nullptr));
     char* ws = static_cast<char*>(workspace);
     SignArgs A{};
     A.indptr = indptr;
@@ -927,8 +1133,11 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.rows = rows_per_band;
     A.write_sig = write_sig;
 
-    // sched and hist are contiguous at the start of the workspace
-    int rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
+    // keys (fused band epilogue) have no STATIC instances: they keep the sorted plan
+    const bool small_plan = n_sets <= kSmallPlan && keys == nullptr;
+    // sched and hist are contiguous at the start of the workspace (zeroed: the sorted
+    // plan's histogram, or the small plan's look-back state)
+    rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
     if (rc) return rc;
     if (status) {
         rc = cuda_check(cudaMemsetAsync(status, 0, sizeof(int32_t), st), "memset status");
@@ -936,15 +1145,20 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     }
     if (n_sets == 0) return MHB_OK;
 
-    DeviceInfo dev;
-    rc = current_device_info(&dev);
-    if (rc) return rc;
     // random family with p <= 2^23: float-quotient lanes (walk2_random_fpq); the plan
     // kernels build their lane tables, so the flag is set before they launch
     const bool fpq = !keys && kind == KIND_RANDOM && prime <= (1ull << 23) && (geo.K == 16 || geo.K == 8);
     A.fpq = fpq ? 1 : 0;
 
-    {
+    if (small_plan) {
+        const unsigned tiles = (unsigned)((n_sets + kSmallTile - 1) / kSmallTile);
+        if (out_dtype == MHB_OUT_I64)
+            plan_small_kernel<long long><<<tiles, kSmallTile, 0, st>>>(A);
+        else
+            plan_small_kernel<uint32_t><<<tiles, kSmallTile, 0, st>>>(A);
+        rc = cuda_check(cudaGetLastError(), "plan_small launch");
+        if (rc) return rc;
+    } else {
         int64_t work = n_sets > geo.n_tot ? n_sets : geo.n_tot;
         int64_t blocks = (work + 255) / 256;
         int64_t cap = (int64_t)dev.sms * 4;
@@ -968,16 +1182,24 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
 
     const bool narrow = (3ull * prime) < (1ull << 32);
     const bool skew = !keys && kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
-    SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K)
-                      : fpq  ? select_fpq_kernel(out_dtype, geo.K)
-                      : skew ? select_skew_kernel(narrow, out_dtype)
-                             : select_kernel(kind, narrow, out_dtype, geo.K);
-    if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
+    // small batches (few items per warp slot) take the STATIC-schedule instances; the
+    // grid and the slot count use the dynamic kernel's occupancy (same registers and smem)
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0);
-    const int occ = blocks_per_sm(fn, smem, dev);
     const int64_t max_vsets = n_sets + nnz / kChunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
+    // small batches (one-CTA unsorted plan) take the STATIC instances: static work
+    // assignment and the group's largest set by a warp max; the grid uses the dynamic
+    // kernel's occupancy (same registers and smem)
+    SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K)
+                      : fpq  ? select_fpq_kernel(out_dtype, geo.K, false)
+                      : skew ? select_skew_kernel(narrow, out_dtype)
+                             : select_kernel(kind, narrow, out_dtype, geo.K, false);
+    if (small_plan) fn = fpq ? select_fpq_kernel(out_dtype, geo.K, true) : select_kernel(kind, narrow, out_dtype, geo.K, true);
+    if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
+    SignKernelFn occ_fn = fpq ? select_fpq_kernel(out_dtype, geo.K, false) : select_kernel(kind, narrow, out_dtype, geo.K, false);
+    const int occ = blocks_per_sm(keys || skew ? fn : occ_fn, smem, dev);
+    if (small_plan) blocks_per_sm(fn, smem, dev);  // sets its dynamic-smem limit once
     int64_t blocks = (items_ub + (kBlock / 32) - 1) / (kBlock / 32);
     const int64_t cap = (int64_t)occ * dev.sms;
     if (blocks > cap) blocks = cap;
@@ -998,6 +1220,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         // for tens of thousands of empty blocks
         int64_t fb = nnz / (kChunk + 1);
         if (fb > (int64_t)dev.sms * 16) fb = (int64_t)dev.sms * 16;
+        if (small_plan && fb > 32) fb = 32;  // a small batch holds few long sets
         if (fb < 1) fb = 1;
         if (out_dtype == MHB_OUT_I64)
             finalize_kernel<long long><<<(unsigned)fb, 256, 0, st>>>(A);

@@ -78,7 +78,9 @@ struct SignArgs {
     int32_t fpq;        // random family, p <= 2^23: lane tables hold rd(w/p) and the folded offset
 };
 
-Geometry choose_geometry(int kind, int32_t n_hash);
+// K = 0: the default lanes per thread for n_hash (large batches); K in {8,16,32,64}
+// forces it (small batches take a smaller K so the grid fills the SMs: pick_lanes).
+Geometry choose_geometry(int kind, int32_t n_hash, int K = 0);
 
 // 64-bit-residue path for primes 2^31 <= p < 2^63 (wide.cu).
 int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int64_t n_sets, uint64_t a, uint64_t b,
