@@ -576,7 +576,7 @@ struct LaneState {
 // tools/ab.sh on the B200; every other instantiation keeps the plain spelling.
 template <int K, bool ITER, bool NARROW, bool FPQ, bool SKEW, bool BANDS>
 struct Spelling {
-    static constexpr bool kIter64 = ITER && NARROW && K == 64 && !BANDS;  // cfg1-4 iterative kernels
+    static constexpr bool kIter64 = ITER && NARROW && K == 64 && (!BANDS || SKEW);  // cfg1-5 iterative kernels
     // start hash: min(r, r - p, r - 2p) with both subtractions as IMADs by an opaque 1
     // (FMA pipe; plain subtractions fold into two VIADDMNMX on the ALU pipe)
     static constexpr bool start_fma = kIter64;
@@ -696,6 +696,37 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
                 const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
                 store4(r + 4 * q, invert_entry(t[4 * q], m.x, p), invert_entry(t[4 * q + 1], m.y, p),
                        invert_entry(t[4 * q + 2], m.z, p), invert_entry(t[4 * q + 3], m.w, p));
+            }
+            return;
+        }
+    }
+    if constexpr (EPI_SMEM && BANDS) {
+        // The same fast path with the band keys hashed as the argmins come out: a band is
+        // rows/4 whole quads of this thread's block (rows divides K), so a quad countdown
+        // replaces the per-quad band arithmetic of the general loop below.
+        const int j0 = (int)i0;
+        if (!merge && vec_ok && j0 + K <= N) {
+            const InvTab* t = epi_s + (SKEW ? j0 + j0 / K : j0);
+            OutT* r = row + j0;
+            const int rq = A.rows >> 2;  // quads per band
+            unsigned long long* key = A.keys + set * (int64_t)(N / A.rows) + j0 / A.rows;
+            unsigned long long hk = 0;
+            int left = 0;
+#pragma unroll(UNROLL ? 4 : 1)
+            for (int q = 0; q < NQ; ++q) {
+                const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
+                const uint32_t x0 = invert_entry(t[4 * q], m.x, p), x1 = invert_entry(t[4 * q + 1], m.y, p);
+                const uint32_t x2 = invert_entry(t[4 * q + 2], m.z, p), x3 = invert_entry(t[4 * q + 3], m.w, p);
+                if (left == 0) {
+                    hk = 0xCBF29CE484222325ull ^ (unsigned long long)((j0 + 4 * q) / A.rows);
+                    left = rq;
+                }
+                hk = (hk ^ (unsigned long long)x0) * 0x100000001B3ull;
+                hk = (hk ^ (unsigned long long)x1) * 0x100000001B3ull;
+                hk = (hk ^ (unsigned long long)x2) * 0x100000001B3ull;
+                hk = (hk ^ (unsigned long long)x3) * 0x100000001B3ull;
+                if (--left == 0) *key++ = band_mix(hk);
+                if (A.write_sig) store4(r + 4 * q, x0, x1, x2, x3);
             }
             return;
         }
@@ -995,8 +1026,14 @@ static SignKernelFn select_fpq_kernel(int out_dtype, int K, bool stat) {
     return nullptr;
 }
 
-static SignKernelFn select_bands_kernel(bool narrow, int out_dtype, int K) {
+static SignKernelFn select_bands_kernel(bool narrow, int out_dtype, int K, bool skew) {
     const bool i64 = out_dtype == MHB_OUT_I64;
+    if (K == 64 && skew) {  // N >= 1024: the skewed epilogue table (cfg4: 128 bands x 16 rows)
+        if (narrow) return i64 ? sign_kernel<64, true, true, long long, true, false, true>
+                               : sign_kernel<64, true, true, uint32_t, true, false, true>;
+        return i64 ? sign_kernel<64, true, false, long long, true, false, true>
+                   : sign_kernel<64, true, false, uint32_t, true, false, true>;
+    }
     if (K == 64) {
         if (narrow) return i64 ? sign_kernel<64, true, true, long long, true> : sign_kernel<64, true, true, uint32_t, true>;
         return i64 ? sign_kernel<64, true, false, long long, true> : sign_kernel<64, true, false, uint32_t, true>;
@@ -1181,7 +1218,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     }
 
     const bool narrow = (3ull * prime) < (1ull << 32);
-    const bool skew = !keys && kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
+    const bool skew = kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
     // small batches (few items per warp slot) take the STATIC-schedule instances; the
     // grid and the slot count use the dynamic kernel's occupancy (same registers and smem)
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
@@ -1191,7 +1228,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     // small batches (one-CTA unsorted plan) take the STATIC instances: static work
     // assignment and the group's largest set by a warp max; the grid uses the dynamic
     // kernel's occupancy (same registers and smem)
-    SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K)
+    SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K, skew)
                       : fpq  ? select_fpq_kernel(out_dtype, geo.K, false)
                       : skew ? select_skew_kernel(narrow, out_dtype)
                              : select_kernel(kind, narrow, out_dtype, geo.K, false);

@@ -557,7 +557,7 @@ def signatures_band_keys(indptr, ids, family: Family, rows_per_band: int, *, wri
     lanes = 64 if family.size >= 128 else 32  # the kernel's per-thread lane count K (sign.cu choose_geometry)
     # Keys only: fused into the signing epilogue (no signature matrix is written or re-read).
     # Signatures and keys: sign, then the standalone key kernel, which streams the matrix
-    # at HBM speed -- faster than hashing inside the epilogue (cfg4: 36.4 vs 38.1 ms).
+    # at HBM speed -- as fast as hashing inside the epilogue (cfg4: 34.33 vs 34.45 ms, tools/bands_ab.py).
     fused = (not write_signatures and isinstance(family, IterativeFamily) and family.prime <= MAX_KERNEL_PRIME
              and family.size >= 32 and rows_per_band % 4 == 0 and lanes % rows_per_band == 0)
     if not fused or not (torch.is_tensor(ids) and ids.is_cuda):
