@@ -28,6 +28,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <mutex>
 
 #include "common.h"
@@ -76,8 +77,8 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // Lanes per thread for this batch.  The default K amortises each feature's start hash
 // over many lanes, but a small batch then has too few work items (warps) to fill the
 // SMs: cfg1 (10,000 sets, N = 128) gives 625 warps at K = 64 for 148 SMs x 16 warps.
-// Halve K (iterative family; more lane groups per set, so more warps) until the
-// items cover one wave of warp slots.  MHB_SIGN_K forces K (tuning).
+// Iterative family: take the K (64, 32, 16, 8: more lane groups per set, so more warps)
+// with the fewest waves x per-item work.  MHB_SIGN_K forces K (tuning).
 static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fixed) {
     static const int forced = [] {
         const char* e = std::getenv("MHB_SIGN_K");
@@ -87,15 +88,21 @@ static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fi
     if (forced == 8 || forced == 16 || (kind == KIND_ITERATIVE && (forced == 32 || forced == 64)))
         return fixed ? K0 : forced;
     if (fixed || kind != KIND_ITERATIVE) return K0;
+    // cost(K) ~ waves of items x per-item work: a thread's round costs ~2.5 K + 14
+    // instructions (the walk plus the per-feature start hash, steps and loads)
     const int64_t slots = (int64_t)sms * 2 * (kBlock / 32);  // one wave of warp slots (2 CTAs/SM)
-    int K = K0;
-    while (K > 8) {
+    int best = K0;
+    int64_t best_cost = -1;
+    for (int K = K0; K >= 8; K /= 2) {
         const Geometry g = choose_geometry(kind, n_hash, K);
         const int64_t items = (n_sets + g.F - 1) / g.F * g.n_super;
-        if (items >= slots) break;
-        K /= 2;
+        const int64_t cost = (items + slots - 1) / slots * (5 * K + 28);
+        if (best_cost < 0 || cost < best_cost) {
+            best = K;
+            best_cost = cost;
+        }
     }
-    return K;
+    return best;
 }
 
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
@@ -307,14 +314,11 @@ constexpr int kSmallTile = 256;  // sets per tile = threads per CTA
 // hist[] doubles as the look-back state: [0] ticket counter, [2 + 2k] / [3 + 2k] tile
 // k's (chunks, long sets) aggregate + 1 (0 = not yet published).
 template <typename OutT>
-__global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
-    __shared__ unsigned warp_c[kSmallTile / 32], warp_b[kSmallTile / 32];
-    __shared__ unsigned tile_s, excl_c, excl_b, warp_tot2[2], warp_totb2[2];
+__device__ __forceinline__ void plan_small_tile(const SignArgs& A, unsigned tile, unsigned n_tiles, unsigned* warp_c,
+                                                unsigned* warp_b, unsigned& excl_c, unsigned& excl_b,
+                                                unsigned* warp_tot2, unsigned* warp_totb2) {
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     volatile unsigned* flags = A.hist;
-    if (t == 0) tile_s = atomicAdd(&A.hist[0], 1u);
-    __syncthreads();
-    const unsigned tile = tile_s;
     const int64_t s = (int64_t)tile * kSmallTile + t;
     int64_t lo = 0, n = 0;
     if (s < A.n_sets) {
@@ -392,7 +396,6 @@ __global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
         const unsigned pc = warp_tot2[0] + warp_tot2[1], pb = warp_totb2[0] + warp_totb2[1];
         excl_c = pc;
         excl_b = pb;
-        const unsigned n_tiles = (unsigned)((A.n_sets + kSmallTile - 1) / kSmallTile);
         if (tile + 1 == n_tiles) {
             A.sched->next = 0;
             A.sched->n_vsets = pc + own_c;
@@ -417,6 +420,18 @@ __global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
             for (int i = 0; i < A.n_hash; ++i) row[i] = (OutT)(~0u);
         }
     }
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
+    __shared__ unsigned warp_c[kSmallTile / 32], warp_b[kSmallTile / 32];
+    __shared__ unsigned tile_s, excl_c, excl_b, warp_tot2[2], warp_totb2[2];
+    const int t = threadIdx.x;
+    if (t == 0) tile_s = atomicAdd(&A.hist[0], 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const unsigned n_tiles = (unsigned)((A.n_sets + kSmallTile - 1) / kSmallTile);
+    if (tile < n_tiles) plan_small_tile<OutT>(A, tile, n_tiles, warp_c, warp_b, excl_c, excl_b, warp_tot2, warp_totb2);
     for (int64_t i = (int64_t)tile * kSmallTile + t; i < A.n_tot; i += (int64_t)gridDim.x * kSmallTile)
         fill_lane_tables(A, i);
 }
@@ -1188,11 +1203,14 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.fpq = fpq ? 1 : 0;
 
     if (small_plan) {
-        const unsigned tiles = (unsigned)((n_sets + kSmallTile - 1) / kSmallTile);
+        // tiles of sets, plus CTAs enough to spread the lane tables (N may be 10^5)
+        int64_t tiles = (n_sets + kSmallTile - 1) / kSmallTile;
+        const int64_t lane_ctas = std::min<int64_t>((geo.n_tot + kSmallTile - 1) / kSmallTile, (int64_t)dev.sms * 4);
+        if (tiles < lane_ctas) tiles = lane_ctas;
         if (out_dtype == MHB_OUT_I64)
-            plan_small_kernel<long long><<<tiles, kSmallTile, 0, st>>>(A);
+            plan_small_kernel<long long><<<(unsigned)tiles, kSmallTile, 0, st>>>(A);
         else
-            plan_small_kernel<uint32_t><<<tiles, kSmallTile, 0, st>>>(A);
+            plan_small_kernel<uint32_t><<<(unsigned)tiles, kSmallTile, 0, st>>>(A);
         rc = cuda_check(cudaGetLastError(), "plan_small launch");
         if (rc) return rc;
     } else {

@@ -19,7 +19,7 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-STEP = ("plan_count", "plan_scan", "plan_scatter", "sign_kernel", "finalize_kernel")
+STEP = ("plan_count", "plan_scan", "plan_scatter", "plan_small", "sign_kernel", "finalize_kernel", "band_keys")
 METRICS = (
     "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "launch__registers_per_thread",
     "sm__warps_active.avg.per_cycle_active", "smsp__issue_active.avg.per_cycle_active", "smsp__inst_executed.sum",
