@@ -664,10 +664,34 @@ def _timed_graph(args, ctx, step):
     return ctx.max_over_ranks(e0.elapsed_time(e1))
 
 
+def _row_checksums(block):
+    """(sum, position-weighted sum) of a uint32 [rows, N] block as int64 (exact mod 2^64)
+    on its device, in row chunks: a cheap equality check of row ranges without moving them."""
+    import torch
+
+    acc = torch.zeros(2, dtype=torch.int64, device=block.device)
+    if block.numel() == 0:
+        return acc
+    n_rows, n = block.shape
+    w = torch.arange(1, n + 1, dtype=torch.int64, device=block.device)
+    step = max(1, (1 << 26) // n)
+    for r0 in range(0, n_rows, step):
+        v = block[r0:r0 + step].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        rw = torch.arange(r0 + 1, r0 + v.shape[0] + 1, dtype=torch.int64, device=block.device)
+        acc[0] += v.sum()
+        acc[1] += ((v * w).sum(dim=1) * rw).sum()
+    return acc
+
+
+def _agree(ctx, ok: bool) -> bool:
+    """Every rank learns whether all ranks succeeded (one all-reduce, issued by every rank)."""
+    return ctx.sum_over_ranks(0.0 if ok else 1.0) == 0.0
+
+
 def _gather_nccl(args, ctx, W, out):
     """Gather-inclusive leg, baseline: every rank's uint32 block to rank 0 with the
     variable-size, unpadded dist.gather_blocks (NCCL point-to-point into rank 0's matrix
-    rows).  Returns max-over-ranks ms per gather."""
+    rows).  Returns (max-over-ranks ms per gather, the gathered rows' checksums on rank 0)."""
     import torch
 
     from paper_1401_6124_b200.dist import gather_blocks
@@ -677,14 +701,12 @@ def _gather_nccl(args, ctx, W, out):
 
     def once():
         blk = out.cpu() if shared else out  # gloo (shared-GPU test mode) moves host tensors
-        full = gather_blocks(blk, rows, dst=0)
-        return full
+        return gather_blocks(blk, rows, dst=0)
 
     full = once()  # warm-up (NCCL p2p setup) and the check
+    sums = None
     if ctx.rank == 0:
-        mine = full[:rows[0]]
-        if not torch.equal(mine.view(torch.int32).to(out.device), out.view(torch.int32)):
-            raise SystemExit("nccl gather: rank 0's rows differ")
+        sums = [_row_checksums(full[W.cuts[r]:W.cuts[r + 1]].to(out.device)) for r in range(ctx.world)]
     del full
     reps = 3
     torch.cuda.synchronize()
@@ -697,47 +719,85 @@ def _gather_nccl(args, ctx, W, out):
     ms = (time.perf_counter() - t0) * 1e3 / reps
     ctx.barrier()
     torch.cuda.empty_cache()
-    return ctx.max_over_ranks(ms)
+    return ctx.max_over_ranks(ms), sums
+
+
+def _rows_match_rank0(ctx, rank0_sums, out):
+    """Each rank's local checksums against the ones rank 0 computed over its rows of the
+    gathered matrix; every rank runs the same collectives."""
+    import torch
+
+    mine = _row_checksums(out).to(torch.float64).cpu()
+    gathered = torch.zeros((ctx.world, 2), dtype=torch.float64)
+    gathered[ctx.rank] = mine
+    t = gathered.to("cpu" if ctx.shared else ctx.dev)
+    if ctx.world > 1:
+        ctx.dist.all_reduce(t)
+    ok = True
+    if ctx.rank == 0 and rank0_sums is not None:
+        ref = torch.stack([x.to(torch.float64).cpu() for x in rank0_sums])
+        ok = bool(torch.equal(ref, t.cpu()))
+    return _agree(ctx, ok)
 
 
 def _gather_peer(args, ctx, W, fam, out, status, stream):
     """Gather-inclusive leg, fused: every step signs straight into rank 0's [S, N] matrix
-    (CUDA IPC mapping, NVLink stores from the signing epilogue); no separate gather."""
+    (CUDA IPC mapping, NVLink stores from the signing epilogue); no separate gather.
+    Only the owner reads the matrix; the ranks agree on every outcome before the next
+    collective, so an error on one rank cannot leave the others in a mismatched one."""
     import torch
 
     from paper_1401_6124_b200.dist import PeerMatrix
     from paper_1401_6124_b200.minhash import sign_csr_to_ptr
 
     N = out.shape[1]
-    owner = PeerMatrix.allocate(W.n_total, N, 4, ctx.local) if ctx.rank == 0 else None
+    owner, view, err = None, None, None
+    try:
+        if ctx.rank == 0:
+            owner = PeerMatrix.allocate(W.n_total, N, 4, ctx.local)
+    except Exception as e:  # noqa: BLE001
+        err = e
     box = [owner.handle if owner is not None else None]
     if ctx.world > 1:
         ctx.dist.broadcast_object_list(box, src=0)
-    view = owner if ctx.rank == 0 else PeerMatrix.open(box[0], W.n_total, N, 4, ctx.local)
+    if not _agree(ctx, err is None and box[0] is not None):
+        if owner is not None:
+            owner.close()
+        raise RuntimeError(f"peer matrix allocation failed: {err}")
+    ms, sums = None, None
     try:
-        dst_ptr = view.ptr(W.s0)
-        reps = max(3, min(args.steps, 10))
-        for _ in range(2):
-            sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
-        torch.cuda.synchronize()
-        ctx.barrier()
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
-        torch.cuda.synchronize()
-        ctx.barrier()  # every rank's rows have landed in rank 0's matrix
-        ms = ctx.max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
-        mine = view.tensor()[W.s0:W.s1]
-        ok = torch.equal(mine.view(torch.int32), out.view(torch.int32))
-        if ctx.sum_over_ranks(0.0 if ok else 1.0) > 0:
-            raise SystemExit("peer gather: a rank's rows in rank 0's matrix differ from its local signatures")
+        view = owner if ctx.rank == 0 else PeerMatrix.open(box[0], W.n_total, N, 4, ctx.local)
+    except Exception as e:  # noqa: BLE001
+        err = e
+    ok = _agree(ctx, err is None)
+    try:
+        if ok:
+            dst_ptr = view.ptr(W.s0)
+            reps = max(3, min(args.steps, 10))
+            for _ in range(2):
+                sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
+            torch.cuda.synchronize()
+            ctx.barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
+            torch.cuda.synchronize()
+            ctx.barrier()  # every rank's rows have landed in rank 0's matrix
+            ms = ctx.max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
+            if ctx.rank == 0:
+                mat = owner.tensor()
+                sums = [_row_checksums(mat[W.cuts[r]:W.cuts[r + 1]]) for r in range(ctx.world)]
+            if not _rows_match_rank0(ctx, sums, out):
+                raise SystemExit("peer gather: a rank's rows in rank 0's matrix differ from its local signatures")
     finally:
         ctx.barrier()
-        if ctx.rank != 0:
+        if view is not None and ctx.rank != 0:
             view.close()
         ctx.barrier()
         if owner is not None:
             owner.close()
+    if not ok:
+        raise RuntimeError(f"peer matrix mapping failed on a rank: {err}")
     return ms
 
 
@@ -999,22 +1059,30 @@ def main():
     gather = None
     if ctx.world > 1 and args.gather != "none":
         gather = {"bytes_to_rank0_per_step": W.n_total * N * 4}
-        try:
-            if args.gather in ("auto", "nccl"):
-                g_ms = _gather_nccl(args, ctx, W, out)
+        if args.gather in ("auto", "nccl"):
+            try:
+                g_ms, sums = _gather_nccl(args, ctx, W, out)
+                if not _rows_match_rank0(ctx, sums, out):
+                    raise SystemExit("nccl gather: rank 0's gathered rows differ from the ranks' signatures")
                 gather["nccl"] = {"ms": g_ms, "gbs_into_rank0": W.n_total * N * 4 / (g_ms / 1e3) / 1e9,
                                   "compute_plus_gather_entries_per_s": W.n_total * N / ((ms_per_step + g_ms) / 1e3),
                                   "path": "sign on every rank, then dist.gather_blocks: variable-size unpadded "
-                                          "NCCL send/recv straight into rank 0's [S, N] rows"}
-            if args.gather in ("auto", "peer"):
+                                          "NCCL send/recv straight into rank 0's [S, N] rows; checked by row checksums"}
+            except SystemExit:
+                raise
+            except Exception as e:  # noqa: BLE001 -- the compute-phase line still stands
+                gather["nccl_error"] = f"{type(e).__name__}: {e}"
+        if args.gather in ("auto", "peer"):
+            try:
                 p_ms = _gather_peer(args, ctx, W, fam, out, status, stream)
                 gather["peer"] = {"ms_per_step": p_ms, "entries_per_s": W.n_total * N / (p_ms / 1e3),
                                   "path": "fused: mhb_sign_* with out = rank 0's matrix mapped over CUDA IPC "
-                                          "(epilogue stores cross NVLink tile by tile; csrc/peer.cu)"}
-        except SystemExit:
-            raise
-        except Exception as e:  # noqa: BLE001 -- the compute-phase line still stands
-            gather["error"] = f"{type(e).__name__}: {e}"
+                                          "(epilogue stores cross NVLink tile by tile; csrc/peer.cu); checked by "
+                                          "row checksums on the owner"}
+            except SystemExit:
+                raise
+            except Exception as e:  # noqa: BLE001
+                gather["peer_error"] = f"{type(e).__name__}: {e}"
     roofline = _roofline(args, ctx, W, fam, kernel_ms, ms_per_step, clocks, stream)
     e2e = None if args.no_e2e or not W.n_sets else _e2e(args, ctx, W, fam, out)
     e2e_ref = (None if args.no_e2e or args.no_dropin or not W.n_sets

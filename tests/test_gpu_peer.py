@@ -119,7 +119,7 @@ def test_bench_two_ranks_on_one_gpu():
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] == "strong"
     assert line["config"]["n_sets"] == 50000
     g = line["gather"]
-    assert "error" not in g, g
+    assert not any(k.endswith("error") for k in g), g
     assert g["bytes_to_rank0_per_step"] == 50000 * 256 * 4
     assert g["nccl"]["ms"] > 0 and g["peer"]["ms_per_step"] > 0
     assert line["e2e"]["sets_per_step"] > 0 and line["e2e_reference_convention"]["value"] > 0
