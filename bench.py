@@ -1016,7 +1016,7 @@ def main():
     import torch
 
     from paper_1401_6124_b200 import band_keys, make_family
-    from paper_1401_6124_b200.minhash import sign_csr_device
+    from paper_1401_6124_b200.minhash import sign_csr_bands_device, sign_csr_device
 
     ctx = _Ctx()
     W = _Workload(args, ctx)
@@ -1028,23 +1028,55 @@ def main():
     status = torch.zeros(1, dtype=torch.int32, device=ctx.dev)
     stream = torch.cuda.current_stream(ctx.dev)
 
-    def step(st=stream):  # one pass of the hot path over this rank's resident shard
+    def step(st=stream):  # one pass of the hot path (signing) over this rank's resident shard
         if W.n_sets:
             sign_csr_device(W.indptr, W.ids, fam, out, status, st)
-            if keys is not None:  # cfg4: LSH band keys (uint64) emitted from the signatures
-                band_keys(out, W.bands, keys=keys, stream=st)
+
+    def step_keys(st=stream):  # cfg4's full output: signatures + uint64 band keys, fused
+        if W.n_sets:
+            sign_csr_bands_device(W.indptr, W.ids, fam, W.bands, keys, out, status, st)
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     _guard(ctx, W.indptr, W.ids, fam, out, status)
+    bands = None
     if keys is not None and W.n_sets:
+        # cfg4 emits uint64 band keys: the same pass with the keys hashed in the signing
+        # epilogue, timed beside the signature-only step and checked against the oracle
         from oracle import oracle
 
+        for _ in range(2):
+            step_keys()
+        torch.cuda.synchronize()
         k = min(200, W.n_sets)
         want = oracle.band_keys(out[:k].cpu().numpy(), W.bands)
         if not np.array_equal(keys[:k].cpu().numpy().view(np.uint64), want):
             raise SystemExit("bench guard: band keys differ from the oracle")
+        if not torch.equal(keys.view(torch.int64), band_keys(out, W.bands).view(torch.int64)):
+            raise SystemExit("bench guard: fused band keys differ from the standalone key kernel")
+        _guard(ctx, W.indptr, W.ids, fam, out, status)  # the fused pass's signatures too
+        reps = max(3, min(args.steps, 10))
+        ctx.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            step_keys()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        f_ms = ctx.max_over_ranks(e0.elapsed_time(e1) / reps)
+        e0.record(stream)
+        for _ in range(reps):
+            band_keys(out, W.bands, keys=keys, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        k_ms = ctx.max_over_ranks(e0.elapsed_time(e1) / reps)
+        bands = {"rows_per_band": W.bands, "bands": N // W.bands,
+                 "fused_ms_per_step": f_ms, "entries_per_s_with_keys": W.n_total * N / (f_ms / 1e3),
+                 "standalone_keys_ms": k_ms,
+                 "path": "mhb_sign_iterative_csr_bands: signatures and uint64 band keys from one pass (keys hashed "
+                         "in the signing epilogue, csrc/bandhash.cuh); checked vs oracle.band_keys and mhb_band_keys"}
 
     max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream)
     eager_ms = None
@@ -1091,7 +1123,8 @@ def main():
            if args.aux and ctx.rank == 0 else None)
     cpu = _cpu_baseline(args, W, fam) if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None
     per_set = _per_set(ctx) if ctx.rank == 0 and ctx.world == 1 and not args.no_e2e else None
-    launches = (5 + (1 if keys is not None else 0)) * args.steps  # plan x3, sign, finalize (+ band keys)
+    # per step: plan (3 kernels; 1 for shards of <= 16,384 sets), sign, finalize
+    launches = (3 if W.n_sets <= 16384 else 5) * args.steps
 
     if ctx.rank == 0:
         line = {
@@ -1100,7 +1133,8 @@ def main():
             "scaling": "strong" if ctx.world > 1 else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: " + _workload_name(cfg, args.family, W.n_total)
-                                   + (f"; {W.bands}-row band keys (uint64) per step" if W.bands else ""),
+                                   + (f"; its {W.bands}-row uint64 band keys timed beside the step (`bands`)"
+                                      if W.bands else ""),
                        "n_sets": W.n_total, "nnz": W.nnz_total, "n_hash": N, "prime": cfg.prime,
                        "family": args.family, "out": "uint32 argmin ids, resident in HBM",
                        "split": (f"one global batch, nnz-balanced row shards {W.cuts} (dist.nnz_balanced_cuts); "
@@ -1119,6 +1153,8 @@ def main():
             line["graph"] = {"replayed": True, "eager_ms_per_step": eager_ms, "launches_per_replay": launches // args.steps}
         if gather is not None:
             line["gather"] = gather
+        if bands is not None:
+            line["bands"] = bands
         if aux is not None:
             line["aux"] = aux
         print(json.dumps(line), flush=True)

@@ -188,8 +188,10 @@ int mhb_jaccard_block(const void* sig_a, int64_t n_rows, const void* sig_b, int6
 /*
  * LSH band keys (the reference has no banding): the N
  * signature positions form N/rows_per_band bands of consecutive rows, and
- *   keys[s*n_bands + band] = splitmix64(h), h = FNV-1a-64 over the band's argmin ids
- *   (as uint32 words), seeded with 0xCBF29CE484222325 ^ band.
+ *   keys[s*n_bands + band] = splitmix64(h1 << 32 | h2), where over the band's argmin ids x
+ *   (uint32, row order) h1 <- h1*0x9E3779B1 + x and h2 <- h2*0x85EBCA6B + x (mod 2^32),
+ *   seeded h1 = 0x811C9DC5 ^ band, h2 = 0xC2B2AE35 ^ (band*0x27D4EB2F) (csrc/bandhash.cuh:
+ *   two IMADs per id, so the signing epilogue hashes its bands off the ALU pipe).
  * sig: [n_sets, n_hash] of sig_dtype; rows_per_band must divide n_hash.
  */
 int mhb_band_keys(const void* sig, int32_t sig_dtype, int64_t n_sets, int32_t n_hash,

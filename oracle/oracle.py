@@ -123,17 +123,24 @@ def jaccard_estimate(m1: np.ndarray, m2: np.ndarray) -> float:
 
 
 def band_keys(sig: np.ndarray, rows_per_band: int) -> np.ndarray:
-    """LSH band keys as defined in include/mhb.h: splitmix64(FNV-1a-64 over the band's
-    argmin ids as uint32 words, seeded with 0xCBF29CE484222325 ^ band)."""
+    """LSH band keys as defined in include/mhb.h / csrc/bandhash.cuh: over the band's
+    argmin ids (uint32, row order) h1 <- h1*0x9E3779B1 + x and h2 <- h2*0x85EBCA6B + x
+    mod 2^32, seeded 0x811C9DC5 ^ band and 0xC2B2AE35 ^ (band*0x27D4EB2F); the key is
+    splitmix64(h1 << 32 | h2)."""
     sig = np.asarray(sig).astype(np.uint64) & np.uint64(0xFFFFFFFF)
     n_sets, n_hash = sig.shape
     nb = n_hash // rows_per_band
+    m32 = np.uint64(0xFFFFFFFF)
+    band = np.arange(nb, dtype=np.uint64)[None, :].repeat(n_sets, 0)
     with np.errstate(over="ignore"):
-        h = np.uint64(0xCBF29CE484222325) ^ np.arange(nb, dtype=np.uint64)[None, :].repeat(n_sets, 0)
+        h1 = np.uint64(0x811C9DC5) ^ band
+        h2 = np.uint64(0xC2B2AE35) ^ ((band * np.uint64(0x27D4EB2F)) & m32)
         blocks = sig.reshape(n_sets, nb, rows_per_band)
         for j in range(rows_per_band):
-            h = (h ^ blocks[:, :, j]) * np.uint64(0x100000001B3)
-        z = h + np.uint64(0x9E3779B97F4A7C15)
+            h1 = (h1 * np.uint64(0x9E3779B1) + blocks[:, :, j]) & m32
+            h2 = (h2 * np.uint64(0x85EBCA6B) + blocks[:, :, j]) & m32
+        z = (h1 << np.uint64(32)) | h2
+        z = z + np.uint64(0x9E3779B97F4A7C15)
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         return z ^ (z >> np.uint64(31))

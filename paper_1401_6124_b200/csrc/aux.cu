@@ -9,6 +9,7 @@
 
 #include <cstdint>
 
+#include "bandhash.cuh"
 #include "common.h"
 #include "modarith.cuh"
 
@@ -449,16 +450,7 @@ static int launch_hist_wide(const IdT* xs, int64_t n_x, int kind, uint64_t a, ui
 }
 
 // ---------------------------------------------------------------------------
-// LSH band keys: key(s, band) = splitmix64(FNV-1a-64 over the band's argmin ids,
-// seeded with the band index).  One thread per (set, band).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
+// LSH band keys (bandhash.cuh): one thread per (set, band).
 template <typename T>
 __global__ void band_keys_kernel(const T* __restrict__ sig, int64_t n_sets, int32_t n_hash, int32_t rows,
                                  int32_t n_bands, unsigned long long* __restrict__ keys) {
@@ -468,12 +460,9 @@ __global__ void band_keys_kernel(const T* __restrict__ sig, int64_t n_sets, int3
         const int64_t s = t / n_bands;
         const int band = (int)(t - s * n_bands);
         const T* row = sig + s * (int64_t)n_hash + (int64_t)band * rows;
-        unsigned long long h = 0xCBF29CE484222325ull ^ (unsigned long long)band;
-        for (int j = 0; j < rows; ++j) {
-            h ^= (unsigned long long)(uint32_t)__ldg(row + j);
-            h *= 0x100000001B3ull;
-        }
-        keys[t] = splitmix64(h);
+        BandHash h((uint32_t)band);
+        for (int j = 0; j < rows; ++j) h.add((uint32_t)__ldg(row + j));
+        keys[t] = h.key();
     }
 }
 
@@ -489,15 +478,15 @@ __global__ void band_keys_vec4_kernel(const uint32_t* __restrict__ sig, int64_t 
         const int64_t s = t / n_bands;
         const int band = (int)(t - s * n_bands);
         const uint4* row = reinterpret_cast<const uint4*>(sig + s * (int64_t)n_hash + (int64_t)band * rows);
-        unsigned long long h = 0xCBF29CE484222325ull ^ (unsigned long long)band;
+        BandHash h((uint32_t)band);
         for (int j = 0; j < q; ++j) {
             const uint4 v = __ldg(row + j);
-            h = (h ^ v.x) * 0x100000001B3ull;
-            h = (h ^ v.y) * 0x100000001B3ull;
-            h = (h ^ v.z) * 0x100000001B3ull;
-            h = (h ^ v.w) * 0x100000001B3ull;
+            h.add(v.x);
+            h.add(v.y);
+            h.add(v.z);
+            h.add(v.w);
         }
-        keys[t] = splitmix64(h);
+        keys[t] = h.key();
     }
 }
 

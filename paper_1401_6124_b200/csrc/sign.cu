@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "bandhash.cuh"
 #include "common.h"
 #include "modarith.cuh"
 #include "sign_internal.h"
@@ -450,15 +451,6 @@ __device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, ui
 // Long-set chunks merge with a fire-and-forget `red.global.min`.  Written as PTX:
 // the C++ atomicMin in this loop makes ptxas move p out of the uniform datapath
 // (every VIADDMNMX then reads -p from a vector register: -10% visit rate).
-// LSH band keys (include/mhb.h): splitmix64(FNV-1a-64 over the band's argmin ids,
-// seeded with 0xCBF29CE484222325 ^ band).
-__device__ __forceinline__ unsigned long long band_mix(unsigned long long z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
 __device__ __forceinline__ void atomic_min_out(uint32_t* p, uint32_t v) {
     asm volatile("red.global.min.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -589,18 +581,47 @@ struct LaneState {
 // rate by several percent.  Chosen per kernel with
 // tools/variant_search.py (static bank-conflict score of the loop) and confirmed with
 // tools/ab.sh on the B200; every other instantiation keeps the plain spelling.
+#ifndef MHB_BV_START
+#define MHB_BV_START 1
+#endif
+#ifndef MHB_BV_MAXID
+#define MHB_BV_MAXID 1
+#endif
+#ifndef MHB_BV_SWAP
+#define MHB_BV_SWAP 1
+#endif
+#ifndef MHB_BV_ADDR
+#define MHB_BV_ADDR 1
+#endif
+#ifndef MHB_BV_U1
+#define MHB_BV_U1 0
+#endif
+#ifndef MHB_BV_NREG
+#define MHB_BV_NREG 120
+#endif
+#ifndef MHB_SV_ADDR
+#define MHB_SV_ADDR 0
+#endif
+#ifndef MHB_SV_NREG
+#define MHB_SV_NREG 128
+#endif
+#ifndef MHB_SV_START
+#define MHB_SV_START 1
+#endif
 template <int K, bool ITER, bool NARROW, bool FPQ, bool SKEW, bool BANDS>
 struct Spelling {
     static constexpr bool kIter64 = ITER && NARROW && K == 64 && (!BANDS || SKEW);  // cfg1-5 iterative kernels
+    static constexpr bool kBands64 = kIter64 && BANDS;  // cfg4 fused band keys (MHB_BV_*: A/B knobs)
+    static constexpr bool kSkew64 = kIter64 && SKEW && !BANDS;  // cfg4 signatures only (MHB_SV_*)
     // start hash: min(r, r - p, r - 2p) with both subtractions as IMADs by an opaque 1
     // (FMA pipe; plain subtractions fold into two VIADDMNMX on the ALU pipe)
-    static constexpr bool start_fma = kIter64;
+    static constexpr bool start_fma = kBands64 ? MHB_BV_START : kSkew64 ? MHB_SV_START : kIter64;
     // round loop: the id maximum after the round, the features passed as (b, a)
-    static constexpr bool maxid_after = kIter64;
-    static constexpr bool swap_features = kIter64;
+    static constexpr bool maxid_after = kBands64 ? MHB_BV_MAXID : kIter64;
+    static constexpr bool swap_features = kBands64 ? MHB_BV_SWAP : kIter64;
     // id address as one IMAD.WIDE by an opaque 4 instead of IADD3 + LEA + LEA.HI.X
-    static constexpr bool addr_fma = kIter64 && !SKEW;
-    static constexpr int maxnreg = (kIter64 && !SKEW) || FPQ ? 120 : 128;
+    static constexpr bool addr_fma = kBands64 ? MHB_BV_ADDR : kSkew64 ? MHB_SV_ADDR : kIter64 && !SKEW;
+    static constexpr int maxnreg = kBands64 ? MHB_BV_NREG : kSkew64 ? MHB_SV_NREG : (kIter64 && !SKEW) || FPQ ? 120 : 128;
 };
 
 // Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
@@ -725,7 +746,7 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
             OutT* r = row + j0;
             const int rq = A.rows >> 2;  // quads per band
             unsigned long long* key = A.keys + set * (int64_t)(N / A.rows) + j0 / A.rows;
-            unsigned long long hk = 0;
+            BandHash hk(0u);
             int left = 0;
 #pragma unroll(UNROLL ? 4 : 1)
             for (int q = 0; q < NQ; ++q) {
@@ -733,20 +754,20 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
                 const uint32_t x0 = invert_entry(t[4 * q], m.x, p), x1 = invert_entry(t[4 * q + 1], m.y, p);
                 const uint32_t x2 = invert_entry(t[4 * q + 2], m.z, p), x3 = invert_entry(t[4 * q + 3], m.w, p);
                 if (left == 0) {
-                    hk = 0xCBF29CE484222325ull ^ (unsigned long long)((j0 + 4 * q) / A.rows);
+                    hk = BandHash((uint32_t)((j0 + 4 * q) / A.rows));
                     left = rq;
                 }
-                hk = (hk ^ (unsigned long long)x0) * 0x100000001B3ull;
-                hk = (hk ^ (unsigned long long)x1) * 0x100000001B3ull;
-                hk = (hk ^ (unsigned long long)x2) * 0x100000001B3ull;
-                hk = (hk ^ (unsigned long long)x3) * 0x100000001B3ull;
-                if (--left == 0) *key++ = band_mix(hk);
+                hk.add(x0);
+                hk.add(x1);
+                hk.add(x2);
+                hk.add(x3);
+                if (--left == 0) *key++ = hk.key();
                 if (A.write_sig) store4(r + 4 * q, x0, x1, x2, x3);
             }
             return;
         }
     }
-    unsigned long long hk = 0;  // running band hash (BANDS)
+    BandHash hk(0u);  // running band hash (BANDS)
 #pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
         const int64_t i = i0 + 4 * q;
@@ -770,10 +791,10 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
             // bands are runs of A.rows lanes; rows divides K and n_hash, so a band never
             // straddles threads or the row end
             const int64_t band = i / A.rows;
-            if (i - band * A.rows == 0) hk = 0xCBF29CE484222325ull ^ (unsigned long long)band;
+            if (i - band * A.rows == 0) hk = BandHash((uint32_t)band);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) hk = (hk ^ (unsigned long long)x[e]) * 0x100000001B3ull;
-            if (i + 4 - band * A.rows == A.rows) A.keys[set * (int64_t)(N / A.rows) + band] = band_mix(hk);
+            for (int e = 0; e < 4; ++e) hk.add(x[e]);
+            if (i + 4 - band * A.rows == A.rows) A.keys[set * (int64_t)(N / A.rows) + band] = hk.key();
             if (!A.write_sig) continue;
         }
         if (vec_ok && i + 3 < N) {
@@ -953,7 +974,7 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
             const bool merge = (ec.meta >> 11) & 1;
             const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
             dump_best<K>(best, dump_row, lane);
-            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, SKEW || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
+            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, (SKEW && !(BANDS && MHB_BV_U1)) || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
             else emit_lanes<K, OutT, false, BANDS, SKEW, SKEW || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
         }
 
@@ -980,9 +1001,9 @@ __global__ void finalize_kernel(SignArgs A) {
             __syncthreads();
             const int n_bands = A.n_hash / A.rows;
             for (int band = threadIdx.x; band < n_bands; band += blockDim.x) {
-                unsigned long long hk = 0xCBF29CE484222325ull ^ (unsigned long long)band;
-                for (int j = 0; j < A.rows; ++j) hk = (hk ^ (unsigned long long)(uint32_t)row[band * A.rows + j]) * 0x100000001B3ull;
-                A.keys[s * (int64_t)n_bands + band] = band_mix(hk);
+                BandHash hk((uint32_t)band);
+                for (int j = 0; j < A.rows; ++j) hk.add((uint32_t)row[band * A.rows + j]);
+                A.keys[s * (int64_t)n_bands + band] = hk.key();
             }
             __syncthreads();
         }

@@ -135,6 +135,31 @@ def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) 
     sign_csr_to_ptr(indptr, ids, family, out.data_ptr(), out.dtype == torch.int64, status, stream)
 
 
+def sign_csr_bands_device(indptr, ids, family: Family, rows_per_band: int, keys, out, status=None,
+                          stream=None) -> None:
+    """Raw asynchronous device call of the fused signing + band-key kernel
+    (mhb_sign_iterative_csr_bands): out uint32/int64 [S, N] and keys uint64
+    [S, N / rows_per_band] preallocated on the device.  No validation beyond the
+    library's, no sync."""
+    torch = _torch()
+    lib = _lib.load()
+    if not isinstance(family, IterativeFamily):
+        raise TypeError("fused band keys need an iterative family")
+    dev = ids.device
+    n_sets = indptr.numel() - 1
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, ids.numel(), family.size)
+        with torch.cuda.stream(st):
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        rc = lib.mhb_sign_iterative_csr_bands(
+            indptr.data_ptr(), ids.data_ptr(), n_sets, ids.numel(), family.base.a, family.base.b, family.prime,
+            family.size, rows_per_band, keys.data_ptr(), out.data_ptr(),
+            _lib.OUT_I64 if out.dtype == torch.int64 else _lib.OUT_U32, 1,
+            status.data_ptr() if status is not None else None, ws.data_ptr(), ws_bytes, st.cuda_stream)
+    _lib.check(rc)
+
+
 def sign_csr_to_ptr(indptr, ids, family: Family, out_ptr: int, out_int64: bool = False, status=None,
                     stream=None) -> None:
     """sign_csr_device with the output given as a device address: rows [S, family.size]
@@ -517,7 +542,8 @@ def band_keys(sig, rows_per_band: int, *, keys=None, stream=None):
     """LSH band keys: uint64 [S, N/rows] from a device signature matrix [S, N].
 
     Bands are runs of `rows_per_band` consecutive hash positions; each key is
-    splitmix64 of FNV-1a-64 over the band's argmin ids (include/mhb.h).  Equal keys
+    splitmix64 of two polynomial hashes mod 2^32 over the band's argmin ids
+    (include/mhb.h, csrc/bandhash.cuh).  Equal keys
     mean the two sets agree on every row of the band (the LSH candidate test).
     ``keys``: an optional preallocated uint64 [S, N/rows] output; ``stream``: the
     launch stream (default: the current one)."""
@@ -544,10 +570,10 @@ def signatures_band_keys(indptr, ids, family: Family, rows_per_band: int, *, wri
                          out_dtype: str = "uint32", validate: bool = True):
     """Signatures and their LSH band keys (device tensors).
 
-    ``write_signatures=False`` returns (None, keys) with the keys hashed inside the
-    signing epilogue (mhb_sign_iterative_csr_bands, iterative family on the u32
-    kernels): the signature matrix is never stored.  Otherwise the batch is signed and
-    the standalone band-key kernel streams the matrix.  The keys always equal
+    The keys are hashed inside the signing epilogue (mhb_sign_iterative_csr_bands,
+    iterative family on the u32 kernels) when ``write_signatures=False`` (the matrix is
+    never stored) or N >= 1024; otherwise the batch is signed and the standalone
+    band-key kernel streams the matrix.  The keys always equal
     ``band_keys(signatures_csr(...), rows)``.
     """
     _check_family(family)
@@ -556,10 +582,13 @@ def signatures_band_keys(indptr, ids, family: Family, rows_per_band: int, *, wri
         raise ValueError(f"rows_per_band {rows_per_band} must divide the signature length {family.size}")
     lanes = 64 if family.size >= 128 else 32  # the kernel's per-thread lane count K (sign.cu choose_geometry)
     # Keys only: fused into the signing epilogue (no signature matrix is written or re-read).
-    # Signatures and keys: sign, then the standalone key kernel, which streams the matrix
-    # at HBM speed -- as fast as hashing inside the epilogue (cfg4: 34.33 vs 34.45 ms, tools/bands_ab.py).
-    fused = (not write_signatures and isinstance(family, IterativeFamily) and family.prime <= MAX_KERNEL_PRIME
-             and family.size >= 32 and rows_per_band % 4 == 0 and lanes % rows_per_band == 0)
+    # Signatures and keys: fused too for N >= 1024 (the skewed K = 64 kernels: cfg4 31.80 ms
+    # against 34.33 ms for sign + the standalone key kernel, tools/bands_ab.py); below
+    # that, sign, then the standalone key kernel, which streams the matrix at HBM speed
+    # (cfg3 N = 512: 5.92 vs 6.49 ms fused).
+    fusable = (isinstance(family, IterativeFamily) and family.prime <= MAX_KERNEL_PRIME and family.size >= 32
+               and rows_per_band % 4 == 0 and lanes % rows_per_band == 0)
+    fused = fusable and (not write_signatures or family.size >= 1024)
     if not fused or not (torch.is_tensor(ids) and ids.is_cuda):
         sig = signatures_csr(indptr, ids, family, out_dtype=out_dtype, validate=validate)
         if not torch.is_tensor(sig):

@@ -145,3 +145,26 @@ def test_wide_ids_restatement(golden):
         assert ids.max() > 2**32
         for s in range(ip.size - 1):
             assert np.array_equal(oracle.brute_force_row(ids[ip[s]:ip[s + 1]], fam), z[f"out{k}"][s]), m
+
+
+def test_band_key_definition_scalar():
+    """oracle.band_keys (vectorised) against a scalar restatement of the band-key
+    definition in include/mhb.h / csrc/bandhash.cuh (the reference defines no banding)."""
+    M, M64 = 2**32, 2**64
+
+    def key(row, band):
+        h1, h2 = 0x811C9DC5 ^ band, 0xC2B2AE35 ^ ((band * 0x27D4EB2F) % M)
+        for x in row:
+            h1, h2 = (h1 * 0x9E3779B1 + int(x)) % M, (h2 * 0x85EBCA6B + int(x)) % M
+        z = ((h1 << 32) | h2) + 0x9E3779B97F4A7C15
+        z %= M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) % M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) % M64
+        return z ^ (z >> 31)
+
+    rng = np.random.default_rng(3)
+    for rows in (4, 16):
+        sig = rng.integers(0, 2**32, size=(7, 4 * rows), dtype=np.uint64)
+        got = oracle.band_keys(sig, rows)
+        want = [[key(sig[s, b * rows:(b + 1) * rows], b) for b in range(4)] for s in range(7)]
+        assert [[int(v) for v in r] for r in got] == want
