@@ -608,20 +608,45 @@ struct LaneState {
 #ifndef MHB_SV_START
 #define MHB_SV_START 1
 #endif
+#ifndef MHB_RV_NREG
+#define MHB_RV_NREG 112
+#endif
+#ifndef MHB_RV_ADDR
+#define MHB_RV_ADDR 1
+#endif
+#ifndef MHB_IV_NREG
+#define MHB_IV_NREG 120
+#endif
+#ifndef MHB_IV_ADDR
+#define MHB_IV_ADDR 1
+#endif
+#ifndef MHB_IV_START
+#define MHB_IV_START 1
+#endif
+#ifndef MHB_SV_MAXID
+#define MHB_SV_MAXID 1
+#endif
+#ifndef MHB_SV_SWAP
+#define MHB_SV_SWAP 1
+#endif
 template <int K, bool ITER, bool NARROW, bool FPQ, bool SKEW, bool BANDS>
 struct Spelling {
     static constexpr bool kIter64 = ITER && NARROW && K == 64 && (!BANDS || SKEW);  // cfg1-5 iterative kernels
     static constexpr bool kBands64 = kIter64 && BANDS;  // cfg4 fused band keys (MHB_BV_*: A/B knobs)
     static constexpr bool kSkew64 = kIter64 && SKEW && !BANDS;  // cfg4 signatures only (MHB_SV_*)
+    static constexpr bool kFpq = FPQ && !BANDS;                 // cfg1/cfg3 random family (MHB_RV_*)
+    static constexpr bool kPlain64 = kIter64 && !SKEW && !BANDS;  // cfg1/2/3/5 iterative (MHB_IV_*)
     // start hash: min(r, r - p, r - 2p) with both subtractions as IMADs by an opaque 1
     // (FMA pipe; plain subtractions fold into two VIADDMNMX on the ALU pipe)
-    static constexpr bool start_fma = kBands64 ? MHB_BV_START : kSkew64 ? MHB_SV_START : kIter64;
+    static constexpr bool start_fma = kBands64 ? MHB_BV_START : kSkew64 ? MHB_SV_START : kPlain64 ? MHB_IV_START : kIter64;
     // round loop: the id maximum after the round, the features passed as (b, a)
-    static constexpr bool maxid_after = kBands64 ? MHB_BV_MAXID : kIter64;
-    static constexpr bool swap_features = kBands64 ? MHB_BV_SWAP : kIter64;
+    static constexpr bool maxid_after = kBands64 ? MHB_BV_MAXID : kSkew64 ? MHB_SV_MAXID : kIter64;
+    static constexpr bool swap_features = kBands64 ? MHB_BV_SWAP : kSkew64 ? MHB_SV_SWAP : kIter64;
     // id address as one IMAD.WIDE by an opaque 4 instead of IADD3 + LEA + LEA.HI.X
-    static constexpr bool addr_fma = kBands64 ? MHB_BV_ADDR : kSkew64 ? MHB_SV_ADDR : kIter64 && !SKEW;
-    static constexpr int maxnreg = kBands64 ? MHB_BV_NREG : kSkew64 ? MHB_SV_NREG : (kIter64 && !SKEW) || FPQ ? 120 : 128;
+    static constexpr bool addr_fma = kBands64 ? MHB_BV_ADDR : kSkew64 ? MHB_SV_ADDR : kFpq ? MHB_RV_ADDR
+                                    : kPlain64 ? MHB_IV_ADDR : false;
+    static constexpr int maxnreg = kBands64 ? MHB_BV_NREG : kSkew64 ? MHB_SV_NREG : kFpq ? MHB_RV_NREG
+                                   : kPlain64 ? MHB_IV_NREG : 128;
 };
 
 // Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
