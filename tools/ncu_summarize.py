@@ -19,7 +19,17 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-STEP = ("plan_count", "plan_scan", "plan_scatter", "plan_small", "sign_kernel", "finalize_kernel", "band_keys")
+STEP = ("plan_count", "plan_scan", "plan_scatter", "plan_small", "sign_kernel", "finalize_kernel")
+
+
+def _is_step(name):
+    """The timed step's kernels: the plan, the signature kernel (not a BANDS instance:
+    bench.py times the fused band-key pass beside the step) and finalize."""
+    import re as _re
+    if not any(s in name for s in STEP):
+        return False
+    m = _re.search(r"sign_kernel<(\d+), (\d), (\d), [^,]+, (\d)", name)
+    return not (m and m.group(4) == "1")
 METRICS = (
     "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "launch__registers_per_thread",
     "sm__warps_active.avg.per_cycle_active", "smsp__issue_active.avg.per_cycle_active", "smsp__inst_executed.sum",
@@ -37,8 +47,7 @@ def read_launch_csv(path):
         if r["Metric Name"] != "gpu__time_duration.sum":
             continue
         name = r["Kernel Name"]
-        short = next((s for s in STEP if s in name), None)
-        if short is None:
+        if not _is_step(name):
             continue
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
