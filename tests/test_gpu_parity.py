@@ -672,3 +672,67 @@ def test_extreme_sets(cuda_device, kind):
                          torch.as_tensor(ids.astype(np.int64), device=cuda_device).to(torch.uint32), fam)
     assert np.array_equal(got.cpu().numpy(), want)
     assert np.array_equal(signatures_csr(ip, ids, fam), want)  # host pipeline, chunked
+
+
+def test_signatures_list_api_ids_beyond_2_32(golden, cuda_device):
+    """signatures() once narrowed int64 ids to uint32 without a check, so ids
+    >= 2^32 (primes >= 2^32) were signed as different ids.  Now they reach the 64-bit-id
+    path and equal the reference's outputs."""
+    z = np.load(golden / "wide_ids.npz")
+    for k, m in enumerate(json.loads((golden / "wide_ids.json").read_text())):
+        fam = make_family(m["kind"], m["seed"], m["n"], m["p"])
+        ip, ids, want = z[f"indptr{k}"], z[f"ids{k}"], z[f"out{k}"]
+        if int(ids.max()) <= 2**32 - 1:
+            continue
+        sets = [FeatureSet(ids[ip[s]:ip[s + 1]]) for s in range(ip.size - 1)]
+        got = signatures(sets, fam)
+        assert all(np.array_equal(g.mins, want[s]) for s, g in enumerate(got)), m
+
+
+def test_indptr_validation(cuda_device):
+    """ids are read at the absolute offsets indptr[s]; indptr must start at
+    >= 0, end at <= nnz and never decrease -- host and device batches both reject the rest
+    before any launch."""
+    import torch
+
+    fam = make_family("iterative", 2, 64, 1_048_583)
+    ids = np.arange(10, dtype=np.uint32)
+    bad = [np.array([1, 5, 12], dtype=np.int64),   # ends past nnz (reads past the end from a nonzero start)
+           np.array([-1, 5, 10], dtype=np.int64),  # negative start
+           np.array([0, 6, 4, 10], dtype=np.int64)]  # decreasing
+    for ip in bad:
+        with pytest.raises(ValueError):
+            signatures_csr(ip, ids, fam)
+        with pytest.raises(ValueError):
+            signatures_csr(torch.as_tensor(ip, device=cuda_device), torch.as_tensor(ids.astype(np.int64),
+                           device=cuda_device).to(torch.uint32), fam)
+    # a nonzero start that stays inside ids is fine (the ABI addresses ids[indptr[s]..])
+    ip = np.array([2, 5, 10], dtype=np.int64)
+    want = oracle.sign_family_csr(np.array([0, 3, 8]), ids[2:], fam)
+    assert np.array_equal(signatures_csr(ip, ids, fam), want)
+
+
+def test_sign_csr_device_on_a_side_stream(cuda_device):
+    """the workspace belongs to the launch stream, so signing on a side stream
+    while the current stream allocates and frees is safe (bit-exact, many rounds)."""
+    import torch
+
+    from paper_1401_6124_b200.minhash import sign_csr_device
+
+    indptr, ids = gen.cfg1_numpy(n_sets=2000, seed=31)
+    fam = make_family("iterative", 4, 128, 1_048_583)
+    want = oracle.sign_family_csr(indptr, ids, fam)
+    ip, di = _dev(indptr, ids, cuda_device)
+    side = torch.cuda.Stream(cuda_device)
+    outs = []
+    for _ in range(20):
+        out = torch.empty((indptr.size - 1, 128), dtype=torch.uint32, device=cuda_device)
+        side.wait_stream(torch.cuda.current_stream())
+        sign_csr_device(ip, di, fam, out, stream=side)
+        junk = torch.randint(0, 1 << 30, (1 << 20,), device=cuda_device)  # current-stream churn
+        del junk
+        out.record_stream(side)
+        outs.append(out)
+    torch.cuda.synchronize()
+    for out in outs:
+        assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
