@@ -6,7 +6,8 @@ Each case draws a family (random / iterative), N, a prime (tiny .. 2^31, and wid
 ones up to 2^32), set sizes (1 .. a few chunks, repeated ids), and an entry path:
 device CSR, host pipeline (pinned / pageable, uint32 / int64, pinned int64), small-batch
 host path (doorbell block / launched grid, wide N up to 100,000), the per-set
-signature() API, fused band keys (keys only), 64-bit ids.  Any mismatch is printed with its seed and the
+signature() API, fused band keys (keys only, and with signatures), 64-bit ids; batch
+sizes on both sides of the one-launch small plan (16,384 sets).  Any mismatch is printed with its seed and the
 run exits non-zero.
 """
 import sys
@@ -34,7 +35,13 @@ def case(rng, dev):
     if kind == "random" and p > 2**31 - 1:
         p = 2_147_483_647 if rng.random() < 0.5 else 1_073_741_827
     fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
-    n_sets = int(rng.choice([1, 2, 7, 64, 65, 300, 2000]))
+    n_sets = int(rng.choice([1, 2, 7, 64, 65, 300, 2000, 16384, 16385, 20000],
+                            p=[.12, .12, .12, .12, .12, .12, .12, .05, .05, .06]))
+    if n_sets > 2000 and n_hash > 512:  # keep the oracle's share of a case in seconds
+        n_hash = int(rng.choice([16, 64, 128, 256]))
+        if kind == "iterative" and 2 * n_hash + 3 >= p:
+            n_hash = max(1, (p - 4) // 2)
+        fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
     if rng.random() < 0.15:  # wide small batches: the launched (hash slice, set) grid, device staging
         n_sets = int(rng.choice([1, 3, 20]))
         n_hash = int(rng.choice([4000, 8192, 20_000, 100_000]))
@@ -42,7 +49,8 @@ def case(rng, dev):
             p = 1_073_741_827
         fam = make_family(kind, int(rng.integers(1 << 30)), n_hash, p)
     sizes = rng.choice([1, 2, 3, 50, 200, 1023, 1024, 1025, 3000], size=n_sets,
-                       p=[.1, .1, .1, .3, .2, .05, .05, .05, .05])
+                       p=[.1, .1, .1, .3, .2, .05, .05, .05, .05] if n_sets <= 2000
+                       else [.2, .2, .2, .3, .09, .004, .003, .002, .001])
     rows = []
     hi = min(p, 1 << 32)
     for n in sizes:
@@ -53,8 +61,8 @@ def case(rng, dev):
     ip = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int64)
     ids = np.concatenate(rows)
     want = oracle.sign_family_csr(ip, ids, fam)
-    path = rng.choice(["device", "host_pinned", "host_pageable", "host_int64", "bands", "ids64", "per_set",
-                       "host_pinned_int64"])
+    path = rng.choice(["device", "host_pinned", "host_pageable", "host_int64", "bands", "bands_sig", "ids64",
+                       "per_set", "host_pinned_int64"])
     if path == "device":
         got = signatures_csr(torch.as_tensor(ip, device=dev), torch.as_tensor(ids.astype(np.int64), device=dev),
                              fam, out_dtype=str(rng.choice(["uint32", "int64"]))).cpu().numpy().astype(np.int64)
@@ -81,6 +89,15 @@ def case(rng, dev):
                                        torch.as_tensor(ids.astype(np.int64), device=dev), fam, rows_b,
                                        write_signatures=False)
         ok = np.array_equal(keys.cpu().numpy().view(np.uint64), oracle.band_keys(want, rows_b))
+        return kind, p, n_hash, n_sets, path, ok
+    elif path == "bands_sig":  # signatures and keys together (fused for N >= 1024)
+        rows_b = next((r for r in (16, 8, 4) if n_hash % r == 0), None)
+        if rows_b is None:
+            return kind, p, n_hash, n_sets, path, True
+        sig, keys = signatures_band_keys(torch.as_tensor(ip, device=dev),
+                                         torch.as_tensor(ids.astype(np.int64), device=dev), fam, rows_b)
+        ok = (np.array_equal(keys.cpu().numpy().view(np.uint64), oracle.band_keys(want, rows_b))
+              and np.array_equal(sig.cpu().numpy().astype(np.int64), want))
         return kind, p, n_hash, n_sets, path, ok
     else:  # 64-bit ids only apply when the prime admits ids >= 2^32; use brute force on a few rows
         if p < 2**32 or kind == "random":
