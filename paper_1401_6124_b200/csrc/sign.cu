@@ -870,7 +870,9 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     const unsigned long long W = (unsigned long long)gridDim.x * (kBlock / 32);
     unsigned long long it = 0, itn = 0, itnn = 0;
     if constexpr (STATIC) {
-        it = (unsigned long long)blockIdx.x * (kBlock / 32) + warp;
+        // warp w of CTA c takes items w * gridDim + c (+ k W): the first items spread over
+        // all CTAs (hence all SMs) before any CTA gets a second one
+        it = (unsigned long long)warp * gridDim.x + blockIdx.x;
         itn = it + W;
     } else {
         if (lane == 0) {
@@ -1303,6 +1305,9 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (small_plan) blocks_per_sm(fn, smem, dev);  // sets its dynamic-smem limit once
     int64_t blocks = (items_ub + (kBlock / 32) - 1) / (kBlock / 32);
     const int64_t cap = (int64_t)occ * dev.sms;
+    // static assignment: a whole number of CTAs per SM, so no SM holds twice the work
+    // of the others (cfg1: 157 CTAs put two on 9 SMs, which ran 1.8x longer)
+    if (small_plan && blocks > dev.sms / 2) blocks = (blocks + dev.sms - 1) / dev.sms * dev.sms;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     int prof_slot = -1;
