@@ -168,3 +168,55 @@ def test_split_gather_equals_single_process(cuda_device, world, cfg_name, n_sets
     status, equal, cuts = q.get(timeout=60)
     assert status == "ok", equal
     assert equal, f"gathered shards differ from the single-process batch (cuts {cuts})"
+
+
+def _nccl_worker(rank, world, port, q):
+    """The NCCL backend itself (one rank: the box has one GPU): process-group init with a
+    device id, the device-side cuts, sign_sharded's collective error agreement and the
+    unpadded gather, and sign_gather_peer -- the same calls the multi-GPU bench makes."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1401_6124_b200 import gen, make_family, signatures_csr
+    from paper_1401_6124_b200.dist import nnz_balanced_cuts, sign_gather_peer, sign_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        cfg = gen.CONFIGS["cfg2"]
+        ip_g = gen.global_indptr(cfg, dev, 20_000)
+        ip, ids, _ = gen.make_shard(cfg, 0, 20_000, dev, 20_000, indptr=ip_g)
+        assert nnz_balanced_cuts(ip, 1) == [0, 20_000]
+        fam = make_family("iterative", cfg.family_seed("iterative"), cfg.n_hash, cfg.prime)
+        want = signatures_csr(ip, ids, fam, out_dtype="uint32")
+        block, (s0, s1), full = sign_sharded(ip, ids, fam)
+        ok = bool(torch.equal(full.view(torch.int32), want.view(torch.int32))) and (s0, s1) == (0, 20_000)
+        mat, _ = sign_gather_peer(ip, ids, fam)
+        ok = ok and bool(torch.equal(mat.tensor().view(torch.int32), want.view(torch.int32)))
+        mat.close()
+        bad_ids = ids.clone()
+        bad_ids[5] = cfg.prime  # an id >= p: the reference's ValueError, agreed over the group
+        try:
+            sign_sharded(ip, bad_ids, fam)
+            ok = False
+        except ValueError:
+            pass
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)
+        dist.barrier()
+        q.put(("ok", ok and float(t.item()) == 1.0))
+    except Exception as exc:
+        q.put(("error", repr(exc)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_backend_one_rank(cuda_device):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_nccl_worker, args=(1, _free_port(), q), nprocs=1, join=True, start_method="spawn")
+    status, ok = q.get(timeout=60)
+    assert status == "ok" and ok, ok
