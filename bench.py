@@ -581,7 +581,8 @@ class _Workload:
         self.gen_s = time.perf_counter() - t0
         self.n_sets = self.s1 - self.s0
         self.nnz = int(self.ids.numel())
-        self.bands = 16 if cfg.name == "cfg4" else 0  # cfg4: 128 bands x 16 rows, u64 keys
+        # cfg4: 128 bands x 16 rows, u64 keys (the fused pass is the iterative family's)
+        self.bands = 16 if cfg.name == "cfg4" and args.family == "iterative" else 0
 
 
 def _guard(ctx, indptr, ids, fam, out, status):
