@@ -614,6 +614,12 @@ struct LaneState {
 #ifndef MHB_RV_ADDR
 #define MHB_RV_ADDR 1
 #endif
+#ifndef MHB_HV_NREG
+#define MHB_HV_NREG 128
+#endif
+#ifndef MHB_HV_ADDR
+#define MHB_HV_ADDR 0
+#endif
 #ifndef MHB_IV_NREG
 #define MHB_IV_NREG 120
 #endif
@@ -636,6 +642,7 @@ struct Spelling {
     static constexpr bool kSkew64 = kIter64 && SKEW && !BANDS;  // cfg4 signatures only (MHB_SV_*)
     static constexpr bool kFpq = FPQ && !BANDS;                 // cfg1/cfg3 random family (MHB_RV_*)
     static constexpr bool kPlain64 = kIter64 && !SKEW && !BANDS;  // cfg1/2/3/5 iterative (MHB_IV_*)
+    static constexpr bool kShoup = !ITER && !FPQ && !BANDS;        // random family, p > 2^23 (MHB_HV_*)
     // start hash: min(r, r - p, r - 2p) with both subtractions as IMADs by an opaque 1
     // (FMA pipe; plain subtractions fold into two VIADDMNMX on the ALU pipe)
     static constexpr bool start_fma = kBands64 ? MHB_BV_START : kSkew64 ? MHB_SV_START : kPlain64 ? MHB_IV_START : kIter64;
@@ -644,9 +651,9 @@ struct Spelling {
     static constexpr bool swap_features = kBands64 ? MHB_BV_SWAP : kSkew64 ? MHB_SV_SWAP : kIter64;
     // id address as one IMAD.WIDE by an opaque 4 instead of IADD3 + LEA + LEA.HI.X
     static constexpr bool addr_fma = kBands64 ? MHB_BV_ADDR : kSkew64 ? MHB_SV_ADDR : kFpq ? MHB_RV_ADDR
-                                    : kPlain64 ? MHB_IV_ADDR : false;
+                                    : kPlain64 ? MHB_IV_ADDR : kShoup ? MHB_HV_ADDR : false;
     static constexpr int maxnreg = kBands64 ? MHB_BV_NREG : kSkew64 ? MHB_SV_NREG : kFpq ? MHB_RV_NREG
-                                   : kPlain64 ? MHB_IV_NREG : 128;
+                                   : kPlain64 ? MHB_IV_NREG : kShoup ? MHB_HV_NREG : 128;
 };
 
 // Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
