@@ -839,6 +839,30 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
     }
 }
 
+// Long sets: rows hold min hash values after the main kernel; invert in place
+// (one block per row, threads over hash lanes).
+template <typename OutT>
+__device__ __forceinline__ void finalize_rows(const SignArgs& A, unsigned long long e0, unsigned long long stride) {
+    const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
+    OutT* out = reinterpret_cast<OutT*>(A.out);
+    for (unsigned long long e = e0; e < n_big; e += stride) {
+        const int64_t s = A.big[e];
+        OutT* row = out + s * (int64_t)A.n_hash;
+        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x)
+            row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
+        if (A.keys) {  // band keys of long sets (their chunks merged in `out`)
+            __syncthreads();
+            const int n_bands = A.n_hash / A.rows;
+            for (int band = threadIdx.x; band < n_bands; band += blockDim.x) {
+                BandHash hk((uint32_t)band);
+                for (int j = 0; j < A.rows; ++j) hk.add((uint32_t)row[band * A.rows + j]);
+                A.keys[s * (int64_t)n_bands + band] = hk.key();
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
@@ -1018,30 +1042,32 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
         en = load_vset(A, itn, n_vsets, f);
     }
     if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
-}
-
-// Long sets: rows hold min hash values after the main kernel; invert in place
-// (one block per row, threads over hash lanes).
-template <typename OutT>
-__global__ void finalize_kernel(SignArgs A) {
-    const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
-    OutT* out = reinterpret_cast<OutT*>(A.out);
-    for (unsigned long long e = blockIdx.x; e < n_big; e += gridDim.x) {
-        const int64_t s = A.big[e];
-        OutT* row = out + s * (int64_t)A.n_hash;
-        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x)
-            row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
-        if (A.keys) {  // band keys of long sets (their chunks merged in `out`)
-            __syncthreads();
-            const int n_bands = A.n_hash / A.rows;
-            for (int band = threadIdx.x; band < n_bands; band += blockDim.x) {
-                BandHash hk((uint32_t)band);
-                for (int j = 0; j < A.rows; ++j) hk.add((uint32_t)row[band * A.rows + j]);
-                A.keys[s * (int64_t)n_bands + band] = hk.key();
-            }
-            __syncthreads();
+    if constexpr (STATIC) {
+        // small batches: the last CTA to finish inverts the merged long-set rows (no
+        // finalize launch); the fence orders every CTA's red.global.min merges before
+        // its count, and the last one's reads after all of them
+        __shared__ int last_cta;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last_cta = atomicAdd(&A.sched->done, 1ull) == (unsigned long long)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last_cta) {
+            __threadfence();
+            finalize_rows<OutT>(A, 0, 1);
+            // the status word accumulated in the workspace (zeroed with the plan state) goes
+            // to the caller's word, which the host passes in this kernel's copy of `hist`
+            // (unused by the sign kernel; SignArgs keeps its layout: the large-batch
+            // kernels' codegen moves with any change of it)
+            if (threadIdx.x == 0 && A.hist) *reinterpret_cast<int32_t*>(A.hist) = *((volatile int32_t*)&A.sched->status);
         }
     }
+}
+
+template <typename OutT>
+__global__ void finalize_kernel(SignArgs A) {
+    finalize_rows<OutT>(A, blockIdx.x, gridDim.x);
 }
 
 // ----------------------------------------------------------------------------
@@ -1148,8 +1174,15 @@ static int blocks_per_sm(SignKernelFn fn, size_t smem, const DeviceInfo& dev) {
             if (cache[i].smem == smem) return cache[i].occ;
         }
     }
-    if (!seen)
-        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dev.smem_optin);
+    if (!seen) {
+        // the dynamic limit is what the opt-in maximum leaves after the kernel's static smem
+        cudaFuncAttributes fa{};
+        size_t stat = 0;
+        if (cudaFuncGetAttributes(&fa, (const void*)fn) == cudaSuccess) stat = fa.sharedSizeBytes;
+        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(dev.smem_optin > stat ? dev.smem_optin - stat : 0));
+        cudaGetLastError();
+    }
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kBlock, smem) != cudaSuccess)
         occ = 1;
@@ -1241,12 +1274,18 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.write_sig = write_sig;
 
     // keys (fused band epilogue) have no STATIC instances: they keep the sorted plan
-    const bool small_plan = n_sets <= kSmallPlan && keys == nullptr;
+    const bool small_plan = n_sets > 0 && n_sets <= kSmallPlan && keys == nullptr;
     // sched and hist are contiguous at the start of the workspace (zeroed: the sorted
     // plan's histogram, or the small plan's look-back state)
     rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
     if (rc) return rc;
-    if (status) {
+    int32_t* status_out = nullptr;
+    if (small_plan && status) {
+        // no status memset: plan and sign OR into the (zeroed) workspace word, and the
+        // STATIC kernel's last CTA stores it into *status
+        A.status = &A.sched->status;
+        status_out = status;
+    } else if (status) {
         rc = cuda_check(cudaMemsetAsync(status, 0, sizeof(int32_t), st), "memset status");
         if (rc) return rc;
     }
@@ -1323,17 +1362,18 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
     }
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p, 1u);
+    SignArgs As = A;  // the sign kernel's copy (see finalize in sign_kernel<STATIC>)
+    if (small_plan) As.hist = reinterpret_cast<unsigned*>(status_out);
+    fn<<<(unsigned)blocks, kBlock, smem, st>>>(As, A.p, A.b, 0u - A.p, 1u);
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
     rc = cuda_check(cudaGetLastError(), "sign_kernel launch");
     if (rc) return rc;
 
-    {
+    if (!small_plan) {  // small batches: the STATIC kernel's last CTA finalizes
         // blocks loop over long-set rows; 16 per SM hide the row loads without paying
         // for tens of thousands of empty blocks
         int64_t fb = nnz / (kChunk + 1);
         if (fb > (int64_t)dev.sms * 16) fb = (int64_t)dev.sms * 16;
-        if (small_plan && fb > 32) fb = 32;  // a small batch holds few long sets
         if (fb < 1) fb = 1;
         if (out_dtype == MHB_OUT_I64)
             finalize_kernel<long long><<<(unsigned)fb, 256, 0, st>>>(A);

@@ -33,7 +33,9 @@ struct Sched {
     unsigned long long next;     // dynamic counter over work items (group, lane pass)
     unsigned long long n_vsets;  // virtual sets planned
     unsigned long long n_big;    // sets in merge mode (finalize list)
-    unsigned long long pad;
+    unsigned long long done;     // CTAs finished (STATIC kernels: the last one finalizes)
+    int32_t status;              // small batches: the call's status word, copied out by the last CTA
+    int32_t pad2;
 };
 
 struct Geometry {
@@ -64,7 +66,8 @@ struct SignArgs {
     LaneTab* tab;
     InvTab* inv;
     Sched* sched;
-    unsigned* hist;   // [2*kChunk]: virtual-set size histogram, then scatter cursors
+    unsigned* hist;   // [2*kChunk]: virtual-set size histogram, then scatter cursors (plan kernels);
+                      // in a STATIC sign kernel's copy: the caller's status word, or null
     int64_t* big;
     VSet* vsets;
     int32_t* status;

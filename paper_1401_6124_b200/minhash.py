@@ -135,6 +135,30 @@ def sign_csr_device(indptr, ids, family: Family, out, status=None, stream=None) 
     sign_csr_to_ptr(indptr, ids, family, out.data_ptr(), out.dtype == torch.int64, status, stream)
 
 
+class _Workspaces(threading.local):
+    """Per-thread signing workspaces, one per (device, stream), grown on demand.  A
+    workspace belongs to its launch stream (allocated on it, only ever used on it), so
+    reuse across calls is stream-ordered; reuse saves an allocation per call, which
+    matters for launch-bound small batches."""
+
+    def __init__(self):
+        self.by_stream = {}
+
+
+_WS = _Workspaces()
+
+
+def _workspace(dev, st, nbytes: int):
+    torch = _torch()
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), st.cuda_stream)
+    ws = _WS.by_stream.get(key)
+    if ws is None or ws.numel() < nbytes:
+        with torch.cuda.stream(st):
+            ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        _WS.by_stream[key] = ws
+    return ws
+
+
 def sign_csr_bands_device(indptr, ids, family: Family, rows_per_band: int, keys, out, status=None,
                           stream=None) -> None:
     """Raw asynchronous device call of the fused signing + band-key kernel
@@ -150,8 +174,7 @@ def sign_csr_bands_device(indptr, ids, family: Family, rows_per_band: int, keys,
     with torch.cuda.device(dev):
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, ids.numel(), family.size)
-        with torch.cuda.stream(st):
-            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        ws = _workspace(dev, st, ws_bytes)
         rc = lib.mhb_sign_iterative_csr_bands(
             indptr.data_ptr(), ids.data_ptr(), n_sets, ids.numel(), family.base.a, family.base.b, family.prime,
             family.size, rows_per_band, keys.data_ptr(), out.data_ptr(),
@@ -175,11 +198,8 @@ def sign_csr_to_ptr(indptr, ids, family: Family, out_ptr: int, out_int64: bool =
     ws_bytes = lib.mhb_sign_workspace_bytes(n_sets, nnz, n_hash)
     with torch.cuda.device(dev):
         st = stream if stream is not None else torch.cuda.current_stream(dev)
-        # the workspace belongs to the launch stream: allocated on it, the caching allocator
-        # cannot hand the block to another stream while the kernels still use it
-        with torch.cuda.stream(st):
-            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         sptr = st.cuda_stream
+        ws = _workspace(dev, st, ws_bytes)
         status_ptr = status.data_ptr() if status is not None else None
         if isinstance(family, IterativeFamily):
             rc = lib.mhb_sign_iterative_csr(indptr.data_ptr(), ids.data_ptr(), n_sets, nnz,
