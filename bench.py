@@ -603,10 +603,38 @@ def _guard(ctx, indptr, ids, fam, out, status):
         raise SystemExit(f"bench guard: rank {ctx.rank} GPU signatures differ from the oracle")
 
 
-def _timed_steps(args, ctx, step, stream):
+L2_BYTES = 126 * 2**20  # B200 L2
+
+
+class L2Flush:
+    """Between timed steps of a working set smaller than 2x L2 (cfg1, small shards): a
+    256 MB write evicts the step's inputs and outputs, and each step is timed alone with
+    its own event pair (the flush stays outside the timed region)."""
+
+    def __init__(self, working_bytes, stream):
+        import torch
+
+        self.on = working_bytes < 2 * L2_BYTES
+        self.stream = stream
+        self.buf = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda") if self.on else None
+
+    def __call__(self, stream=None):
+        import torch
+
+        if self.on:
+            with torch.cuda.stream(stream or self.stream):
+                self.buf.fill_(1)
+
+    def describe(self):
+        return "L2 flushed between timed steps (256 MB write, outside the timed region)"
+
+
+def _timed_steps(args, ctx, step, stream, flush=None):
     """W warm-up steps, then K steps between a barrier + synchronize on both sides, timed
     with CUDA events on the launch stream (main-kernel time from the library's per-launch
-    events) while nvidia-smi samples the clocks.  Returns (max-over-ranks ms, kernel ms, clocks)."""
+    events) while nvidia-smi samples the clocks.  With `flush` on (working set < 2x L2),
+    every step is timed alone after an L2 flush and the K step times are summed.
+    Returns (max-over-ranks ms, kernel ms, clocks)."""
     import ctypes as C
 
     import torch
@@ -617,25 +645,39 @@ def _timed_steps(args, ctx, step, stream):
     clk.start()
     time.sleep(0.3)
     for _ in range(args.warmup):
+        if flush is not None:
+            flush()
         step()
     ctx.barrier()
     torch.cuda.synchronize()
     _lib.check(ctx.lib.mhb_profile_begin(args.steps))
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if flush is not None and flush.on:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a, b in evs:
+            flush()
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        total = sum(a.elapsed_time(b) for a, b in evs)
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total = e0.elapsed_time(e1)
     ctx.barrier()
     kms, kn = C.c_float(0), C.c_int32(0)
     _lib.check(ctx.lib.mhb_profile_end(C.byref(kms), C.byref(kn)))
     clocks = clk.stop()
-    return ctx.max_over_ranks(e0.elapsed_time(e1)), kms.value / max(kn.value, 1), clocks
+    return ctx.max_over_ranks(total), kms.value / max(kn.value, 1), clocks
 
 
-def _timed_graph(args, ctx, step):
+def _timed_graph(args, ctx, step, flush=None):
     """The step captured once as a CUDA graph and replayed K times (after W replays),
     timed like _timed_steps.  For launch-bound batches (cfg1) the launches of a step
     cost more than their kernels."""
@@ -656,13 +698,25 @@ def _timed_graph(args, ctx, step):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        graph.replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if flush is not None and flush.on:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a, b in evs:
+            flush(stream)
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        total = sum(a.elapsed_time(b) for a, b in evs)
+    else:
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total = e0.elapsed_time(e1)
     ctx.barrier()
-    return ctx.max_over_ranks(e0.elapsed_time(e1))
+    return ctx.max_over_ranks(total)
 
 
 def _row_checksums(block):
@@ -1079,12 +1133,13 @@ def main():
                  "path": "mhb_sign_iterative_csr_bands: signatures and uint64 band keys from one pass (keys hashed "
                          "in the signing epilogue, csrc/bandhash.cuh); checked vs oracle.band_keys and mhb_band_keys"}
 
-    max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream)
+    flush = L2Flush(4 * W.nnz + 8 * (W.n_sets + 1) + 4 * W.n_sets * N, stream)
+    max_ms, kernel_ms, clocks = _timed_steps(args, ctx, step, stream, flush)
     eager_ms = None
     if args.graph:
         eager_ms = max_ms / args.steps
         out.view(torch.int32).zero_()
-        max_ms = _timed_graph(args, ctx, step)
+        max_ms = _timed_graph(args, ctx, step, flush)
         _guard(ctx, W.indptr, W.ids, fam, out, status)  # the replays produced the signatures
     ms_per_step = max_ms / args.steps
     value = W.n_total * N * args.steps / (max_ms / 1e3)
@@ -1141,7 +1196,9 @@ def main():
                        "split": (f"one global batch, nnz-balanced row shards {W.cuts} (dist.nnz_balanced_cuts); "
                                  f"every rank generated only its own shard (gen.make_shard)"),
                        "shard_sets_rank0": W.n_sets, "shard_nnz_rank0": W.nnz,
-                       "l2": "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per rank per step vs 126 MB L2)"
+                       "l2": (flush.describe() + "; ids %.4f GB + signatures %.4f GB per rank per step vs 126 MB L2"
+                              if flush.on else
+                              "inputs larger than L2 (ids %.2f GB + signatures %.2f GB per rank per step vs 126 MB L2)")
                              % (4 * W.nnz / 1e9, 4 * W.n_sets * N / 1e9),
                        "parallelism": f"dp{ctx.world} (row shards, no collective in the step)",
                        "gen_seconds": round(W.gen_s, 2)},

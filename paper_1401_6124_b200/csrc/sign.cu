@@ -307,8 +307,8 @@ __global__ void plan_scatter_kernel(SignArgs A) {
 // tiles before it in parallel (a CTA takes its tile from a ticket counter and waits
 // only for tiles whose tickets were taken before its own -- CTAs already running).  The three sorted-plan kernels
 // cost ~16 us at 10,000 sets; a one-CTA plan ~24 us (one SM, latency-bound).  A warp
-// group then holds sets of unequal sizes, so the STATIC kernel instances run the
-// group's largest set (a warp max).  Lane tables: every CTA fills a slice.
+// group then holds sets of unequal sizes, so sign_small_batch_kernel runs the group's
+// largest part (a warp max).  Lane tables: every CTA fills a slice.
 constexpr int64_t kSmallPlan = 1 << 14;
 constexpr int kSmallTile = 256;  // sets per tile = threads per CTA
 
@@ -424,10 +424,13 @@ __device__ __forceinline__ void plan_small_tile(const SignArgs& A, unsigned tile
 }
 
 template <typename OutT>
-__global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A) {
+__global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A, int32_t* status_out) {
     __shared__ unsigned warp_c[kSmallTile / 32], warp_b[kSmallTile / 32];
     __shared__ unsigned tile_s, excl_c, excl_b, warp_tot2[2], warp_totb2[2];
     const int t = threadIdx.x;
+    // the caller's status word: zeroed here, ORed by sign_small_batch_kernel (which also
+    // adds the flags this plan raises in the workspace word)
+    if (blockIdx.x == 0 && t == 0 && status_out) *status_out = 0;
     if (t == 0) tile_s = atomicAdd(&A.hist[0], 1u);
     __syncthreads();
     const unsigned tile = tile_s;
@@ -866,8 +869,7 @@ __device__ __forceinline__ void finalize_rows(const SignArgs& A, unsigned long l
 // p and b arrive as separate scalar parameters so ptxas keeps them in uniform
 // registers: VIADDMNMX t, -UR, t reads one vector register instead of two
 // (tools/visit_probe.cu: 41.9 vs 37.8 visits/clk/SM).
-template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false,
-          bool STATIC = false>
+template <int K, bool ITER, bool NARROW, typename OutT, bool BANDS = false, bool FPQ = false, bool SKEW = false>
 __global__ void __maxnreg__((Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>::maxnreg))  // 128: 2 CTAs of 256 per SM
 sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) {
     using S = Spelling<K, ITER, NARROW, FPQ, SKEW, BANDS>;
@@ -895,24 +897,14 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     // Work items flow through a 3-deep pipeline: the id of the item after next is
     // claimed while the current one runs, the next item's set entry is loaded, and
     // the last round of the current item prefetches the next item's first features.
-    // STATIC (small batches): warp w takes items w, w + W, w + 2W, ... -- one work
-    // counter's serialised atomics would be a large share of a short kernel.  Otherwise
-    // items come from the counter (dynamic balance of the size-sorted work).
-    const unsigned long long W = (unsigned long long)gridDim.x * (kBlock / 32);
+    // Items come from the counter (dynamic balance of the size-sorted work).
     unsigned long long it = 0, itn = 0, itnn = 0;
-    if constexpr (STATIC) {
-        // warp w of CTA c takes items w * gridDim + c (+ k W): the first items spread over
-        // all CTAs (hence all SMs) before any CTA gets a second one
-        it = (unsigned long long)warp * gridDim.x + blockIdx.x;
-        itn = it + W;
-    } else {
-        if (lane == 0) {
-            it = atomicAdd(&A.sched->next, 1ull);
-            itn = atomicAdd(&A.sched->next, 1ull);
-        }
-        it = __shfl_sync(0xffffffffu, it, 0);
-        itn = __shfl_sync(0xffffffffu, itn, 0);
+    if (lane == 0) {
+        it = atomicAdd(&A.sched->next, 1ull);
+        itn = atomicAdd(&A.sched->next, 1ull);
     }
+    it = __shfl_sync(0xffffffffu, it, 0);
+    itn = __shfl_sync(0xffffffffu, itn, 0);
     VSet ec = load_vset(A, it, n_vsets, f);
     VSet en = load_vset(A, itn, n_vsets, f);
 
@@ -932,11 +924,7 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     }
 
     while (it < n_items) {
-        if constexpr (STATIC) {
-            itnn = itn + W;
-        } else {
-            if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
-        }
+        if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
         int sb = 0;
         if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
         if (sb != cur_sb) {  // lane constants change only with the lane pass
@@ -958,9 +946,8 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
         const int n = valid ? (int)(ec.meta & 2047) + 1 : 1;
         const int last = n - 1;
         const uint32_t* base = A.ids + (valid ? ec.f0 : 0);
-        // the group's first set is its largest (descending sort); STATIC instances serve
-        // the unsorted small-batch plan: the group's largest set by a warp max
-        const int n_max = STATIC ? (int)__reduce_max_sync(0xffffffffu, (unsigned)n) : __shfl_sync(0xffffffffu, n, 0);
+        // the group's first set is its largest (descending sort)
+        const int n_max = __shfl_sync(0xffffffffu, n, 0);
         const int rounds = (n_max + 1) >> 1;
         const bool odd = n_max & 1;
         // next item's first features (cross-item prefetch)
@@ -1038,30 +1025,276 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
 
         it = itn;
         ec = en;
-        itn = STATIC ? itnn : __shfl_sync(0xffffffffu, itnn, 0);
+        itn = __shfl_sync(0xffffffffu, itnn, 0);
         en = load_vset(A, itn, n_vsets, f);
     }
     if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
-    if constexpr (STATIC) {
-        // small batches: the last CTA to finish inverts the merged long-set rows (no
-        // finalize launch); the fence orders every CTA's red.global.min merges before
-        // its count, and the last one's reads after all of them
-        __shared__ int last_cta;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            last_cta = atomicAdd(&A.sched->done, 1ull) == (unsigned long long)gridDim.x - 1;
+}
+
+// ----------------------------------------------------------------------------
+// Small batches (n_sets <= kSmallPlan): latency-shaped kernel
+// ----------------------------------------------------------------------------
+//
+// cfg1 (10,000 sets, N = 128) has ~1,250 warp items for 2,368 warp slots, so the
+// large-batch kernel's static item -> warp map left half the slots idle and put two
+// items on scheduler 0 of every SM (warps 0 and 4 of a CTA share an SMSP) while the
+// others ran one: the kernel took 2x its ALU time.  Here
+//   * every set is cut into Q contiguous parts (Q = 1, 2, 4): Q threads walk one
+//     (set, lane block) and meet in a shuffle min, so there are Q x more, Q x shorter
+//     items;
+//   * each CTA owns a contiguous range of items and its warps claim them from a
+//     shared-memory counter, so the 2 warps per SMSP of a CTA balance each other;
+//   * the Q threads of a (set, lane block) split its epilogue quads;
+//   * the plan kernel zeroes the caller's status word and the sign kernel ORs into it
+//     (no last-CTA copy), and the last-CTA finalize runs only when the plan found long
+//     sets (n_big > 0): no fence or atomic round trips at the end of a typical batch.
+struct SmallArgs {
+    int32_t* status_out;  // the caller's status word (zeroed by plan_small_kernel), or null
+    int32_t log2Q;        // parts per (set, lane block)
+};
+
+template <int K, typename OutT>
+__device__ __forceinline__ void emit_quads(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
+                                           bool merge, int64_t i0, const InvTab* epi_s, bool epi_smem, int qlo,
+                                           int qhi) {
+    constexpr int NQ = K / 4;
+    constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
+    const uint32_t p = A.p;
+    const int32_t N = A.n_hash;
+    const bool vec_ok = (N & 3) == 0;
+    OutT* row = reinterpret_cast<OutT*>(A.out) + set * (int64_t)N;
+#pragma unroll 1
+    for (int q = qlo; q < qhi; ++q) {
+        const int64_t i = i0 + 4 * q;
+        if (i >= N) break;
+        const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
+        const uint32_t h[4] = {m.x, m.y, m.z, m.w};
+        if (merge) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (i + e < N) atomic_min_out(row + i + e, h[e]);
+            continue;
         }
-        __syncthreads();
-        if (last_cta) {
-            __threadfence();
-            finalize_rows<OutT>(A, 0, 1);
-            // the status word accumulated in the workspace (zeroed with the plan state) goes
-            // to the caller's word, which the host passes in this kernel's copy of `hist`
-            // (unused by the sign kernel; SignArgs keeps its layout: the large-batch
-            // kernels' codegen moves with any change of it)
-            if (threadIdx.x == 0 && A.hist) *reinterpret_cast<int32_t*>(A.hist) = *((volatile int32_t*)&A.sched->status);
+        uint32_t x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int64_t ie = min(i + e, A.n_tot - 1);
+            const InvTab t = epi_smem ? epi_s[ie] : A.inv[ie];
+            x[e] = invert_entry(t, h[e], p);
         }
+        if (vec_ok && i + 3 < N) {
+            store4(row + i, x[0], x[1], x[2], x[3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (i + e < N) row[i + e] = (OutT)x[e];
+        }
+    }
+}
+
+// Ids of a warp item staged in shared memory: an item's sets are consecutive virtual
+// sets, so their features are ONE contiguous range of ids.  Each warp copies the range of
+// its next item with cp.async while it walks the current one (double buffer), so a walk
+// round never waits on an L2/HBM round trip (a lone warp's rounds did: 0.5 us each).
+// ids per buffer (wider items walk from global memory); K = 64 takes half, so that
+// two CTAs still fit an SM next to its 64 KB of dump rows
+__host__ __device__ constexpr int stage_ids(int K) { return K >= 64 ? 256 : 512; }
+
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const uint32_t* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int K, bool ITER, bool NARROW, typename OutT, bool FPQ = false>
+__global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one, SmallArgs SA) {
+    constexpr int kStageIds_ = stage_ids(K);
+    extern __shared__ uint4 smem_raw[];
+    __shared__ unsigned s_next;
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint32_t* dump_row = reinterpret_cast<uint32_t*>(smem_raw) + (warp * 32 + lane) * K;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K + warp * 2 * kStageIds_;
+    InvTab* epi_s = reinterpret_cast<InvTab*>(reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K +
+                                              (kBlock / 32) * 2 * kStageIds_);
+
+    const int log2Q = SA.log2Q;
+    const int Q = 1 << log2Q;
+    const int F = A.F;
+    const int g = lane >> A.log2F;
+    const int f = lane & (F - 1);
+    const int jset = f >> log2Q;         // set slot of the warp group
+    const int part = f & (Q - 1);        // part of the set this thread walks
+    const int log2Fs = A.log2F - log2Q;  // sets per warp group = F / Q
+
+    // the plan's counts and the epilogue table load together, before the one barrier
+    const unsigned long long n_vsets = *((volatile unsigned long long*)&A.sched->n_vsets);
+    const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
+    const bool epi_smem = A.n_tot <= kEpiSmemLanes;
+    if (epi_smem)
+        for (int i = threadIdx.x; i < A.n_tot; i += blockDim.x) epi_s[i] = A.inv[i];
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+
+    const unsigned long long n_groups = (n_vsets + (1ull << log2Fs) - 1) >> log2Fs;
+    const unsigned long long n_items = n_groups * (unsigned)A.n_super;
+    const unsigned long long per = (n_items + gridDim.x - 1) / gridDim.x;
+    const unsigned long long lo = per * blockIdx.x;
+    const unsigned long long hi = min(lo + per, n_items);
+
+    auto claim = [&]() -> unsigned long long {
+        unsigned v = 0;
+        if (lane == 0) v = atomicAdd(&s_next, 1u);
+        return lo + __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto vset_of = [&](unsigned long long it) -> VSet {
+        VSet v;
+        v.f0 = 0;
+        v.meta = -1;
+        if (it < hi) {
+            const unsigned long long group = A.n_super == 1 ? it : it / (unsigned)A.n_super;
+            const unsigned long long k = (group << log2Fs) + jset;
+            if (k < n_vsets) v = A.vsets[k];
+        }
+        return v;
+    };
+    // The item's id range [r0, r0 + width): slot 0 (lane 0) holds its first virtual set.
+    // Staged (width <= kStageIds_): every lane copies ids r0 + lane + 32 j into `buf`.
+    auto stage_item = [&](const VSet& v, uint32_t* buf, long long& r0) -> bool {
+        r0 = __shfl_sync(0xffffffffu, v.f0, 0);
+        const unsigned end = v.meta >= 0 ? (unsigned)(v.f0 + (v.meta & 2047) + 1 - r0) : 0u;
+        const unsigned width = __reduce_max_sync(0xffffffffu, end);
+        const bool staged = width > 0 && width <= (unsigned)kStageIds_;
+        if (staged) {
+            const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(buf);
+            for (unsigned t = lane; t < width; t += 32) cp_async4(sbuf + 4 * t, A.ids + r0 + t);
+        }
+        cp_async_commit();
+        return staged;
+    };
+
+    unsigned long long it = claim();
+    VSet ec = vset_of(it);
+    int cur = 0;
+    long long r0c;
+    bool stc = stage_item(ec, stage, r0c);
+
+    LaneState<K, ITER> ls;
+    ls.negp = negp;
+    ls.one = one;
+    int cur_sb = -1;
+    uint32_t maxid = 0;
+
+    while (it < hi) {  // uniform: lane 0's claim, broadcast
+        // the next item's ids go into the other buffer while this one is walked
+        const unsigned long long itn = claim();
+        const VSet en = vset_of(itn);
+        long long r0n;
+        const bool stn = stage_item(en, stage + (cur ^ 1) * kStageIds_, r0n);
+
+        int sb = 0;
+        if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
+        if (sb != cur_sb) {
+            const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+            if constexpr (ITER) {
+                const LaneTab t = A.tab[i0];
+                ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+            } else {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const LaneTab t = A.tab[i0 + k];
+                    ls.cA[k] = t.A; ls.cAp[k] = t.Ap; ls.cB[k] = t.B;
+                }
+            }
+            cur_sb = sb;
+        }
+        // this thread's part [s0, s0 + n) of its virtual set (parts past the end repeat
+        // the last feature, harmless for a minimum; idle slots walk ids[0])
+        const bool valid = ec.meta >= 0;
+        int n = 1;
+        const uint32_t* base = A.ids;
+        if (valid) {
+            const int nv = (int)(ec.meta & 2047) + 1;
+            const int c = (nv + Q - 1) >> log2Q;
+            const int s0 = min(part * c, nv - 1);
+            n = max(min(s0 + c, nv) - s0, 1);
+            base = stc ? stage + cur * kStageIds_ + (ec.f0 - r0c) + s0 : A.ids + ec.f0 + s0;
+        } else if (stc) {
+            base = stage + cur * kStageIds_;
+        }
+        cp_async_wait1();  // this item's copies (the next item's may still be in flight)
+        __syncwarp();
+        const int last = n - 1;
+        const int n_max = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+        const int rounds = (n_max + 1) >> 1;
+        const bool odd = n_max & 1;
+
+        uint32_t best[K];
+        uint32_t xa = base[0], xb = base[min(1, last)];
+        if (rounds == 1) {
+            maxid = __vimax3_u32(maxid, xa, xb);
+            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
+        } else {
+            uint32_t pa = base[min(2, last)], pb = base[min(3, last)];
+            maxid = __vimax3_u32(maxid, xa, xb);
+            round2<K, ITER, NARROW, true, FPQ>(best, ls, xa, xb, p, bpar);
+            xa = pa; xb = pb;
+            int o = 4;
+#pragma unroll 1
+            for (int r = 1; r + 1 < rounds; ++r, o += 2) {
+                pa = base[min(o, last)];
+                pb = base[min(o + 1, last)];
+                maxid = __vimax3_u32(maxid, xa, xb);
+                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
+                xa = pa; xb = pb;
+            }
+            if (odd) {
+                maxid = max(maxid, xa);
+                round1<K, ITER, NARROW, FPQ>(best, ls, xa, p, bpar);
+            } else {
+                maxid = __vimax3_u32(maxid, xa, xb);
+                round2<K, ITER, NARROW, false, FPQ>(best, ls, xa, xb, p, bpar);
+            }
+        }
+        // the Q parts of a (set, lane block) meet: afterwards every part holds the minima
+        for (int o = 1; o < Q; o <<= 1) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) best[k] = min(best[k], __shfl_xor_sync(0xffffffffu, best[k], o));
+        }
+        if (valid) {
+            const int64_t set = ec.meta >> 12;
+            const bool merge = (ec.meta >> 11) & 1;
+            const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+            dump_best<K>(best, dump_row, lane);
+            constexpr int NQ = K / 4;
+            emit_quads<K, OutT>(A, dump_row, lane, set, merge, i0, epi_s, epi_smem, (part * NQ) >> log2Q,
+                                ((part + 1) * NQ) >> log2Q);
+        }
+        __syncwarp();  // every lane is done with this buffer before it is restaged
+        it = itn;
+        ec = en;
+        r0c = r0n;
+        stc = stn;
+        cur ^= 1;
+    }
+    if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && SA.status_out)
+        atomicOr(SA.status_out, MHB_STATUS_ID_GE_PRIME);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && SA.status_out) {
+        const int32_t plan_status = *((volatile int32_t*)&A.sched->status);  // empty sets, bad parameters
+        if (plan_status) atomicOr(SA.status_out, plan_status);
+    }
+    if (n_big == 0) return;
+    // long sets: the last CTA to finish inverts their merged rows
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&A.sched->done, 1ull) == (unsigned long long)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        finalize_rows<OutT>(A, 0, 1);
     }
 }
 
@@ -1085,15 +1318,15 @@ cudaEvent_t* g_prof_ev = nullptr;
 
 using SignKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t, uint32_t);
 
-template <bool ITER, bool NARROW, typename OutT, bool STATIC = false>
+template <bool ITER, bool NARROW, typename OutT>
 static SignKernelFn pick_kernel(int K) {
     switch (K) {
-        case 8: return sign_kernel<8, ITER, NARROW, OutT, false, false, false, STATIC>;
-        case 16: return sign_kernel<16, ITER, NARROW, OutT, false, false, false, STATIC>;
-        case 32: return sign_kernel<32, ITER, NARROW, OutT, false, false, false, STATIC>;
+        case 8: return sign_kernel<8, ITER, NARROW, OutT>;
+        case 16: return sign_kernel<16, ITER, NARROW, OutT>;
+        case 32: return sign_kernel<32, ITER, NARROW, OutT>;
         default: break;
     }
-    if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT, false, false, false, STATIC>;
+    if constexpr (ITER) return sign_kernel<64, ITER, NARROW, OutT>;
     return nullptr;
 }
 
@@ -1106,15 +1339,8 @@ static SignKernelFn select_skew_kernel(bool narrow, int out_dtype) {
                : sign_kernel<64, true, false, uint32_t, false, false, true>;
 }
 
-static SignKernelFn select_fpq_kernel(int out_dtype, int K, bool stat) {
+static SignKernelFn select_fpq_kernel(int out_dtype, int K) {
     const bool i64 = out_dtype == MHB_OUT_I64;
-    if (stat) {
-        if (K == 16) return i64 ? sign_kernel<16, false, true, long long, false, true, false, true>
-                                : sign_kernel<16, false, true, uint32_t, false, true, false, true>;
-        if (K == 8) return i64 ? sign_kernel<8, false, true, long long, false, true, false, true>
-                               : sign_kernel<8, false, true, uint32_t, false, true, false, true>;
-        return nullptr;
-    }
     if (K == 16) return i64 ? sign_kernel<16, false, true, long long, false, true>
                             : sign_kernel<16, false, true, uint32_t, false, true>;
     if (K == 8) return i64 ? sign_kernel<8, false, true, long long, false, true>
@@ -1141,16 +1367,8 @@ static SignKernelFn select_bands_kernel(bool narrow, int out_dtype, int K, bool 
     return nullptr;
 }
 
-static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K, bool stat) {
+static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K) {
     const bool i64 = out_dtype == MHB_OUT_I64;
-    if (stat) {
-        if (kind == KIND_ITERATIVE) {
-            if (narrow) return i64 ? pick_kernel<true, true, long long, true>(K) : pick_kernel<true, true, uint32_t, true>(K);
-            return i64 ? pick_kernel<true, false, long long, true>(K) : pick_kernel<true, false, uint32_t, true>(K);
-        }
-        if (narrow) return i64 ? pick_kernel<false, true, long long, true>(K) : pick_kernel<false, true, uint32_t, true>(K);
-        return i64 ? pick_kernel<false, false, long long, true>(K) : pick_kernel<false, false, uint32_t, true>(K);
-    }
     if (kind == KIND_ITERATIVE) {
         if (narrow) return i64 ? pick_kernel<true, true, long long>(K) : pick_kernel<true, true, uint32_t>(K);
         return i64 ? pick_kernel<true, false, long long>(K) : pick_kernel<true, false, uint32_t>(K);
@@ -1159,9 +1377,58 @@ static SignKernelFn select_kernel(int kind, bool narrow, int out_dtype, int K, b
     return i64 ? pick_kernel<false, false, long long>(K) : pick_kernel<false, false, uint32_t>(K);
 }
 
+using SmallKernelFn = void (*)(SignArgs, uint32_t, uint32_t, uint32_t, uint32_t, SmallArgs);
+
+template <bool ITER, bool NARROW, typename OutT>
+static SmallKernelFn pick_small(int K) {
+    switch (K) {
+        case 8: return sign_small_batch_kernel<8, ITER, NARROW, OutT>;
+        case 16: return sign_small_batch_kernel<16, ITER, NARROW, OutT>;
+        default: break;
+    }
+    // the random family keeps K <= 16 (three constants per lane in registers)
+    if constexpr (ITER) return K == 32 ? sign_small_batch_kernel<32, ITER, NARROW, OutT>
+                                       : sign_small_batch_kernel<64, ITER, NARROW, OutT>;
+    return nullptr;
+}
+
+static SmallKernelFn select_small_kernel(int kind, bool narrow, int out_dtype, int K, bool fpq) {
+    const bool i64 = out_dtype == MHB_OUT_I64;
+    if (fpq) {
+        if (K == 16) return i64 ? sign_small_batch_kernel<16, false, true, long long, true>
+                                : sign_small_batch_kernel<16, false, true, uint32_t, true>;
+        if (K == 8) return i64 ? sign_small_batch_kernel<8, false, true, long long, true>
+                               : sign_small_batch_kernel<8, false, true, uint32_t, true>;
+        return nullptr;
+    }
+    if (kind == KIND_ITERATIVE) {
+        if (narrow) return i64 ? pick_small<true, true, long long>(K) : pick_small<true, true, uint32_t>(K);
+        return i64 ? pick_small<true, false, long long>(K) : pick_small<true, false, uint32_t>(K);
+    }
+    if (narrow) return i64 ? pick_small<false, true, long long>(K) : pick_small<false, true, uint32_t>(K);
+    return i64 ? pick_small<false, false, long long>(K) : pick_small<false, false, uint32_t>(K);
+}
+
+// Parts per (set, lane block) for the small-batch kernel: enough items for about two
+// per warp slot (the CTAs' shared counters then balance their SMSPs), but parts of at
+// least ~8 features.  MHB_SMALL_Q forces it (tuning).
+static int pick_parts(int64_t n_sets, int64_t nnz, const Geometry& geo, int sms, int occ) {
+    static const int forced = [] {
+        const char* e = std::getenv("MHB_SMALL_Q");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2 || forced == 4) return forced <= geo.F ? forced : geo.F;
+    const int64_t items = (n_sets + geo.F - 1) / geo.F * geo.n_super;
+    const int64_t slots = (int64_t)sms * occ * (kBlock / 32);
+    const int64_t mean = n_sets > 0 ? nnz / n_sets : 0;
+    int Q = 1;
+    while (Q < 4 && Q < geo.F && items * Q < 2 * slots && mean / (2 * Q) >= 8) Q *= 2;
+    return Q;
+}
+
 // Occupancy (CTAs per SM) per (kernel, device, dynamic smem); computed once.  The
 // dynamic-smem limit is raised to the device maximum the first time a kernel is seen.
-static int blocks_per_sm(SignKernelFn fn, size_t smem, const DeviceInfo& dev) {
+static int blocks_per_sm(const void* fn, size_t smem, const DeviceInfo& dev) {
     static std::mutex mu;
     struct Entry { const void* fn; int dev; size_t smem; int occ; };
     static Entry cache[512];
@@ -1273,7 +1540,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.rows = rows_per_band;
     A.write_sig = write_sig;
 
-    // keys (fused band epilogue) have no STATIC instances: they keep the sorted plan
+    // keys (fused band epilogue) have no small-batch instances: they keep the sorted plan
     const bool small_plan = n_sets > 0 && n_sets <= kSmallPlan && keys == nullptr;
     // sched and hist are contiguous at the start of the workspace (zeroed: the sorted
     // plan's histogram, or the small plan's look-back state)
@@ -1281,8 +1548,8 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (rc) return rc;
     int32_t* status_out = nullptr;
     if (small_plan && status) {
-        // no status memset: plan and sign OR into the (zeroed) workspace word, and the
-        // STATIC kernel's last CTA stores it into *status
+        // no status memset: plan_small_kernel zeroes *status and ORs its flags into the
+        // (zeroed) workspace word; sign_small_batch_kernel ORs both into *status
         A.status = &A.sched->status;
         status_out = status;
     } else if (status) {
@@ -1302,9 +1569,9 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         const int64_t lane_ctas = std::min<int64_t>((geo.n_tot + kSmallTile - 1) / kSmallTile, (int64_t)dev.sms * 4);
         if (tiles < lane_ctas) tiles = lane_ctas;
         if (out_dtype == MHB_OUT_I64)
-            plan_small_kernel<long long><<<(unsigned)tiles, kSmallTile, 0, st>>>(A);
+            plan_small_kernel<long long><<<(unsigned)tiles, kSmallTile, 0, st>>>(A, status_out);
         else
-            plan_small_kernel<uint32_t><<<(unsigned)tiles, kSmallTile, 0, st>>>(A);
+            plan_small_kernel<uint32_t><<<(unsigned)tiles, kSmallTile, 0, st>>>(A, status_out);
         rc = cuda_check(cudaGetLastError(), "plan_small launch");
         if (rc) return rc;
     } else {
@@ -1331,29 +1598,47 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
 
     const bool narrow = (3ull * prime) < (1ull << 32);
     const bool skew = kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
-    // small batches (few items per warp slot) take the STATIC-schedule instances; the
-    // grid and the slot count use the dynamic kernel's occupancy (same registers and smem)
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0);
     const int64_t max_vsets = n_sets + nnz / kChunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
-    // small batches (one-CTA unsorted plan) take the STATIC instances: static work
-    // assignment and the group's largest set by a warp max; the grid uses the dynamic
-    // kernel's occupancy (same registers and smem)
+    // small batches (one-launch unsorted plan): sign_small_batch_kernel
+    if (small_plan) {
+        SmallKernelFn sfn = select_small_kernel(kind, narrow, out_dtype, geo.K, fpq);
+        if (!sfn) return set_error(MHB_ERR_INVALID, "no small-batch kernel instance for K=%d", geo.K);
+        const size_t ssmem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
+                             (size_t)(kBlock / 32) * 2 * stage_ids(geo.K) * sizeof(uint32_t) +
+                             (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
+        const int occ = blocks_per_sm((const void*)sfn, ssmem, dev);
+        const int Q = pick_parts(n_sets, nnz, geo, dev.sms, occ);
+        SmallArgs SA{status_out, 0};
+        while ((1 << SA.log2Q) < Q) ++SA.log2Q;
+        // one CTA per 8 items (a warp each) up to the resident grid; a CTA's warps share
+        // its item range through a shared-memory counter
+        const int64_t items = (n_sets * Q + geo.F - 1) / geo.F * geo.n_super;
+        int64_t blocks = (items + (kBlock / 32) - 1) / (kBlock / 32);
+        const int64_t cap = (int64_t)occ * dev.sms;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        int prof_slot = -1;
+        {
+            std::lock_guard<std::mutex> lock(g_prof_mu);
+            if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
+        }
+        if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
+        sfn<<<(unsigned)blocks, kBlock, ssmem, st>>>(A, A.p, A.b, 0u - A.p, 1u, SA);
+        if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
+        return cuda_check(cudaGetLastError(), "sign_small_batch_kernel launch");
+    }
     SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K, skew)
-                      : fpq  ? select_fpq_kernel(out_dtype, geo.K, false)
+                      : fpq  ? select_fpq_kernel(out_dtype, geo.K)
                       : skew ? select_skew_kernel(narrow, out_dtype)
-                             : select_kernel(kind, narrow, out_dtype, geo.K, false);
-    if (small_plan) fn = fpq ? select_fpq_kernel(out_dtype, geo.K, true) : select_kernel(kind, narrow, out_dtype, geo.K, true);
+                             : select_kernel(kind, narrow, out_dtype, geo.K);
     if (!fn) return set_error(MHB_ERR_INVALID, "no kernel instance for K=%d", geo.K);
-    SignKernelFn occ_fn = fpq ? select_fpq_kernel(out_dtype, geo.K, false) : select_kernel(kind, narrow, out_dtype, geo.K, false);
-    const int occ = blocks_per_sm(keys || skew ? fn : occ_fn, smem, dev);
-    if (small_plan) blocks_per_sm(fn, smem, dev);  // sets its dynamic-smem limit once
+    SignKernelFn occ_fn = fpq ? select_fpq_kernel(out_dtype, geo.K) : select_kernel(kind, narrow, out_dtype, geo.K);
+    const int occ = blocks_per_sm((const void*)(keys || skew ? fn : occ_fn), smem, dev);
     int64_t blocks = (items_ub + (kBlock / 32) - 1) / (kBlock / 32);
     const int64_t cap = (int64_t)occ * dev.sms;
-    // static assignment: a whole number of CTAs per SM, so no SM holds twice the work
-    // of the others (cfg1: 157 CTAs put two on 9 SMs, which ran 1.8x longer)
-    if (small_plan && blocks > dev.sms / 2) blocks = (blocks + dev.sms - 1) / dev.sms * dev.sms;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     int prof_slot = -1;
@@ -1362,14 +1647,12 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
     }
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-    SignArgs As = A;  // the sign kernel's copy (see finalize in sign_kernel<STATIC>)
-    if (small_plan) As.hist = reinterpret_cast<unsigned*>(status_out);
-    fn<<<(unsigned)blocks, kBlock, smem, st>>>(As, A.p, A.b, 0u - A.p, 1u);
+    fn<<<(unsigned)blocks, kBlock, smem, st>>>(A, A.p, A.b, 0u - A.p, 1u);
     if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
     rc = cuda_check(cudaGetLastError(), "sign_kernel launch");
     if (rc) return rc;
 
-    if (!small_plan) {  // small batches: the STATIC kernel's last CTA finalizes
+    {
         // blocks loop over long-set rows; 16 per SM hide the row loads without paying
         // for tens of thousands of empty blocks
         int64_t fb = nnz / (kChunk + 1);

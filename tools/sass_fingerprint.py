@@ -11,11 +11,11 @@ ROOT = Path(__file__).resolve().parents[1]
 LIB = ROOT / "paper_1401_6124_b200" / "lib" / "libmhb.so"
 REF = ROOT / "tools" / "sass_fingerprints.txt"
 KERNELS = {
-    "cfg1-3,5 iterative (K=64)": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb0ELb0EEEvNS_8SignArgsEjjjj",
-    "cfg4 iterative (K=64, skew)": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb1ELb0EEEvNS_8SignArgsEjjjj",
-    "cfg4 fused band keys": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb1ELb0ELb1ELb0EEEvNS_8SignArgsEjjjj",
-    "random float-quotient (K=16)": "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb1ELb0ELb0EEEvNS_8SignArgsEjjjj",
-    "random Shoup (K=16)": "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb0ELb0ELb0EEEvNS_8SignArgsEjjjj",
+    "cfg1-3,5 iterative (K=64)": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb0EEEvNS_8SignArgsEjjjj",
+    "cfg4 iterative (K=64, skew)": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb0ELb0ELb1EEEvNS_8SignArgsEjjjj",
+    "cfg4 fused band keys": "_ZN3mhb11sign_kernelILi64ELb1ELb1EjLb1ELb0ELb1EEEvNS_8SignArgsEjjjj",
+    "random float-quotient (K=16)": "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb1ELb0EEEvNS_8SignArgsEjjjj",
+    "random Shoup (K=16)": "_ZN3mhb11sign_kernelILi16ELb0ELb1EjLb0ELb0ELb0EEEvNS_8SignArgsEjjjj",
 }
 
 
