@@ -766,12 +766,17 @@ def _gather_nccl(args, ctx, W, out):
     reps = 3
     torch.cuda.synchronize()
     ctx.barrier()
+    # device time on this rank's stream (the NCCL works make it wait for the transfers);
+    # the gloo test mode moves host tensors, so it keeps the host clock
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    e0.record()
     for _ in range(reps):
         full = once()
         del full
+    e1.record()
     torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3 / reps
+    ms = ((time.perf_counter() - t0) * 1e3 if shared else e0.elapsed_time(e1)) / reps
     ctx.barrier()
     torch.cuda.empty_cache()
     return ctx.max_over_ranks(ms), sums
@@ -833,12 +838,14 @@ def _gather_peer(args, ctx, W, fam, out, status, stream):
                 sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
             torch.cuda.synchronize()
             ctx.barrier()
-            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             for _ in range(reps):
                 sign_csr_to_ptr(W.indptr, W.ids, fam, dst_ptr, False, status, stream)
+            e1.record(stream)
             torch.cuda.synchronize()
             ctx.barrier()  # every rank's rows have landed in rank 0's matrix
-            ms = ctx.max_over_ranks((time.perf_counter() - t0) * 1e3 / reps)
+            ms = ctx.max_over_ranks(e0.elapsed_time(e1) / reps)
             if ctx.rank == 0:
                 mat = owner.tensor()
                 sums = [_row_checksums(mat[W.cuts[r]:W.cuts[r + 1]]) for r in range(ctx.world)]
