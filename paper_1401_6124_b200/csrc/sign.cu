@@ -1128,6 +1128,9 @@ __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p,
     const int part = f & (Q - 1);        // part of the set this thread walks
     const int log2Fs = A.log2F - log2Q;  // sets per warp group = F / Q
 
+    // launched with programmatic stream serialization (PDL): this grid may start while
+    // plan_small_kernel finishes; everything below reads the plan's outputs
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // the plan's counts and the epilogue table load together, before the one barrier
     const unsigned long long n_vsets = *((volatile unsigned long long*)&A.sched->n_vsets);
     const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
@@ -1626,9 +1629,25 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
             if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
         }
         if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
-        sfn<<<(unsigned)blocks, kBlock, ssmem, st>>>(A, A.p, A.b, 0u - A.p, 1u, SA);
+        // programmatic dependent launch: the grid is set up while the plan kernel runs
+        // (the kernel waits on griddepcontrol before its first read); MHB_PDL=0 turns it off
+        static const bool pdl = [] {
+            const char* e = std::getenv("MHB_PDL");
+            return !(e && e[0] == '0');
+        }();
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = ssmem;
+        cfg.stream = st;
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        rc = cuda_check(cudaLaunchKernelEx(&cfg, sfn, A, A.p, A.b, 0u - A.p, 1u, SA), "sign_small_batch_kernel launch");
         if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
-        return cuda_check(cudaGetLastError(), "sign_small_batch_kernel launch");
+        return rc;
     }
     SignKernelFn fn = keys   ? select_bands_kernel(narrow, out_dtype, geo.K, skew)
                       : fpq  ? select_fpq_kernel(out_dtype, geo.K)
