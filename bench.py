@@ -1186,8 +1186,9 @@ def main():
            if args.aux and ctx.rank == 0 else None)
     cpu = _cpu_baseline(args, W, fam) if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline else None
     per_set = _per_set(ctx) if ctx.rank == 0 and ctx.world == 1 and not args.no_e2e else None
-    # per step: plan (3 kernels; 1 for shards of <= 16,384 sets), sign, finalize
-    launches = (3 if W.n_sets <= 16384 else 5) * args.steps
+    # per step: plan (3 kernels), sign, finalize; shards of <= 16,384 sets: plan_small_kernel
+    # + sign_small_batch_kernel (the workspace memset is a driver fill, not counted)
+    launches = (2 if W.n_sets <= 16384 else 5) * args.steps
 
     if ctx.rank == 0:
         line = {
