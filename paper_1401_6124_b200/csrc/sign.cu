@@ -106,6 +106,28 @@ static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fi
     return best;
 }
 
+int choose_chunk(int64_t n_sets, int64_t nnz, int32_t n_hash) {
+    static const int forced = [] {
+        const char* e = std::getenv("MHB_CHUNK");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 256 || v == 512 || v == 1024) ? v : 0;
+    }();
+    if (forced) return forced;
+    // A virtual set is one slice's item; the descending-size schedule starts the largest
+    // first, but a few of them landing on one SMSP set the kernel's tail once they are a
+    // sizeable share of an SMSP's work.  So the chunk shrinks with the batch's visits
+    // N * nnz, but never below ~1.25x the mean set, so typical sets are not split (each
+    // split set pays N merge atomics and a finalize pass).  tools/scaling_projection.py
+    // (cfg2 shards, ms per shard at 1024 / 512 / 256): 197M ids 4.81 / 4.96 / 5.35,
+    // 99M 2.62 / 2.51 / 2.70, 49M 1.56 / 1.35 / 1.41, 25M 1.25 / 0.85 / 0.77; cfg3
+    // (Poisson(300) sets) 0.89 / 0.89 / 1.32 at 15M ids.
+    const double visits = (double)(nnz > 0 ? nnz : 0) * (double)(n_hash > 0 ? n_hash : 1);
+    int chunk = visits >= 34359738368.0 ? 1024 : visits >= 8589934592.0 ? 512 : 256;  // 2^35, 2^33
+    const double mean = n_sets > 0 ? (double)nnz / (double)n_sets : 0.0;
+    while (chunk < kChunk && chunk < 1.25 * mean) chunk *= 2;
+    return chunk;
+}
+
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
     // Both families and every lane count share one layout; size for the largest lane table.
     int64_t n_tot = 0;
@@ -116,9 +138,10 @@ WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
         }
     int64_t nnz_pos = nnz > 0 ? nnz : 0;
     int64_t sets = n_sets > 0 ? n_sets : 0;
-    int64_t max_big = nnz_pos / (kChunk + 1);
+    const int chunk = choose_chunk(n_sets, nnz, n_hash);
+    int64_t max_big = nnz_pos / (chunk + 1);
     if (max_big > sets) max_big = sets;
-    int64_t max_vsets = sets + nnz_pos / kChunk;
+    int64_t max_vsets = sets + nnz_pos / chunk;
 
     WorkspaceLayout w{};
     size_t off = 0;
@@ -203,11 +226,11 @@ __global__ void plan_count_kernel(SignArgs A) {
             if (A.status) atomicOr(A.status, MHB_STATUS_EMPTY_SET);
             continue;
         }
-        const int64_t nch = (n + kChunk - 1) / kChunk;
-        const int last = (int)(n - (nch - 1) * kChunk);
+        const int64_t nch = (n + A.chunk - 1) / A.chunk;
+        const int last = (int)(n - (nch - 1) * A.chunk);
         atomicAdd(&sh[last - 1], 1u);
         if (nch > 1) {
-            atomicAdd(&sh[kChunk - 1], (unsigned)(nch - 1));
+            atomicAdd(&sh[A.chunk - 1], (unsigned)(nch - 1));
             const unsigned long long k = atomicAdd(&A.sched->n_big, 1ull);
             A.big[k] = s;
         }
@@ -266,9 +289,9 @@ __global__ void plan_scatter_kernel(SignArgs A) {
     for (int64_t s = s_begin + threadIdx.x; s < s_end; s += blockDim.x) {
         const int64_t n = A.indptr[s + 1] - A.indptr[s];
         if (n <= 0) continue;
-        const int64_t nch = (n + kChunk - 1) / kChunk;
-        atomicAdd(&cnt[(int)(n - (nch - 1) * kChunk) - 1], 1u);
-        if (nch > 1) atomicAdd(&cnt[kChunk - 1], (unsigned)(nch - 1));
+        const int64_t nch = (n + A.chunk - 1) / A.chunk;
+        atomicAdd(&cnt[(int)(n - (nch - 1) * A.chunk) - 1], 1u);
+        if (nch > 1) atomicAdd(&cnt[A.chunk - 1], (unsigned)(nch - 1));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
@@ -280,13 +303,13 @@ __global__ void plan_scatter_kernel(SignArgs A) {
         const int64_t lo = A.indptr[s];
         const int64_t n = A.indptr[s + 1] - lo;
         if (n <= 0) continue;
-        const int64_t nch = (n + kChunk - 1) / kChunk;
+        const int64_t nch = (n + A.chunk - 1) / A.chunk;
         const long long merge = nch > 1 ? 1 : 0;
         for (int64_t c = 0; c < nch; ++c) {
-            const int size = (int)((c + 1 < nch) ? kChunk : n - c * kChunk);
+            const int size = (int)((c + 1 < nch) ? A.chunk : n - c * A.chunk);
             const unsigned pos = base[size - 1] + atomicAdd(&cnt[size - 1], 1u);
             VSet v;
-            v.f0 = lo + c * kChunk;
+            v.f0 = lo + c * A.chunk;
             v.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
             A.vsets[pos] = v;
         }
@@ -331,7 +354,7 @@ __device__ __forceinline__ void plan_small_tile(const SignArgs& A, unsigned tile
         if (n <= 0) {
             if (A.status) atomicOr(A.status, MHB_STATUS_EMPTY_SET);
         } else {
-            const int64_t nch = (n + kChunk - 1) / kChunk;
+            const int64_t nch = (n + A.chunk - 1) / A.chunk;
             chunks = (unsigned)nch;
             bigs = nch > 1 ? 1u : 0u;
         }
@@ -408,9 +431,9 @@ __device__ __forceinline__ void plan_small_tile(const SignArgs& A, unsigned tile
         unsigned pos = excl_c + warp_c[w] + ci - chunks;
         const long long merge = chunks > 1 ? 1 : 0;
         for (unsigned c = 0; c < chunks; ++c) {
-            const int size = (int)((c + 1 < chunks) ? kChunk : n - (int64_t)c * kChunk);
+            const int size = (int)((c + 1 < chunks) ? A.chunk : n - (int64_t)c * A.chunk);
             VSet vs;
-            vs.f0 = lo + (int64_t)c * kChunk;
+            vs.f0 = lo + (int64_t)c * A.chunk;
             vs.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
             A.vsets[pos++] = vs;
         }
@@ -1542,6 +1565,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.keys = keys;
     A.rows = rows_per_band;
     A.write_sig = write_sig;
+    A.chunk = choose_chunk(n_sets, nnz, n_hash);
 
     // keys (fused band epilogue) have no small-batch instances: they keep the sorted plan
     const bool small_plan = n_sets > 0 && n_sets <= kSmallPlan && keys == nullptr;
@@ -1603,7 +1627,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool skew = kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0);
-    const int64_t max_vsets = n_sets + nnz / kChunk;
+    const int64_t max_vsets = n_sets + nnz / A.chunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
     // small batches (one-launch unsorted plan): sign_small_batch_kernel
     if (small_plan) {
@@ -1674,7 +1698,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     {
         // blocks loop over long-set rows; 16 per SM hide the row loads without paying
         // for tens of thousands of empty blocks
-        int64_t fb = nnz / (kChunk + 1);
+        int64_t fb = nnz / (A.chunk + 1);
         if (fb > (int64_t)dev.sms * 16) fb = (int64_t)dev.sms * 16;
         if (fb < 1) fb = 1;
         if (out_dtype == MHB_OUT_I64)

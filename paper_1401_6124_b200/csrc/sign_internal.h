@@ -9,7 +9,7 @@ namespace mhb {
 
 enum { KIND_ITERATIVE = 0, KIND_RANDOM = 1 };
 
-constexpr int kChunk = 1024;         // max features per virtual set; longer sets are split
+constexpr int kChunk = 1024;         // largest virtual set (SignArgs::chunk <= kChunk); longer sets are split
 constexpr int kBlock = 256;          // threads per CTA of the main kernel
 constexpr int kEpiSmemLanes = 2048;  // epilogue table staged in shared memory up to this many lanes
 
@@ -79,6 +79,8 @@ struct SignArgs {
     int32_t rows;       // rows per band (divides K and n_hash)
     int32_t write_sig;  // 0: keys only (out still serves long-set rows as scratch)
     int32_t fpq;        // random family, p <= 2^23: lane tables hold rd(w/p) and the folded offset
+    int32_t chunk;      // features per virtual set of this launch (256, 512 or 1024: choose_chunk);
+                        // appended last so the main kernels' parameter layout is unchanged
 };
 
 // K = 0: the default lanes per thread for n_hash (large batches); K in {8,16,32,64}
@@ -90,6 +92,9 @@ int launch_sign_wide(bool iter, const int64_t* indptr, const uint32_t* ids, int6
                      const uint64_t* ra, const uint64_t* rb, uint64_t prime, int32_t n_hash, void* out,
                      int32_t out_dtype, int32_t* status, cudaStream_t st);
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash);
+// Virtual-set size for a batch (a function of its shape alone, so the workspace size and
+// the launch agree).
+int choose_chunk(int64_t n_sets, int64_t nnz, int32_t n_hash);
 
 // Host-side parameter checks shared by every signing entry (errors as in launch_sign).
 int check_sign_params(int kind, uint64_t a, uint64_t b, bool have_random_arrays, uint64_t prime, int32_t n_hash);
