@@ -106,13 +106,20 @@ static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fi
     return best;
 }
 
-int choose_chunk(int64_t n_sets, int64_t nnz, int32_t n_hash) {
+static int forced_chunk() {
     static const int forced = [] {
         const char* e = std::getenv("MHB_CHUNK");
         const int v = e ? std::atoi(e) : 0;
         return (v == 256 || v == 512 || v == 1024) ? v : 0;
     }();
-    if (forced) return forced;
+    return forced;
+}
+
+constexpr double kChunkVisits1024 = 34359738368.0;  // 2^35 visits and up: chunk 1024
+constexpr double kChunkVisits512 = 8589934592.0;    // 2^33 visits and up: chunk 512, else 256
+
+int choose_chunk(int64_t n_sets, int64_t nnz, int32_t n_hash) {
+    if (const int forced = forced_chunk()) return forced;
     // A virtual set is one slice's item; the descending-size schedule starts the largest
     // first, but a few of them landing on one SMSP set the kernel's tail once they are a
     // sizeable share of an SMSP's work.  So the chunk shrinks with the batch's visits
@@ -122,10 +129,25 @@ int choose_chunk(int64_t n_sets, int64_t nnz, int32_t n_hash) {
     // 99M 2.62 / 2.51 / 2.70, 49M 1.56 / 1.35 / 1.41, 25M 1.25 / 0.85 / 0.77; cfg3
     // (Poisson(300) sets) 0.89 / 0.89 / 1.32 at 15M ids.
     const double visits = (double)(nnz > 0 ? nnz : 0) * (double)(n_hash > 0 ? n_hash : 1);
-    int chunk = visits >= 34359738368.0 ? 1024 : visits >= 8589934592.0 ? 512 : 256;  // 2^35, 2^33
+    int chunk = visits >= kChunkVisits1024 ? 1024 : visits >= kChunkVisits512 ? 512 : 256;
     const double mean = n_sets > 0 ? (double)nnz / (double)n_sets : 0.0;
     while (chunk < kChunk && chunk < 1.25 * mean) chunk *= 2;
     return chunk;
+}
+
+// Upper bound on the extra virtual sets (chunks beyond each set's first) of ANY batch
+// with at most `nnz` ids: the max over nnz' <= nnz of nnz' / chunk(nnz').  It is
+// monotone in nnz, so a workspace sized for a batch also fits every smaller one (the
+// chunk shrinks with the batch, so nnz / chunk alone is not).
+static int64_t extra_vsets_bound(int64_t nnz, int32_t n_hash) {
+    if (nnz <= 0) return 0;
+    if (const int forced = forced_chunk()) return nnz / forced;
+    const double n = n_hash > 0 ? (double)n_hash : 1.0;
+    const int64_t t512 = (int64_t)(kChunkVisits512 / n), t1024 = (int64_t)(kChunkVisits1024 / n);
+    int64_t b = nnz / 1024;
+    b = std::max<int64_t>(b, std::min<int64_t>(nnz, t1024) / 512);
+    b = std::max<int64_t>(b, std::min<int64_t>(nnz, t512) / 256);
+    return b;
 }
 
 WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
@@ -138,10 +160,11 @@ WorkspaceLayout workspace_layout(int64_t n_sets, int64_t nnz, int32_t n_hash) {
         }
     int64_t nnz_pos = nnz > 0 ? nnz : 0;
     int64_t sets = n_sets > 0 ? n_sets : 0;
-    const int chunk = choose_chunk(n_sets, nnz, n_hash);
-    int64_t max_big = nnz_pos / (chunk + 1);
+    // every long set has at least one extra chunk
+    const int64_t extra = extra_vsets_bound(nnz_pos, n_hash);
+    int64_t max_big = extra;
     if (max_big > sets) max_big = sets;
-    int64_t max_vsets = sets + nnz_pos / chunk;
+    int64_t max_vsets = sets + extra;
 
     WorkspaceLayout w{};
     size_t off = 0;

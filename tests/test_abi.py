@@ -79,3 +79,18 @@ def test_workspace_too_small_rejected():
     rc = lib.mhb_sign_iterative_csr(C.addressof(dummy), C.addressof(dummy), 1, 1, 5, 3, 7757, 4,
                                     C.addressof(dummy), 0, None, C.addressof(dummy), 8, None)
     assert rc == _lib.MHB_ERR_INVALID and "workspace" in _lib.last_error()
+
+
+def test_workspace_bytes_fit_smaller_batches():
+    """A workspace sized for a batch fits every smaller batch: the virtual-set size
+    shrinks with the batch (choose_chunk), so the bound must not (host-only call)."""
+    from paper_1401_6124_b200 import _lib
+
+    lib = _lib.load()
+    for n_hash in (1, 128, 256, 2048, 100_000):
+        for n_sets in (1, 1000, 1_000_000):
+            prev = 0
+            for nnz in [0, 10, 10**4] + [int(1e5 * 1.25**k) for k in range(60)]:
+                b = lib.mhb_sign_workspace_bytes(n_sets, nnz, n_hash)
+                assert b >= prev, (n_hash, n_sets, nnz)
+                prev = b
