@@ -78,7 +78,9 @@ const char* mhb_version(void);
 /* Text of the last error raised on the calling thread ("" if none). */
 const char* mhb_last_error(void);
 
-/* Scratch bytes mhb_sign_* needs for this problem shape (same for both families). */
+/* Scratch bytes mhb_sign_* needs for this problem shape (same for both families).
+ * Monotone in n_sets and nnz: a workspace sized for the largest batch of a given n_hash
+ * serves every smaller one. */
 size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash);
 
 /*
