@@ -80,6 +80,8 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // SMs: cfg1 (10,000 sets, N = 128) gives 625 warps at K = 64 for 148 SMs x 16 warps.
 // Iterative family: take the K (64, 32, 16, 8: more lane groups per set, so more warps)
 // with the fewest waves x per-item work.  MHB_SIGN_K forces K (tuning).
+constexpr int64_t kSmallPlanSets = 1 << 14;  // = kSmallPlan (batches signed by the one-launch plan)
+
 static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fixed) {
     static const int forced = [] {
         const char* e = std::getenv("MHB_SIGN_K");
@@ -93,11 +95,16 @@ static int pick_lanes(int kind, int32_t n_hash, int64_t n_sets, int sms, bool fi
     // instructions (the walk plus the per-feature start hash, steps and loads)
     const int64_t slots = (int64_t)sms * 2 * (kBlock / 32);  // one wave of warp slots (2 CTAs/SM)
     int best = K0;
-    int64_t best_cost = -1;
+    double best_cost = -1.0;
     for (int K = K0; K >= 8; K /= 2) {
         const Geometry g = choose_geometry(kind, n_hash, K);
         const int64_t items = (n_sets + g.F - 1) / g.F * g.n_super;
-        const int64_t cost = (items + slots - 1) / slots * (5 * K + 28);
+        // small batches (one-launch plan, unsorted): whole waves; large batches (sorted,
+        // dynamic counter): fractional waves plus half a wave of tail (cfg3 50k-set
+        // shards: K = 64 at 5.3 waves beats K = 32 at 10.6)
+        const double waves = n_sets <= kSmallPlanSets ? (double)((items + slots - 1) / slots)
+                                                       : (double)items / (double)slots + 0.5;
+        const double cost = waves * (5 * K + 28);
         if (best_cost < 0 || cost < best_cost) {
             best = K;
             best_cost = cost;
@@ -263,6 +270,28 @@ __global__ void plan_count_kernel(SignArgs A) {
         if (sh[i]) atomicAdd(&A.hist[i], sh[i]);
 }
 
+// Rows A.big[e0 .. n_big) (strided by the grid's warps) start at UINT_MAX: one warp per
+// row, the next row's index loaded while this one is written (a block per row with the
+// index load on the critical path took 108 us for cfg2's 27k long sets at 256-id chunks).
+template <typename OutT>
+__device__ __forceinline__ void init_long_rows(const SignArgs& A, unsigned long long b0, unsigned long long nb,
+                                               unsigned long long n_big) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nw = blockDim.x >> 5;
+    const unsigned long long stride = nb * nw;
+    unsigned long long e = b0 * nw + (threadIdx.x >> 5);
+    OutT* out = reinterpret_cast<OutT*>(A.out);
+    int64_t s = e < n_big ? A.big[e] : 0;
+    while (e < n_big) {
+        const unsigned long long en = e + stride;
+        const int64_t sn = en < n_big ? A.big[en] : 0;
+        OutT* row = out + s * (int64_t)A.n_hash;
+        for (int i = lane; i < A.n_hash; i += 32) row[i] = (OutT)(~0u);
+        e = en;
+        s = sn;
+    }
+}
+
 // One block of kChunk threads: cursor[size-1] = number of virtual sets larger than
 // `size` (descending order), total -> sched->n_vsets.
 __global__ void plan_scan_kernel(SignArgs A) {
@@ -328,22 +357,25 @@ __global__ void plan_scatter_kernel(SignArgs A) {
         if (n <= 0) continue;
         const int64_t nch = (n + A.chunk - 1) / A.chunk;
         const long long merge = nch > 1 ? 1 : 0;
-        for (int64_t c = 0; c < nch; ++c) {
-            const int size = (int)((c + 1 < nch) ? A.chunk : n - c * A.chunk);
-            const unsigned pos = base[size - 1] + atomicAdd(&cnt[size - 1], 1u);
+        // the nch - 1 full chunks take one run of the `chunk` bin with a single atomic
+        // (one per chunk serialised on that bin: 108 us at 256-id chunks of cfg2)
+        unsigned pos_full = 0;
+        if (nch > 1) pos_full = base[A.chunk - 1] + atomicAdd(&cnt[A.chunk - 1], (unsigned)(nch - 1));
+        for (int64_t c = 0; c + 1 < nch; ++c) {
             VSet v;
             v.f0 = lo + c * A.chunk;
-            v.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
-            A.vsets[pos] = v;
+            v.meta = ((long long)s << 12) | (merge << 11) | (long long)(A.chunk - 1);
+            A.vsets[pos_full + c] = v;
         }
+        const int size = (int)(n - (nch - 1) * A.chunk);
+        VSet v;
+        v.f0 = lo + (nch - 1) * A.chunk;
+        v.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
+        A.vsets[base[size - 1] + atomicAdd(&cnt[size - 1], 1u)] = v;
     }
     // rows of long sets start at UINT_MAX (their chunks merge with atomicMin)
     const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
-    OutT* out = reinterpret_cast<OutT*>(A.out);
-    for (unsigned long long e = blockIdx.x; e < n_big; e += gridDim.x) {
-        OutT* row = out + A.big[e] * (int64_t)A.n_hash;
-        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x) row[i] = (OutT)(~0u);
-    }
+    init_long_rows<OutT>(A, blockIdx.x, gridDim.x, n_big);
 }
 
 // Small batches (n_sets <= kSmallPlan = 16384): the whole plan in ONE launch.  No size
@@ -355,7 +387,7 @@ __global__ void plan_scatter_kernel(SignArgs A) {
 // cost ~16 us at 10,000 sets; a one-CTA plan ~24 us (one SM, latency-bound).  A warp
 // group then holds sets of unequal sizes, so sign_small_batch_kernel runs the group's
 // largest part (a warp max).  Lane tables: every CTA fills a slice.
-constexpr int64_t kSmallPlan = 1 << 14;
+constexpr int64_t kSmallPlan = kSmallPlanSets;
 constexpr int kSmallTile = 256;  // sets per tile = threads per CTA
 
 // hist[] doubles as the look-back state: [0] ticket counter, [2 + 2k] / [3 + 2k] tile
@@ -460,11 +492,16 @@ __device__ __forceinline__ void plan_small_tile(const SignArgs& A, unsigned tile
             vs.meta = ((long long)s << 12) | (merge << 11) | (long long)(size - 1);
             A.vsets[pos++] = vs;
         }
-        if (merge) {
-            A.big[excl_b + warp_b[w] + bi - bigs] = s;
-            // rows of long sets start at UINT_MAX (their chunks merge with red.global.min)
-            OutT* row = reinterpret_cast<OutT*>(A.out) + s * (int64_t)A.n_hash;
-            for (int i = 0; i < A.n_hash; ++i) row[i] = (OutT)(~0u);
+        if (merge) A.big[excl_b + warp_b[w] + bi - bigs] = s;
+    }
+    // rows of this tile's long sets start at UINT_MAX (their chunks merge with
+    // red.global.min): the CTA's warps share them
+    if (own_b) {
+        __syncthreads();
+        const int lane = t & 31;
+        for (unsigned e = excl_b + w; e < excl_b + own_b; e += kSmallTile / 32) {
+            OutT* row = reinterpret_cast<OutT*>(A.out) + A.big[e] * (int64_t)A.n_hash;
+            for (int i = lane; i < A.n_hash; i += 32) row[i] = (OutT)(~0u);
         }
     }
 }
@@ -892,23 +929,32 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 // (one block per row, threads over hash lanes).
 template <typename OutT>
 __device__ __forceinline__ void finalize_rows(const SignArgs& A, unsigned long long e0, unsigned long long stride) {
+    // one warp per row (block e0 of `stride` blocks), the next row's index loaded ahead
     const unsigned long long n_big = *((volatile unsigned long long*)&A.sched->n_big);
     OutT* out = reinterpret_cast<OutT*>(A.out);
-    for (unsigned long long e = e0; e < n_big; e += stride) {
-        const int64_t s = A.big[e];
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nw = blockDim.x >> 5;
+    const unsigned long long step = stride * nw;
+    unsigned long long e = e0 * nw + (threadIdx.x >> 5);
+    int64_t s = e < n_big ? A.big[e] : 0;
+    while (e < n_big) {
+        const unsigned long long en = e + step;
+        const int64_t sn = en < n_big ? A.big[en] : 0;
         OutT* row = out + s * (int64_t)A.n_hash;
-        for (int i = threadIdx.x; i < A.n_hash; i += blockDim.x)
-            row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
+#pragma unroll 4
+        for (int i = lane; i < A.n_hash; i += 32) row[i] = (OutT)invert_entry(A.inv[i], (uint32_t)row[i], A.p);
         if (A.keys) {  // band keys of long sets (their chunks merged in `out`)
-            __syncthreads();
+            __syncwarp();
             const int n_bands = A.n_hash / A.rows;
-            for (int band = threadIdx.x; band < n_bands; band += blockDim.x) {
+            for (int band = lane; band < n_bands; band += 32) {
                 BandHash hk((uint32_t)band);
                 for (int j = 0; j < A.rows; ++j) hk.add((uint32_t)row[band * A.rows + j]);
                 A.keys[s * (int64_t)n_bands + band] = hk.key();
             }
-            __syncthreads();
+            __syncwarp();
         }
+        e = en;
+        s = sn;
     }
 }
 
@@ -1719,9 +1765,9 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     if (rc) return rc;
 
     {
-        // blocks loop over long-set rows; 16 per SM hide the row loads without paying
-        // for tens of thousands of empty blocks
-        int64_t fb = nnz / (A.chunk + 1);
+        // warps loop over long-set rows (finalize_rows); up to 16 blocks of 8 warps per SM
+        // hide the row loads, and a batch without long sets pays for few empty blocks
+        int64_t fb = (nnz / (A.chunk + 1) + 7) / 8;
         if (fb > (int64_t)dev.sms * 16) fb = (int64_t)dev.sms * 16;
         if (fb < 1) fb = 1;
         if (out_dtype == MHB_OUT_I64)
