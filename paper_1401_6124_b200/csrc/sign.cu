@@ -246,7 +246,6 @@ __global__ void plan_count_kernel(SignArgs A) {
     __syncthreads();
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const uint32_t p = A.p;
 
     for (int64_t i = tid; i < A.n_tot; i += stride) fill_lane_tables(A, i);
 
@@ -1186,30 +1185,63 @@ __device__ __forceinline__ void emit_quads(const SignArgs& A, const uint32_t* du
 
 // Ids of a warp item staged in shared memory: an item's sets are consecutive virtual
 // sets, so their features are ONE contiguous range of ids.  Each warp copies the range of
-// its next item with cp.async while it walks the current one (double buffer), so a walk
-// round never waits on an L2/HBM round trip (a lone warp's rounds did: 0.5 us each).
+// its next item while it walks the current one (double buffer): the 16-byte-aligned
+// middle of the range with one TMA bulk copy (cp.async.bulk, completion counted on a
+// per-buffer mbarrier), the < 4 ids at each unaligned end with 4-byte cp.async.
 // ids per buffer (wider items walk from global memory); K = 64 takes half, so that
-// two CTAs still fit an SM next to its 64 KB of dump rows
+// two CTAs still fit an SM next to its 64 KB of dump rows.  A buffer holds 4 more
+// (the range starts at its global address's offset within 16 bytes).
 __host__ __device__ constexpr int stage_ids(int K) { return K >= 64 ? 256 : 512; }
+#ifndef MHB_STAGE_TMA
+#define MHB_STAGE_TMA 0  // 1: the middle by one TMA bulk copy + mbarrier (cfg1 kernel 23.9 us vs 22.7 with cp.async)
+#endif
+__host__ __device__ constexpr int stage_stride(int K) { return stage_ids(K) + 4; }
 
 __device__ __forceinline__ void cp_async4(uint32_t saddr, const uint32_t* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
 }
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+}
+// One thread: expect `bytes` on the barrier, then the bulk copy that delivers them.
+__device__ __forceinline__ void tma_load_1d(uint32_t sdst, const void* gsrc, uint32_t bytes, uint32_t mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred P;\n"
+                 "MHB_WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+                 "@!P bra MHB_WAIT_%=;\n\t}" ::"r"(mbar), "r"(parity) : "memory");
+}
 
 template <int K, bool ITER, bool NARROW, typename OutT, bool FPQ = false>
 __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one, SmallArgs SA) {
     constexpr int kStageIds_ = stage_ids(K);
+    constexpr int kStride = stage_stride(K);
     extern __shared__ uint4 smem_raw[];
     __shared__ unsigned s_next;
     __shared__ int s_last;
+    __shared__ __align__(8) unsigned long long s_mbar[kBlock / 32][2];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint32_t* dump_row = reinterpret_cast<uint32_t*>(smem_raw) + (warp * 32 + lane) * K;
-    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K + warp * 2 * kStageIds_;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K + warp * 2 * kStride;
     InvTab* epi_s = reinterpret_cast<InvTab*>(reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K +
-                                              (kBlock / 32) * 2 * kStageIds_);
+                                              (kBlock / 32) * 2 * kStride);
+    const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s_mbar[warp][0]);
+    if (lane == 0) {
+        mbar_init(mbar0);
+        mbar_init(mbar0 + 8);
+        // make the initialised barriers visible to the async (TMA) proxy
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     const int log2Q = SA.log2Q;
     const int Q = 1 << log2Q;
@@ -1255,25 +1287,54 @@ __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p,
         return v;
     };
     // The item's id range [r0, r0 + width): slot 0 (lane 0) holds its first virtual set.
-    // Staged (width <= kStageIds_): every lane copies ids r0 + lane + 32 j into `buf`.
-    auto stage_item = [&](const VSet& v, uint32_t* buf, long long& r0) -> bool {
+    // Staged (width <= kStageIds_) into buffer b: buffer index k holds id r0 - pad + k,
+    // pad = r0's 4-byte offset within its 16-byte line, so buffer and global 16-byte
+    // boundaries coincide.  The aligned middle goes by TMA (lane 0; `tma` = issued), the
+    // ends by cp.async (one commit group per item, even when empty).
+    auto stage_item = [&](const VSet& v, int b, long long& r0, int& pad, bool& tma) -> bool {
         r0 = __shfl_sync(0xffffffffu, v.f0, 0);
         const unsigned end = v.meta >= 0 ? (unsigned)(v.f0 + (v.meta & 2047) + 1 - r0) : 0u;
         const unsigned width = __reduce_max_sync(0xffffffffu, end);
         const bool staged = width > 0 && width <= (unsigned)kStageIds_;
+        tma = false;
+        pad = 0;
         if (staged) {
-            const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(buf);
-            for (unsigned t = lane; t < width; t += 32) cp_async4(sbuf + 4 * t, A.ids + r0 + t);
+            const uint32_t* g0 = A.ids + r0;
+            pad = (int)(((uintptr_t)g0 >> 2) & 3);
+            const uint32_t* gb = g0 - pad;  // 16-byte aligned; buffer index 0
+            const uint32_t sbuf = (uint32_t)__cvta_generic_to_shared(stage + b * kStride);
+            const int k0 = pad, k1 = pad + (int)width;     // buffer range of the item
+            const int m0 = (k0 + 3) & ~3, m1 = k1 & ~3;    // aligned middle [m0, m1)
+            const int h1 = min(m0, k1);                    // head [k0, h1)
+            const int t0 = max(m1, h1);                    // tail [t0, k1)
+            const int nh = h1 - k0, nt = k1 - t0;
+            if (lane < nh) cp_async4(sbuf + 4 * (k0 + lane), gb + k0 + lane);
+            else if (lane >= 8 && lane < 8 + nt) cp_async4(sbuf + 4 * (t0 + lane - 8), gb + t0 + lane - 8);
+            if (m1 > m0) {
+#if MHB_STAGE_TMA
+                tma = true;
+                // the buffer's previous contents were read through the generic proxy
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    tma_load_1d(sbuf + 4 * m0, gb + m0, 4u * (uint32_t)(m1 - m0), mbar0 + 8 * b);
+                }
+#else
+                for (int k = m0 + 4 * lane; k < m1; k += 128) cp_async16(sbuf + 4 * k, gb + k);
+#endif
+            }
         }
         cp_async_commit();
         return staged;
     };
 
+    uint32_t phase = 0;  // bit b: parity of buffer b's barrier for its next completion
     unsigned long long it = claim();
     VSet ec = vset_of(it);
     int cur = 0;
     long long r0c;
-    bool stc = stage_item(ec, stage, r0c);
+    int padc;
+    bool tmac;
+    bool stc = stage_item(ec, 0, r0c, padc, tmac);
 
     LaneState<K, ITER> ls;
     ls.negp = negp;
@@ -1286,7 +1347,9 @@ __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p,
         const unsigned long long itn = claim();
         const VSet en = vset_of(itn);
         long long r0n;
-        const bool stn = stage_item(en, stage + (cur ^ 1) * kStageIds_, r0n);
+        int padn;
+        bool tman;
+        const bool stn = stage_item(en, cur ^ 1, r0n, padn, tman);
 
         int sb = 0;
         if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
@@ -1314,11 +1377,15 @@ __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p,
             const int c = (nv + Q - 1) >> log2Q;
             const int s0 = min(part * c, nv - 1);
             n = max(min(s0 + c, nv) - s0, 1);
-            base = stc ? stage + cur * kStageIds_ + (ec.f0 - r0c) + s0 : A.ids + ec.f0 + s0;
+            base = stc ? stage + cur * kStride + padc + (ec.f0 - r0c) + s0 : A.ids + ec.f0 + s0;
         } else if (stc) {
-            base = stage + cur * kStageIds_;
+            base = stage + cur * kStride + padc;
         }
-        cp_async_wait1();  // this item's copies (the next item's may still be in flight)
+        cp_async_wait1();  // this item's end copies (the next item's may still be in flight)
+        if (tmac) {         // and its TMA middle
+            mbar_wait(mbar0 + 8 * cur, (phase >> cur) & 1u);
+            phase ^= 1u << cur;
+        }
         __syncwarp();
         const int last = n - 1;
         const int n_max = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
@@ -1370,6 +1437,8 @@ __global__ void __maxnreg__(128) sign_small_batch_kernel(SignArgs A, uint32_t p,
         it = itn;
         ec = en;
         r0c = r0n;
+        padc = padn;
+        tmac = tman;
         stc = stn;
         cur ^= 1;
     }
@@ -1703,7 +1772,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
         SmallKernelFn sfn = select_small_kernel(kind, narrow, out_dtype, geo.K, fpq);
         if (!sfn) return set_error(MHB_ERR_INVALID, "no small-batch kernel instance for K=%d", geo.K);
         const size_t ssmem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
-                             (size_t)(kBlock / 32) * 2 * stage_ids(geo.K) * sizeof(uint32_t) +
+                             (size_t)(kBlock / 32) * 2 * stage_stride(geo.K) * sizeof(uint32_t) +
                              (geo.n_tot <= kEpiSmemLanes ? (size_t)geo.n_tot * sizeof(InvTab) : 0);
         const int occ = blocks_per_sm((const void*)sfn, ssmem, dev);
         const int Q = pick_parts(n_sets, nnz, geo, dev.sms, occ);
