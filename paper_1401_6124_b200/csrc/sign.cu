@@ -688,7 +688,7 @@ struct LaneState {
 #define MHB_SV_ADDR 0
 #endif
 #ifndef MHB_SV_NREG
-#define MHB_SV_NREG 128
+#define MHB_SV_NREG 116  // staged loop: 116 (bank score 72, 30.97 ms) vs 120 (72, 31.06) vs 128 (133, 34.0)
 #endif
 #ifndef MHB_SV_START
 #define MHB_SV_START 1
@@ -718,7 +718,10 @@ struct LaneState {
 #define MHB_SV_MAXID 1
 #endif
 #ifndef MHB_SV_SWAP
-#define MHB_SV_SWAP 1
+#define MHB_SV_SWAP 0
+#endif
+#ifndef MHB_SV_STAGE
+#define MHB_SV_STAGE 1  // cfg4 kernel: ids staged per set (see Spelling::staged)
 #endif
 template <int K, bool ITER, bool NARROW, bool FPQ, bool SKEW, bool BANDS>
 struct Spelling {
@@ -739,7 +742,11 @@ struct Spelling {
                                     : kPlain64 ? MHB_IV_ADDR : kShoup ? MHB_HV_ADDR : false;
     static constexpr int maxnreg = kBands64 ? MHB_BV_NREG : kSkew64 ? MHB_SV_NREG : kFpq ? MHB_RV_NREG
                                    : kPlain64 ? MHB_IV_NREG : kShoup ? MHB_HV_NREG : 128;
+    // one set per warp (F == 1, N >= 2048): the set's ids staged in shared memory and
+    // walked with LDS.64 pairs -- no address arithmetic or clamps in the round loop
+    static constexpr bool staged = kSkew64 && MHB_SV_STAGE;
 };
+constexpr int kSetStage = 136;  // u32 per staging buffer of the staged kernel (sets of <= 133 ids)
 
 // Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
 template <int K, bool ITER>
@@ -926,6 +933,10 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 
 // Long sets: rows hold min hash values after the main kernel; invert in place
 // (one block per row, threads over hash lanes).
+__device__ __forceinline__ void cpa4(uint32_t saddr, const uint32_t* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+
 template <typename OutT>
 __device__ __forceinline__ void finalize_rows(const SignArgs& A, unsigned long long e0, unsigned long long stride) {
     // one warp per row (block e0 of `stride` blocks), the next row's index loaded ahead
@@ -1005,6 +1016,94 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
     const uint32_t four = one << 2;
     int cur_sb = -1;
     uint32_t maxid = 0;
+
+    if constexpr (S::staged) {
+        if (F == 1) {
+            // Every lane of the warp walks the same set.  Its ids (plus a copy of the last,
+            // so an odd set's final pair is valid) are staged into one of two per-warp
+            // buffers with cp.async while the previous item is walked; the rounds read
+            // LDS.64 pairs.  Sets longer than the buffer walk from global memory.
+            uint32_t* wbuf = reinterpret_cast<uint32_t*>(smem_raw) + kBlock * K +
+                             (epi_smem ? 4 * (int)(A.n_tot + A.n_tot / K + 1) : 0) + warp * 2 * kSetStage;
+            auto stage = [&](const VSet& v, int b) -> bool {
+                const int n = v.meta >= 0 ? (int)(v.meta & 2047) + 1 : 0;
+                const bool st = n > 0 && n + 3 <= kSetStage;
+                if (st) {
+                    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(wbuf + b * kSetStage);
+                    const uint32_t* gsrc = A.ids + v.f0;
+                    for (int j = lane; j <= n; j += 32) cpa4(sa + 4 * j, gsrc + min(j, n - 1));
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                return st;
+            };
+            int cur = 0;
+            bool stc = stage(ec, 0);
+            while (it < n_items) {
+                if (lane == 0) itnn = atomicAdd(&A.sched->next, 1ull);
+                const bool stn = stage(en, cur ^ 1);
+                int sb = 0;
+                if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
+                if (sb != cur_sb) {
+                    const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+                    const LaneTab t = A.tab[i0];
+                    ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+                    cur_sb = sb;
+                }
+                const bool valid = ec.meta >= 0;
+                const int n = __shfl_sync(0xffffffffu, valid ? (int)(ec.meta & 2047) + 1 : 1, 0);
+                const int rounds = (n + 1) >> 1;
+                uint32_t best[K];
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                __syncwarp();
+                if (stc) {
+                    const uint32_t* b = wbuf + cur * kSetStage;
+                    for (int j = lane; j < n; j += 32) maxid = max(maxid, b[j]);
+                    uint2 v = *reinterpret_cast<const uint2*>(b);
+                    uint2 nx = *reinterpret_cast<const uint2*>(b + 2);
+                    round2<K, ITER, NARROW, true, FPQ, S::start_fma>(best, ls, v.x, v.y, p, bpar);
+                    const uint2* pp = reinterpret_cast<const uint2*>(b + 4);
+#pragma unroll 1
+                    for (int r = 1; r < rounds; ++r) {
+                        v = nx;
+                        nx = *pp++;  // one pair ahead; past the set it reads unused buffer words
+                        if constexpr (S::swap_features) round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, v.y, v.x, p, bpar);
+                        else round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, v.x, v.y, p, bpar);
+                    }
+                } else {
+                    const uint32_t* gsrc = A.ids + (valid ? ec.f0 : 0);
+                    const int last = n - 1;
+                    uint32_t xa = __ldg(gsrc), xb = __ldg(gsrc + min(1, last));
+                    maxid = __vimax3_u32(maxid, xa, xb);
+                    round2<K, ITER, NARROW, true, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
+#pragma unroll 1
+                    for (int r = 1; r < rounds; ++r) {
+                        xa = __ldg(gsrc + min(2 * r, last));
+                        xb = __ldg(gsrc + min(2 * r + 1, last));
+                        maxid = __vimax3_u32(maxid, xa, xb);
+                        round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
+                    }
+                }
+                if (valid) {
+                    const int64_t set = ec.meta >> 12;
+                    const bool merge = (ec.meta >> 11) & 1;
+                    const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
+                    dump_best<K>(best, dump_row, lane);
+                    if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, true>(A, dump_row, lane, set, merge, i0, epi_s);
+                    else emit_lanes<K, OutT, false, BANDS, SKEW, true>(A, dump_row, lane, set, merge, i0, epi_s);
+                }
+                __syncwarp();  // the buffer is restaged two items later
+                it = itn;
+                ec = en;
+                itn = __shfl_sync(0xffffffffu, itnn, 0);
+                en = load_vset(A, itn, n_vsets, f);
+                stc = stn;
+                cur ^= 1;
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            if (__any_sync(0xffffffffu, maxid >= p) && lane == 0 && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
+            return;
+        }
+    }
 
     uint32_t xa = 0, xb = 0;
     {
@@ -1764,7 +1863,8 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool narrow = (3ull * prime) < (1ull << 32);
     const bool skew = kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
-                        (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0);
+                        (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0) +
+                        (MHB_SV_STAGE && skew && !keys ? (size_t)kBlock / 32 * 2 * kSetStage * sizeof(uint32_t) : 0);
     const int64_t max_vsets = n_sets + nnz / A.chunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
     // small batches (one-launch unsorted plan): sign_small_batch_kernel
