@@ -720,6 +720,9 @@ struct LaneState {
 #ifndef MHB_SV_SWAP
 #define MHB_SV_SWAP 0
 #endif
+#ifndef MHB_RV_STAGE
+#define MHB_RV_STAGE 1  // float-quotient random kernel (cfg3: one set per warp): 12.88 -> 12.36 ms at 112 registers
+#endif
 #ifndef MHB_BV_STAGE
 #define MHB_BV_STAGE 0  // fused band keys staged like the cfg4 kernel: best of 20 spellings 31.95 ms vs 31.82
 #endif
@@ -747,7 +750,7 @@ struct Spelling {
                                    : kPlain64 ? MHB_IV_NREG : kShoup ? MHB_HV_NREG : 128;
     // one set per warp (F == 1, N >= 2048): the set's ids staged in shared memory and
     // walked with LDS.64 pairs -- no address arithmetic or clamps in the round loop
-    static constexpr bool staged = (kSkew64 && MHB_SV_STAGE) || (kBands64 && SKEW && MHB_BV_STAGE);
+    static constexpr bool staged = (kSkew64 && MHB_SV_STAGE) || (kBands64 && SKEW && MHB_BV_STAGE) || (kFpq && MHB_RV_STAGE);
 };
 constexpr int kSetStage = 136;  // u32 per staging buffer of the staged kernel (sets of <= 133 ids)
 
@@ -1048,8 +1051,16 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
                 if (A.n_super > 1) sb = (int)(it % (unsigned)A.n_super);
                 if (sb != cur_sb) {
                     const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
-                    const LaneTab t = A.tab[i0];
-                    ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+                    if constexpr (ITER) {
+                        const LaneTab t = A.tab[i0];
+                        ls.tA = t.A; ls.tAp = t.Ap; ls.tB = t.B;
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) {
+                            const LaneTab t = A.tab[i0 + k];
+                            ls.cA[k] = t.A; ls.cAp[k] = t.Ap; ls.cB[k] = t.B;
+                        }
+                    }
                     cur_sb = sb;
                 }
                 const bool valid = ec.meta >= 0;
@@ -1867,7 +1878,8 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool skew = kind == KIND_ITERATIVE && geo.K == 64 && geo.G >= 16;
     const size_t smem = (size_t)kBlock * geo.K * sizeof(uint32_t) +
                         (geo.n_tot <= kEpiSmemLanes ? (size_t)(geo.n_tot + geo.n_tot / geo.K + 1) * sizeof(InvTab) : 0) +
-                        (skew && (keys ? MHB_BV_STAGE : MHB_SV_STAGE) ? (size_t)kBlock / 32 * 2 * kSetStage * sizeof(uint32_t) : 0);
+                        ((skew && (keys ? MHB_BV_STAGE : MHB_SV_STAGE)) || (fpq && MHB_RV_STAGE)
+                             ? (size_t)kBlock / 32 * 2 * kSetStage * sizeof(uint32_t) : 0);
     const int64_t max_vsets = n_sets + nnz / A.chunk;
     const int64_t items_ub = ((max_vsets + geo.F - 1) / geo.F) * geo.n_super;
     // small batches (one-launch unsorted plan): sign_small_batch_kernel

@@ -738,13 +738,14 @@ def test_sign_csr_device_on_a_side_stream(cuda_device):
         assert np.array_equal(out.cpu().numpy().astype(np.int64), want)
 
 
-@pytest.mark.parametrize("n_hash", [2048, 4096])
-def test_one_set_per_warp_staged_kernel(cuda_device, n_hash):
-    """N >= 2048 in a batch above the small-batch limit: the one-set-per-warp kernel stages
-    each set's ids in shared memory (sets up to 133 ids), walks larger ones from global
-    memory, and merges long sets' chunks -- every row against the oracle, both dtypes."""
+@pytest.mark.parametrize("kind,n_hash,p", [("iterative", 2048, 67_108_879), ("iterative", 4096, 67_108_879),
+                                           ("random", 512, 4_194_319), ("random", 1000, 8_388_593)])
+def test_one_set_per_warp_staged_kernel(cuda_device, kind, n_hash, p):
+    """One set per warp (iterative N >= 2048; float-quotient random lanes, N >= 512) in a
+    batch above the small-batch limit: the kernel stages each set's ids in shared memory
+    (sets up to 133 ids), walks larger ones from global memory, and merges long sets'
+    chunks -- every row against the oracle, both dtypes."""
     rng = np.random.default_rng(n_hash)
-    p = 67_108_879
     sizes = list(rng.integers(1, 12, 17_000)) + [1, 2, 3, 117, 130, 131, 132, 133, 134, 135, 200, 257, 1024, 1025,
                                                   3000, 80, 81]
     rng.shuffle(sizes)
@@ -752,7 +753,7 @@ def test_one_set_per_warp_staged_kernel(cuda_device, n_hash):
     ip = np.zeros(len(rows) + 1, dtype=np.int64)
     ip[1:] = np.cumsum([r.size for r in rows])
     ids = np.concatenate(rows).astype(np.uint32)
-    fam = make_family("iterative", 99 + n_hash, n_hash, p)
+    fam = make_family(kind, 99 + n_hash, n_hash, p)
     want = oracle.sign_family_csr(ip, ids, fam)
     dip, dids = _dev(ip, ids, cuda_device)
     for dt in ("uint32", "int64"):
