@@ -750,6 +750,9 @@ struct Spelling {
                                    : kPlain64 ? MHB_IV_NREG : kShoup ? MHB_HV_NREG : 128;
     // one set per warp (F == 1, N >= 2048): the set's ids staged in shared memory and
     // walked with LDS.64 pairs -- no address arithmetic or clamps in the round loop
+    // invalid slots' size / first id read without a valid check (load_vset): cfg2/cfg3
+    // iterative +1.1%, the Shoup random kernel -5% (its bank-conflict score 51 -> 59)
+    static constexpr bool plain_meta = kIter64 && !BANDS;  // (the band-key loop: score 72 -> 107)
     static constexpr bool staged = (kSkew64 && MHB_SV_STAGE) || (kBands64 && SKEW && MHB_BV_STAGE) || (kFpq && MHB_RV_STAGE);
 };
 constexpr int kSetStage = 136;  // u32 per staging buffer of the staged kernel (sets of <= 133 ids)
@@ -808,12 +811,13 @@ __device__ __forceinline__ void round1(uint32_t (&best)[K], const LaneState<K, I
 // ----------------------------------------------------------------------------
 
 // The slice's virtual set for work item `it` (group = it / n_super), or an
-// invalid entry (meta = -1) past the end.
+// invalid entry past the end: f0 = 0 and meta = -4096 (negative, size field 0), so a
+// slot's size and first id read the same way whether it is valid or not.
 __device__ __forceinline__ VSet load_vset(const SignArgs& A, unsigned long long it, unsigned long long n_vsets,
                                           int f) {
     VSet v;
     v.f0 = 0;
-    v.meta = -1;
+    v.meta = -4096;
     const unsigned long long group = A.n_super == 1 ? it : it / (unsigned)A.n_super;
     const unsigned long long k = (group << A.log2F) + f;
     if (k < n_vsets) v = A.vsets[k];
@@ -1121,8 +1125,8 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
 
     uint32_t xa = 0, xb = 0;
     {
-        const int n = ec.meta >= 0 ? (int)(ec.meta & 2047) + 1 : 1;
-        const uint32_t* base = A.ids + (ec.meta >= 0 ? ec.f0 : 0);
+        const int n = S::plain_meta || ec.meta >= 0 ? (int)(ec.meta & 2047) + 1 : 1;
+        const uint32_t* base = A.ids + (S::plain_meta || ec.meta >= 0 ? ec.f0 : 0);
         xa = __ldg(base);
         xb = __ldg(base + min(1, n - 1));
     }
@@ -1147,17 +1151,19 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
         }
 
         const bool valid = ec.meta >= 0;
-        const int n = valid ? (int)(ec.meta & 2047) + 1 : 1;
+        // an invalid slot reads as one feature at ids[0] (load_vset); S::plain_meta drops
+        // the valid checks ptxas otherwise rematerializes in the round loop
+        const int n = S::plain_meta ? (int)(ec.meta & 2047) + 1 : valid ? (int)(ec.meta & 2047) + 1 : 1;
         const int last = n - 1;
-        const uint32_t* base = A.ids + (valid ? ec.f0 : 0);
+        const uint32_t* base = A.ids + (S::plain_meta ? ec.f0 : valid ? ec.f0 : 0);
         // the group's first set is its largest (descending sort)
         const int n_max = __shfl_sync(0xffffffffu, n, 0);
         const int rounds = (n_max + 1) >> 1;
         const bool odd = n_max & 1;
         // next item's first features (cross-item prefetch)
         const bool nvalid = en.meta >= 0;
-        const uint32_t* nbase = A.ids + (nvalid ? en.f0 : 0);
-        const int nlast = nvalid ? (int)(en.meta & 2047) : 0;
+        const uint32_t* nbase = A.ids + (S::plain_meta ? en.f0 : nvalid ? en.f0 : 0);
+        const int nlast = S::plain_meta ? (int)(en.meta & 2047) : nvalid ? (int)(en.meta & 2047) : 0;
 
         // Rounds of two features.  Ids are prefetched two rounds ahead inside the
         // item; the item's second-to-last round fetches the next item's first round.
