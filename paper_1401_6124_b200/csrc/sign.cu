@@ -688,7 +688,7 @@ struct LaneState {
 #define MHB_SV_ADDR 0
 #endif
 #ifndef MHB_SV_NREG
-#define MHB_SV_NREG 116  // staged loop: 116 (bank score 72, 30.97 ms) vs 120 (72, 31.06) vs 128 (133, 34.0)
+#define MHB_SV_NREG 120  // staged loop + prefetching fallback: 120 (bank score 72) 31.00 ms; 116 (100); 108 (38) 32.0
 #endif
 #ifndef MHB_SV_START
 #define MHB_SV_START 1
@@ -755,7 +755,9 @@ struct Spelling {
     static constexpr bool plain_meta = kIter64 && !BANDS;  // (the band-key loop: score 72 -> 107)
     static constexpr bool staged = (kSkew64 && MHB_SV_STAGE) || (kBands64 && SKEW && MHB_BV_STAGE) || (kFpq && MHB_RV_STAGE);
 };
-constexpr int kSetStage = 136;  // u32 per staging buffer of the staged kernel (sets of <= 133 ids)
+// u32 per staging buffer of the staged kernels (sets of <= 241 ids; two buffers per warp keep two
+// 256-thread CTAs of the cfg4 kernel on an SM: 64 KB dump rows + 33 KB epilogue table + 15.6 KB)
+constexpr int kSetStage = 244;
 
 // Start hash h_{i0}(x) for 3p < 2^32 (see Spelling::start_fma).
 template <int K, bool ITER>
@@ -1088,15 +1090,20 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
                         else round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, v.x, v.y, p, bpar);
                     }
                 } else {
+                    // longer sets: global loads one round ahead (an odd set's last pair
+                    // repeats its last id, harmless for a minimum)
                     const uint32_t* gsrc = A.ids + (valid ? ec.f0 : 0);
                     const int last = n - 1;
                     uint32_t xa = __ldg(gsrc), xb = __ldg(gsrc + min(1, last));
+                    uint32_t na = __ldg(gsrc + min(2, last)), nb = __ldg(gsrc + min(3, last));
                     maxid = __vimax3_u32(maxid, xa, xb);
                     round2<K, ITER, NARROW, true, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
 #pragma unroll 1
                     for (int r = 1; r < rounds; ++r) {
-                        xa = __ldg(gsrc + min(2 * r, last));
-                        xb = __ldg(gsrc + min(2 * r + 1, last));
+                        xa = na;
+                        xb = nb;
+                        na = __ldg(gsrc + min(2 * r + 2, last));
+                        nb = __ldg(gsrc + min(2 * r + 3, last));
                         maxid = __vimax3_u32(maxid, xa, xb);
                         round2<K, ITER, NARROW, false, FPQ, S::start_fma>(best, ls, xa, xb, p, bpar);
                     }
