@@ -17,5 +17,6 @@ ncu --metrics gpu__time_duration.sum,sm__cycles_active.max --clock-control none 
 python bench.py --config cfg4 --aux --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02/bench_cfg4_aux.json 2>/dev/null
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r02/bench_reference_arm.json 2>/dev/null
 python bench.py --config c6 --steps 5 --warmup 2 > gpurun_out/r02/bench_c6.json 2>/dev/null
+python bench.py --config cfg5 --steps 5 --warmup 3 > gpurun_out/r02/bench_cfg5_full_n1.json 2>/dev/null
 python -m pytest tests -m gpu -q > gpurun_out/r02/pytest_gpu.log 2>&1
 ls -la gpurun_out/r02
