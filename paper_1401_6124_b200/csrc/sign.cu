@@ -517,9 +517,16 @@ __global__ void __launch_bounds__(kSmallTile) plan_small_kernel(SignArgs A, int3
     __syncthreads();
     const unsigned tile = tile_s;
     const unsigned n_tiles = (unsigned)((A.n_sets + kSmallTile - 1) / kSmallTile);
-    if (tile < n_tiles) plan_small_tile<OutT>(A, tile, n_tiles, warp_c, warp_b, excl_c, excl_b, warp_tot2, warp_totb2);
-    for (int64_t i = (int64_t)tile * kSmallTile + t; i < A.n_tot; i += (int64_t)gridDim.x * kSmallTile)
-        fill_lane_tables(A, i);
+    // the first n_tiles tickets take the set tiles, the rest the lane tables: the two
+    // latency chains (tile look-back; the lanes' modular inverses) run side by side
+    if (tile < n_tiles) {
+        plan_small_tile<OutT>(A, tile, n_tiles, warp_c, warp_b, excl_c, excl_b, warp_tot2, warp_totb2);
+    } else {
+        const unsigned n_lane_ctas = gridDim.x - n_tiles;
+        for (int64_t i = (int64_t)(tile - n_tiles) * kSmallTile + t; i < A.n_tot;
+             i += (int64_t)n_lane_ctas * kSmallTile)
+            fill_lane_tables(A, i);
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -1855,10 +1862,9 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.fpq = fpq ? 1 : 0;
 
     if (small_plan) {
-        // tiles of sets, plus CTAs enough to spread the lane tables (N may be 10^5)
-        int64_t tiles = (n_sets + kSmallTile - 1) / kSmallTile;
+        // tiles of sets, then CTAs for the lane tables (N may be 10^5)
         const int64_t lane_ctas = std::min<int64_t>((geo.n_tot + kSmallTile - 1) / kSmallTile, (int64_t)dev.sms * 4);
-        if (tiles < lane_ctas) tiles = lane_ctas;
+        const int64_t tiles = (n_sets + kSmallTile - 1) / kSmallTile + lane_ctas;
         if (out_dtype == MHB_OUT_I64)
             plan_small_kernel<long long><<<(unsigned)tiles, kSmallTile, 0, st>>>(A, status_out);
         else
