@@ -3,14 +3,16 @@
 Mirrors ``minhashlab.corpus`` (reference src/corpus.py:18-80): ``tokenize``,
 ``Vocabulary``, ``CorpusData``, ``build_corpus`` keep their names, arguments and
 results.  The work runs in libmhb behind one ``mhb_corpus_*`` handle API with two
-backends:
+backends, chosen explicitly by the caller (no automatic dispatch, no fallback):
 
-* device (csrc/corpus_gpu.cu, the default when a GPU is visible): tokens, vocabulary
+* device (csrc/corpus_gpu.cu, ``backend="gpu"``, the default; it raises when no GPU is
+  visible): tokens, vocabulary
   and documents are computed on the GPU; non-ASCII lines too, with this Python's own
   ``str.isalnum`` / ``str.lower`` (and Final_Sigma) tables (``unicode_tables``), so
   only lines with invalid UTF-8 come back here -- to raise the reference's
   ``UnicodeDecodeError``;
-* host (csrc/corpus.cpp, multi-threaded): pure-ASCII segments natively, segments with
+* host (csrc/corpus.cpp, multi-threaded, only when ``backend="host"`` is named --
+  the CPU test suite and the bench's comparison leg): pure-ASCII segments natively, segments with
   non-ASCII bytes (whole lines holding U+03A3) tokenized here with the reference's
   rule (``[^\\W_]+`` over ``str.lower()``) and handed back.
 
@@ -226,27 +228,28 @@ def _deferred_terms(line: bytes) -> tuple[str, ...]:
 
 
 def _resolve_backend(backend: str, device):
-    if backend not in ("auto", "gpu", "host"):
-        raise ValueError(f"backend must be 'auto', 'gpu' or 'host', got {backend!r}")
+    if backend not in ("gpu", "host"):
+        raise ValueError(f"backend must be 'gpu' or 'host', got {backend!r}")
     if backend == "host":
         return None
     import torch
 
-    if backend == "auto" and not torch.cuda.is_available():
-        return None
+    if not torch.cuda.is_available():
+        raise RuntimeError("corpus ingest: backend='gpu' needs a visible CUDA device "
+                           "(the host ingest is opt-in: backend='host')")
     if device is None:
         return torch.cuda.current_device()
     return torch.device(device).index or 0
 
 
-def build_corpus_csr(path_or_bytes, threads: int | None = None, *, backend: str = "auto", device=None,
+def build_corpus_csr(path_or_bytes, threads: int | None = None, *, backend: str = "gpu", device=None,
                      on_device: bool = False) -> CorpusCSR:
     """Ingest a one-document-per-line UTF-8 file (or its bytes) into a CSR batch.
 
     Same documents, vocabulary and empty-document tally as ``build_corpus``; the
     rows are the documents' sorted ids, ready for ``signatures_csr``.
-    backend: "gpu" (csrc/corpus_gpu.cu), "host" (csrc/corpus.cpp, `threads` workers)
-    or "auto" (the GPU when one is visible).  on_device (GPU backend): indptr / ids
+    backend: "gpu" (csrc/corpus_gpu.cu, the default) or "host" (csrc/corpus.cpp,
+    `threads` workers), named by the caller: nothing is chosen for it.  on_device (GPU backend): indptr / ids
     come back as CUDA tensors instead of numpy arrays."""
     dev = _resolve_backend(backend, device)
     if on_device and dev is None:
@@ -302,10 +305,11 @@ def _staging(n: int) -> np.ndarray:
     return buf.numpy()[:n]
 
 
-def build_corpus(path) -> CorpusData:
+def build_corpus(path, *, backend: str = "gpu") -> CorpusData:
     """Read a one-document-per-line UTF-8 file into id feature sets
-    (reference corpus.py:67-80); empty documents are kept and tallied."""
-    c = build_corpus_csr(path)
+    (reference corpus.py:67-80); empty documents are kept and tallied.
+    backend: as in build_corpus_csr (the GPU unless "host" is named)."""
+    c = build_corpus_csr(path, backend=backend)
     ip, ids = c.indptr, c.ids.astype(np.int64)
     docs = [FeatureSet(ids[ip[d]:ip[d + 1]]) for d in range(ip.size - 1)]
     return CorpusData(c.vocabulary, docs, c.empty_documents)
@@ -342,7 +346,7 @@ def synth_corpus(n_docs: int, doc_size: int, seed: int, id_space: int | None = N
 
 
 def sign_corpus(corpus, out, *, family: str, hashes: int = 128, prime: int | None = None, seed: int = 0,
-                fmt: str = "text", threads: int | None = None, backend: str = "auto",
+                fmt: str = "text", threads: int | None = None, backend: str = "gpu",
                 log=sys.stderr) -> tuple[int, int]:
     """The reference CLI's ``sign`` (cli.py:205-230): ingest `corpus`, build the family,
     sign every non-empty document on the GPU and write (doc_id, signature) records to

@@ -1,4 +1,5 @@
-"""Corpus ingest (reference corpus.py:18-80) through libmhb's native host ingest (CPU only).
+"""Corpus ingest (reference corpus.py:18-80) through libmhb's native host ingest (CPU only;
+named explicitly: backend="host" -- the default is the GPU, tests/test_gpu_parity.py).
 
 The golden fixture (tests/golden/corpus.{json,npz}, made by make_golden.py) holds the
 reference's own build_corpus output -- vocabulary order, documents, empty tally --
@@ -57,7 +58,7 @@ def test_vocabulary():
 def test_build_corpus_worked_pair(tmp_path):
     path = tmp_path / "docs.txt"
     path.write_text(f"{D1}\n{D2}\n", encoding="utf-8")
-    vocab, docs, empty = build_corpus(path)
+    vocab, docs, empty = build_corpus(path, backend="host")
     assert len(vocab) == 5 and len(docs) == 2 and empty == 0
     assert exact_jaccard(docs[0], docs[1]) == pytest.approx(3 / 5)
 
@@ -65,13 +66,13 @@ def test_build_corpus_worked_pair(tmp_path):
 def test_build_corpus_empty_duplicates_blank(tmp_path):
     path = tmp_path / "empty.txt"
     path.write_text("", encoding="utf-8")
-    vocab, docs, empty = build_corpus(path)
+    vocab, docs, empty = build_corpus(path, backend="host")
     assert len(vocab) == 0 and docs == [] and empty == 0
     path.write_text(f"{D1}\n{D1}\n", encoding="utf-8")
-    _, docs, _ = build_corpus(path)
+    _, docs, _ = build_corpus(path, backend="host")
     assert docs[0] == docs[1]
     path.write_text(f"{D1}\n\n...\n{D2}\n", encoding="utf-8")
-    _, docs, empty = build_corpus(path)
+    _, docs, empty = build_corpus(path, backend="host")
     assert len(docs) == 4 and empty == 2 and len(docs[1]) == 0 and len(docs[2]) == 0
 
 
@@ -89,7 +90,7 @@ def test_synth_pair_and_corpus():
 @pytest.mark.parametrize("threads", [1, 3, 8])
 def test_golden_corpora(golden, threads):
     for k, data, case, indptr, ids in _cases(golden):
-        c = build_corpus_csr(data, threads=threads)
+        c = build_corpus_csr(data, threads=threads, backend="host")
         assert list(c.vocabulary.terms) == case["terms"], k
         assert c.empty_documents == case["empty"], k
         assert np.array_equal(c.indptr, indptr), k
@@ -100,7 +101,7 @@ def test_golden_build_corpus_feature_sets(golden, tmp_path):
     for k, data, case, indptr, ids in _cases(golden):
         path = tmp_path / f"c{k}.txt"
         path.write_bytes(data)
-        vocab, docs, empty = build_corpus(path)
+        vocab, docs, empty = build_corpus(path, backend="host")
         assert list(vocab.terms) == case["terms"] and empty == case["empty"]
         assert len(docs) == indptr.size - 1
         for d in range(0, len(docs), max(1, len(docs) // 50)):
@@ -109,16 +110,16 @@ def test_golden_build_corpus_feature_sets(golden, tmp_path):
 
 def test_threads_invariant_large():
     text = gen.synth_text_corpus(30000, 5, vocab=50000, unicode_frac=0.02)
-    a = build_corpus_csr(text, threads=1)
+    a = build_corpus_csr(text, threads=1, backend="host")
     for t in (2, 7, 16):
-        b = build_corpus_csr(text, threads=t)
+        b = build_corpus_csr(text, threads=t, backend="host")
         assert a.vocabulary.terms == b.vocabulary.terms
         assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.ids, b.ids)
 
 
 def test_invalid_utf8_raises_like_the_reference():
     with pytest.raises(UnicodeDecodeError):
-        build_corpus_csr(b"fine line\nbad \xff\xfe bytes\n")
+        build_corpus_csr(b"fine line\nbad \xff\xfe bytes\n", backend="host")
 
 
 def test_abi_deferred_protocol_errors():
@@ -166,3 +167,15 @@ def test_fuzz_host_backend_against_oracle(seed):
         c = build_corpus_csr(data, threads=threads, backend="host")
         assert list(c.vocabulary.terms) == terms and c.empty_documents == empty
         assert np.array_equal(c.indptr, ip) and np.array_equal(c.ids.astype(np.int64), x)
+
+
+def test_gpu_backend_is_the_default_and_never_falls_back(monkeypatch):
+    """No dispatch: the default ingest is the GPU's, and without a visible device it
+    raises instead of quietly running the host code."""
+    import torch
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    with pytest.raises(RuntimeError, match="backend='gpu'"):
+        build_corpus_csr(b"a b c\n")
+    with pytest.raises(ValueError):
+        build_corpus_csr(b"a b c\n", backend="auto")
