@@ -235,7 +235,9 @@ __device__ __forceinline__ void fill_lane_tables(const SignArgs& A, int64_t i) {
     v.B = c;
     v.inv = inv_mod(w, p);
     v.invp = companion_fast(v.inv, p);
-    v.pad = 0;
+    // -c * w^{-1} mod p: the argmin is then one multiply-add, (h * w^{-1} + pad) mod p
+    const uint32_t cw = reduce_once(shoup_lazy(v.inv, v.invp, c, p), p);
+    v.pad = cw ? p - cw : 0u;
     A.inv[i] = v;
 }
 
@@ -539,6 +541,14 @@ __device__ __forceinline__ uint32_t invert_entry(const InvTab& v, uint32_t h, ui
     d = __viaddmin_u32(d, p, d);  // d in [0,p)
     return reduce_once(shoup_lazy(v.inv, v.invp, d, p), p);
 }
+// The same for 3p < 2^32 with one ALU instruction: x = h * A^{-1} + (-B A^{-1}) mod p
+// (InvTab::pad), r = Shoup(h) + pad in [0, 3p); the two subtractions are IMADs by an
+// opaque 1 (FMA pipe) and one VIMNMX3 picks the residue, as in start_hash_fma.
+__device__ __forceinline__ uint32_t invert_entry_fma(const InvTab& v, uint32_t h, uint32_t negp, uint32_t one) {
+    const uint32_t q = __umulhi(v.invp, h);
+    const uint32_t r = v.inv * h + v.pad + q * negp;
+    return __vimin3_u32(r, r * one + negp, r * one + 2u * negp);
+}
 
 // Long-set chunks merge with a fire-and-forget `red.global.min`.  Written as PTX:
 // the C++ atomicMin in this loop makes ptxas move p out of the uniform datapath
@@ -733,6 +743,15 @@ struct LaneState {
 #ifndef MHB_BV_STAGE
 #define MHB_BV_STAGE 0  // fused band keys staged like the cfg4 kernel: best of 20 spellings 31.95 ms vs 31.82
 #endif
+#ifndef MHB_SV_INVF
+#define MHB_SV_INVF 0  // cfg4: 31.01 -> 31.37 ms (register assignment); cfg2/cfg3 kernel +0.45%
+#endif
+#ifndef MHB_IV_INVF
+#define MHB_IV_INVF 1  // cfg2 4.698 -> 4.676 ms, cfg3 5.672 -> 5.648 ms (A/B, 3 rounds)
+#endif
+#ifndef MHB_RV_INVF
+#define MHB_RV_INVF 0  // float-quotient kernel: loop bank score 52 -> 80
+#endif
 #ifndef MHB_SV_STAGE
 #define MHB_SV_STAGE 1  // cfg4 kernel: ids staged per set (see Spelling::staged)
 #endif
@@ -760,6 +779,8 @@ struct Spelling {
     // invalid slots' size / first id read without a valid check (load_vset): cfg2/cfg3
     // iterative +1.1%, the Shoup random kernel -5% (its bank-conflict score 51 -> 59)
     static constexpr bool plain_meta = kIter64 && !BANDS;  // (the band-key loop: score 72 -> 107)
+    // argmin recovery in the epilogue fast path with one ALU instruction per entry
+    static constexpr bool inv_fma = NARROW && !BANDS && (kSkew64 ? MHB_SV_INVF : kPlain64 ? MHB_IV_INVF : kFpq ? MHB_RV_INVF : false);
     static constexpr bool staged = (kSkew64 && MHB_SV_STAGE) || (kBands64 && SKEW && MHB_BV_STAGE) || (kFpq && MHB_RV_STAGE);
 };
 // u32 per staging buffer of the staged kernels (sets of <= 241 ids; two buffers per warp keep two
@@ -851,9 +872,10 @@ __host__ __device__ constexpr int kLog2() { return K <= 1 ? 0 : 1 + kLog2<K / 2>
 // SKEW: the shared-memory epilogue table holds lane i at i + i/K.  With large G (lane
 // blocks of the warp's threads K apart, N >= 16*K) the 8 threads of an LDS.128 phase
 // would otherwise all hit one bank group (an 8-way conflict at G = 32).
-template <int K, typename OutT, bool EPI_SMEM, bool BANDS, bool SKEW, bool UNROLL>
+template <int K, typename OutT, bool EPI_SMEM, bool BANDS, bool SKEW, bool UNROLL, bool INV_FMA = false>
 __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* dump_row, int lane, int64_t set,
-                                           bool merge, int64_t i0, const InvTab* epi_s) {
+                                           bool merge, int64_t i0, const InvTab* epi_s, uint32_t negp = 0,
+                                           uint32_t one = 1) {
     constexpr int NQ = K / 4;
     constexpr int SWZ = (NQ < 8 ? NQ : 8) - 1;
     const uint32_t p = A.p;
@@ -873,8 +895,13 @@ __device__ __forceinline__ void emit_lanes(const SignArgs& A, const uint32_t* du
 #pragma unroll(UNROLL ? 4 : 1)
             for (int q = 0; q < NQ; ++q) {
                 const uint4 m = *reinterpret_cast<const uint4*>(dump_row + ((q ^ (lane & SWZ)) << 2));
-                store4(r + 4 * q, invert_entry(t[4 * q], m.x, p), invert_entry(t[4 * q + 1], m.y, p),
-                       invert_entry(t[4 * q + 2], m.z, p), invert_entry(t[4 * q + 3], m.w, p));
+                if constexpr (INV_FMA)
+                    store4(r + 4 * q, invert_entry_fma(t[4 * q], m.x, negp, one),
+                           invert_entry_fma(t[4 * q + 1], m.y, negp, one), invert_entry_fma(t[4 * q + 2], m.z, negp, one),
+                           invert_entry_fma(t[4 * q + 3], m.w, negp, one));
+                else
+                    store4(r + 4 * q, invert_entry(t[4 * q], m.x, p), invert_entry(t[4 * q + 1], m.y, p),
+                           invert_entry(t[4 * q + 2], m.z, p), invert_entry(t[4 * q + 3], m.w, p));
             }
             return;
         }
@@ -1120,7 +1147,7 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
                     const bool merge = (ec.meta >> 11) & 1;
                     const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
                     dump_best<K>(best, dump_row, lane);
-                    if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, true>(A, dump_row, lane, set, merge, i0, epi_s);
+                    if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, true, S::inv_fma>(A, dump_row, lane, set, merge, i0, epi_s, negp, one);
                     else emit_lanes<K, OutT, false, BANDS, SKEW, true>(A, dump_row, lane, set, merge, i0, epi_s);
                 }
                 __syncwarp();  // the buffer is restaged two items later
@@ -1243,7 +1270,7 @@ sign_kernel(SignArgs A, uint32_t p, uint32_t bpar, uint32_t negp, uint32_t one) 
             const bool merge = (ec.meta >> 11) & 1;
             const int64_t i0 = (int64_t)sb * A.L + (int64_t)g * K;
             dump_best<K>(best, dump_row, lane);
-            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, (SKEW && !(BANDS && MHB_BV_U1)) || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
+            if (epi_smem) emit_lanes<K, OutT, true, BANDS, SKEW, (SKEW && !(BANDS && MHB_BV_U1)) || FPQ, S::inv_fma>(A, dump_row, lane, set, merge, i0, epi_s, negp, one);
             else emit_lanes<K, OutT, false, BANDS, SKEW, SKEW || FPQ>(A, dump_row, lane, set, merge, i0, epi_s);
         }
 
