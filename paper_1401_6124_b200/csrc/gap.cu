@@ -1,0 +1,393 @@
+// gap.cu -- output-sensitive signing for the iterative family (kernels.py:44-73).
+//
+// The iterative generator makes lane i's hash of a feature an arithmetic progression
+// mod p:  h_i(x) = ((a+i) x + i b) mod p = (h_0(x) + i d) mod p,  d = (x + b) mod p
+// (families.py:124-131, kernels.py:62-72).  A signature entry is min_x h_i(x), and with n
+// features that minimum is almost surely below T = p c / n.  So instead of VISITING every
+// (feature, lane) pair -- N n visits per set, what sign_kernel does at 2.66 instructions
+// each -- this kernel ENUMERATES, per feature, only the lanes i < N with h_i(x) < T: about
+// N c / n of them, N c per set whatever its size.
+//
+// Enumeration (three-gap / Slater structure of a rotation, all in exact integers).  For an
+// interval [0, L) the first-return map of v -> v + d mod p is a two-interval exchange
+//     v <  w : v += u, i += n          (u = n d mod p,  the smallest "upward" return)
+//     v >= w : v -= w, i += m          (w = -m d mod p, the smallest "downward" return)
+// with L = u + w.  It starts as the rotation itself (u = d, w = p - d, n = m = 1, L = p)
+// and shrinks Euclid-style: u >= w lets L drop by j w (u -= j w, n += j m), else by j u
+// (w -= j u, m += j n); the orbit's first entry point (v, i) is carried along with at most
+// one jump per level.  The descent stops at the last level with L >= T, where u, w < T,
+// and the return map of [0, T) itself has three branches (Slater):
+//     v <  T - u : (+u, +n)      v >= w : (-w, +m)      else : (u - w, n + m).
+// Each hit is one `red.shared.min` into the set's N running minima in shared memory.
+//
+// Exactness.  Every recorded value is a true hash value, and every h_i(x) < T is recorded;
+// so an entry whose minimum ends below T is the exact minimum.  The others (probability
+// ~e^-c each) are recomputed from all the set's features (fallback list, a thread per
+// entry).  c = ln(0.73 n) balances the two costs.  The argmin id is recovered from the
+// minimum hash as in sign_kernel: x = (h - B_i) A_i^-1 mod p.
+//
+// Work per tile of G consecutive sets (one CTA, G N minima in shared memory): thread k
+// takes features k, k + 256, ... of the tile's contiguous id range; then the CTA inverts
+// and stores the G rows with 16-byte stores.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.h"
+#include "modarith.cuh"
+#include "sign_internal.h"
+
+namespace mhb {
+
+namespace {
+
+constexpr int kGapThreads = 256;
+constexpr int kGapMaxSets = 64;        // sets per tile (upper bound)
+constexpr int kGapFailCap = 2048;      // fallback list entries per tile (overflow: inline)
+constexpr size_t kGapBestBytes = 56 * 1024;  // running minima per CTA: 3 CTAs per SM
+
+struct GapArgs {
+    const int64_t* indptr;
+    const uint32_t* ids;
+    int64_t n_sets;
+    uint32_t p, b, a, ap;   // a mod p and its Shoup companion: h_0(x) = a x mod p
+    int32_t n_hash;
+    int32_t G;              // sets per tile
+    float cmul;             // threshold scale inside the log (0.73: the cost balance)
+    const LaneTab* tab;
+    const InvTab* inv;
+    unsigned long long* next;  // tile counter (zeroed by the caller)
+    int32_t* status;
+    void* out;
+};
+
+__device__ __forceinline__ void reds_min(uint32_t saddr, uint32_t v) {
+    asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void gap_store4(uint32_t* dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(a, b, c, d);
+}
+__device__ __forceinline__ void gap_store4(long long* dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    longlong2* v = reinterpret_cast<longlong2*>(dst);
+    v[0] = make_longlong2((long long)a, (long long)b);
+    v[1] = make_longlong2((long long)c, (long long)d);
+}
+
+__device__ __forceinline__ uint32_t gap_invert(const InvTab& t, uint32_t h, uint32_t p) {
+    uint32_t d = h - t.B;
+    d = __viaddmin_u32(d, p, d);
+    return reduce_once(shoup_lazy(t.inv, t.invp, d, p), p);
+}
+
+// All lanes i < N with h_i(x) < T for one feature: descent, then the three-branch walk.
+// `sbase` is the shared address of the set's minima row.
+__device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32_t sbase, const GapArgs& A) {
+    const uint32_t p = A.p, N = (uint32_t)A.n_hash;
+    const uint32_t d = reduce_once(x + A.b, p);
+    uint32_t v = reduce_once(shoup_lazy(A.a, A.ap, x, p), p);  // h_0(x)
+    uint32_t t = 0;
+    uint32_t u, n, w, m;
+    if (d == 0) {
+        // constant orbit: every lane hashes x to h_0(x)
+        if (v >= T) return;
+        u = 0; n = 1; w = T; m = N;
+    } else {
+        u = d; n = 1; w = p - d; m = 1;
+        uint32_t L = p;
+        for (;;) {
+            const uint32_t mn = min(u, w);
+            if (mn == 0 || L - mn < T || t >= N) break;
+            const uint32_t room = L - T;  // >= mn
+            if (u >= w) {
+                const uint32_t j = min(u / w, room / w);
+                const uint32_t L2 = L - j * w;
+                u -= j * w;
+                n += j * m;
+                if (v >= L2) {
+                    const uint32_t s = (v - L2) / w + 1;
+                    v -= s * w;
+                    t += s * m;
+                }
+                L = L2;
+            } else {
+                const uint32_t j = min(w / u, room / u);
+                const uint32_t L2 = L - j * u;
+                if (v >= L2) {
+                    const uint32_t i = (L - 1 - v) / u;
+                    v -= w - i * u;
+                    t += m + i * n;
+                }
+                w -= j * u;
+                m += j * n;
+                L = L2;
+            }
+        }
+        if (t >= N) return;
+        if (v >= T) {  // the level's interval is [0, L) with T <= L: one more return step
+            v -= w;
+            t += m;
+            if (t >= N) return;
+        }
+    }
+    // return map of [0, T) as the level's two-branch map followed, when it lands in [T, L),
+    // by one more downward step (the third branch); steps in bytes of the minima row,
+    // clipped to the row
+    const uint32_t n4 = min(n, N) * 4u, m4 = min(m, N) * 4u;
+    const uint32_t negw = 0u - w;
+    uint32_t addr = sbase + t * 4u;
+    const uint32_t end = sbase + N * 4u;
+    while (addr < end) {
+        reds_min(addr, v);
+        const bool up = v < w;
+        v += up ? u : negw;
+        addr += up ? n4 : m4;
+        if (v >= T) {
+            v += negw;
+            addr += m4;
+        }
+    }
+}
+
+// Entry (set s, lane i) whose minimum stayed >= T: the exact minimum over every feature.
+template <typename OutT>
+__device__ __forceinline__ void fallback_entry(const GapArgs& A, int64_t f0, int64_t f1, uint32_t i, OutT* row) {
+    const uint32_t p = A.p;
+    const LaneTab lt = A.tab[i];
+    uint32_t h = 0xFFFFFFFFu;
+    for (int64_t f = f0; f < f1; ++f) h = min(h, mul_add_mod(lt.A, lt.Ap, lt.B, __ldg(A.ids + f), p));
+    row[i] = (OutT)gap_invert(A.inv[i], h, p);
+}
+
+// REG_INV: n_hash is a multiple of 4 up to 2048, and this thread's (at most two) lane quads'
+// argmin-recovery constants stay in registers for the whole launch.
+template <typename OutT, bool REG_INV>
+__global__ void __launch_bounds__(kGapThreads) sign_gap_kernel(GapArgs A) {
+    extern __shared__ uint4 gap_smem4[];
+    __shared__ long long sip[kGapMaxSets + 1];
+    __shared__ uint32_t sT[kGapMaxSets];
+    __shared__ uint32_t flist[kGapFailCap];
+    __shared__ unsigned fcount;
+    __shared__ unsigned long long s_tile;
+    uint32_t* best = reinterpret_cast<uint32_t*>(gap_smem4);
+    const uint32_t sbest = (uint32_t)__cvta_generic_to_shared(best);
+    const int tid = threadIdx.x;
+    const uint32_t p = A.p, N = (uint32_t)A.n_hash;
+    const int64_t n_tiles = (A.n_sets + A.G - 1) / A.G;
+    bool bad_id = false;
+    InvTab rinv[REG_INV ? 8 : 1];
+    if (REG_INV) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t i = ((uint32_t)tid + (uint32_t)(k / 4) * kGapThreads) * 4u + (uint32_t)(k & 3);
+            rinv[k] = A.inv[min(i, N - 1u)];
+        }
+    }
+
+    for (;;) {
+        __syncthreads();  // the previous tile's shared state is no longer read
+        if (tid == 0) {
+            s_tile = atomicAdd(A.next, 1ull);
+            fcount = 0;
+        }
+        __syncthreads();
+        const int64_t tile = (int64_t)s_tile;
+        if (tile >= n_tiles) break;
+        const int64_t g0 = tile * A.G;
+        const int Gt = (int)min((long long)A.G, (long long)(A.n_sets - g0));
+        if (tid <= Gt) sip[tid] = A.indptr[g0 + tid];
+        for (uint32_t q = tid; q < (uint32_t)Gt * N / 4u + 1u; q += kGapThreads)
+            gap_smem4[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        __syncthreads();
+        if (tid < Gt) {
+            // T = p c / n with c = ln(cmul n) >= 1: entries miss it with probability ~e^-c
+            const long long n = sip[tid + 1] - sip[tid];
+            uint32_t T = 0;
+            if (n > 0) {
+                const float nf = (float)n;
+                const float c = fmaxf(1.0f, __logf(A.cmul * nf));
+                const float Tf = (float)p * (c / nf);
+                T = Tf >= (float)p ? p : max(1u, (uint32_t)Tf);
+            }
+            sT[tid] = T;
+        }
+        __syncthreads();
+        const int64_t fbeg = sip[0], fend = sip[Gt];
+        for (int64_t f = fbeg + tid; f < fend; f += kGapThreads) {
+            int lo = 0, hi = Gt;  // the set holding feature f: largest s with sip[s] <= f
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (sip[mid] <= f) lo = mid; else hi = mid;
+            }
+            const uint32_t x = __ldg(A.ids + f);
+            if (x >= p) {
+                bad_id = true;
+                continue;
+            }
+            enumerate_feature(x, sT[lo], sbest + (uint32_t)lo * N * 4u, A);
+        }
+        __syncthreads();
+        // rows out: minima below T are exact; the rest go to the fallback list
+        OutT* out = reinterpret_cast<OutT*>(A.out) + g0 * (int64_t)N;
+        if ((N & 3u) == 0) {
+            const uint32_t nq = N / 4u;
+            for (int s = 0; s < Gt; ++s) {
+                const uint32_t T = sT[s];
+                OutT* row = out + (int64_t)s * N;
+                const uint4* hrow = gap_smem4 + (uint32_t)s * nq;
+                if (REG_INV) {
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const uint32_t q = tid + r * kGapThreads;
+                        if (q < nq) {
+                            const uint4 h4 = hrow[q];
+                            const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
+                            uint32_t x[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                x[k] = gap_invert(rinv[r * 4 + k], hs[k], p);
+                                if (hs[k] >= T) {
+                                    const unsigned slot = atomicAdd(&fcount, 1u);
+                                    if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
+                                }
+                            }
+                            gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
+                        }
+                    }
+                } else {
+                    const uint4* inv4 = reinterpret_cast<const uint4*>(A.inv);
+                    for (uint32_t q = tid; q < nq; q += kGapThreads) {
+                        const uint4 h4 = hrow[q];
+                        const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
+                        uint32_t x[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint4 tv = __ldg(inv4 + q * 4u + k);
+                            InvTab it;
+                            it.B = tv.x; it.inv = tv.y; it.invp = tv.z; it.pad = tv.w;
+                            x[k] = gap_invert(it, hs[k], p);
+                            if (hs[k] >= T) {
+                                const unsigned slot = atomicAdd(&fcount, 1u);
+                                if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
+                            }
+                        }
+                        gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
+                    }
+                }
+            }
+        } else {
+            const uint32_t ents = (uint32_t)Gt * N;
+            for (uint32_t e = tid; e < ents; e += kGapThreads) {
+                const uint32_t s = e / N, i = e - s * N;
+                const uint32_t h = best[e];
+                out[e] = (OutT)gap_invert(A.inv[i], h, p);
+                if (h >= sT[s]) {
+                    const unsigned slot = atomicAdd(&fcount, 1u);
+                    if (slot < kGapFailCap) flist[slot] = e;
+                }
+            }
+        }
+        __syncthreads();
+        const unsigned nf = fcount;
+        if (nf <= kGapFailCap) {
+            for (unsigned k = tid; k < nf; k += kGapThreads) {
+                const uint32_t e = flist[k], s = e / N, i = e - s * N;
+                fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
+            }
+        } else {
+            // list overflow (thresholds far too low for this tile): every failing entry, in place
+            const uint32_t ents = (uint32_t)Gt * N;
+            for (uint32_t e = tid; e < ents; e += kGapThreads) {
+                const uint32_t s = e / N, i = e - s * N;
+                if (best[e] >= sT[s]) fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
+            }
+        }
+    }
+    if (bad_id && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
+}
+
+}  // namespace
+
+int gap_sets_per_tile(int32_t n_hash) {
+    const int64_t g = (int64_t)kGapBestBytes / ((int64_t)n_hash * 4);
+    return (int)std::min<int64_t>(g, kGapMaxSets);
+}
+
+// Sets per tile for a batch: the tile's features are dealt to the CTA's threads in
+// rounds, so pick the count whose expected features (plus 1.5 sigma, Poisson-like) waste
+// the least of the last round.
+static int gap_pick_sets(int32_t n_hash, int64_t n_sets, int64_t nnz) {
+    const int gmax = gap_sets_per_tile(n_hash);
+    const double mean = std::max(1.0, (double)nnz / (double)std::max<int64_t>(n_sets, 1));
+    int best = gmax;
+    double best_eff = 0.0;
+    for (int g = std::max(1, gmax / 2); g <= gmax; ++g) {
+        const double f = g * mean, hi = f + 1.5 * std::sqrt(f);
+        const double eff = f / (kGapThreads * std::ceil(hi / kGapThreads));
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = g;
+        }
+    }
+    return best;
+}
+
+// The enumeration pays when a feature's N visits cost more than its descent plus its
+// ~N c / n hits (11 instructions each) and the set's fallback entries.
+bool gap_supported(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz) {
+    if (kind != KIND_ITERATIVE || prime >= (1ull << 31)) return false;
+    if (gap_sets_per_tile(n_hash) < 1 || n_sets < 1 || nnz < 1) return false;
+    return true;
+}
+
+bool gap_preferred(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz) {
+    const char* env = std::getenv("MHB_GAP");  // read per call: tests and A/B runs switch it
+    const int mode = env ? std::atoi(env) : -1;
+    if (mode == 0 || !gap_supported(kind, prime, n_hash, n_sets, nnz)) return false;
+    if (mode == 1) return true;
+    const double mean = (double)nnz / (double)n_sets;
+    const double c = std::max(1.0, std::log(0.73 * std::max(mean, 1.0)));
+    const double old_cost = 2.7 * n_hash * mean;                         // visits
+    const double new_cost = mean * (600.0 + 11.5 * n_hash * c / std::max(mean, 1.0)) +  // descent + hits
+                            n_hash * (10.0 + std::exp(-c) * mean * 8.0);                // rows + fallback
+    return new_cost * 1.3 < old_cost;
+}
+
+int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const DeviceInfo& dev, cudaStream_t st) {
+    GapArgs A{};
+    A.indptr = S.indptr;
+    A.ids = S.ids;
+    A.n_sets = S.n_sets;
+    A.p = S.p;
+    A.b = S.b;
+    A.a = (uint32_t)(S.ia % S.p);
+    A.ap = shoup_companion(A.a, S.p);
+    A.n_hash = S.n_hash;
+    A.G = gap_pick_sets(S.n_hash, S.n_sets, nnz);
+    if (const char* ge = std::getenv("MHB_GAP_SETS")) A.G = std::max(1, std::min(std::atoi(ge), gap_sets_per_tile(S.n_hash)));
+    const char* ce = std::getenv("MHB_GAP_CMUL");
+    A.cmul = ce ? (float)std::atof(ce) : 0.73f;
+    A.tab = S.tab;
+    A.inv = S.inv;
+    A.next = &S.sched->next;
+    A.status = S.status;
+    A.out = S.out;
+    const size_t smem = (size_t)A.G * S.n_hash * 4 + 16;
+    const bool reg_inv = (S.n_hash & 3) == 0 && S.n_hash <= 8 * kGapThreads;
+    auto fn = out_dtype == MHB_OUT_I64
+                  ? (reg_inv ? sign_gap_kernel<long long, true> : sign_gap_kernel<long long, false>)
+                  : (reg_inv ? sign_gap_kernel<uint32_t, true> : sign_gap_kernel<uint32_t, false>);
+    int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "gap kernel shared memory");
+    if (rc) return rc;
+    int occ = 0;
+    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kGapThreads, smem), "gap occupancy");
+    if (rc) return rc;
+    if (occ < 1) return set_error(MHB_ERR_INVALID, "gap kernel does not fit an SM (n_hash %d)", S.n_hash);
+    const int64_t tiles = (S.n_sets + A.G - 1) / A.G;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ * dev.sms));
+    fn<<<(unsigned)blocks, kGapThreads, smem, st>>>(A);
+    return cuda_check(cudaGetLastError(), "sign_gap_kernel launch");
+}
+
+}  // namespace mhb

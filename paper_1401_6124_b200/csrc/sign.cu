@@ -1888,6 +1888,7 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool fpq = !keys && kind == KIND_RANDOM && prime <= (1ull << 23) && (geo.K == 16 || geo.K == 8);
     A.fpq = fpq ? 1 : 0;
 
+    const bool gap = !small_plan && keys == nullptr && gap_preferred(kind, prime, n_hash, n_sets, nnz);
     if (small_plan) {
         // tiles of sets, then CTAs for the lane tables (N may be 10^5)
         const int64_t lane_ctas = std::min<int64_t>((geo.n_tot + kSmallTile - 1) / kSmallTile, (int64_t)dev.sms * 4);
@@ -1908,6 +1909,20 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
             plan_count_kernel<long long><<<(unsigned)blocks, 256, 0, st>>>(A);
         else
             plan_count_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(A);
+        if (gap) {
+            // gap.cu: the lane tables are all it needs of the plan
+            rc = cuda_check(cudaGetLastError(), "plan_count launch");
+            if (rc) return rc;
+            int prof_slot = -1;
+            {
+                std::lock_guard<std::mutex> lock(g_prof_mu);
+                if (g_prof_on && g_prof_n < g_prof_cap && g_prof_dev == dev.device) prof_slot = g_prof_n++;
+            }
+            if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot], st);
+            rc = launch_sign_gap(A, nnz, out_dtype, dev, st);
+            if (prof_slot >= 0) cudaEventRecord(g_prof_ev[2 * prof_slot + 1], st);
+            return rc;
+        }
         plan_scan_kernel<<<1, kChunk, 0, st>>>(A);
         int64_t sblocks = (n_sets + 1023) / 1024;
         if (sblocks > (int64_t)dev.sms * 4) sblocks = (int64_t)dev.sms * 4;

@@ -105,4 +105,12 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
                 size_t workspace_bytes, cudaStream_t st, unsigned long long* keys = nullptr,
                 int32_t rows_per_band = 0, int32_t write_sig = 1);
 
+// Output-sensitive iterative-family kernel (gap.cu): enumerates, per feature, only the
+// lanes whose hash falls below the set's threshold.  `gap_preferred` is the cost model
+// (MHB_GAP=0/1 forces it off/on); launch_sign_gap needs the lane tables of plan_count_kernel
+// and a zeroed Sched::next.
+struct DeviceInfo;
+bool gap_preferred(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz);
+int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const DeviceInfo& dev, cudaStream_t st);
+
 }  // namespace mhb
