@@ -23,7 +23,7 @@
 // Exactness.  Every recorded value is a true hash value, and every h_i(x) < T is recorded;
 // so an entry whose minimum ends below T is the exact minimum.  The others (probability
 // ~e^-c each) are recomputed from all the set's features (fallback list, a thread per
-// entry).  c = ln(0.73 n) balances the two costs.  The argmin id is recovered from the
+// entry).  c = ln(n) balances the two costs (ln(0.4 n) .. ln(1.5 n) swept on cfg4).  The argmin id is recovered from the
 // minimum hash as in sign_kernel: x = (h - B_i) A_i^-1 mod p.
 //
 // Work per tile of G consecutive sets (one CTA, G N minima in shared memory): thread k
@@ -41,10 +41,10 @@ namespace mhb {
 
 namespace {
 
-constexpr int kGapThreads = 256;
+constexpr int kGapThreads = 256;  // default CTA size (template parameter THREADS)
 constexpr int kGapMaxSets = 64;        // sets per tile (upper bound)
-constexpr int kGapFailCap = 2048;      // fallback list entries per tile (overflow: inline)
-constexpr size_t kGapBestBytes = 56 * 1024;  // running minima per CTA: 3 CTAs per SM
+constexpr int kGapFailCap = 1024;      // fallback list entries per tile (overflow: inline)
+constexpr size_t kGapBestBytes = 104 * 1024;  // running minima per CTA: two CTAs per SM at most
 
 struct GapArgs {
     const int64_t* indptr;
@@ -53,7 +53,8 @@ struct GapArgs {
     uint32_t p, b, a, ap;   // a mod p and its Shoup companion: h_0(x) = a x mod p
     int32_t n_hash;
     int32_t G;              // sets per tile
-    float cmul;             // threshold scale inside the log (0.73: the cost balance)
+    float cmul;             // threshold scale inside the log (1: measured best on cfg4, 0.4-1.5 swept)
+    uint32_t one;           // 1, opaque to the compiler (IMAD-spelled adds)
     const LaneTab* tab;
     const InvTab* inv;
     unsigned long long* next;  // tile counter (zeroed by the caller)
@@ -100,7 +101,7 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
             if (mn == 0 || L - mn < T || t >= N) break;
             const uint32_t room = L - T;  // >= mn
             if (u >= w) {
-                const uint32_t j = min(u / w, room / w);
+                const uint32_t j = min(u, room) / w;
                 const uint32_t L2 = L - j * w;
                 u -= j * w;
                 n += j * m;
@@ -111,7 +112,7 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
                 }
                 L = L2;
             } else {
-                const uint32_t j = min(w / u, room / u);
+                const uint32_t j = min(w, room) / u;
                 const uint32_t L2 = L - j * u;
                 if (v >= L2) {
                     const uint32_t i = (L - 1 - v) / u;
@@ -137,15 +138,25 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
     const uint32_t negw = 0u - w;
     uint32_t addr = sbase + t * 4u;
     const uint32_t end = sbase + N * 4u;
+    // The selects are predicated adds: the value's on the FMA pipe (multiply by an opaque
+    // one), the address's on the ALU pipe, so neither pipe carries all nine operations.
+    const uint32_t one = A.one;
     while (addr < end) {
         reds_min(addr, v);
-        const bool up = v < w;
-        v += up ? u : negw;
-        addr += up ? n4 : m4;
-        if (v >= T) {
-            v += negw;
-            addr += m4;
-        }
+        asm volatile(
+            "{\n\t"
+            ".reg .pred up, ov;\n\t"
+            "setp.lt.u32 up, %0, %2;\n\t"
+            "@up  mad.lo.u32 %0, %3, %8, %0;\n\t"
+            "@!up mad.lo.u32 %0, %4, %8, %0;\n\t"
+            "@up  add.u32 %1, %1, %5;\n\t"
+            "@!up add.u32 %1, %1, %6;\n\t"
+            "setp.ge.u32 ov, %0, %7;\n\t"
+            "@ov  mad.lo.u32 %0, %4, %8, %0;\n\t"
+            "@ov  add.u32 %1, %1, %6;\n\t"
+            "}"
+            : "+r"(v), "+r"(addr)
+            : "r"(w), "r"(u), "r"(negw), "r"(n4), "r"(m4), "r"(T), "r"(one));
     }
 }
 
@@ -161,14 +172,14 @@ __device__ __forceinline__ void fallback_entry(const GapArgs& A, int64_t f0, int
 
 // REG_INV: n_hash is a multiple of 4 up to 2048, and this thread's (at most two) lane quads'
 // argmin-recovery constants stay in registers for the whole launch.
-template <typename OutT, bool REG_INV>
-__global__ void __launch_bounds__(kGapThreads) sign_gap_kernel(GapArgs A) {
+template <typename OutT, bool REG_INV, int THREADS>
+__global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
     extern __shared__ uint4 gap_smem4[];
     __shared__ long long sip[kGapMaxSets + 1];
     __shared__ uint32_t sT[kGapMaxSets];
     __shared__ uint32_t flist[kGapFailCap];
     __shared__ unsigned fcount;
-    __shared__ unsigned long long s_tile;
+    __shared__ unsigned long long s_tile[2];
     uint32_t* best = reinterpret_cast<uint32_t*>(gap_smem4);
     const uint32_t sbest = (uint32_t)__cvta_generic_to_shared(best);
     const int tid = threadIdx.x;
@@ -179,41 +190,44 @@ __global__ void __launch_bounds__(kGapThreads) sign_gap_kernel(GapArgs A) {
     if (REG_INV) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const uint32_t i = ((uint32_t)tid + (uint32_t)(k / 4) * kGapThreads) * 4u + (uint32_t)(k & 3);
+            const uint32_t i = ((uint32_t)tid + (uint32_t)(k / 4) * THREADS) * 4u + (uint32_t)(k & 3);
             rinv[k] = A.inv[min(i, N - 1u)];
         }
     }
 
-    for (;;) {
-        __syncthreads();  // the previous tile's shared state is no longer read
+    // minima start at UINT_MAX; the row pass below resets what it reads
+    for (uint32_t q = tid; q < (uint32_t)A.G * N / 4u + 1u; q += THREADS)
+        gap_smem4[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (tid == 0) s_tile[0] = atomicAdd(A.next, 1ull);
+    for (int par = 0;; par ^= 1) {
+        __syncthreads();  // the previous tile's shared state is no longer read; s_tile[par] is set
+        const int64_t tile = (int64_t)s_tile[par];
+        if (tile >= n_tiles) break;
         if (tid == 0) {
-            s_tile = atomicAdd(A.next, 1ull);
+            s_tile[par ^ 1] = atomicAdd(A.next, 1ull);  // the next tile, claimed a tile ahead
             fcount = 0;
         }
-        __syncthreads();
-        const int64_t tile = (int64_t)s_tile;
-        if (tile >= n_tiles) break;
         const int64_t g0 = tile * A.G;
         const int Gt = (int)min((long long)A.G, (long long)(A.n_sets - g0));
-        if (tid <= Gt) sip[tid] = A.indptr[g0 + tid];
-        for (uint32_t q = tid; q < (uint32_t)Gt * N / 4u + 1u; q += kGapThreads)
-            gap_smem4[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        __syncthreads();
-        if (tid < Gt) {
-            // T = p c / n with c = ln(cmul n) >= 1: entries miss it with probability ~e^-c
-            const long long n = sip[tid + 1] - sip[tid];
-            uint32_t T = 0;
-            if (n > 0) {
-                const float nf = (float)n;
-                const float c = fmaxf(1.0f, __logf(A.cmul * nf));
-                const float Tf = (float)p * (c / nf);
-                T = Tf >= (float)p ? p : max(1u, (uint32_t)Tf);
+        if (tid <= Gt) {
+            const long long i0 = A.indptr[g0 + tid];
+            sip[tid] = i0;
+            if (tid < Gt) {
+                // T = p c / n with c = ln(cmul n) >= 1: entries miss it with probability ~e^-c
+                const long long n = A.indptr[g0 + tid + 1] - i0;
+                uint32_t T = 0;
+                if (n > 0) {
+                    const float nf = (float)n;
+                    const float c = fmaxf(1.0f, __logf(A.cmul * nf));
+                    const float Tf = (float)p * (c / nf);
+                    T = Tf >= (float)p ? p : max(1u, (uint32_t)Tf);
+                }
+                sT[tid] = T;
             }
-            sT[tid] = T;
         }
         __syncthreads();
         const int64_t fbeg = sip[0], fend = sip[Gt];
-        for (int64_t f = fbeg + tid; f < fend; f += kGapThreads) {
+        for (int64_t f = fbeg + tid; f < fend; f += THREADS) {
             int lo = 0, hi = Gt;  // the set holding feature f: largest s with sip[s] <= f
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
@@ -234,32 +248,37 @@ __global__ void __launch_bounds__(kGapThreads) sign_gap_kernel(GapArgs A) {
             for (int s = 0; s < Gt; ++s) {
                 const uint32_t T = sT[s];
                 OutT* row = out + (int64_t)s * N;
-                const uint4* hrow = gap_smem4 + (uint32_t)s * nq;
+                uint4* hrow = gap_smem4 + (uint32_t)s * nq;
                 if (REG_INV) {
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
-                        const uint32_t q = tid + r * kGapThreads;
+                        const uint32_t q = tid + r * THREADS;
                         if (q < nq) {
                             const uint4 h4 = hrow[q];
+                            hrow[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
                             const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
-                            uint32_t x[4];
+                            uint32_t x[4], ovf = 0;
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 x[k] = gap_invert(rinv[r * 4 + k], hs[k], p);
                                 if (hs[k] >= T) {
                                     const unsigned slot = atomicAdd(&fcount, 1u);
                                     if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
+                                    else ovf |= 1u << k;  // list full: redone in place, after the row store
                                 }
                             }
                             gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
+                            for (int k = 0; ovf && k < 4; ++k)
+                                if (ovf >> k & 1u) fallback_entry<OutT>(A, sip[s], sip[s + 1], q * 4u + k, row);
                         }
                     }
                 } else {
                     const uint4* inv4 = reinterpret_cast<const uint4*>(A.inv);
-                    for (uint32_t q = tid; q < nq; q += kGapThreads) {
+                    for (uint32_t q = tid; q < nq; q += THREADS) {
                         const uint4 h4 = hrow[q];
+                        hrow[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
                         const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
-                        uint32_t x[4];
+                        uint32_t x[4], ovf = 0;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const uint4 tv = __ldg(inv4 + q * 4u + k);
@@ -269,38 +288,34 @@ __global__ void __launch_bounds__(kGapThreads) sign_gap_kernel(GapArgs A) {
                             if (hs[k] >= T) {
                                 const unsigned slot = atomicAdd(&fcount, 1u);
                                 if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
+                                    else ovf |= 1u << k;  // list full: redone in place, after the row store
                             }
                         }
                         gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
+                        for (int k = 0; ovf && k < 4; ++k)
+                            if (ovf >> k & 1u) fallback_entry<OutT>(A, sip[s], sip[s + 1], q * 4u + k, row);
                     }
                 }
             }
         } else {
             const uint32_t ents = (uint32_t)Gt * N;
-            for (uint32_t e = tid; e < ents; e += kGapThreads) {
+            for (uint32_t e = tid; e < ents; e += THREADS) {
                 const uint32_t s = e / N, i = e - s * N;
                 const uint32_t h = best[e];
+                best[e] = 0xFFFFFFFFu;
                 out[e] = (OutT)gap_invert(A.inv[i], h, p);
                 if (h >= sT[s]) {
                     const unsigned slot = atomicAdd(&fcount, 1u);
                     if (slot < kGapFailCap) flist[slot] = e;
+                    else fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
                 }
             }
         }
         __syncthreads();
-        const unsigned nf = fcount;
-        if (nf <= kGapFailCap) {
-            for (unsigned k = tid; k < nf; k += kGapThreads) {
-                const uint32_t e = flist[k], s = e / N, i = e - s * N;
-                fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
-            }
-        } else {
-            // list overflow (thresholds far too low for this tile): every failing entry, in place
-            const uint32_t ents = (uint32_t)Gt * N;
-            for (uint32_t e = tid; e < ents; e += kGapThreads) {
-                const uint32_t s = e / N, i = e - s * N;
-                if (best[e] >= sT[s]) fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
-            }
+        const unsigned nf = min(fcount, (unsigned)kGapFailCap);
+        for (unsigned k = tid; k < nf; k += THREADS) {
+            const uint32_t e = flist[k], s = e / N, i = e - s * N;
+            fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
         }
     }
     if (bad_id && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
@@ -314,17 +329,20 @@ int gap_sets_per_tile(int32_t n_hash) {
 }
 
 // Sets per tile for a batch: the tile's features are dealt to the CTA's threads in
-// rounds, so pick the count whose expected features (plus 1.5 sigma, Poisson-like) waste
+// rounds, so pick the count whose expected features (plus one sigma, Poisson-like) waste
 // the least of the last round.
-static int gap_pick_sets(int32_t n_hash, int64_t n_sets, int64_t nnz) {
+static int gap_pick_sets(int32_t n_hash, int64_t n_sets, int64_t nnz, int threads) {
     const int gmax = gap_sets_per_tile(n_hash);
     const double mean = std::max(1.0, (double)nnz / (double)std::max<int64_t>(n_sets, 1));
-    int best = gmax;
+    int best = 1;
     double best_eff = 0.0;
-    for (int g = std::max(1, gmax / 2); g <= gmax; ++g) {
-        const double f = g * mean, hi = f + 1.5 * std::sqrt(f);
-        const double eff = f / (kGapThreads * std::ceil(hi / kGapThreads));
-        if (eff > best_eff + 1e-9) {
+    // four resident CTAs (~54 KB of minima and tables each) hide one another's barriers
+    const int g4 = std::max<int>(1, std::min<int64_t>(gmax, (int64_t)(50 * 1024) / ((int64_t)n_hash * 4)));
+    for (int g = 1; g <= g4; ++g) {
+        if (g * mean < 0.9 * threads && g < g4) continue;  // at least about one round
+        const double f = g * mean, hi = f + 1.0 * std::sqrt(f);
+        const double eff = f / (threads * std::ceil(hi / threads));
+        if (eff > best_eff - 1e-9) {  // ties go to the larger tile (fewer claims and barriers per set)
             best_eff = eff;
             best = g;
         }
@@ -363,30 +381,45 @@ int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const Dev
     A.a = (uint32_t)(S.ia % S.p);
     A.ap = shoup_companion(A.a, S.p);
     A.n_hash = S.n_hash;
-    A.G = gap_pick_sets(S.n_hash, S.n_sets, nnz);
-    if (const char* ge = std::getenv("MHB_GAP_SETS")) A.G = std::max(1, std::min(std::atoi(ge), gap_sets_per_tile(S.n_hash)));
     const char* ce = std::getenv("MHB_GAP_CMUL");
-    A.cmul = ce ? (float)std::atof(ce) : 0.73f;
+    A.cmul = ce ? (float)std::atof(ce) : 1.0f;
+    A.one = 1u;
     A.tab = S.tab;
     A.inv = S.inv;
     A.next = &S.sched->next;
     A.status = S.status;
     A.out = S.out;
+    int threads = kGapThreads;
+    if (const char* te = std::getenv("MHB_GAP_THREADS")) threads = std::atoi(te);
+    if (threads != 64 && threads != 128 && threads != 512) threads = 256;
+    A.G = gap_pick_sets(S.n_hash, S.n_sets, nnz, threads);
+    if (const char* ge = std::getenv("MHB_GAP_SETS")) A.G = std::max(1, std::min(std::atoi(ge), gap_sets_per_tile(S.n_hash)));
     const size_t smem = (size_t)A.G * S.n_hash * 4 + 16;
-    const bool reg_inv = (S.n_hash & 3) == 0 && S.n_hash <= 8 * kGapThreads;
-    auto fn = out_dtype == MHB_OUT_I64
-                  ? (reg_inv ? sign_gap_kernel<long long, true> : sign_gap_kernel<long long, false>)
-                  : (reg_inv ? sign_gap_kernel<uint32_t, true> : sign_gap_kernel<uint32_t, false>);
+    const bool reg_inv = threads >= 256 && (S.n_hash & 3) == 0 && S.n_hash <= 8 * 256;
+    using Fn = void (*)(GapArgs);
+    Fn fn;
+    if (out_dtype == MHB_OUT_I64)
+        fn = threads == 64    ? (Fn)sign_gap_kernel<long long, false, 64>
+             : threads == 128 ? (Fn)sign_gap_kernel<long long, false, 128>
+             : threads == 512 ? (reg_inv ? (Fn)sign_gap_kernel<long long, true, 512> : (Fn)sign_gap_kernel<long long, false, 512>)
+             : reg_inv        ? (Fn)sign_gap_kernel<long long, true, 256>
+                              : (Fn)sign_gap_kernel<long long, false, 256>;
+    else
+        fn = threads == 64    ? (Fn)sign_gap_kernel<uint32_t, false, 64>
+             : threads == 128 ? (Fn)sign_gap_kernel<uint32_t, false, 128>
+             : threads == 512 ? (reg_inv ? (Fn)sign_gap_kernel<uint32_t, true, 512> : (Fn)sign_gap_kernel<uint32_t, false, 512>)
+             : reg_inv        ? (Fn)sign_gap_kernel<uint32_t, true, 256>
+                              : (Fn)sign_gap_kernel<uint32_t, false, 256>;
     int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "gap kernel shared memory");
     if (rc) return rc;
     int occ = 0;
-    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kGapThreads, smem), "gap occupancy");
+    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem), "gap occupancy");
     if (rc) return rc;
     if (occ < 1) return set_error(MHB_ERR_INVALID, "gap kernel does not fit an SM (n_hash %d)", S.n_hash);
     const int64_t tiles = (S.n_sets + A.G - 1) / A.G;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ * dev.sms));
-    fn<<<(unsigned)blocks, kGapThreads, smem, st>>>(A);
+    fn<<<(unsigned)blocks, threads, smem, st>>>(A);
     return cuda_check(cudaGetLastError(), "sign_gap_kernel launch");
 }
 

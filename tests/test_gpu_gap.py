@@ -78,7 +78,7 @@ def test_gap_small_prime_thresholds_of_one(cuda_device):
     p = 101
     sizes = rng.choice([1, 5, 40, 700, 3000], size=N_SETS, p=[.2, .3, .3, .15, .05])
     indptr, ids = _batch(rng, p, sizes)
-    fam = make_family("iterative", 11, 60, p)
+    fam = make_family("iterative", 11, 40, p)
     _check(cuda_device, indptr, ids, fam, "uint32", np.arange(0, N_SETS, 7))
 
 
