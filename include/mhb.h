@@ -83,6 +83,16 @@ const char* mhb_last_error(void);
  * serves every smaller one. */
 size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash);
 
+/* Which kernel mhb_sign_iterative_csr runs for this batch shape (a report for benchmarks
+ * and profiles; results are identical either way):
+ *   0  visiting kernel: every (feature, hash) pair, 2.5 instructions per visit
+ *      (sign_kernel / sign_small_batch_kernel, csrc/sign.cu);
+ *   1  enumerating kernel: per feature only the hashes under the set's threshold, found
+ *      through the three-gap structure of the iterative family's arithmetic progression
+ *      (sign_gap_kernel, csrc/gap.cu; kernels.py:62-72 is the progression it exploits).
+ * The choice is a cost model over (n_hash, mean set size); MHB_GAP=0/1 forces it. */
+int32_t mhb_sign_iterative_path(int64_t n_sets, int64_t nnz, uint64_t prime, int32_t n_hash);
+
 /*
  * Iterative family signatures (replaces kernels.sign_iterative, kernels.py:44-73,
  * for a whole CSR batch).  a, b are the family base parameters
@@ -110,7 +120,9 @@ int mhb_sign_random_csr(const int64_t* indptr, const uint32_t* ids,
  * Iterative signatures with the LSH band keys of mhb_band_keys computed in the
  * signing epilogue (no re-read of the signature matrix).  keys: device uint64
  * [n_sets * n_hash/rows_per_band].  write_signatures = 0 skips storing the
- * signatures (out is still required: long sets use their rows as merge scratch).
+ * signatures (out is still required, all n_sets * n_hash entries: long sets use their
+ * rows as merge scratch, and batches signed by the enumerating kernel -- see
+ * mhb_sign_iterative_path -- store the rows and hash the keys from them).
  * Needs the K = 32/64 lane geometry (n_hash >= 32), rows_per_band a multiple of 4
  * dividing both K and n_hash, and prime < 2^31; else MHB_ERR_UNSUPPORTED.
  */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "mhb_version": (C.c_char_p, []),
     "mhb_last_error": (C.c_char_p, []),
     "mhb_sign_workspace_bytes": (_SZ, [_I64, _I64, _I32]),
+    "mhb_sign_iterative_path": (_I32, [_I64, _I64, _U64, _I32]),
     "mhb_sign_iterative_csr": (C.c_int, [_P, _P, _I64, _I64, _U64, _U64, _U64, _I32, _P, _I32, _P, _P, _SZ, _P]),
     "mhb_sign_random_csr": (C.c_int, [_P, _P, _I64, _I64, _P, _P, _U64, _I32, _P, _I32, _P, _P, _SZ, _P]),
     "mhb_sign_iterative_csr_bands": (C.c_int, [_P, _P, _I64, _I64, _U64, _U64, _U64, _I32, _I32, _P, _P, _I32,

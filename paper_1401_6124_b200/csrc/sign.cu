@@ -2074,6 +2074,11 @@ extern "C" int mhb_profile_end(float* total_ms, int32_t* n_launches) {
     return MHB_OK;
 }
 
+extern "C" int32_t mhb_sign_iterative_path(int64_t n_sets, int64_t nnz, uint64_t prime, int32_t n_hash) {
+    const bool small_plan = n_sets > 0 && n_sets <= mhb::kSmallPlan;
+    return !small_plan && mhb::gap_preferred(mhb::KIND_ITERATIVE, prime, n_hash, n_sets, nnz) ? 1 : 0;
+}
+
 extern "C" size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash) {
     if (n_hash < 1) n_hash = 1;
     return mhb::workspace_layout(n_sets, nnz, n_hash).total;
@@ -2105,6 +2110,15 @@ extern "C" int mhb_sign_iterative_csr_bands(const int64_t* indptr, const uint32_
         return set_error(MHB_ERR_UNSUPPORTED,
                          "fused band keys need 32 <= n_hash, rows_per_band dividing %d and prime < 2^31; "
                          "use mhb_sign_iterative_csr + mhb_band_keys", geo.K);
+    if (n_sets > kSmallPlan && gap_preferred(KIND_ITERATIVE, prime, n_hash, n_sets, nnz)) {
+        // where the enumerating kernel (gap.cu) is the faster signer, signatures first and
+        // the keys from the stored rows (cfg4: 18.9 + 2.8 ms against 31.8 ms fused into
+        // the visiting kernel); the keys are the same function of the signatures either way
+        int rc = launch_sign(KIND_ITERATIVE, indptr, ids, n_sets, nnz, a, b, nullptr, nullptr, prime, n_hash, out,
+                             out_dtype, status, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+        if (rc) return rc;
+        return mhb_band_keys(out, out_dtype, n_sets, n_hash, rows_per_band, keys, stream);
+    }
     return launch_sign(KIND_ITERATIVE, indptr, ids, n_sets, nnz, a, b, nullptr, nullptr, prime, n_hash, out,
                        out_dtype, status, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), keys,
                        rows_per_band, write_signatures ? 1 : 0);

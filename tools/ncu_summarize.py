@@ -19,7 +19,7 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-STEP = ("plan_count", "plan_scan", "plan_scatter", "plan_small", "sign_kernel", "finalize_kernel")
+STEP = ("plan_count", "plan_scan", "plan_scatter", "plan_small", "sign_kernel", "sign_gap_kernel", "finalize_kernel")
 
 
 def _is_step(name):
