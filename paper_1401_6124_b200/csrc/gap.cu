@@ -170,6 +170,21 @@ __device__ __forceinline__ void fallback_entry(const GapArgs& A, int64_t f0, int
     row[i] = (OutT)gap_invert(A.inv[i], h, p);
 }
 
+// The entries of one lane quad whose minimum stayed at or above the threshold: one
+// counter bump per thread, then the list (or, the list full, the fallback in place).
+template <typename OutT>
+__device__ __forceinline__ void push_failures(const GapArgs& A, uint32_t mask, uint32_t e0, uint32_t i0, OutT* row,
+                                              int64_t f0, int64_t f1, unsigned* fcount, uint32_t* flist) {
+    unsigned slot = atomicAdd(fcount, (unsigned)__popc(mask));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (mask >> k & 1u) {
+            if (slot < kGapFailCap) flist[slot] = e0 + k;
+            else fallback_entry<OutT>(A, f0, f1, i0 + k, row);
+            ++slot;
+        }
+}
+
 // REG_INV: n_hash is a multiple of 4 up to 2048, and this thread's (at most two) lane quads'
 // argmin-recovery constants stay in registers for the whole launch.
 template <typename OutT, bool REG_INV, int THREADS>
@@ -257,19 +272,16 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                             const uint4 h4 = hrow[q];
                             hrow[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
                             const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
-                            uint32_t x[4], ovf = 0;
+                            uint32_t x[4];
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                x[k] = gap_invert(rinv[r * 4 + k], hs[k], p);
-                                if (hs[k] >= T) {
-                                    const unsigned slot = atomicAdd(&fcount, 1u);
-                                    if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
-                                    else ovf |= 1u << k;  // list full: redone in place, after the row store
-                                }
-                            }
+                            for (int k = 0; k < 4; ++k) x[k] = gap_invert(rinv[r * 4 + k], hs[k], p);
                             gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
-                            for (int k = 0; ovf && k < 4; ++k)
-                                if (ovf >> k & 1u) fallback_entry<OutT>(A, sip[s], sip[s + 1], q * 4u + k, row);
+                            if (max(max(hs[0], hs[1]), max(hs[2], hs[3])) >= T) {
+                                const uint32_t mask = (hs[0] >= T ? 1u : 0u) | (hs[1] >= T ? 2u : 0u) |
+                                                      (hs[2] >= T ? 4u : 0u) | (hs[3] >= T ? 8u : 0u);
+                                push_failures<OutT>(A, mask, (uint32_t)s * N + q * 4u, q * 4u, row, sip[s], sip[s + 1],
+                                                    &fcount, flist);
+                            }
                         }
                     }
                 } else {
@@ -278,22 +290,21 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                         const uint4 h4 = hrow[q];
                         hrow[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
                         const uint32_t hs[4] = {h4.x, h4.y, h4.z, h4.w};
-                        uint32_t x[4], ovf = 0;
+                        uint32_t x[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const uint4 tv = __ldg(inv4 + q * 4u + k);
                             InvTab it;
                             it.B = tv.x; it.inv = tv.y; it.invp = tv.z; it.pad = tv.w;
                             x[k] = gap_invert(it, hs[k], p);
-                            if (hs[k] >= T) {
-                                const unsigned slot = atomicAdd(&fcount, 1u);
-                                if (slot < kGapFailCap) flist[slot] = (uint32_t)s * N + q * 4u + k;
-                                    else ovf |= 1u << k;  // list full: redone in place, after the row store
-                            }
                         }
                         gap_store4(row + q * 4u, x[0], x[1], x[2], x[3]);
-                        for (int k = 0; ovf && k < 4; ++k)
-                            if (ovf >> k & 1u) fallback_entry<OutT>(A, sip[s], sip[s + 1], q * 4u + k, row);
+                        if (max(max(hs[0], hs[1]), max(hs[2], hs[3])) >= T) {
+                            const uint32_t mask = (hs[0] >= T ? 1u : 0u) | (hs[1] >= T ? 2u : 0u) |
+                                                  (hs[2] >= T ? 4u : 0u) | (hs[3] >= T ? 8u : 0u);
+                            push_failures<OutT>(A, mask, (uint32_t)s * N + q * 4u, q * 4u, row, sip[s], sip[s + 1],
+                                                &fcount, flist);
+                        }
                     }
                 }
             }

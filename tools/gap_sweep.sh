@@ -1,2 +1,3 @@
-for a in "cfg4 400000" "cfg4 2000000" "cfg3 400000"; do timeout 300 python tools/gap_check.py $a 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['config'], d['n_sets'], d['ms_visit'], d['ms_gap'], d['equal'], d['oracle_rows_equal'])"; done
-for c in 0.4 0.55 1.0 1.5; do echo -n "cmul $c: "; MHB_GAP_CMUL=$c timeout 300 python tools/gap_check.py cfg4 400000 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['config'], d['n_sets'], d['ms_visit'], d['ms_gap'], d['equal'], d['oracle_rows_equal'])"; done
+python -m pytest tests/test_gpu_gap.py -x -q 2>&1 | tail -2
+run() { timeout 300 python tools/gap_check.py $1 $2 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['config'], d['n_sets'], d['ms_visit'], d['ms_gap'], d['equal'], d['oracle_rows_equal'])"; }
+run cfg4 400000; run cfg4 2000000; run cfg3 400000
