@@ -171,16 +171,23 @@ __device__ __forceinline__ void fallback_entry(const GapArgs& A, int64_t f0, int
 }
 
 // The entries of one lane quad whose minimum stayed at or above the threshold: one
-// counter bump per thread, then the list (or, the list full, the fallback in place).
-template <typename OutT>
-__device__ __forceinline__ void push_failures(const GapArgs& A, uint32_t mask, uint32_t e0, uint32_t i0, OutT* row,
-                                              int64_t f0, int64_t f1, unsigned* fcount, uint32_t* flist) {
-    unsigned slot = atomicAdd(fcount, (unsigned)__popc(mask));
+// counter bump per thread, then the list; the list full, the entry's (already reset)
+// minimum is marked instead and the tile makes one more pass over its minima.
+constexpr uint32_t kGapRedo = 0xFFFFFFFEu;
+__device__ __forceinline__ void push_failures(uint32_t mask, uint32_t e0, uint32_t* best, unsigned* fcount,
+                                              uint32_t* flist) {
+    // PTX atom: the C++ atomicAdd here compiles to a warp-wide scan (five shuffles) that
+    // every warp with one failing lane would run
+    unsigned slot;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                 : "=r"(slot)
+                 : "r"((uint32_t)__cvta_generic_to_shared(fcount)), "r"((unsigned)__popc(mask))
+                 : "memory");
 #pragma unroll
     for (int k = 0; k < 4; ++k)
         if (mask >> k & 1u) {
             if (slot < kGapFailCap) flist[slot] = e0 + k;
-            else fallback_entry<OutT>(A, f0, f1, i0 + k, row);
+            else best[e0 + k] = kGapRedo;
             ++slot;
         }
 }
@@ -279,8 +286,7 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                             if (max(max(hs[0], hs[1]), max(hs[2], hs[3])) >= T) {
                                 const uint32_t mask = (hs[0] >= T ? 1u : 0u) | (hs[1] >= T ? 2u : 0u) |
                                                       (hs[2] >= T ? 4u : 0u) | (hs[3] >= T ? 8u : 0u);
-                                push_failures<OutT>(A, mask, (uint32_t)s * N + q * 4u, q * 4u, row, sip[s], sip[s + 1],
-                                                    &fcount, flist);
+                                push_failures(mask, (uint32_t)s * N + q * 4u, best, &fcount, flist);
                             }
                         }
                     }
@@ -302,8 +308,7 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                         if (max(max(hs[0], hs[1]), max(hs[2], hs[3])) >= T) {
                             const uint32_t mask = (hs[0] >= T ? 1u : 0u) | (hs[1] >= T ? 2u : 0u) |
                                                   (hs[2] >= T ? 4u : 0u) | (hs[3] >= T ? 8u : 0u);
-                            push_failures<OutT>(A, mask, (uint32_t)s * N + q * 4u, q * 4u, row, sip[s], sip[s + 1],
-                                                &fcount, flist);
+                            push_failures(mask, (uint32_t)s * N + q * 4u, best, &fcount, flist);
                         }
                     }
                 }
@@ -318,15 +323,25 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                 if (h >= sT[s]) {
                     const unsigned slot = atomicAdd(&fcount, 1u);
                     if (slot < kGapFailCap) flist[slot] = e;
-                    else fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
+                    else best[e] = kGapRedo;
                 }
             }
         }
         __syncthreads();
-        const unsigned nf = min(fcount, (unsigned)kGapFailCap);
+        const unsigned nfail = fcount;
+        const unsigned nf = min(nfail, (unsigned)kGapFailCap);
         for (unsigned k = tid; k < nf; k += THREADS) {
             const uint32_t e = flist[k], s = e / N, i = e - s * N;
             fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
+        }
+        if (nfail > kGapFailCap) {  // list overflow: the marked minima, in place
+            const uint32_t ents = (uint32_t)Gt * N;
+            for (uint32_t e = tid; e < ents; e += THREADS)
+                if (best[e] == kGapRedo) {
+                    best[e] = 0xFFFFFFFFu;
+                    const uint32_t s = e / N, i = e - s * N;
+                    fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
+                }
         }
     }
     if (bad_id && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);

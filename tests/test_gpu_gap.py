@@ -124,6 +124,19 @@ def test_gap_matches_visiting_kernel_everywhere(cuda_device, monkeypatch):
     assert torch.equal(got.view(torch.int32), want.view(torch.int32))
 
 
+def test_gap_fallback_list_overflow(cuda_device, monkeypatch):
+    """A threshold scale of 1e-4 drops c to its floor of 1: ~37% of the entries stay above
+    the threshold, far more than the tile's fallback list holds, so the marked-minima
+    pass redoes them in place."""
+    monkeypatch.setenv("MHB_GAP_CMUL", "0.0001")
+    rng = np.random.default_rng(21)
+    p = 67_108_879
+    indptr, ids = _batch(rng, p, rng.choice([40, 80, 120], size=N_SETS))
+    for n_hash, dt in ((2048, "uint32"), (250, "int64")):
+        fam = make_family("iterative", 77, n_hash, p)
+        _check(cuda_device, indptr, ids, fam, dt, np.arange(0, N_SETS, 41))
+
+
 def test_gap_status_flags(cuda_device):
     import torch
 
