@@ -32,6 +32,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.h"
 #include "modarith.cuh"
@@ -99,30 +102,32 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
         for (;;) {
             const uint32_t mn = min(u, w);
             if (mn == 0 || L - mn < T || t >= N) break;
-            const uint32_t room = L - T;  // >= mn
-            if (u >= w) {
-                const uint32_t j = min(u, room) / w;
-                const uint32_t L2 = L - j * w;
-                u -= j * w;
-                n += j * m;
-                if (v >= L2) {
-                    const uint32_t s = (v - L2) / w + 1;
-                    v -= s * w;
-                    t += s * m;
-                }
-                L = L2;
-            } else {
-                const uint32_t j = min(w, room) / u;
-                const uint32_t L2 = L - j * u;
-                if (v >= L2) {
-                    const uint32_t i = (L - 1 - v) / u;
-                    v -= w - i * u;
-                    t += m + i * n;
-                }
-                w -= j * u;
-                m += j * n;
-                L = L2;
+            // One level, both cases in one instruction stream (a warp's lanes differ in
+            // which return is the larger): the larger return `big` (time tb) loses j
+            // copies of the smaller `mn` (time ts), and so does L.
+            const bool up_big = u >= w;  // reduce u by w, else w by u
+            const uint32_t big = up_big ? u : w, tb = up_big ? n : m, ts = up_big ? m : n;
+            const uint32_t j = min(big, L - T) / mn;
+            const uint32_t L2 = L - j * mn;
+            // the entry point, if it lies in the part cut off [L2, L): up_big: s = q + 1
+            // downward steps of w; else the one downward step of the level it sits in,
+            // w - q u (time m + q n)
+            const uint32_t q = (up_big ? v - L2 : L - 1u - v) / mn;
+            const uint32_t dv = up_big ? (q + 1u) * mn : big - q * mn;
+            const uint32_t dt = up_big ? (q + 1u) * ts : tb + q * ts;
+            if (v >= L2) {
+                v -= dv;
+                t += dt;
             }
+            const uint32_t big2 = big - j * mn, tb2 = tb + j * ts;
+            if (up_big) {
+                u = big2;
+                n = tb2;
+            } else {
+                w = big2;
+                m = tb2;
+            }
+            L = L2;
         }
         if (t >= N) return;
         if (v >= T) {  // the level's interval is [0, L) with T <= L: one more return step
@@ -436,12 +441,27 @@ int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const Dev
              : threads == 512 ? (reg_inv ? (Fn)sign_gap_kernel<uint32_t, true, 512> : (Fn)sign_gap_kernel<uint32_t, false, 512>)
              : reg_inv        ? (Fn)sign_gap_kernel<uint32_t, true, 256>
                               : (Fn)sign_gap_kernel<uint32_t, false, 256>;
-    int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "gap kernel shared memory");
-    if (rc) return rc;
+    // the attribute and the occupancy query once per (device, kernel, shared-memory size)
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, size_t>, int> occ_of;
     int occ = 0;
-    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem), "gap occupancy");
-    if (rc) return rc;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const auto key = std::make_tuple(dev.device, (const void*)fn, smem);
+        const auto it = occ_of.find(key);
+        if (it != occ_of.end()) {
+            occ = it->second;
+        } else {
+            // the limit is per kernel, not per launch: always the largest tile
+            int rc = cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)(kGapBestBytes + 16)),
+                                "gap kernel shared memory");
+            if (rc) return rc;
+            rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem), "gap occupancy");
+            if (rc) return rc;
+            occ_of[key] = occ;
+        }
+    }
     if (occ < 1) return set_error(MHB_ERR_INVALID, "gap kernel does not fit an SM (n_hash %d)", S.n_hash);
     const int64_t tiles = (S.n_sets + A.G - 1) / A.G;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)occ * dev.sms));
