@@ -128,16 +128,40 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "power_w_max": max(power) if power else None}
 
 
-def _ncu_traffic(config: str, family: str):
-    """Per-launch DRAM bytes of the main kernel from the committed ncu --set full summary."""
+def _ncu_entry(config: str, family: str):
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
-        return None, None
-    d = json.loads(p.read_text())
-    ent = d.get(f"{config}/{family}")
+        return None
+    return json.loads(p.read_text()).get(f"{config}/{family}")
+
+
+def _ncu_traffic(config: str, family: str):
+    """Per-launch DRAM bytes of the main kernel from the committed ncu --set full summary."""
+    ent = _ncu_entry(config, family)
     if not ent:
         return None, None
     return ent.get("dram_bytes_per_launch"), ent.get("source")
+
+
+def _ncu_issue(config: str, family: str):
+    """Executed warp instructions and issue-slot use of the committed capture (static
+    evidence beside the live timing: what the kernel's own bound looks like)."""
+    ent = _ncu_entry(config, family)
+    if not ent:
+        return None
+    m = ent.get("metrics", {})
+
+    def num(suffix):
+        for k, v in m.items():
+            if k.endswith(suffix):
+                return float(str(v).split()[0].replace(",", ""))
+        return None
+
+    return {"kernel": ent.get("kernel"), "warp_instructions_per_launch": num("smsp__inst_executed.sum"),
+            "issue_slots_busy": num("smsp__issue_active.avg.per_cycle_active"),
+            "alu_pipe_pct": num("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "fma_pipe_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            "source": ent.get("source")}
 
 
 def cpu_baseline_run(indptr_h, ids_h, fam, budget_s: float, threads: int):
@@ -959,6 +983,7 @@ def _roofline(args, ctx, W, fam, kernel_ms, ms_per_step, clocks, stream):
                 "peak_gbs": hbm_gbs, "frac": alg_bytes / (kernel_ms / 1e3) / 1e9 / hbm_gbs,
                 "traffic_source": traffic_src},
         "path": path,
+        "ncu": (_ncu_issue(args.config, args.family) if args.n_sets is None and ctx.world == 1 else None),
     }
 
 
