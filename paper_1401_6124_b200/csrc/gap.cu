@@ -23,12 +23,17 @@
 // Exactness.  Every recorded value is a true hash value, and every h_i(x) < T is recorded;
 // so an entry whose minimum ends below T is the exact minimum.  The others (probability
 // ~e^-c each) are recomputed from all the set's features (fallback list, a thread per
-// entry).  c = ln(n) balances the two costs (ln(0.4 n) .. ln(1.5 n) swept on cfg4).  The argmin id is recovered from the
-// minimum hash as in sign_kernel: x = (h - B_i) A_i^-1 mod p.
+// entry).  c = ln(n) balances the two costs (ln(0.4 n) .. ln(1.5 n) swept on cfg4).  The
+// argmin id is recovered from the minimum hash as in sign_kernel: x = (h - B_i) A_i^-1
+// mod p.  The threshold decides cost only, never the result: a set of n copies of one id
+// sends nearly every lane to the fallback (about 3x the visiting kernel's time for that
+// set) and is still signed exactly.
 //
 // Work per tile of G consecutive sets (one CTA, G N minima in shared memory): thread k
 // takes features k, k + 256, ... of the tile's contiguous id range; then the CTA inverts
-// and stores the G rows with 16-byte stores.
+// and stores the G rows with 16-byte stores, resets the minima it read and lists the
+// entries for the fallback.  tests/test_gap_enumeration.py restates the descent in Python
+// against brute force; tests/test_gpu_gap.py and tools/stress_gap.py pin the kernel.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
