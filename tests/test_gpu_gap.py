@@ -109,6 +109,21 @@ def test_gap_constant_orbit_and_extremes(cuda_device):
     _check(cuda_device, indptr, ids, fam, "int64", sel)
 
 
+def test_gap_sets_of_one_repeated_id(cuda_device):
+    """Sets of thousands of copies of one id: the threshold (sized for n distinct features)
+    is far too low, nearly every lane goes to the fallback, the result is still exact."""
+    rng = np.random.default_rng(13)
+    p = 67_108_879
+    fam = make_family("iterative", 9, 512, p)
+    rows = [rng.integers(0, p, 70).astype(np.int64) for _ in range(N_SETS)]
+    for s in (5, 4000, 16_499):
+        rows[s] = np.full(6000, int(rng.integers(0, p)), dtype=np.int64)
+    rows[77] = np.concatenate([np.full(3000, 12345), np.full(3000, 54321)]).astype(np.int64)
+    indptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    sel = np.unique(np.concatenate([np.arange(0, 120), np.arange(3990, 4010), np.arange(16_490, 16_500)]))
+    _check(cuda_device, indptr, np.concatenate(rows), fam, "uint32", sel)
+
+
 def test_gap_matches_visiting_kernel_everywhere(cuda_device, monkeypatch):
     """The whole matrix of a cfg4-shaped batch equals the visiting kernel's, entry by entry."""
     import torch
