@@ -386,6 +386,11 @@ static int gap_pick_sets(int32_t n_hash, int64_t n_sets, int64_t nnz, int thread
     return best;
 }
 
+int64_t gap_full_wave_sets(int32_t n_hash, int64_t n_sets, int64_t nnz) {
+    if (gap_sets_per_tile(n_hash) < 1 || n_sets < 1) return INT64_MAX;
+    return (int64_t)4 * 148 * gap_pick_sets(n_hash, n_sets, nnz, kGapThreads);
+}
+
 // The enumeration pays when a feature's N visits cost more than its descent plus its
 // ~N c / n hits (11 instructions each) and the set's fallback entries.
 bool gap_supported(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz) {

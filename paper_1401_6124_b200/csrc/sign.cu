@@ -389,6 +389,16 @@ __global__ void plan_scatter_kernel(SignArgs A) {
 // group then holds sets of unequal sizes, so sign_small_batch_kernel runs the group's
 // largest part (a warp max).  Lane tables: every CTA fills a slice.
 constexpr int64_t kSmallPlan = kSmallPlanSets;
+// The enumerating kernel (gap.cu) where its cost model prefers it.  Batches that the
+// one-launch small-batch plan could take go to it only with a full wave of tiles (below
+// that the small-batch kernel's finer work items fill the SMs better: cfg4 shapes cross
+// over near 4,096 sets, cfg3 shapes near 12,000).
+static bool gap_wanted(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz) {
+    if (!gap_preferred(kind, prime, n_hash, n_sets, nnz)) return false;
+    if (n_sets > kSmallPlan) return true;
+    const char* e = std::getenv("MHB_GAP_MIN_SETS");
+    return n_sets >= (e ? std::atoll(e) : gap_full_wave_sets(n_hash, n_sets, nnz));
+}
 constexpr int kSmallTile = 256;  // sets per tile = threads per CTA
 
 // hist[] doubles as the look-back state: [0] ticket counter, [2 + 2k] / [3 + 2k] tile
@@ -1866,7 +1876,10 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     A.chunk = choose_chunk(n_sets, nnz, n_hash);
 
     // keys (fused band epilogue) have no small-batch instances: they keep the sorted plan
-    const bool small_plan = n_sets > 0 && n_sets <= kSmallPlan && keys == nullptr;
+    // the enumerating kernel (gap.cu) where its cost model prefers it (gap_wanted); the
+    // rest of the batches of <= kSmallPlan sets keep the one-launch small-batch plan
+    const bool gap = keys == nullptr && gap_wanted(kind, prime, n_hash, n_sets, nnz);
+    const bool small_plan = n_sets > 0 && n_sets <= kSmallPlan && keys == nullptr && !gap;
     // sched and hist are contiguous at the start of the workspace (zeroed: the sorted
     // plan's histogram, or the small plan's look-back state)
     rc = cuda_check(cudaMemsetAsync(ws, 0, wl.tab, st), "memset plan state");
@@ -1888,7 +1901,6 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
     const bool fpq = !keys && kind == KIND_RANDOM && prime <= (1ull << 23) && (geo.K == 16 || geo.K == 8);
     A.fpq = fpq ? 1 : 0;
 
-    const bool gap = !small_plan && keys == nullptr && gap_preferred(kind, prime, n_hash, n_sets, nnz);
     if (small_plan) {
         // tiles of sets, then CTAs for the lane tables (N may be 10^5)
         const int64_t lane_ctas = std::min<int64_t>((geo.n_tot + kSmallTile - 1) / kSmallTile, (int64_t)dev.sms * 4);
@@ -2075,8 +2087,7 @@ extern "C" int mhb_profile_end(float* total_ms, int32_t* n_launches) {
 }
 
 extern "C" int32_t mhb_sign_iterative_path(int64_t n_sets, int64_t nnz, uint64_t prime, int32_t n_hash) {
-    const bool small_plan = n_sets > 0 && n_sets <= mhb::kSmallPlan;
-    return !small_plan && mhb::gap_preferred(mhb::KIND_ITERATIVE, prime, n_hash, n_sets, nnz) ? 1 : 0;
+    return mhb::gap_wanted(mhb::KIND_ITERATIVE, prime, n_hash, n_sets, nnz) ? 1 : 0;
 }
 
 extern "C" size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash) {
@@ -2110,7 +2121,7 @@ extern "C" int mhb_sign_iterative_csr_bands(const int64_t* indptr, const uint32_
         return set_error(MHB_ERR_UNSUPPORTED,
                          "fused band keys need 32 <= n_hash, rows_per_band dividing %d and prime < 2^31; "
                          "use mhb_sign_iterative_csr + mhb_band_keys", geo.K);
-    if (n_sets > kSmallPlan && gap_preferred(KIND_ITERATIVE, prime, n_hash, n_sets, nnz)) {
+    if (gap_wanted(KIND_ITERATIVE, prime, n_hash, n_sets, nnz)) {
         // where the enumerating kernel (gap.cu) is the faster signer, signatures first and
         // the keys from the stored rows (cfg4: 18.9 + 2.8 ms against 31.8 ms fused into
         // the visiting kernel); the keys are the same function of the signatures either way

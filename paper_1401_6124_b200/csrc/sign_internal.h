@@ -111,6 +111,8 @@ int launch_sign(int kind, const int64_t* indptr, const uint32_t* ids, int64_t n_
 // and a zeroed Sched::next.
 struct DeviceInfo;
 bool gap_preferred(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz);
+// Sets that make one full wave of the enumerating kernel's tiles on a B200 (4 CTAs x 148 SMs).
+int64_t gap_full_wave_sets(int32_t n_hash, int64_t n_sets, int64_t nnz);
 int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const DeviceInfo& dev, cudaStream_t st);
 
 }  // namespace mhb

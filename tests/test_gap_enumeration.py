@@ -84,7 +84,7 @@ def test_enumeration_matches_brute_force(seed):
 
 def test_cost_model_choices_for_baseline_shapes(monkeypatch):
     """cfg4 and cfg3 (many lanes per feature) take the enumerating kernel; cfg2 / cfg5
-    (N = 256) and batches of <= 16,384 sets keep the visiting kernel; MHB_GAP forces."""
+    (N = 256) and small batches short of a full wave of tiles keep the visiting kernel; MHB_GAP forces."""
     monkeypatch.delenv("MHB_GAP", raising=False)
     lib = _lib.load()
 
@@ -98,10 +98,12 @@ def test_cost_model_choices_for_baseline_shapes(monkeypatch):
     assert path("cfg2", 1_000_000, 198) == 0
     assert path("cfg5", 12_500_000, 123) == 0
     assert path("cfg1", 10_000, 50) == 0
-    assert path("cfg4", 16_384, 80) == 0           # the small-batch plan
+    assert path("cfg4", 16_384, 80) == 1           # a full wave of tiles (592 x 6 sets) and more
+    assert path("cfg4", 3_000, 80) == 0            # under a wave: the small-batch plan
+    assert path("cfg3", 8_000, 300) == 0           # 24-set tiles: a wave is 14,208 sets
     monkeypatch.setenv("MHB_GAP", "0")
     assert path("cfg4", 2_000_000, 80) == 0
     monkeypatch.setenv("MHB_GAP", "1")
     assert path("cfg2", 1_000_000, 198) == 1
-    assert path("cfg4", 16_384, 80) == 0           # still the small-batch plan
+    assert path("cfg4", 3_000, 80) == 0            # still the small-batch plan
     assert lib.mhb_sign_iterative_path(100_000, 8_000_000, 2**31 + 11, 256) == 0   # wide primes: wide.cu

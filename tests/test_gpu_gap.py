@@ -152,6 +152,21 @@ def test_gap_fallback_list_overflow(cuda_device, monkeypatch):
         _check(cuda_device, indptr, ids, fam, dt, np.arange(0, N_SETS, 41))
 
 
+def test_gap_small_batches_with_a_full_wave(cuda_device, monkeypatch):
+    """Batches the small-batch plan could take go to the enumerating kernel once they make
+    a full wave of tiles (cfg4 shape: 3,552 sets); MHB_GAP_MIN_SETS moves the floor."""
+    rng = np.random.default_rng(17)
+    p = 67_108_879
+    fam = make_family("iterative", 31, 2048, p)
+    for n_sets, floor_sets in ((4000, None), (700, "1"), (37, "1")):
+        if floor_sets is None:
+            monkeypatch.delenv("MHB_GAP_MIN_SETS", raising=False)
+        else:
+            monkeypatch.setenv("MHB_GAP_MIN_SETS", floor_sets)
+        indptr, ids = _batch(rng, p, np.maximum(1, rng.poisson(80, size=n_sets)))
+        _check(cuda_device, indptr, ids, fam, "uint32", np.arange(0, n_sets, max(1, n_sets // 150)))
+
+
 def test_gap_status_flags(cuda_device):
     import torch
 
