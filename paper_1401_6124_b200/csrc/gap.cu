@@ -202,9 +202,12 @@ __device__ __forceinline__ void push_failures(uint32_t mask, uint32_t e0, uint32
         }
 }
 
-// REG_INV: n_hash is a multiple of 4 up to 2048, and this thread's (at most two) lane quads'
-// argmin-recovery constants stay in registers for the whole launch.
-template <typename OutT, bool REG_INV, int THREADS>
+// INV != 0: n_hash is a multiple of 4 up to 2048, and this thread's (at most two) lane quads'
+// argmin-recovery constants are in registers for the row pass: INV = 1 for the whole launch
+// (few sets per tile, cfg4: 17.9 against 18.7 ms), INV = 2 reloaded per tile just before the
+// barrier, which frees 24 registers in the feature phase (many sets per tile, cfg3: 3.50
+// against 3.70 ms).
+template <typename OutT, int INV, int THREADS>
 __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
     extern __shared__ uint4 gap_smem4[];
     __shared__ long long sip[kGapMaxSets + 1];
@@ -218,8 +221,17 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
     const uint32_t p = A.p, N = (uint32_t)A.n_hash;
     const int64_t n_tiles = (A.n_sets + A.G - 1) / A.G;
     bool bad_id = false;
+    constexpr bool REG_INV = INV != 0;
     InvTab rinv[REG_INV ? 8 : 1];
-    if (REG_INV) {
+    auto load_inv = [&]() {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t i = ((uint32_t)tid + (uint32_t)(k / 4) * THREADS) * 4u + (uint32_t)(k & 3);
+            const uint4 tv = __ldg(reinterpret_cast<const uint4*>(A.inv) + min(i, N - 1u));
+            rinv[k].B = tv.x; rinv[k].inv = tv.y; rinv[k].invp = tv.z; rinv[k].pad = tv.w;
+        }
+    };
+    if (INV == 1) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint32_t i = ((uint32_t)tid + (uint32_t)(k / 4) * THREADS) * 4u + (uint32_t)(k & 3);
@@ -272,6 +284,7 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
             }
             enumerate_feature(x, sT[lo], sbest + (uint32_t)lo * N * 4u, A);
         }
+        if (INV == 2) load_inv();  // lands during the barrier
         __syncthreads();
         // rows out: minima below T are exact; the rest go to the fallback list
         OutT* out = reinterpret_cast<OutT*>(A.out) + g0 * (int64_t)N;
@@ -438,19 +451,24 @@ int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const Dev
     const size_t smem = (size_t)A.G * S.n_hash * 4 + 16;
     const bool reg_inv = threads >= 256 && (S.n_hash & 3) == 0 && S.n_hash <= 8 * 256;
     using Fn = void (*)(GapArgs);
+    // lane constants per tile when a tile holds many sets (the reload amortises), for the launch else
+    int inv_mode = !reg_inv ? 0 : A.G >= 12 ? 2 : 1;
+    if (const char* ie = std::getenv("MHB_GAP_INV")) inv_mode = reg_inv ? std::max(0, std::min(std::atoi(ie), 2)) : 0;
     Fn fn;
     if (out_dtype == MHB_OUT_I64)
-        fn = threads == 64    ? (Fn)sign_gap_kernel<long long, false, 64>
-             : threads == 128 ? (Fn)sign_gap_kernel<long long, false, 128>
-             : threads == 512 ? (reg_inv ? (Fn)sign_gap_kernel<long long, true, 512> : (Fn)sign_gap_kernel<long long, false, 512>)
-             : reg_inv        ? (Fn)sign_gap_kernel<long long, true, 256>
-                              : (Fn)sign_gap_kernel<long long, false, 256>;
+        fn = threads == 64    ? (Fn)sign_gap_kernel<long long, 0, 64>
+             : threads == 128 ? (Fn)sign_gap_kernel<long long, 0, 128>
+             : threads == 512 ? (inv_mode ? (Fn)sign_gap_kernel<long long, 1, 512> : (Fn)sign_gap_kernel<long long, 0, 512>)
+             : inv_mode == 2  ? (Fn)sign_gap_kernel<long long, 2, 256>
+             : inv_mode == 1  ? (Fn)sign_gap_kernel<long long, 1, 256>
+                              : (Fn)sign_gap_kernel<long long, 0, 256>;
     else
-        fn = threads == 64    ? (Fn)sign_gap_kernel<uint32_t, false, 64>
-             : threads == 128 ? (Fn)sign_gap_kernel<uint32_t, false, 128>
-             : threads == 512 ? (reg_inv ? (Fn)sign_gap_kernel<uint32_t, true, 512> : (Fn)sign_gap_kernel<uint32_t, false, 512>)
-             : reg_inv        ? (Fn)sign_gap_kernel<uint32_t, true, 256>
-                              : (Fn)sign_gap_kernel<uint32_t, false, 256>;
+        fn = threads == 64    ? (Fn)sign_gap_kernel<uint32_t, 0, 64>
+             : threads == 128 ? (Fn)sign_gap_kernel<uint32_t, 0, 128>
+             : threads == 512 ? (inv_mode ? (Fn)sign_gap_kernel<uint32_t, 1, 512> : (Fn)sign_gap_kernel<uint32_t, 0, 512>)
+             : inv_mode == 2  ? (Fn)sign_gap_kernel<uint32_t, 2, 256>
+             : inv_mode == 1  ? (Fn)sign_gap_kernel<uint32_t, 1, 256>
+                              : (Fn)sign_gap_kernel<uint32_t, 0, 256>;
     // the attribute and the occupancy query once per (device, kernel, shared-memory size)
     static std::mutex mu;
     static std::map<std::tuple<int, const void*, size_t>, int> occ_of;
