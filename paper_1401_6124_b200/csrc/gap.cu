@@ -141,8 +141,8 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
             if (t >= N) return;
         }
     }
-    // return map of [0, T) as the level's two-branch map followed, when it lands in [T, L),
-    // by one more downward step (the third branch); steps in bytes of the minima row,
+    // return map of [0, T): the upward step when v < w, then the downward step unless that
+    // landed inside [0, T) (the third branch is both); steps in bytes of the minima row,
     // clipped to the row
     const uint32_t n4 = min(n, N) * 4u, m4 = min(m, N) * 4u;
     const uint32_t negw = 0u - w;
@@ -155,15 +155,16 @@ __device__ __forceinline__ void enumerate_feature(uint32_t x, uint32_t T, uint32
         reds_min(addr, v);
         asm volatile(
             "{\n\t"
-            ".reg .pred up, ov;\n\t"
+            // up: the upward step; stay: it landed inside [0, T).  Every other case (no
+            // upward step, or one that overshot T) takes the downward step, so the three
+            // branches are two predicated pairs.
+            ".reg .pred up, stay;\n\t"
             "setp.lt.u32 up, %0, %2;\n\t"
             "@up  mad.lo.u32 %0, %3, %8, %0;\n\t"
-            "@!up mad.lo.u32 %0, %4, %8, %0;\n\t"
             "@up  add.u32 %1, %1, %5;\n\t"
-            "@!up add.u32 %1, %1, %6;\n\t"
-            "setp.ge.u32 ov, %0, %7;\n\t"
-            "@ov  mad.lo.u32 %0, %4, %8, %0;\n\t"
-            "@ov  add.u32 %1, %1, %6;\n\t"
+            "setp.lt.and.u32 stay, %0, %7, up;\n\t"
+            "@!stay mad.lo.u32 %0, %4, %8, %0;\n\t"
+            "@!stay add.u32 %1, %1, %6;\n\t"
             "}"
             : "+r"(v), "+r"(addr)
             : "r"(w), "r"(u), "r"(negw), "r"(n4), "r"(m4), "r"(T), "r"(one));

@@ -4,8 +4,8 @@ brute force: for h_i = (h0 + i d) mod p (kernels.py:62-72: lane i of the iterati
 hashes x to h_0(x) + i (x + b)), list every i < N with h_i < T.
 
 The restatement follows the CUDA line by line (one level of the descent with both cases
-in one stream, the carried entry point, the two-branch return map plus the extra
-downward step), so a change to the kernel's arithmetic has a CPU counterpart to update.
+in one stream, the carried entry point, the return map as an upward step and a downward
+step under two predicates), so a change to the kernel's arithmetic has a CPU counterpart to update.
 Also here: the cost model's choices for the BASELINE shapes through the C ABI
 (`mhb_sign_iterative_path`, host logic only -- no GPU call).
 """
@@ -54,13 +54,11 @@ def enumerate_hits(p, d, h0, T, N):
     out = []
     while t < N:
         out.append((t, v))
-        if v < w:
+        up = v < w
+        if up:
             v += u
             t += n
-        else:
-            v -= w
-            t += m
-        if v >= T:
+        if not (up and v < T):  # no upward step, or one that overshot T: the downward step
             v -= w
             t += m
     return out
