@@ -406,7 +406,8 @@ int64_t gap_full_wave_sets(int32_t n_hash, int64_t n_sets, int64_t nnz) {
 }
 
 // The enumeration pays when a feature's N visits cost more than its descent plus its
-// ~N c / n hits (11 instructions each) and the set's fallback entries.
+// ~N c / n hits (9 instructions each; the model's 11.5 allows for a warp's lanes finishing
+// apart) and the set's fallback entries.
 bool gap_supported(int kind, uint64_t prime, int32_t n_hash, int64_t n_sets, int64_t nnz) {
     if (kind != KIND_ITERATIVE || prime >= (1ull << 31)) return false;
     if (gap_sets_per_tile(n_hash) < 1 || n_sets < 1 || nnz < 1) return false;
