@@ -51,7 +51,7 @@ namespace {
 
 constexpr int kGapThreads = 256;  // default CTA size (template parameter THREADS)
 constexpr int kGapMaxSets = 64;        // sets per tile (upper bound)
-constexpr int kGapFailCap = 1024;      // fallback list entries per tile (overflow: inline)
+constexpr int kGapFailCap = 512;       // fallback list entries per tile, two lists (overflow: marked minima)
 constexpr size_t kGapBestBytes = 104 * 1024;  // running minima per CTA: two CTAs per SM at most
 
 struct GapArgs {
@@ -210,12 +210,15 @@ __device__ __forceinline__ void push_failures(uint32_t mask, uint32_t e0, uint32
 // barrier, which frees 24 registers in the feature phase (many sets per tile, cfg3: 3.50
 // against 3.70 ms).
 template <typename OutT, int INV, int THREADS>
-__global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kernel(GapArgs A) {
     extern __shared__ uint4 gap_smem4[];
-    __shared__ long long sip[kGapMaxSets + 1];
+    // offsets and fallback list of the current and of the previous tile: a tile's fallback
+    // entries are recomputed during the NEXT tile's feature phase (no phase of its own, no
+    // barrier after it, and its uneven per-thread work averages into the longer phase)
+    __shared__ long long sip2[2][kGapMaxSets + 1];
     __shared__ uint32_t sT[kGapMaxSets];
-    __shared__ uint32_t flist[kGapFailCap];
-    __shared__ unsigned fcount;
+    __shared__ uint32_t flist2[2][kGapFailCap];
+    __shared__ unsigned fcount2[2];
     __shared__ unsigned long long s_tile[2];
     uint32_t* best = reinterpret_cast<uint32_t*>(gap_smem4);
     const uint32_t sbest = (uint32_t)__cvta_generic_to_shared(best);
@@ -245,10 +248,41 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
     for (uint32_t q = tid; q < (uint32_t)A.G * N / 4u + 1u; q += THREADS)
         gap_smem4[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     if (tid == 0) s_tile[0] = atomicAdd(A.next, 1ull);
-    for (int par = 0;; par ^= 1) {
-        __syncthreads();  // the previous tile's shared state is no longer read; s_tile[par] is set
+    if (tid < 2) fcount2[tid] = 0;
+    int64_t g0_prev = 0;
+    int Gt_prev = 0;
+    // the previous tile's fallback entries (list, then -- list overflow -- the marked minima)
+    auto previous_fallbacks = [&](int prv, bool marked_only) {
+        OutT* outp = reinterpret_cast<OutT*>(A.out) + g0_prev * (int64_t)N;
+        const long long* sp = sip2[prv];
+        const unsigned nfail = fcount2[prv];
+        if (marked_only) {
+            if (nfail > kGapFailCap) {
+                const uint32_t ents = (uint32_t)Gt_prev * N;
+                for (uint32_t e = tid; e < ents; e += THREADS)
+                    if (best[e] == kGapRedo) {
+                        best[e] = 0xFFFFFFFFu;
+                        const uint32_t s = e / N, i = e - s * N;
+                        fallback_entry<OutT>(A, sp[s], sp[s + 1], i, outp + (int64_t)s * N);
+                    }
+                __syncthreads();  // the minima are clean before the next feature phase
+            }
+            return;
+        }
+        const unsigned nf = min(nfail, (unsigned)kGapFailCap);
+        for (unsigned k = tid; k < nf; k += THREADS) {
+            const uint32_t e = flist2[prv][k], s = e / N, i = e - s * N;
+            fallback_entry<OutT>(A, sp[s], sp[s + 1], i, outp + (int64_t)s * N);
+        }
+    };
+    int par = 0;
+    for (;; par ^= 1) {
+        __syncthreads();  // the tile before last's shared state is no longer read; s_tile[par] is set
         const int64_t tile = (int64_t)s_tile[par];
         if (tile >= n_tiles) break;
+        long long* sip = sip2[par];
+        uint32_t* flist = flist2[par];
+        unsigned& fcount = fcount2[par];
         if (tid == 0) {
             s_tile[par ^ 1] = atomicAdd(A.next, 1ull);  // the next tile, claimed a tile ahead
             fcount = 0;
@@ -272,6 +306,8 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
             }
         }
         __syncthreads();
+        previous_fallbacks(par ^ 1, true);
+        previous_fallbacks(par ^ 1, false);
         const int64_t fbeg = sip[0], fend = sip[Gt];
         for (int64_t f = fbeg + tid; f < fend; f += THREADS) {
             int lo = 0, hi = Gt;  // the set holding feature f: largest s with sip[s] <= f
@@ -352,23 +388,12 @@ __global__ void __launch_bounds__(THREADS) sign_gap_kernel(GapArgs A) {
                 }
             }
         }
-        __syncthreads();
-        const unsigned nfail = fcount;
-        const unsigned nf = min(nfail, (unsigned)kGapFailCap);
-        for (unsigned k = tid; k < nf; k += THREADS) {
-            const uint32_t e = flist[k], s = e / N, i = e - s * N;
-            fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
-        }
-        if (nfail > kGapFailCap) {  // list overflow: the marked minima, in place
-            const uint32_t ents = (uint32_t)Gt * N;
-            for (uint32_t e = tid; e < ents; e += THREADS)
-                if (best[e] == kGapRedo) {
-                    best[e] = 0xFFFFFFFFu;
-                    const uint32_t s = e / N, i = e - s * N;
-                    fallback_entry<OutT>(A, sip[s], sip[s + 1], i, out + (int64_t)s * N);
-                }
-        }
+        g0_prev = g0;
+        Gt_prev = Gt;
     }
+    // the last tile's fallback entries (every thread is past the barrier that followed its row pass)
+    previous_fallbacks(par ^ 1, true);
+    previous_fallbacks(par ^ 1, false);
     if (bad_id && A.status) atomicOr(A.status, MHB_STATUS_ID_GE_PRIME);
 }
 
