@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
     __shared__ uint32_t sT[kGapMaxSets];
     __shared__ uint32_t flist2[2][kGapFailCap];
     __shared__ unsigned fcount2[2];
+    __shared__ unsigned fnext2[2];   // the lists' claim cursors
     __shared__ unsigned long long s_tile[2];
     uint32_t* best = reinterpret_cast<uint32_t*>(gap_smem4);
     const uint32_t sbest = (uint32_t)__cvta_generic_to_shared(best);
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
     for (uint32_t q = tid; q < (uint32_t)A.G * N / 4u + 1u; q += THREADS)
         gap_smem4[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
     if (tid == 0) s_tile[0] = atomicAdd(A.next, 1ull);
-    if (tid < 2) fcount2[tid] = 0;
+    if (tid < 2) fcount2[tid] = fnext2[tid] = 0;
     int64_t g0_prev = 0;
     int Gt_prev = 0;
     // the previous tile's fallback entries (list, then -- list overflow -- the marked minima)
@@ -269,10 +270,19 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
             }
             return;
         }
+        // warps claim the list 32 entries at a time, AFTER their features: the warps that
+        // finish the feature phase early take the entries instead of waiting at the barrier
         const unsigned nf = min(nfail, (unsigned)kGapFailCap);
-        for (unsigned k = tid; k < nf; k += THREADS) {
-            const uint32_t e = flist2[prv][k], s = e / N, i = e - s * N;
-            fallback_entry<OutT>(A, sp[s], sp[s + 1], i, outp + (int64_t)s * N);
+        for (;;) {
+            unsigned base = 0;
+            if ((tid & 31) == 0) base = atomicAdd(&fnext2[prv], 32u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= nf) break;
+            const unsigned k = base + (unsigned)(tid & 31);
+            if (k < nf) {
+                const uint32_t e = flist2[prv][k], s = e / N, i = e - s * N;
+                fallback_entry<OutT>(A, sp[s], sp[s + 1], i, outp + (int64_t)s * N);
+            }
         }
     };
     int par = 0;
@@ -286,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
         if (tid == 0) {
             s_tile[par ^ 1] = atomicAdd(A.next, 1ull);  // the next tile, claimed a tile ahead
             fcount = 0;
+            fnext2[par] = 0;
         }
         const int64_t g0 = tile * A.G;
         const int Gt = (int)min((long long)A.G, (long long)(A.n_sets - g0));
@@ -307,7 +318,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
         }
         __syncthreads();
         previous_fallbacks(par ^ 1, true);
-        previous_fallbacks(par ^ 1, false);
         const int64_t fbeg = sip[0], fend = sip[Gt];
         for (int64_t f = fbeg + tid; f < fend; f += THREADS) {
             int lo = 0, hi = Gt;  // the set holding feature f: largest s with sip[s] <= f
@@ -322,6 +332,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 256 ? 4 : 1) sign_gap_kern
             }
             enumerate_feature(x, sT[lo], sbest + (uint32_t)lo * N * 4u, A);
         }
+        previous_fallbacks(par ^ 1, false);
         if (INV == 2) load_inv();  // lands during the barrier
         __syncthreads();
         // rows out: minima below T are exact; the rest go to the fallback list
