@@ -90,7 +90,9 @@ size_t mhb_sign_workspace_bytes(int64_t n_sets, int64_t nnz, int32_t n_hash);
  *   1  enumerating kernel: per feature only the hashes under the set's threshold, found
  *      through the three-gap structure of the iterative family's arithmetic progression
  *      (sign_gap_kernel, csrc/gap.cu; kernels.py:62-72 is the progression it exploits).
- * The choice is a cost model over (n_hash, mean set size); MHB_GAP=0/1 forces it. */
+ * The choice is a cost model over (n_hash, mean set size); batches of <= 16,384 sets take
+ * kernel 1 only from a full wave of its tiles up (3,552 sets at n_hash 2048).  MHB_GAP=0/1
+ * forces it where it is supported (prime < 2^31, n_hash <= 26,624). */
 int32_t mhb_sign_iterative_path(int64_t n_sets, int64_t nnz, uint64_t prime, int32_t n_hash);
 
 /*

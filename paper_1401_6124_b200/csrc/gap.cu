@@ -487,6 +487,7 @@ int launch_sign_gap(const SignArgs& S, int64_t nnz, int32_t out_dtype, const Dev
     if (threads != 64 && threads != 128 && threads != 512) threads = 256;
     A.G = gap_pick_sets(S.n_hash, S.n_sets, nnz, threads);
     if (const char* ge = std::getenv("MHB_GAP_SETS")) A.G = std::max(1, std::min(std::atoi(ge), gap_sets_per_tile(S.n_hash)));
+    A.G = std::min(A.G, threads - 1);  // thread g loads set g's offset, thread G the end
     const size_t smem = (size_t)A.G * S.n_hash * 4 + 16;
     const bool reg_inv = threads >= 256 && (S.n_hash & 3) == 0 && S.n_hash <= 8 * 256;
     using Fn = void (*)(GapArgs);
